@@ -1,0 +1,149 @@
+/* esp_b200.h -- C ABI of the B200-native ESP (Ewald summation with prolates)
+ * force evaluation.  This is the drop-in boundary: the reference solver is
+ * the header-only C++ API in /root/reference/proj/include/esp (namespace
+ * esp); include/esp/esp.hpp re-exposes that API on top of these entry
+ * points, and INTEGRATION.md shows the ctypes binding.  Every entry point
+ * below names the reference interface it replaces (file:line into
+ * /root/reference/proj/include/esp).
+ *
+ * Conventions (kept from the reference, README.md:149-165):
+ *   * positions are N x 3 doubles, row-major (the std::array<double,3>
+ *     layout of ParticleSystem::pos, system.hpp:19-26); forces likewise;
+ *   * Gaussian units, pair potential q_i q_j / (4 pi r); tinfoil boundary;
+ *   * energy E = 1/2 sum_i q_i u_i;
+ *   * fp64 throughout.
+ * Results are not bitwise reproducible run to run (floating-point atomics
+ * reorder sums on the GPU); they match the reference within the
+ * tolerances stated in DESIGN.md.
+ *
+ * Errors: every function returns ESP_OK (0) or a positive status code and
+ * sets a thread-local message readable with esp_last_error().  No C++
+ * exception crosses this boundary.  The C++ header maps
+ * ESP_ERR_INVALID_ARGUMENT -> std::invalid_argument and
+ * ESP_ERR_NUMERICAL -> esp::NumericalError, as the reference throws them.
+ *
+ * Threading: a plan handle is not re-entrant; use one handle per host
+ * thread.  There is no CPU fallback: device entry points fail with
+ * ESP_ERR_CUDA when no GPU is usable.
+ */
+#ifndef ESP_B200_H
+#define ESP_B200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ESP_OK 0
+#define ESP_ERR_INVALID_ARGUMENT 1 /* std::invalid_argument in the reference */
+#define ESP_ERR_NUMERICAL 2        /* esp::NumericalError (prolate.hpp:17-20) */
+#define ESP_ERR_CUDA 3             /* CUDA / cuFFT runtime failure or no device */
+#define ESP_ERR_NO_DEVICE 4        /* plan was created host-only (device < 0) */
+#define ESP_ERR_INTERNAL 5
+
+#define ESP_FAMILY_PSWF 0     /* SplitFamily::pswf (kernels.hpp:19) */
+#define ESP_FAMILY_GAUSSIAN 1 /* SplitFamily::gaussian */
+#define ESP_FORCE_IK 0        /* ForceMethod::ik (ewald.hpp:28), the default */
+#define ESP_FORCE_AD 1        /* ForceMethod::ad */
+
+typedef struct esp_plan esp_plan;
+
+/* Overrides (ewald.hpp:38-47). Zero-initialise for the reference defaults. */
+typedef struct {
+    int nf;             /* 0 = auto; > 0 pins n_f in every dimension (even) */
+    int P;              /* 0 = auto */
+    double c1;          /* 0 = auto (PSWF window bandwidth) */
+    int force_method;   /* ESP_FORCE_IK | ESP_FORCE_AD */
+    int allow_degraded; /* build plans whose predicted error exceeds eps */
+} esp_overrides;
+
+/* Scalars of EwaldPlan (ewald.hpp:67-94) plus PlanStats (:61-65). */
+typedef struct {
+    int family, force_method, P;
+    int nf[3], base_nf[3];
+    double eps, r_c, shape, c1, chi0;
+    double box[3], h[3], demand[3];
+    double E_A, E_T, E_SI;
+    double self_coef;       /* chi(0) / (4 pi r_c), ewald.hpp:609-615 */
+    int n_split_coef;       /* prolate Legendre terms of the split */
+    int n_window_coef;      /* prolate Legendre terms of the window */
+    int pair_poly_degree;   /* degree of the device pair polynomials */
+    double pair_fit_err;    /* their max deviation from the exact kernels */
+    int device;             /* -1 for a host-only plan */
+    int pair_cells[3];      /* GPU cell-list geometry */
+} esp_plan_info;
+
+/* Per-stage wall time in seconds (EnergyForces::timings keys,
+ * ewald.hpp:628-634) plus the GPU binning stage.  Filled only by the
+ * synchronous entry points when requested (stages are then serialised). */
+typedef struct {
+    double local, spread, fft, scale, ifft, interpolate, bin;
+} esp_timings;
+
+const char* esp_last_error(void);
+const char* esp_version(void);
+/* Number of visible CUDA devices (0 when none; never an error). */
+int esp_device_count(void);
+
+/* build_plan (ewald.hpp:355-405).  device >= 0 creates the device engine
+ * on that CUDA device; device < 0 builds a host-only plan (parameter
+ * selection and tables, no GPU needed).  *out owns all device state. */
+int esp_plan_create(const double box[3], int family, double eps, double r_c,
+                    const esp_overrides* ov, int device, esp_plan** out);
+void esp_plan_destroy(esp_plan* plan);
+int esp_plan_get_info(const esp_plan* plan, esp_plan_info* out);
+
+/* Plan tables (for parity checks).  influence: full nx*ny*nz reference
+ * layout (gridder.hpp:162-210).  which: 0 Psi, 1 chi (16 x 13 Chebyshev-T
+ * coefficients), 2 phi, 3 dphi of dimension dim (4P x 13).  prolate: which
+ * -1 split, 0 window (Legendre coefficients a_k, psi(0) = 1). */
+int esp_plan_get_influence(const esp_plan* plan, double* out);
+int esp_plan_get_table(const esp_plan* plan, int which, int dim, double* out, int* nseg);
+int esp_plan_get_prolate(const esp_plan* plan, int which, double* out, int* n);
+/* Host evaluators of the plan kernels: what 0 Psi, 1 chi, 2 chihat_n,
+ * 3 phi(dim 0), 4 dphi, 5 phi_hat, 6 local potential, 7 local radial force
+ * (kernels.hpp:63-229). */
+int esp_plan_eval_kernel(const esp_plan* plan, int what, long n, const double* x, double* y);
+
+/* evaluate (ewald.hpp:619-649) on HOST buffers: copies in, evaluates on the
+ * GPU, copies out, synchronises, checks charge neutrality.  Raises the
+ * reference's errors: box mismatch -> INVALID_ARGUMENT, non-neutral ->
+ * NUMERICAL.  timings may be NULL (then the stages overlap). */
+int esp_evaluate(esp_plan* plan, const double box[3], long N, const double* pos,
+                 const double* q, double* u, double* F, double* energy, esp_timings* timings);
+
+/* Device-resident evaluate: all pointers are device pointers; energy_dev is
+ * one device double; stream is a cudaStream_t (NULL = legacy default).
+ * Asynchronous; charge neutrality is not checked here (see
+ * esp_check_neutral). */
+int esp_evaluate_device(esp_plan* plan, const double box[3], long N, const double* pos_dev,
+                        const double* q_dev, double* u_dev, double* F_dev, double* energy_dev,
+                        void* stream);
+
+/* require_neutral (system.hpp:39-47) on host data. */
+int esp_check_neutral(long N, const double* q);
+
+/* Parts of the hot path on HOST buffers (synchronous). */
+int esp_local_sum(esp_plan* plan, const double box[3], long N, const double* pos,
+                  const double* q, double* u, double* F);          /* ewald.hpp:419-515 */
+int esp_spectral_sum(esp_plan* plan, const double box[3], long N, const double* pos,
+                     const double* q, double* u, double* F);       /* ewald.hpp:524-604 */
+int esp_self_correction(const esp_plan* plan, long N, const double* q, double* out);
+                                                                    /* ewald.hpp:609-615 */
+int esp_spread(esp_plan* plan, long N, const double* pos, const double* q, double* grid);
+                                                                    /* gridder.hpp:215-241 */
+int esp_interpolate(esp_plan* plan, long N, const double* pos, const double* grid,
+                    double* out);                                   /* gridder.hpp:244-277 */
+int esp_interpolate_gradient(esp_plan* plan, long N, const double* pos, const double* grid,
+                             double* out);                          /* gridder.hpp:280-314 */
+
+/* Kernel launches issued by the last evaluate (our kernels, excluding
+ * cuFFT and CUB scans). */
+int esp_last_launch_count(const esp_plan* plan);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ESP_B200_H */

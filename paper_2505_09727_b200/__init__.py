@@ -1,0 +1,382 @@
+"""B200-native ESP (Ewald summation with prolates) -- Python mirror of the
+reference solver interface (/root/reference/proj/include/esp, namespace esp).
+
+The names, argument meanings and error behaviour follow the reference:
+
+    plan = build_plan(box, "pswf", eps=1e-4, r_c=1.0)          # ewald.hpp:355
+    ef   = evaluate(plan, ParticleSystem(box, q, pos))           # ewald.hpp:619
+    ef.energy, ef.u, ef.F, ef.timings
+
+All compute runs in libesp_b200.so (hand-written sm_100a kernels + cuFFT)
+through the C ABI declared in include/esp_b200.h.  There is no CPU
+fallback: importing this package fails loudly if the library is missing,
+and evaluating on a machine without a GPU raises CudaError.
+
+Exceptions: InvalidArgument (a ValueError) where the reference throws
+std::invalid_argument; NumericalError where it throws esp::NumericalError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+__all__ = [
+    "InvalidArgument", "NumericalError", "CudaError", "Overrides", "EwaldPlan",
+    "ParticleSystem", "EnergyForces", "PartialField", "build_plan", "evaluate",
+    "evaluate_device", "local_sum", "spectral_sum", "self_correction", "spread",
+    "interpolate", "interpolate_gradient", "require_neutral", "fold", "device_count",
+    "LIB_PATH",
+]
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libesp_b200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python paper_2505_09727_b200/build.py` "
+        "(there is no CPU fallback)")
+
+_lib = C.CDLL(LIB_PATH)
+_dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class NumericalError(RuntimeError):
+    """esp::NumericalError (prolate.hpp:17-20)."""
+
+
+class CudaError(RuntimeError):
+    """CUDA / cuFFT failure, or a device entry point on a host-only plan."""
+
+
+class _Overrides(C.Structure):
+    _fields_ = [("nf", C.c_int), ("P", C.c_int), ("c1", C.c_double),
+                ("force_method", C.c_int), ("allow_degraded", C.c_int)]
+
+
+class _Info(C.Structure):
+    _fields_ = [
+        ("family", C.c_int), ("force_method", C.c_int), ("P", C.c_int),
+        ("nf", C.c_int * 3), ("base_nf", C.c_int * 3),
+        ("eps", C.c_double), ("r_c", C.c_double), ("shape", C.c_double), ("c1", C.c_double),
+        ("chi0", C.c_double),
+        ("box", C.c_double * 3), ("h", C.c_double * 3), ("demand", C.c_double * 3),
+        ("E_A", C.c_double), ("E_T", C.c_double), ("E_SI", C.c_double),
+        ("self_coef", C.c_double),
+        ("n_split_coef", C.c_int), ("n_window_coef", C.c_int), ("pair_poly_degree", C.c_int),
+        ("pair_fit_err", C.c_double), ("device", C.c_int), ("pair_cells", C.c_int * 3),
+    ]
+
+
+class _Timings(C.Structure):
+    _fields_ = [(k, C.c_double) for k in
+                ("local", "spread", "fft", "scale", "ifft", "interpolate", "bin")]
+
+
+def _sig(name, args, res=C.c_int):
+    f = getattr(_lib, name)
+    f.argtypes = args
+    f.restype = res
+    return f
+
+
+_vp = C.c_void_p
+_sig("esp_last_error", [], C.c_char_p)
+_sig("esp_version", [], C.c_char_p)
+_sig("esp_device_count", [])
+_sig("esp_plan_create", [_dp, C.c_int, C.c_double, C.c_double, C.POINTER(_Overrides), C.c_int,
+                         C.POINTER(_vp)])
+_sig("esp_plan_destroy", [_vp], None)
+_sig("esp_plan_get_info", [_vp, C.POINTER(_Info)])
+_sig("esp_plan_get_influence", [_vp, _dp])
+_sig("esp_plan_get_table", [_vp, C.c_int, C.c_int, _vp, C.POINTER(C.c_int)])
+_sig("esp_plan_get_prolate", [_vp, C.c_int, _vp, C.POINTER(C.c_int)])
+_sig("esp_plan_eval_kernel", [_vp, C.c_int, C.c_long, _dp, _dp])
+_sig("esp_evaluate", [_vp, _dp, C.c_long, _dp, _dp, _dp, _dp, C.POINTER(C.c_double),
+                      C.POINTER(_Timings)])
+_sig("esp_evaluate_device", [_vp, _dp, C.c_long, _vp, _vp, _vp, _vp, _vp, _vp])
+_sig("esp_check_neutral", [C.c_long, _dp])
+_sig("esp_local_sum", [_vp, _dp, C.c_long, _dp, _dp, _dp, _dp])
+_sig("esp_spectral_sum", [_vp, _dp, C.c_long, _dp, _dp, _dp, _dp])
+_sig("esp_self_correction", [_vp, C.c_long, _dp, _dp])
+_sig("esp_spread", [_vp, C.c_long, _dp, _dp, _dp])
+_sig("esp_interpolate", [_vp, C.c_long, _dp, _dp, _dp])
+_sig("esp_interpolate_gradient", [_vp, C.c_long, _dp, _dp, _dp])
+_sig("esp_last_launch_count", [_vp])
+
+
+def _check(rc: int):
+    if rc == 0:
+        return
+    msg = (_lib.esp_last_error() or b"").decode()
+    if rc == 1:
+        raise InvalidArgument(msg)
+    if rc == 2:
+        raise NumericalError(msg)
+    if rc in (3, 4):
+        raise CudaError(msg)
+    raise RuntimeError(msg)
+
+
+def _f64(a, shape=None):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a.reshape(shape) if shape is not None else a
+
+
+def device_count() -> int:
+    return int(_lib.esp_device_count())
+
+
+def version() -> str:
+    return _lib.esp_version().decode()
+
+
+@dataclass
+class Overrides:
+    """ewald.hpp:38-47."""
+    nf: int = 0
+    P: int = 0
+    c1: float = 0.0
+    force_method: str = "ik"
+    allow_degraded: bool = False
+
+    def _c(self) -> _Overrides:
+        if self.force_method not in ("ik", "ad"):
+            raise InvalidArgument("unknown force method: " + str(self.force_method))
+        return _Overrides(int(self.nf), int(self.P), float(self.c1),
+                          1 if self.force_method == "ad" else 0, int(bool(self.allow_degraded)))
+
+
+@dataclass
+class PlanStats:
+    E_A: float
+    E_T: float
+    E_SI: float
+
+
+class EwaldPlan:
+    """Immutable plan (ewald.hpp:67-94) owning its device state."""
+
+    def __init__(self, handle: C.c_void_p):
+        self._h = handle
+        info = _Info()
+        _check(_lib.esp_plan_get_info(self._h, C.byref(info)))
+        self._info = info
+        self.family = "gaussian" if info.family == 1 else "pswf"
+        self.window_family = "bspline" if info.family == 1 else "pswf"
+        self.force_method = "ad" if info.force_method == 1 else "ik"
+        self.eps = info.eps
+        self.r_c = info.r_c
+        self.box = tuple(info.box)
+        self.nf = tuple(info.nf)
+        self.base_nf = tuple(info.base_nf)
+        self.demand = tuple(info.demand)
+        self.h = tuple(info.h)
+        self.P = info.P
+        self.shape = info.shape
+        self.c1 = info.c1
+        self.chi0 = info.chi0
+        self.self_coef = info.self_coef
+        self.stats = PlanStats(info.E_A, info.E_T, info.E_SI)
+        self.device = info.device
+        self.pair_poly_degree = info.pair_poly_degree
+        self.pair_fit_err = info.pair_fit_err
+        self.pair_cells = tuple(info.pair_cells)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                _lib.esp_plan_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    def total_modes(self) -> int:
+        return int(self.nf[0]) * int(self.nf[1]) * int(self.nf[2])
+
+    def avg_neighbors(self, N: int) -> float:
+        return (4.0 / 3.0) * np.pi * self.r_c ** 3 * N / float(np.prod(self.box))
+
+    @property
+    def influence(self) -> np.ndarray:
+        out = np.empty(self.total_modes())
+        _check(_lib.esp_plan_get_influence(self._h, out))
+        return out.reshape(self.nf)
+
+    def table(self, which: str, dim: int = 0) -> np.ndarray:
+        sel = {"Psi": 0, "chi": 1, "phi": 2, "dphi": 3}[which]
+        n = C.c_int()
+        _check(_lib.esp_plan_get_table(self._h, sel, dim, None, C.byref(n)))
+        out = np.empty(n.value * 13)
+        _check(_lib.esp_plan_get_table(self._h, sel, dim, out.ctypes.data, C.byref(n)))
+        return out.reshape(n.value, 13)
+
+    def prolate_coef(self, which: int = -1) -> np.ndarray:
+        n = C.c_int()
+        _check(_lib.esp_plan_get_prolate(self._h, which, None, C.byref(n)))
+        out = np.empty(n.value)
+        _check(_lib.esp_plan_get_prolate(self._h, which, out.ctypes.data, C.byref(n)))
+        return out
+
+    def eval_kernel(self, what: str, x) -> np.ndarray:
+        sel = {"Psi": 0, "chi": 1, "chihat_n": 2, "phi": 3, "dphi": 4, "phi_hat": 5,
+               "local_pot": 6, "local_fr": 7}[what]
+        x = _f64(np.atleast_1d(x))
+        y = np.empty_like(x)
+        _check(_lib.esp_plan_eval_kernel(self._h, sel, x.size, x, y))
+        return y
+
+    def last_launch_count(self) -> int:
+        return int(_lib.esp_last_launch_count(self._h))
+
+
+@dataclass
+class ParticleSystem:
+    """system.hpp:19-26: box edges, charges, positions (N x 3)."""
+    box: tuple
+    q: np.ndarray
+    pos: np.ndarray
+
+    def __post_init__(self):
+        self.box = tuple(float(b) for b in self.box)
+        self.q = _f64(self.q)
+        self.pos = _f64(self.pos).reshape(-1, 3)
+        if self.pos.shape[0] != self.q.shape[0]:
+            raise InvalidArgument("positions and charges differ in length")
+
+    def size(self) -> int:
+        return int(self.q.shape[0])
+
+    def volume(self) -> float:
+        return float(np.prod(self.box))
+
+
+@dataclass
+class EnergyForces:
+    """system.hpp:49-55."""
+    energy: float
+    u: np.ndarray
+    F: np.ndarray
+    timings: dict = field(default_factory=dict)
+
+
+@dataclass
+class PartialField:
+    """ewald.hpp:411-414."""
+    u: np.ndarray
+    F: np.ndarray
+
+
+def build_plan(box, family: str = "pswf", eps: float = 1e-4, r_c: float = 1.0,
+               ov: Overrides | None = None, device: int | None = None) -> EwaldPlan:
+    """ewald.hpp:355-405.  device=None picks GPU 0 when one is visible and
+    builds a host-only plan (parameters and tables, no evaluation) otherwise."""
+    if family not in ("pswf", "gaussian"):
+        raise InvalidArgument("unknown screen family: " + str(family))
+    if device is None:
+        device = 0 if device_count() > 0 else -1
+    ov = ov or Overrides()
+    h = C.c_void_p()
+    _check(_lib.esp_plan_create(_f64(box, (3,)), 1 if family == "gaussian" else 0, float(eps),
+                                float(r_c), C.byref(ov._c()), int(device), C.byref(h)))
+    return EwaldPlan(h)
+
+
+def select_parameters(family: str, eps: float, box, r_c: float, ov: Overrides | None = None):
+    """ewald.hpp:338-349 (host-only plan; same selection as build_plan)."""
+    return build_plan(box, family, eps, r_c, ov, device=-1)
+
+
+def fold(system: ParticleSystem) -> ParticleSystem:
+    """system.hpp:29-36 (host helper; the device path folds inside K0)."""
+    L = np.asarray(system.box)
+    p = system.pos - L * np.floor(system.pos / L)
+    p = np.where(p >= L, 0.0, p)
+    return ParticleSystem(system.box, system.q.copy(), p)
+
+
+def require_neutral(system: ParticleSystem) -> None:
+    """system.hpp:39-47."""
+    _check(_lib.esp_check_neutral(system.size(), system.q))
+
+
+def evaluate(plan: EwaldPlan, system: ParticleSystem, timings: bool = False) -> EnergyForces:
+    """ewald.hpp:619-649 on host arrays (H2D, GPU evaluation, D2H).
+
+    timings=True serialises the stages and reports them under the
+    reference's keys (seconds) plus 'bin'."""
+    N = system.size()
+    u = np.empty(N)
+    F = np.empty((N, 3))
+    e = C.c_double()
+    t = _Timings() if timings else None
+    _check(_lib.esp_evaluate(plan._h, _f64(system.box, (3,)), N, system.pos, system.q, u, F,
+                             C.byref(e), C.byref(t) if t is not None else None))
+    tim = {k: getattr(t, k) for k, _ in _Timings._fields_} if t is not None else {
+        k: 0.0 for k in ("local", "spread", "fft", "scale", "ifft", "interpolate")}
+    return EnergyForces(e.value, u, F, tim)
+
+
+def evaluate_device(plan: EwaldPlan, box, N: int, pos_ptr: int, q_ptr: int, u_ptr: int,
+                    F_ptr: int, energy_ptr: int, stream: int = 0) -> None:
+    """Device-resident evaluate (asynchronous on `stream`); pointers are raw
+    device addresses (e.g. torch.Tensor.data_ptr())."""
+    _check(_lib.esp_evaluate_device(plan._h, _f64(box, (3,)), int(N), C.c_void_p(pos_ptr),
+                                    C.c_void_p(q_ptr), C.c_void_p(u_ptr), C.c_void_p(F_ptr),
+                                    C.c_void_p(energy_ptr), C.c_void_p(stream)))
+
+
+def local_sum(plan: EwaldPlan, system: ParticleSystem) -> PartialField:
+    """ewald.hpp:419-515."""
+    N = system.size()
+    u = np.empty(N)
+    F = np.empty((N, 3))
+    _check(_lib.esp_local_sum(plan._h, _f64(system.box, (3,)), N, system.pos, system.q, u, F))
+    return PartialField(u, F)
+
+
+def spectral_sum(plan: EwaldPlan, system: ParticleSystem) -> PartialField:
+    """ewald.hpp:524-604."""
+    N = system.size()
+    u = np.empty(N)
+    F = np.empty((N, 3))
+    _check(_lib.esp_spectral_sum(plan._h, _f64(system.box, (3,)), N, system.pos, system.q, u,
+                                 F))
+    return PartialField(u, F)
+
+
+def self_correction(plan: EwaldPlan, q) -> np.ndarray:
+    """ewald.hpp:609-615."""
+    q = _f64(q)
+    out = np.empty_like(q)
+    _check(_lib.esp_self_correction(plan._h, q.size, q, out))
+    return out
+
+
+def spread(plan: EwaldPlan, system: ParticleSystem) -> np.ndarray:
+    """gridder.hpp:215-241: the real charge grid (nx, ny, nz)."""
+    g = np.empty(plan.total_modes())
+    _check(_lib.esp_spread(plan._h, system.size(), system.pos, system.q, g))
+    return g.reshape(plan.nf)
+
+
+def interpolate(plan: EwaldPlan, grid, system: ParticleSystem) -> np.ndarray:
+    """gridder.hpp:244-277 of a real grid."""
+    out = np.empty(system.size())
+    _check(_lib.esp_interpolate(plan._h, system.size(), system.pos, _f64(grid).ravel(), out))
+    return out
+
+
+def interpolate_gradient(plan: EwaldPlan, grid, system: ParticleSystem) -> np.ndarray:
+    """gridder.hpp:280-314."""
+    out = np.empty((system.size(), 3))
+    _check(_lib.esp_interpolate_gradient(plan._h, system.size(), system.pos,
+                                         _f64(grid).ravel(), out))
+    return out

@@ -1,0 +1,421 @@
+// C ABI (include/esp_b200.h) over the host plan builder and the device engine.
+
+#include "../../include/esp_b200.h"
+
+#include "engine.hpp"
+#include "plan.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+struct esp_plan {
+    espb::Plan plan;
+    std::unique_ptr<espb::Engine> eng;
+    int device = -1;
+    // device staging for the host-pointer entry points
+    double* d_pos = nullptr;
+    double* d_q = nullptr;
+    double* d_u = nullptr;
+    double* d_F = nullptr;
+    double* d_e = nullptr;  // energy + qsum[2]
+    long cap = 0;
+    cudaStream_t stream = nullptr;
+
+    ~esp_plan() {
+        if (device >= 0) {
+            cudaSetDevice(device);
+            cudaFree(d_pos);
+            cudaFree(d_q);
+            cudaFree(d_u);
+            cudaFree(d_F);
+            cudaFree(d_e);
+            if (stream) cudaStreamDestroy(stream);
+        }
+    }
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return ESP_OK;
+    } catch (const espb::InvalidArgument& e) {
+        g_err = e.what();
+        return ESP_ERR_INVALID_ARGUMENT;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return ESP_ERR_INVALID_ARGUMENT;
+    } catch (const espb::NumericalError& e) {
+        g_err = e.what();
+        return ESP_ERR_NUMERICAL;
+    } catch (const espb::CudaError& e) {
+        g_err = e.what();
+        return ESP_ERR_CUDA;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return ESP_ERR_INTERNAL;
+    }
+}
+
+void cuda_ok(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw espb::CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+espb::Engine& engine(esp_plan* p) {
+    if (!p) throw espb::InvalidArgument("null plan");
+    if (!p->eng) throw espb::CudaError("plan was created host-only (device < 0)");
+    return *p->eng;
+}
+
+void check_box(const esp_plan* p, const double* box, const char* who) {
+    // evaluate / spectral_sum require box == plan.box exactly (ewald.hpp:620-621)
+    if (!box) return;
+    for (int d = 0; d < 3; ++d)
+        if (box[d] != p->plan.box[d])
+            throw espb::InvalidArgument(std::string(who) + ": system box does not match plan box");
+}
+
+void require_neutral(long N, const double* q) {
+    // system.hpp:39-47
+    double total = 0.0, abssum = 0.0;
+    for (long i = 0; i < N; ++i) {
+        total += q[i];
+        abssum += std::fabs(q[i]);
+    }
+    if (std::fabs(total) > 1e-12 * std::max(abssum, 1.0))
+        throw espb::NumericalError("system is not charge neutral");
+}
+
+void stage(esp_plan* p, long N) {
+    cuda_ok(cudaSetDevice(p->device), "cudaSetDevice");
+    if (!p->stream) cuda_ok(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking), "stream");
+    if (!p->d_e) cuda_ok(cudaMalloc(&p->d_e, 4 * sizeof(double)), "cudaMalloc");
+    if (N <= p->cap) return;
+    cudaFree(p->d_pos);
+    cudaFree(p->d_q);
+    cudaFree(p->d_u);
+    cudaFree(p->d_F);
+    long c = std::max<long>(N, 1);
+    cuda_ok(cudaMalloc(&p->d_pos, 3 * c * sizeof(double)), "cudaMalloc");
+    cuda_ok(cudaMalloc(&p->d_q, c * sizeof(double)), "cudaMalloc");
+    cuda_ok(cudaMalloc(&p->d_u, 3 * c * sizeof(double)), "cudaMalloc");
+    cuda_ok(cudaMalloc(&p->d_F, 3 * c * sizeof(double)), "cudaMalloc");
+    p->cap = c;
+}
+
+void h2d(esp_plan* p, double* dst, const double* src, long n) {
+    if (n > 0)
+        cuda_ok(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyHostToDevice, p->stream),
+                "H2D");
+}
+void d2h(esp_plan* p, double* dst, const double* src, long n) {
+    if (n > 0)
+        cuda_ok(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToHost, p->stream),
+                "D2H");
+}
+void sync(esp_plan* p) { cuda_ok(cudaStreamSynchronize(p->stream), "synchronize"); }
+
+void check_n(long N) {
+    if (N < 0) throw espb::InvalidArgument("N must be non-negative");
+    if (N > 0x7fffffffL) throw espb::InvalidArgument("N exceeds the 2^31-1 atom limit");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* esp_last_error(void) { return g_err.c_str(); }
+const char* esp_version(void) { return "esp-b200 0.1 (sm_100a)"; }
+
+int esp_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int esp_plan_create(const double box[3], int family, double eps, double r_c,
+                    const esp_overrides* ov, int device, esp_plan** out) {
+    return guarded([&] {
+        if (!out || !box) throw espb::InvalidArgument("null argument");
+        *out = nullptr;
+        espb::Overrides o;
+        if (ov) {
+            o.nf = ov->nf;
+            o.P = ov->P;
+            o.c1 = ov->c1;
+            o.force_method = ov->force_method == ESP_FORCE_AD ? espb::ForceMethod::ad
+                                                              : espb::ForceMethod::ik;
+            o.allow_degraded = ov->allow_degraded != 0;
+        }
+        auto h = std::make_unique<esp_plan>();
+        h->plan = espb::build_plan({box[0], box[1], box[2]},
+                                   family == ESP_FAMILY_GAUSSIAN ? espb::Family::gaussian
+                                                                 : espb::Family::pswf,
+                                   eps, r_c, o);
+        if (device >= 0) {
+            int n = 0;
+            if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+                cudaGetLastError();
+                throw espb::CudaError("no CUDA device available");
+            }
+            if (device >= n) throw espb::InvalidArgument("device index out of range");
+            h->device = device;
+            h->eng = std::make_unique<espb::Engine>(h->plan, device);
+        }
+        *out = h.release();
+    });
+}
+
+void esp_plan_destroy(esp_plan* plan) { delete plan; }
+
+int esp_plan_get_info(const esp_plan* p, esp_plan_info* o) {
+    return guarded([&] {
+        if (!p || !o) throw espb::InvalidArgument("null argument");
+        const espb::Plan& P = p->plan;
+        std::memset(o, 0, sizeof(*o));
+        o->family = static_cast<int>(P.family);
+        o->force_method = static_cast<int>(P.force_method);
+        o->P = P.P;
+        for (int d = 0; d < 3; ++d) {
+            o->nf[d] = P.nf[d];
+            o->base_nf[d] = P.base_nf[d];
+            o->box[d] = P.box[d];
+            o->h[d] = P.h[d];
+            o->demand[d] = P.demand[d];
+            o->pair_cells[d] = std::max(1, static_cast<int>(std::floor(P.box[d] / P.r_c)));
+        }
+        o->eps = P.eps;
+        o->r_c = P.r_c;
+        o->shape = P.shape;
+        o->c1 = P.c1;
+        o->chi0 = P.chi0;
+        o->E_A = P.E_A;
+        o->E_T = P.E_T;
+        o->E_SI = P.E_SI;
+        o->self_coef = P.self_coef;
+        o->n_split_coef = static_cast<int>(P.split.a.size());
+        o->n_window_coef = static_cast<int>(P.window.a.size());
+        o->pair_poly_degree = static_cast<int>(P.pair_G.size()) - 1;
+        o->pair_fit_err = P.pair_fit_err;
+        o->device = p->device;
+    });
+}
+
+int esp_plan_get_influence(const esp_plan* p, double* out) {
+    return guarded([&] {
+        auto v = espb::influence_full(p->plan);
+        std::memcpy(out, v.data(), v.size() * sizeof(double));
+    });
+}
+
+int esp_plan_get_table(const esp_plan* p, int which, int dim, double* out, int* nseg) {
+    return guarded([&] {
+        const espb::PiecewisePoly* pp = nullptr;
+        if (dim < 0 || dim > 2) throw espb::InvalidArgument("dim out of range");
+        switch (which) {
+            case 0: pp = &p->plan.Psi; break;
+            case 1: pp = &p->plan.chi; break;
+            case 2: pp = &p->plan.phi[dim]; break;
+            case 3: pp = &p->plan.dphi[dim]; break;
+            default: throw espb::InvalidArgument("table selector out of range");
+        }
+        if (nseg) *nseg = pp->nseg;
+        if (out) std::memcpy(out, pp->cheb.data(), pp->cheb.size() * sizeof(double));
+    });
+}
+
+int esp_plan_get_prolate(const esp_plan* p, int which, double* out, int* n) {
+    return guarded([&] {
+        const auto& a = which < 0 ? p->plan.split.a : p->plan.window.a;
+        if (n) *n = static_cast<int>(a.size());
+        if (out) std::memcpy(out, a.data(), a.size() * sizeof(double));
+    });
+}
+
+int esp_plan_eval_kernel(const esp_plan* p, int what, long n, const double* x, double* y) {
+    return guarded([&] {
+        const espb::Plan& P = p->plan;
+        for (long i = 0; i < n; ++i) {
+            switch (what) {
+                case 0: y[i] = P.Psi_at(x[i]); break;
+                case 1: y[i] = P.chi_at(x[i]); break;
+                case 2: y[i] = P.chihat_n(x[i]); break;
+                case 3: y[i] = P.phi_at(0, x[i]); break;
+                case 4: y[i] = P.dphi_at(0, x[i]); break;
+                case 5: y[i] = P.phi_hat(0, x[i]); break;
+                case 6: y[i] = P.local_kernel(x[i]).first; break;
+                case 7: y[i] = P.local_kernel(x[i]).second; break;
+                default: throw espb::InvalidArgument("kernel selector out of range");
+            }
+        }
+    });
+}
+
+int esp_check_neutral(long N, const double* q) {
+    return guarded([&] { require_neutral(N, q); });
+}
+
+int esp_self_correction(const esp_plan* p, long N, const double* q, double* out) {
+    return guarded([&] {
+        const double s0 = p->plan.self_coef;  // ewald.hpp:611
+        for (long i = 0; i < N; ++i) out[i] = q[i] * s0;
+    });
+}
+
+int esp_evaluate(esp_plan* p, const double box[3], long N, const double* pos, const double* q,
+                 double* u, double* F, double* energy, esp_timings* timings) {
+    return guarded([&] {
+        espb::Engine& e = engine(p);
+        check_box(p, box, "evaluate");
+        check_n(N);
+        stage(p, N);
+        h2d(p, p->d_pos, pos, 3 * N);
+        h2d(p, p->d_q, q, N);
+        espb::StageTimes st;
+        e.evaluate(N, p->d_pos, p->d_q, p->d_u, p->d_F, p->d_e, p->d_e + 1, p->stream,
+                   timings ? &st : nullptr);
+        d2h(p, u, p->d_u, N);
+        d2h(p, F, p->d_F, 3 * N);
+        double hv[3];
+        cuda_ok(cudaMemcpyAsync(hv, p->d_e, 3 * sizeof(double), cudaMemcpyDeviceToHost, p->stream),
+                "D2H");
+        sync(p);
+        // require_neutral (system.hpp:39-47) from the fused device sums
+        if (std::fabs(hv[1]) > 1e-12 * std::max(hv[2], 1.0))
+            throw espb::NumericalError("system is not charge neutral");
+        *energy = hv[0];
+        if (timings) {
+            timings->local = st.local;
+            timings->spread = st.spread;
+            timings->fft = st.fft;
+            timings->scale = st.scale;
+            timings->ifft = st.ifft;
+            timings->interpolate = st.interpolate;
+            timings->bin = st.bin;
+        }
+    });
+}
+
+int esp_evaluate_device(esp_plan* p, const double box[3], long N, const double* pos_dev,
+                        const double* q_dev, double* u_dev, double* F_dev, double* energy_dev,
+                        void* stream) {
+    return guarded([&] {
+        espb::Engine& e = engine(p);
+        check_box(p, box, "evaluate");
+        check_n(N);
+        cuda_ok(cudaSetDevice(p->device), "cudaSetDevice");
+        e.evaluate(N, pos_dev, q_dev, u_dev, F_dev, energy_dev, nullptr,
+                   static_cast<cudaStream_t>(stream), nullptr);
+    });
+}
+
+int esp_local_sum(esp_plan* p, const double box[3], long N, const double* pos, const double* q,
+                  double* u, double* F) {
+    return guarded([&] {
+        espb::Engine& e = engine(p);
+        // local_sum requires r_c < min(L)/2 of the system box (ewald.hpp:420-422)
+        if (box) {
+            double Lmin = std::min({box[0], box[1], box[2]});
+            if (!(p->plan.r_c < Lmin / 2.0))
+                throw espb::InvalidArgument("local_sum: require r_c < min(L)/2");
+            check_box(p, box, "local_sum");
+        }
+        check_n(N);
+        stage(p, N);
+        h2d(p, p->d_pos, pos, 3 * N);
+        h2d(p, p->d_q, q, N);
+        e.local_sum(N, p->d_pos, p->d_q, p->d_u, p->d_F, p->stream);
+        d2h(p, u, p->d_u, N);
+        d2h(p, F, p->d_F, 3 * N);
+        sync(p);
+    });
+}
+
+int esp_spectral_sum(esp_plan* p, const double box[3], long N, const double* pos,
+                     const double* q, double* u, double* F) {
+    return guarded([&] {
+        espb::Engine& e = engine(p);
+        check_box(p, box, "spectral_sum");
+        check_n(N);
+        stage(p, N);
+        h2d(p, p->d_pos, pos, 3 * N);
+        h2d(p, p->d_q, q, N);
+        e.spectral_sum(N, p->d_pos, p->d_q, p->d_u, p->d_F, p->stream);
+        d2h(p, u, p->d_u, N);
+        d2h(p, F, p->d_F, 3 * N);
+        sync(p);
+    });
+}
+
+int esp_spread(esp_plan* p, long N, const double* pos, const double* q, double* grid) {
+    return guarded([&] {
+        espb::Engine& e = engine(p);
+        check_n(N);
+        stage(p, N);
+        const long M = static_cast<long>(p->plan.nf[0]) * p->plan.nf[1] * p->plan.nf[2];
+        double* d_grid = nullptr;
+        cuda_ok(cudaMalloc(&d_grid, M * sizeof(double)), "cudaMalloc");
+        try {
+            h2d(p, p->d_pos, pos, 3 * N);
+            h2d(p, p->d_q, q, N);
+            e.spread(N, p->d_pos, p->d_q, d_grid, p->stream);
+            d2h(p, grid, d_grid, M);
+            sync(p);
+        } catch (...) {
+            cudaFree(d_grid);
+            throw;
+        }
+        cudaFree(d_grid);
+    });
+}
+
+static int interp_common(esp_plan* p, long N, const double* pos, const double* grid, double* out,
+                         bool gradient) {
+    return guarded([&] {
+        espb::Engine& e = engine(p);
+        check_n(N);
+        stage(p, N);
+        const long M = static_cast<long>(p->plan.nf[0]) * p->plan.nf[1] * p->plan.nf[2];
+        double* d_grid = nullptr;
+        cuda_ok(cudaMalloc(&d_grid, M * sizeof(double)), "cudaMalloc");
+        try {
+            h2d(p, p->d_pos, pos, 3 * N);
+            h2d(p, d_grid, grid, M);
+            if (gradient) e.interpolate_gradient(N, p->d_pos, d_grid, p->d_u, p->stream);
+            else e.interpolate(N, p->d_pos, d_grid, p->d_u, p->stream);
+            d2h(p, out, p->d_u, gradient ? 3 * N : N);
+            sync(p);
+        } catch (...) {
+            cudaFree(d_grid);
+            throw;
+        }
+        cudaFree(d_grid);
+    });
+}
+
+int esp_interpolate(esp_plan* p, long N, const double* pos, const double* grid, double* out) {
+    return interp_common(p, N, pos, grid, out, false);
+}
+
+int esp_interpolate_gradient(esp_plan* p, long N, const double* pos, const double* grid,
+                             double* out) {
+    return interp_common(p, N, pos, grid, out, true);
+}
+
+int esp_last_launch_count(const esp_plan* p) { return p && p->eng ? p->eng->last_launches() : 0; }
+
+}  // extern "C"

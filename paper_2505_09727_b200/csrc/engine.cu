@@ -1,0 +1,1194 @@
+// B200 (sm_100a) kernels and orchestration for the ESP force evaluation.
+//
+// Hot path per evaluation (ewald.hpp:619-649 in the reference):
+//   fold+bin      fold positions into [0,L), pair-cell and spread-bin index,
+//                 per-bin counters (fused neutrality sums)       -> 2 counting sorts
+//   K4 pair sum   real-space PSWF-split sum over the cell list   (ewald.hpp:419-515)
+//   K1 spread     window spreading onto the real grid            (gridder.hpp:215-241)
+//   cuFFT D2Z     forward transform                              (gridder.hpp:85-100)
+//   K2 multiply   p_k and i*xi_d on the half spectrum            (ewald.hpp:545-548, 567-595)
+//   cuFFT Z2D     batched inverse (4 fields for ik, 1 for ad)
+//   K3 interp     4-field interpolation + combine + self + energy (gridder.hpp:244-314,
+//                 ewald.hpp:609-647)
+// K4 runs on the caller's stream while the grid pipeline runs on an auxiliary
+// stream; K3 joins them.  All arithmetic is fp64; no tensor cores (nothing on
+// the path is a dense contraction).
+
+#include "engine.hpp"
+
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+namespace espb {
+
+struct GridArgs {
+    int nf[3];
+    double h[3];
+    double half[3];
+    int nb[3];
+    int S;
+    int W;
+    int P;
+    const double* win;  // 3 x 4P x 13 (phi) then 3 x 4P x 13 (dphi)
+};
+
+namespace {
+
+#define CK(x)                                                                         \
+    do {                                                                              \
+        cudaError_t e_ = (x);                                                         \
+        if (e_ != cudaSuccess)                                                        \
+            throw CudaError(std::string("CUDA error: ") + cudaGetErrorString(e_) +    \
+                            " at " __FILE__ ":" + std::to_string(__LINE__));          \
+    } while (0)
+
+#define CF(x)                                                                         \
+    do {                                                                              \
+        cufftResult r_ = (x);                                                         \
+        if (r_ != CUFFT_SUCCESS)                                                      \
+            throw CudaError("cuFFT error " + std::to_string(static_cast<int>(r_)) +   \
+                            " at " __FILE__ ":" + std::to_string(__LINE__));          \
+    } while (0)
+
+constexpr double kPi = 3.14159265358979323846;
+constexpr int kNc = 13;        // coefficients per window piece (degree 12)
+constexpr int kPairCap = 1024; // candidates staged per pair-kernel chunk
+constexpr int kQcap = 64;      // per-lane pair queue depth (power of two)
+constexpr int kMaxPoly = 40;   // max pair-polynomial coefficients
+
+// ----------------------------------------------------------------------------
+// small device helpers
+// ----------------------------------------------------------------------------
+
+__device__ __forceinline__ double fold1(double x, double L) {
+    // system.hpp:29-36
+    x -= L * floor(x / L);
+    if (x >= L) x = 0.0;
+    return x;
+}
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+__device__ __forceinline__ int wrapi(int l, int n) {
+    int r = l % n;
+    return r < 0 ? r + n : r;
+}
+
+// Per-dimension footprint (gridder.hpp:108-139): first node and the shared
+// window-piece coordinate.  Node j's argument x - h(first+j) lies in window
+// piece 4(P-1-j)+s at the same local coordinate t for every j.
+struct Foot {
+    int first;
+    int s;
+    double t;
+    bool zero_lo;  // node 0 at/after +half (weight forced to 0)
+    bool zero_hi;  // node P-1 at/before -half
+};
+
+__device__ __forceinline__ Foot footprint(int P, double x, double h, double half) {
+    Foot f;
+    double u = (P % 2 == 0) ? x / h : x / h + 0.5;
+    double fl = floor(u);
+    int l0 = static_cast<int>(fl);
+    f.first = (P % 2 == 0) ? l0 - (P / 2 - 1) : l0 - (P - 1) / 2;
+    double g = u - fl;  // in [0,1)
+    double g4 = 4.0 * g;
+    int s = static_cast<int>(g4);
+    s = s > 3 ? 3 : (s < 0 ? 0 : s);
+    f.s = s;
+    f.t = 2.0 * (g4 - s) - 1.0;
+    // the reference returns 0 for |arg| >= half (kernels.hpp:188-195)
+    double a0 = x - h * static_cast<double>(f.first);
+    double a1 = x - h * static_cast<double>(f.first + P - 1);
+    f.zero_lo = fabs(a0) >= half;
+    f.zero_hi = fabs(a1) >= half;
+    return f;
+}
+
+__device__ __forceinline__ double horner13(const double* __restrict__ c, double t) {
+    double r = c[12];
+#pragma unroll
+    for (int k = 11; k >= 0; --k) r = fma(r, t, c[k]);
+    return r;
+}
+
+template <int MP>
+__device__ __forceinline__ void weights(int P, const double* __restrict__ tab, const Foot& f,
+                                        double* w) {
+#pragma unroll
+    for (int j = 0; j < MP; ++j)
+        if (j < P) w[j] = horner13(tab + (4 * (P - 1 - j) + f.s) * kNc, f.t);
+    if (f.zero_lo) w[0] = 0.0;
+    if (f.zero_hi) w[P - 1] = 0.0;
+}
+
+// ----------------------------------------------------------------------------
+// fold + bin + count
+// ----------------------------------------------------------------------------
+
+struct BinArgs {
+    long N;
+    const double* pos;  // N x 3
+    const double* q;
+    double box[3];
+    int nc[3];
+    double cw[3];
+    int nb[3];
+    int S;
+    double h[3];
+    double4* tmp;
+    int* cellA;
+    int* rankA;
+    int* countA;
+    int* cellB;
+    int* rankB;
+    int* countB;
+    double* qsum;  // [2]
+};
+
+__global__ void __launch_bounds__(256) k_fold_bin(BinArgs a) {
+    long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+    double qi = 0.0;
+    if (i < a.N) {
+        double x = fold1(a.pos[3 * i + 0], a.box[0]);
+        double y = fold1(a.pos[3 * i + 1], a.box[1]);
+        double z = fold1(a.pos[3 * i + 2], a.box[2]);
+        qi = a.q[i];
+        a.tmp[i] = make_double4(x, y, z, qi);
+        // pair cell (ewald.hpp:479-482)
+        int cx = clampi(static_cast<int>(x / a.cw[0]), 0, a.nc[0] - 1);
+        int cy = clampi(static_cast<int>(y / a.cw[1]), 0, a.nc[1] - 1);
+        int cz = clampi(static_cast<int>(z / a.cw[2]), 0, a.nc[2] - 1);
+        int c = (cx * a.nc[1] + cy) * a.nc[2] + cz;
+        a.cellA[i] = c;
+        a.rankA[i] = atomicAdd(&a.countA[c], 1);
+        // spread bin: S grid cells per side, by floor(x/h)
+        int bx = clampi(static_cast<int>(floor(x / a.h[0])) / a.S, 0, a.nb[0] - 1);
+        int by = clampi(static_cast<int>(floor(y / a.h[1])) / a.S, 0, a.nb[1] - 1);
+        int bz = clampi(static_cast<int>(floor(z / a.h[2])) / a.S, 0, a.nb[2] - 1);
+        int b = (bx * a.nb[1] + by) * a.nb[2] + bz;
+        a.cellB[i] = b;
+        a.rankB[i] = atomicAdd(&a.countB[b], 1);
+    }
+    // neutrality sums (system.hpp:39-47), one pair of atomics per warp
+    double s1 = qi, s2 = fabs(qi);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if ((threadIdx.x & 31) == 0 && a.qsum) {
+        atomicAdd(&a.qsum[0], s1);
+        atomicAdd(&a.qsum[1], s2);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_scatter(long N, const double4* __restrict__ tmp,
+                                                 const int* __restrict__ cellA,
+                                                 const int* __restrict__ rankA,
+                                                 const int* __restrict__ startA,
+                                                 double4* __restrict__ xyzqA, int* __restrict__ origA,
+                                                 const int* __restrict__ cellB,
+                                                 const int* __restrict__ rankB,
+                                                 const int* __restrict__ startB,
+                                                 double4* __restrict__ xyzqB, int* __restrict__ origB) {
+    long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+    if (i >= N) return;
+    double4 v = tmp[i];
+    int da = startA[cellA[i]] + rankA[i];
+    xyzqA[da] = v;
+    origA[da] = static_cast<int>(i);
+    int db = startB[cellB[i]] + rankB[i];
+    xyzqB[db] = v;
+    origB[db] = static_cast<int>(i);
+}
+
+// ----------------------------------------------------------------------------
+// K4: real-space pair sum (ewald.hpp:419-515, kernels.hpp:143-163)
+// ----------------------------------------------------------------------------
+
+struct PairConsts {
+    double rc2;        // r_c^2
+    double two_irc2;   // 2 / r_c^2
+    double irc;        // 1 / r_c
+    double inv4pi;
+    float rc2_test;    // fp32 screening radius^2 (superset of the exact test)
+    int pad;
+    double G[kMaxPoly];  // chi(y)   = sum G_k z^k,   z = 2y^2 - 1
+    double H[kMaxPoly];  // Psi(y)/y = sum H_k z^k
+};
+
+struct PairArgs {
+    const double4* xyzq;  // sorted by pair cell
+    const int* orig;
+    const int* start;     // ncell + 1
+    double4* loc;         // original order: (u_l, F_l)
+    int nc[3];
+    double cw[3];
+    double box[3];
+};
+
+template <int ND>
+__device__ __forceinline__ void pair_eval(const PairConsts& k, double4 pj, double xi, double yi,
+                                          double zi, double& u, double& fx, double& fy,
+                                          double& fz) {
+    const double dx = pj.x - xi, dy = pj.y - yi, dz = pj.z - zi;
+    const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+    if (r2 < k.rc2 && r2 > 0.0) {
+        const double rinv = rsqrt(r2);
+        const double z = fma(r2, k.two_irc2, -1.0);
+        double G = k.G[ND - 1], H = k.H[ND - 1];
+#pragma unroll
+        for (int m = ND - 2; m >= 0; --m) {
+            G = fma(G, z, k.G[m]);
+            H = fma(H, z, k.H[m]);
+        }
+        const double y = r2 * rinv * k.irc;        // r / r_c
+        const double w = k.inv4pi * rinv;          // 1 / (4 pi r)
+        const double pot = (1.0 - y * H) * w;      // (1 - Psi(y)) / (4 pi r)
+        const double fr = fma(G * w, k.irc, pot * rinv);  // -dS/dr
+        u = fma(pj.w, pot, u);
+        const double c = pj.w * fr * rinv;
+        fx = fma(c, dx, fx);
+        fy = fma(c, dy, fy);
+        fz = fma(c, dz, fz);
+    }
+}
+
+// One CTA per pair cell; lane = target atom i; the 27 neighbour cells are
+// staged in shared memory (fp64 positions with the periodic image shift
+// applied, plus an fp32 copy for screening).  Each lane screens every staged
+// candidate in fp32 and queues the ones inside r_c; whenever every lane has
+// k queued pairs the warp evaluates k rounds fully converged in fp64.
+template <int ND>
+__global__ void __launch_bounds__(256) k_pair(PairArgs a, const __grid_constant__ PairConsts k) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double4* cd = reinterpret_cast<double4*>(smem);
+    float4* cf = reinterpret_cast<float4*>(cd + kPairCap);
+    unsigned short* qall = reinterpret_cast<unsigned short*>(cf + kPairCap);
+    __shared__ int nstart[27], ncount[27], npre[28];
+    __shared__ double nshift[27][3];
+
+    const int nw = blockDim.x >> 5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned short* qw = qall + warp * kQcap * 32;
+
+    const int cell = blockIdx.x;
+    const int cz = cell % a.nc[2];
+    const int cy = (cell / a.nc[2]) % a.nc[1];
+    const int cx = cell / (a.nc[1] * a.nc[2]);
+    const int ib = a.start[cell], ie = a.start[cell + 1];
+    if (ib == ie) return;
+    const double ox = cx * a.cw[0], oy = cy * a.cw[1], oz = cz * a.cw[2];
+
+    if (threadIdx.x < 27) {
+        int t = threadIdx.x;
+        int dx = t / 9 - 1, dy = (t / 3) % 3 - 1, dz = t % 3 - 1;
+        int nx = cx + dx, ny = cy + dy, nz = cz + dz;
+        double sx = nx < 0 ? -a.box[0] : (nx >= a.nc[0] ? a.box[0] : 0.0);
+        double sy = ny < 0 ? -a.box[1] : (ny >= a.nc[1] ? a.box[1] : 0.0);
+        double sz = nz < 0 ? -a.box[2] : (nz >= a.nc[2] ? a.box[2] : 0.0);
+        nx = (nx + a.nc[0]) % a.nc[0];
+        ny = (ny + a.nc[1]) % a.nc[1];
+        nz = (nz + a.nc[2]) % a.nc[2];
+        int c = (nx * a.nc[1] + ny) * a.nc[2] + nz;
+        nstart[t] = a.start[c];
+        ncount[t] = a.start[c + 1] - a.start[c];
+        nshift[t][0] = sx;
+        nshift[t][1] = sy;
+        nshift[t][2] = sz;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int s = 0;
+        for (int t = 0; t < 27; ++t) {
+            npre[t] = s;
+            s += ncount[t];
+        }
+        npre[27] = s;
+    }
+    __syncthreads();
+    const int total = npre[27];
+
+    for (int i0 = ib; i0 < ie; i0 += nw * 32) {
+        const int i = i0 + warp * 32 + lane;
+        const bool valid = i < ie;
+        const bool warp_live = __any_sync(0xffffffffu, valid);
+        double4 pi = valid ? a.xyzq[i] : make_double4(0.0, 0.0, 0.0, 0.0);
+        const float xf = static_cast<float>(pi.x - ox);
+        const float yf = static_cast<float>(pi.y - oy);
+        const float zf = static_cast<float>(pi.z - oz);
+        double u = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
+        int head = 0, tail = 0;
+
+        for (int base = 0; base < total; base += kPairCap) {
+            const int nk = min(kPairCap, total - base);
+            __syncthreads();
+            for (int c = threadIdx.x; c < nk; c += blockDim.x) {
+                const int g = base + c;
+                int t = 0;
+                while (npre[t + 1] <= g) ++t;
+                double4 v = a.xyzq[nstart[t] + (g - npre[t])];
+                v.x += nshift[t][0];
+                v.y += nshift[t][1];
+                v.z += nshift[t][2];
+                cd[c] = v;
+                cf[c] = make_float4(static_cast<float>(v.x - ox), static_cast<float>(v.y - oy),
+                                    static_cast<float>(v.z - oz), 0.0f);
+            }
+            __syncthreads();
+            if (!warp_live) continue;
+            for (int c = 0; c < nk; ++c) {
+                const float4 v = cf[c];
+                const float ddx = v.x - xf, ddy = v.y - yf, ddz = v.z - zf;
+                const float r2 = fmaf(ddz, ddz, fmaf(ddy, ddy, ddx * ddx));
+                if (valid && r2 < k.rc2_test) {
+                    qw[(tail & (kQcap - 1)) * 32 + lane] = static_cast<unsigned short>(c);
+                    ++tail;
+                }
+                if ((c & 31) == 31) {
+                    const int backlog = valid ? tail - head : 0x7fffffff;
+                    const int n = __reduce_min_sync(0xffffffffu, backlog);
+                    for (int r = 0; r < n; ++r) {
+                        const int kk = valid ? qw[((head + r) & (kQcap - 1)) * 32 + lane] : 0;
+                        pair_eval<ND>(k, cd[kk], pi.x, pi.y, pi.z, u, fx, fy, fz);
+                    }
+                    head += n;
+                    while (__any_sync(0xffffffffu, valid && tail - head > kQcap - 32)) {
+                        if (valid && tail - head > kQcap - 32) {
+                            const int kk = qw[(head & (kQcap - 1)) * 32 + lane];
+                            pair_eval<ND>(k, cd[kk], pi.x, pi.y, pi.z, u, fx, fy, fz);
+                            ++head;
+                        }
+                    }
+                }
+            }
+            // drain this chunk's queue (divergent tail)
+            while (__any_sync(0xffffffffu, valid && tail > head)) {
+                if (valid && tail > head) {
+                    const int kk = qw[(head & (kQcap - 1)) * 32 + lane];
+                    pair_eval<ND>(k, cd[kk], pi.x, pi.y, pi.z, u, fx, fy, fz);
+                    ++head;
+                }
+            }
+        }
+        if (valid) {
+            const double qi = pi.w;
+            a.loc[a.orig[i]] = make_double4(u, -qi * fx, -qi * fy, -qi * fz);
+        }
+    }
+}
+
+// All-pairs fallback when some nc_d < 3 (ewald.hpp:457-470): min image by
+// rounding, thread per target atom.
+template <int ND>
+__global__ void __launch_bounds__(128) k_pair_allpairs(long N, const double4* __restrict__ xyzq,
+                                                       double4* __restrict__ loc, double bx,
+                                                       double by, double bz,
+                                                       const __grid_constant__ PairConsts k) {
+    long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+    if (i >= N) return;
+    const double4 pi = xyzq[i];
+    double u = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
+    for (long j = 0; j < N; ++j) {
+        if (j == i) continue;
+        double4 pj = xyzq[j];
+        double dx = pj.x - pi.x, dy = pj.y - pi.y, dz = pj.z - pi.z;
+        dx -= bx * round(dx / bx);
+        dy -= by * round(dy / by);
+        dz -= bz * round(dz / bz);
+        pj.x = pi.x + dx;
+        pj.y = pi.y + dy;
+        pj.z = pi.z + dz;
+        pair_eval<ND>(k, pj, pi.x, pi.y, pi.z, u, fx, fy, fz);
+    }
+    loc[i] = make_double4(u, -pi.w * fx, -pi.w * fy, -pi.w * fz);
+}
+
+// ----------------------------------------------------------------------------
+// K1: spread (gridder.hpp:215-241)
+// ----------------------------------------------------------------------------
+
+// One warp per spread bin (S^3 grid cells): the bin's atoms are accumulated
+// into a shared-memory tile of W^3 nodes (W = S + P + 2 covers every
+// footprint), one atom at a time with lanes over the P^3 footprint nodes, so
+// no two lanes ever touch the same node (no shared atomics -- fp64 shared
+// atomics are CAS loops on sm_100a).  The tile is then added to the global
+// grid with REDG.F64 (nonzero nodes only).  PT > 0 fixes P at compile time;
+// PT == 0 reads it from g.P (max 16).
+template <int PT>
+__global__ void __launch_bounds__(32) k_spread(GridArgs g, const double4* __restrict__ xyzq,
+                                               const int* __restrict__ start,
+                                               double* __restrict__ grid) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* tile = reinterpret_cast<double*>(smem);
+    constexpr int MP = PT > 0 ? PT : 16;
+    __shared__ double wb[3 * MP];
+    const int P = PT > 0 ? PT : g.P;
+    const int P2 = P * P, P3 = P2 * P;
+    const int W = g.W;
+    const int lane = threadIdx.x;
+    const int bin = blockIdx.x;
+    const int bz = bin % g.nb[2], by = (bin / g.nb[2]) % g.nb[1], bx = bin / (g.nb[1] * g.nb[2]);
+    const int ib = start[bin], ie = start[bin + 1];
+    if (ib == ie) return;
+    const int lox = bx * g.S - P / 2, loy = by * g.S - P / 2, loz = bz * g.S - P / 2;
+    const int W3 = W * W * W;
+    for (int t = lane; t < W3; t += 32) tile[t] = 0.0;
+    __syncwarp();
+    for (int i = ib; i < ie; ++i) {
+        const double4 v = xyzq[i];
+        const Foot fx = footprint(P, v.x, g.h[0], g.half[0]);
+        const Foot fy = footprint(P, v.y, g.h[1], g.half[1]);
+        const Foot fz = footprint(P, v.z, g.h[2], g.half[2]);
+        if (lane < 3 * P) {
+            const int d = lane / P, j = lane - d * P;
+            const Foot& f = d == 0 ? fx : (d == 1 ? fy : fz);
+            const double* tab = g.win + static_cast<long>(d) * 4 * P * kNc;
+            double w = horner13(tab + (4 * (P - 1 - j) + f.s) * kNc, f.t);
+            if ((j == 0 && f.zero_lo) || (j == P - 1 && f.zero_hi)) w = 0.0;
+            if (d == 0) w *= v.w;
+            wb[d * MP + j] = w;
+        }
+        __syncwarp();
+        // offsets are in [0, W-P] by construction; clamp for non-finite input
+        const int ox = clampi(fx.first - lox, 0, W - P);
+        const int oy = clampi(fy.first - loy, 0, W - P);
+        const int oz = clampi(fz.first - loz, 0, W - P);
+        for (int p = lane; p < P3; p += 32) {
+            const int jx = p / P2, r = p - jx * P2;
+            const int jy = r / P, jz = r - jy * P;
+            const int off = ((ox + jx) * W + (oy + jy)) * W + (oz + jz);
+            tile[off] += wb[jx] * wb[MP + jy] * wb[2 * MP + jz];
+        }
+        __syncwarp();
+    }
+    for (int t = lane; t < W3; t += 32) {
+        const double val = tile[t];
+        if (val != 0.0) {
+            const int ix = t / (W * W), iy = (t / W) % W, iz = t % W;
+            const int gx = wrapi(lox + ix, g.nf[0]);
+            const int gy = wrapi(loy + iy, g.nf[1]);
+            const int gz = wrapi(loz + iz, g.nf[2]);
+            atomicAdd(&grid[(static_cast<long>(gx) * g.nf[1] + gy) * g.nf[2] + gz], val);
+        }
+    }
+}
+
+// ----------------------------------------------------------------------------
+// K2: influence multiply and ik derivative spectra (ewald.hpp:545-548, 567-595)
+// ----------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(256) k_scale(long Mh, int ny, int nzh, const double* __restrict__ p,
+                                               const double* __restrict__ xi,  // nx+ny+nz
+                                               int nx, int nz,
+                                               const cufftDoubleComplex* __restrict__ in,
+                                               cufftDoubleComplex* __restrict__ out, int nfields) {
+    long m = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+    if (m >= Mh) return;
+    const double pk = p[m];
+    const cufftDoubleComplex b = in[m];
+    const double cr = b.x * pk, ci = b.y * pk;
+    out[m] = make_cuDoubleComplex(cr, ci);
+    if (nfields == 4) {
+        const int iz = static_cast<int>(m % nzh);
+        const long r = m / nzh;
+        const int iy = static_cast<int>(r % ny);
+        const int ix = static_cast<int>(r / ny);
+        const double fx = xi[ix], fy = xi[nx + iy], fz = xi[nx + ny + iz];
+        // (a + ib) * i xi = (-b xi, a xi)
+        out[Mh + m] = make_cuDoubleComplex(-ci * fx, cr * fx);
+        out[2 * Mh + m] = make_cuDoubleComplex(-ci * fy, cr * fy);
+        out[3 * Mh + m] = make_cuDoubleComplex(-ci * fz, cr * fz);
+    }
+}
+
+// ----------------------------------------------------------------------------
+// K3: interpolation + combine (gridder.hpp:244-314, ewald.hpp:571-647)
+// ----------------------------------------------------------------------------
+
+enum InterpMode : int {
+    kCombine = 0,     // u = u_l + u_s - self, F = F_l + F_s, energy partials
+    kSpectral = 1,    // u = u_s, F = F_s
+    kValue = 2,       // out = interpolate(grid) (plain adjoint)
+    kGradient = 3,    // out = interpolate_gradient(grid)
+};
+
+struct InterpArgs {
+    long N;
+    const double4* xyzq;  // sorted by spread bin
+    const int* orig;
+    const double* fields;  // nfields x M
+    long M;
+    const double4* loc;    // original order (combine mode)
+    double self_coef;
+    double* u;             // original order
+    double* F;             // original order, N x 3
+    double* epart;         // per-block energy partial sums
+};
+
+// Thread per atom (spread-bin order, so neighbouring threads share grid
+// lines in L1).  Weights are computed once per atom and dimension and reused
+// for all fields (the reference recomputes the footprint per field,
+// ewald.hpp:571,599).
+template <int PT, int MODE, bool IK>
+__global__ void __launch_bounds__(128) k_interp(GridArgs g, InterpArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* tab = reinterpret_cast<double*>(smem);  // phi (3 x 4P x 13) [+ dphi]
+    constexpr int MP = PT > 0 ? PT : 16;
+    const int P = PT > 0 ? PT : g.P;
+    constexpr bool need_d = (MODE == kGradient) || (!IK && (MODE == kCombine || MODE == kSpectral));
+    const int ntab = (need_d ? 6 : 3) * 4 * P * kNc;
+    for (int t = threadIdx.x; t < ntab; t += blockDim.x) tab[t] = g.win[t];
+    __syncthreads();
+
+    const long k = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+    double e = 0.0;
+    if (k < a.N) {
+        const double4 v = a.xyzq[k];
+        const int o = a.orig[k];
+        const Foot f[3] = {footprint(P, v.x, g.h[0], g.half[0]),
+                           footprint(P, v.y, g.h[1], g.half[1]),
+                           footprint(P, v.z, g.h[2], g.half[2])};
+        double w[3][MP];
+        int idx[3][MP];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            weights<MP>(P, tab + d * 4 * P * kNc, f[d], w[d]);
+#pragma unroll
+            for (int j = 0; j < MP; ++j)
+                if (j < P) idx[d][j] = wrapi(f[d].first + j, g.nf[d]);
+        }
+        const long ny = g.nf[1], nz = g.nf[2];
+        double qi = v.w;
+        double us = 0.0, Fx = 0.0, Fy = 0.0, Fz = 0.0;
+        if (MODE == kValue || (IK && MODE != kGradient)) {
+            constexpr int NFLD = (MODE == kValue) ? 1 : 4;
+            double acc[NFLD];
+#pragma unroll
+            for (int c = 0; c < NFLD; ++c) acc[c] = 0.0;
+#pragma unroll 1
+            for (int jx = 0; jx < P; ++jx) {
+#pragma unroll
+                for (int jy = 0; jy < MP; ++jy) {
+                    if (jy < P) {
+                        const long row = (idx[0][jx] * ny + idx[1][jy]) * nz;
+                        const double wxy = w[0][jx] * w[1][jy];
+#pragma unroll
+                        for (int c = 0; c < NFLD; ++c) {
+                            const double* fld = a.fields + c * a.M + row;
+                            double sz = 0.0;
+#pragma unroll
+                            for (int jz = 0; jz < MP; ++jz)
+                                if (jz < P) sz = fma(w[2][jz], __ldg(fld + idx[2][jz]), sz);
+                            acc[c] = fma(wxy, sz, acc[c]);
+                        }
+                    }
+                }
+            }
+            if (MODE == kValue) {
+                a.u[o] = acc[0];
+            } else {
+                us = acc[0];
+                Fx = -qi * acc[NFLD > 1 ? 1 : 0];
+                Fy = -qi * acc[NFLD > 2 ? 2 : 0];
+                Fz = -qi * acc[NFLD > 3 ? 3 : 0];
+            }
+        } else {
+            // value + gradient from one field with derivative weights
+            double dw[3][MP];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) weights<MP>(P, tab + (3 + d) * 4 * P * kNc, f[d], dw[d]);
+            double val = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
+#pragma unroll 1
+            for (int jx = 0; jx < P; ++jx) {
+#pragma unroll
+                for (int jy = 0; jy < MP; ++jy) {
+                    if (jy < P) {
+                        const long row = (idx[0][jx] * ny + idx[1][jy]) * nz;
+                        double sz = 0.0, sd = 0.0;
+#pragma unroll
+                        for (int jz = 0; jz < MP; ++jz) {
+                            if (jz < P) {
+                                const double gv = __ldg(a.fields + row + idx[2][jz]);
+                                sz = fma(w[2][jz], gv, sz);
+                                sd = fma(dw[2][jz], gv, sd);
+                            }
+                        }
+                        val = fma(w[0][jx] * w[1][jy], sz, val);
+                        gx = fma(dw[0][jx] * w[1][jy], sz, gx);
+                        gy = fma(w[0][jx] * dw[1][jy], sz, gy);
+                        gz = fma(w[0][jx] * w[1][jy], sd, gz);
+                    }
+                }
+            }
+            if (MODE == kGradient) {
+                a.u[3 * o + 0] = gx;
+                a.u[3 * o + 1] = gy;
+                a.u[3 * o + 2] = gz;
+            } else {
+                us = val;
+                Fx = -qi * gx;
+                Fy = -qi * gy;
+                Fz = -qi * gz;
+            }
+        }
+        if (MODE == kCombine || MODE == kSpectral) {
+            if (MODE == kCombine) {
+                const double4 l = a.loc[o];
+                us = (l.x + us) - qi * a.self_coef;
+                Fx += l.y;
+                Fy += l.z;
+                Fz += l.w;
+                e = qi * us;
+            }
+            a.u[o] = us;
+            a.F[3 * o + 0] = Fx;
+            a.F[3 * o + 1] = Fy;
+            a.F[3 * o + 2] = Fz;
+        }
+    }
+    if (MODE == kCombine) {
+        __shared__ double red[4];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = e;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double s = 0.0;
+            for (int w = 0; w < (blockDim.x >> 5); ++w) s += red[w];
+            a.epart[blockIdx.x] = s;
+        }
+    }
+}
+
+// Final energy: E = 1/2 sum of block partials, compensated (ewald.hpp:641-647).
+__global__ void k_energy(const double* __restrict__ part, int n, double* out) {
+    __shared__ double ss[256], cc[256];
+    double s = 0.0, c = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double y = part[i] - c;
+        double t = s + y;
+        c = (t - s) - y;
+        s = t;
+    }
+    ss[threadIdx.x] = s;
+    cc[threadIdx.x] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double S = 0.0, C = 0.0;
+        for (int i = 0; i < blockDim.x; ++i) {
+            double y = (ss[i] - cc[i]) - C;
+            double t = S + y;
+            C = (t - S) - y;
+            S = t;
+        }
+        *out = 0.5 * S;
+    }
+}
+
+// Unpack (u_l, F_l) to the caller's layout (local_sum only).
+__global__ void k_unpack(long N, const double4* __restrict__ loc, double* u, double* F) {
+    long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+    if (i >= N) return;
+    double4 l = loc[i];
+    u[i] = l.x;
+    F[3 * i] = l.y;
+    F[3 * i + 1] = l.z;
+    F[3 * i + 2] = l.w;
+}
+
+template <class T>
+void dfree(T*& p) {
+    if (p) cudaFree(p);
+    p = nullptr;
+}
+
+template <class T>
+void dalloc(T*& p, size_t count) {
+    dfree(p);
+    CK(cudaMalloc(reinterpret_cast<void**>(&p), sizeof(T) * std::max<size_t>(count, 1)));
+}
+
+unsigned grid1(long n, int b) { return static_cast<unsigned>((n + b - 1) / b); }
+
+// ----------------------------------------------------------------------------
+// kernel dispatch on compile-time P / polynomial size
+// ----------------------------------------------------------------------------
+
+template <template <int> class F, class... A>
+void dispatch_P(int P, A&&... args) {
+    if (P < 3 || P > 16) throw InvalidArgument("window order P out of range [3,16]");
+    switch (P) {
+        case 5: F<5>::run(args...); break;
+        case 6: F<6>::run(args...); break;
+        case 7: F<7>::run(args...); break;
+        case 8: F<8>::run(args...); break;
+        default: F<0>::run(args...); break;
+    }
+}
+
+template <int P>
+struct SpreadLaunch {
+    static void run(const GridArgs& g, int nbin, const double4* xyzq, const int* start,
+                    double* grid, cudaStream_t s) {
+        size_t sm = sizeof(double) * g.W * g.W * g.W;
+        if (sm > 48 * 1024)
+            CK(cudaFuncSetAttribute(k_spread<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(sm)));
+        k_spread<P><<<nbin, 32, sm, s>>>(g, xyzq, start, grid);
+        CK(cudaGetLastError());
+    }
+};
+
+template <int P>
+struct InterpLaunch {
+    static void run(int mode, bool ik, const GridArgs& g, const InterpArgs& a, cudaStream_t s) {
+        const int B = 128;
+        const unsigned nblk = grid1(std::max<long>(a.N, 1), B);
+        const int Pr = P > 0 ? P : g.P;
+        size_t sm = sizeof(double) * 6 * 4 * Pr * kNc;
+        auto go = [&](auto kern) {
+            if (sm > 48 * 1024)
+                CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(sm)));
+            kern<<<nblk, B, sm, s>>>(g, a);
+            CK(cudaGetLastError());
+        };
+        switch (mode) {
+            case kCombine: ik ? go(k_interp<P, kCombine, true>) : go(k_interp<P, kCombine, false>); break;
+            case kSpectral: ik ? go(k_interp<P, kSpectral, true>) : go(k_interp<P, kSpectral, false>); break;
+            case kValue: go(k_interp<P, kValue, true>); break;
+            default: go(k_interp<P, kGradient, false>); break;
+        }
+    }
+};
+
+PairConsts make_pair_consts(const Plan& p, int& nd) {
+    PairConsts k{};
+    k.rc2 = p.r_c * p.r_c;
+    k.two_irc2 = 2.0 / k.rc2;
+    k.irc = 1.0 / p.r_c;
+    k.inv4pi = 1.0 / (4.0 * kPi);
+    k.rc2_test = static_cast<float>(k.rc2 * (1.0 + 2e-4));
+    const int n = static_cast<int>(std::max(p.pair_G.size(), p.pair_H.size()));
+    if (n > kMaxPoly) throw NumericalError("pair kernel polynomial too long");
+    nd = n <= 20 ? 20 : (n <= 28 ? 28 : kMaxPoly);
+    for (int i = 0; i < kMaxPoly; ++i) {
+        k.G[i] = i < static_cast<int>(p.pair_G.size()) ? p.pair_G[i] : 0.0;
+        k.H[i] = i < static_cast<int>(p.pair_H.size()) ? p.pair_H[i] : 0.0;
+    }
+    return k;
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------------------
+// Engine
+// ----------------------------------------------------------------------------
+
+Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
+    CK(cudaSetDevice(device_));
+    const Plan& p = plan_;
+    for (int d = 0; d < 3; ++d) nc_[d] = std::max(1, static_cast<int>(std::floor(p.box[d] / p.r_c)));
+    cells_ok_ = nc_[0] >= 3 && nc_[1] >= 3 && nc_[2] >= 3;
+    ncell_ = nc_[0] * nc_[1] * nc_[2];
+    S_ = 8;
+    for (int d = 0; d < 3; ++d) nb_[d] = (p.nf[d] + S_ - 1) / S_;
+    nbin_ = nb_[0] * nb_[1] * nb_[2];
+    W_ = S_ + p.P + 2;
+    M_ = static_cast<long>(p.nf[0]) * p.nf[1] * p.nf[2];
+    Mh_ = static_cast<long>(p.nf[0]) * p.nf[1] * (p.nf[2] / 2 + 1);
+    nfields_ = p.force_method == ForceMethod::ik ? 4 : 1;
+
+    // window tables: phi x3 then dphi x3, each 4P x 13 monomial coefficients
+    std::vector<double> win;
+    for (int d = 0; d < 3; ++d) win.insert(win.end(), p.phi[d].mono.begin(), p.phi[d].mono.end());
+    for (int d = 0; d < 3; ++d) win.insert(win.end(), p.dphi[d].mono.begin(), p.dphi[d].mono.end());
+    dalloc(d_win_, win.size());
+    CK(cudaMemcpy(d_win_, win.data(), sizeof(double) * win.size(), cudaMemcpyHostToDevice));
+    dalloc(d_influence_, Mh_);
+    CK(cudaMemcpy(d_influence_, p.influence_half.data(), sizeof(double) * Mh_,
+                  cudaMemcpyHostToDevice));
+    std::vector<double> xi;
+    for (int d = 0; d < 3; ++d)
+        for (int i = 0; i < p.nf[d]; ++i)
+            xi.push_back(2 * i == p.nf[d] ? 0.0 : 2.0 * kPi * signed_mode(i, p.nf[d]) / p.box[d]);
+    dalloc(d_xi_, xi.size());
+    CK(cudaMemcpy(d_xi_, xi.data(), sizeof(double) * xi.size(), cudaMemcpyHostToDevice));
+
+    dalloc(d_countA_, ncell_ + 1);
+    dalloc(d_startA_, ncell_ + 1);
+    dalloc(d_countB_, nbin_ + 1);
+    dalloc(d_startB_, nbin_ + 1);
+    size_t t1 = 0, t2 = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, t1, d_countA_, d_startA_, ncell_ + 1));
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, t2, d_countB_, d_startB_, nbin_ + 1));
+    scan_tmp_bytes_ = std::max(t1, t2);
+    CK(cudaMalloc(&d_scan_tmp_, std::max<size_t>(scan_tmp_bytes_, 16)));
+    dalloc(d_grid_, M_);
+    dalloc(d_spec_, Mh_);
+    dalloc(d_spec4_, nfields_ * Mh_);
+    dalloc(d_fields_, nfields_ * M_);
+    dalloc(d_qsum_, 2);
+
+    // cuFFT: forward D2Z, batched inverse Z2D
+    CF(cufftCreate(&fwd_));
+    CF(cufftCreate(&inv_));
+    CF(cufftSetAutoAllocation(fwd_, 0));
+    CF(cufftSetAutoAllocation(inv_, 0));
+    size_t w1 = 0, w2 = 0;
+    CF(cufftMakePlan3d(fwd_, p.nf[0], p.nf[1], p.nf[2], CUFFT_D2Z, &w1));
+    int n3[3] = {p.nf[0], p.nf[1], p.nf[2]};
+    int inembed[3] = {p.nf[0], p.nf[1], p.nf[2] / 2 + 1};
+    int onembed[3] = {p.nf[0], p.nf[1], p.nf[2]};
+    CF(cufftMakePlanMany(inv_, 3, n3, inembed, 1, static_cast<int>(Mh_), onembed, 1,
+                         static_cast<int>(M_), CUFFT_Z2D, nfields_, &w2));
+    CK(cudaMalloc(&d_cufft_work_, std::max<size_t>(std::max(w1, w2), 16)));
+    CF(cufftSetWorkArea(fwd_, d_cufft_work_));
+    CF(cufftSetWorkArea(inv_, d_cufft_work_));
+
+    CK(cudaStreamCreateWithFlags(&aux_, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+    for (auto& e : ev_t_) CK(cudaEventCreate(&e));
+    CF(cufftSetStream(fwd_, aux_));
+    CF(cufftSetStream(inv_, aux_));
+
+    // pair kernel occupancy: warps per CTA from the mean cell population
+    pair_warps_ = 4;
+}
+
+Engine::~Engine() {
+    cudaSetDevice(device_);
+    if (fwd_) cufftDestroy(fwd_);
+    if (inv_) cufftDestroy(inv_);
+    if (d_cufft_work_) cudaFree(d_cufft_work_);
+    if (d_scan_tmp_) cudaFree(d_scan_tmp_);
+    dfree(d_win_);
+    dfree(d_influence_);
+    dfree(d_xi_);
+    dfree(d_tmp_);
+    dfree(d_cellA_);
+    dfree(d_rankA_);
+    dfree(d_cellB_);
+    dfree(d_rankB_);
+    dfree(d_xyzqA_);
+    dfree(d_origA_);
+    dfree(d_xyzqB_);
+    dfree(d_origB_);
+    dfree(d_loc_);
+    dfree(d_epart_);
+    dfree(d_countA_);
+    dfree(d_startA_);
+    dfree(d_countB_);
+    dfree(d_startB_);
+    dfree(d_grid_);
+    dfree(d_spec_);
+    dfree(d_spec4_);
+    dfree(d_fields_);
+    dfree(d_qsum_);
+    if (aux_) cudaStreamDestroy(aux_);
+    if (ev_fork_) cudaEventDestroy(ev_fork_);
+    if (ev_join_) cudaEventDestroy(ev_join_);
+    for (auto& e : ev_t_)
+        if (e) cudaEventDestroy(e);
+}
+
+void Engine::ensure_capacity(long N) {
+    if (N <= cap_) return;
+    long c = std::max<long>(N, 1);
+    dalloc(d_tmp_, c);
+    dalloc(d_cellA_, c);
+    dalloc(d_rankA_, c);
+    dalloc(d_cellB_, c);
+    dalloc(d_rankB_, c);
+    dalloc(d_xyzqA_, c);
+    dalloc(d_origA_, c);
+    dalloc(d_xyzqB_, c);
+    dalloc(d_origB_, c);
+    dalloc(d_loc_, c);
+    dalloc(d_epart_, grid1(c, 128) + 1);
+    cap_ = c;
+}
+
+void Engine::prepare(long N, const double* pos, const double* q, double* qsum_dev,
+                     cudaStream_t s) {
+    const Plan& p = plan_;
+    CK(cudaMemsetAsync(d_countA_, 0, sizeof(int) * (ncell_ + 1), s));
+    CK(cudaMemsetAsync(d_countB_, 0, sizeof(int) * (nbin_ + 1), s));
+    if (qsum_dev) CK(cudaMemsetAsync(qsum_dev, 0, sizeof(double) * 2, s));
+    BinArgs a{};
+    a.N = N;
+    a.pos = pos;
+    a.q = q;
+    for (int d = 0; d < 3; ++d) {
+        a.box[d] = p.box[d];
+        a.nc[d] = nc_[d];
+        a.cw[d] = p.box[d] / nc_[d];
+        a.nb[d] = nb_[d];
+        a.h[d] = p.h[d];
+    }
+    a.S = S_;
+    a.tmp = d_tmp_;
+    a.cellA = d_cellA_;
+    a.rankA = d_rankA_;
+    a.countA = d_countA_;
+    a.cellB = d_cellB_;
+    a.rankB = d_rankB_;
+    a.countB = d_countB_;
+    a.qsum = qsum_dev;
+    if (N > 0) {
+        k_fold_bin<<<grid1(N, 256), 256, 0, s>>>(a);
+        CK(cudaGetLastError());
+        ++launches_;
+    }
+    size_t tb = scan_tmp_bytes_;
+    CK(cub::DeviceScan::ExclusiveSum(d_scan_tmp_, tb, d_countA_, d_startA_, ncell_ + 1, s));
+    tb = scan_tmp_bytes_;
+    CK(cub::DeviceScan::ExclusiveSum(d_scan_tmp_, tb, d_countB_, d_startB_, nbin_ + 1, s));
+    launches_ += 2;
+    if (N > 0) {
+        k_scatter<<<grid1(N, 256), 256, 0, s>>>(N, d_tmp_, d_cellA_, d_rankA_, d_startA_, d_xyzqA_,
+                                                 d_origA_, d_cellB_, d_rankB_, d_startB_, d_xyzqB_,
+                                                 d_origB_);
+        CK(cudaGetLastError());
+        ++launches_;
+    }
+}
+
+void Engine::run_pair(long N, cudaStream_t s) {
+    if (N == 0) return;
+    const Plan& p = plan_;
+    int nd = 20;
+    PairConsts k = make_pair_consts(p, nd);
+    if (!cells_ok_) {
+        // all-pairs path works on the folded, original-order copy
+        auto go = [&](auto kern) {
+            kern<<<grid1(N, 128), 128, 0, s>>>(N, d_tmp_, d_loc_, p.box[0], p.box[1], p.box[2], k);
+        };
+        if (nd == 20) go(k_pair_allpairs<20>);
+        else if (nd == 28) go(k_pair_allpairs<28>);
+        else go(k_pair_allpairs<kMaxPoly>);
+        CK(cudaGetLastError());
+        ++launches_;
+        return;
+    }
+    PairArgs a{};
+    a.xyzq = d_xyzqA_;
+    a.orig = d_origA_;
+    a.start = d_startA_;
+    a.loc = d_loc_;
+    for (int d = 0; d < 3; ++d) {
+        a.nc[d] = nc_[d];
+        a.cw[d] = p.box[d] / nc_[d];
+        a.box[d] = p.box[d];
+    }
+    const double mean = static_cast<double>(N) / ncell_;
+    int nw = static_cast<int>(std::ceil(1.15 * mean / 32.0));
+    nw = std::max(1, std::min(8, nw));
+    pair_warps_ = nw;
+    size_t sm = kPairCap * (sizeof(double4) + sizeof(float4)) + nw * kQcap * 32 * sizeof(unsigned short);
+    auto go = [&](auto kern) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(sm)));
+        kern<<<ncell_, nw * 32, sm, s>>>(a, k);
+    };
+    if (nd == 20) go(k_pair<20>);
+    else if (nd == 28) go(k_pair<28>);
+    else go(k_pair<kMaxPoly>);
+    CK(cudaGetLastError());
+    ++launches_;
+}
+
+void Engine::run_spread(long N, cudaStream_t s) {
+    const Plan& p = plan_;
+    CK(cudaMemsetAsync(d_grid_, 0, sizeof(double) * M_, s));
+    if (N == 0) return;
+    const GridArgs g = grid_args();
+    dispatch_P<SpreadLaunch>(p.P, g, nbin_, d_xyzqB_, d_startB_, d_grid_, s);
+    ++launches_;
+}
+
+void Engine::run_grid(long N, cudaStream_t s, StageTimes* t) {
+    run_spread(N, s);
+    if (t) CK(cudaEventRecord(ev_t_[3], s));
+    CF(cufftSetStream(fwd_, s));
+    CF(cufftExecD2Z(fwd_, d_grid_, d_spec_));
+    if (t) CK(cudaEventRecord(ev_t_[4], s));
+    k_scale<<<grid1(Mh_, 256), 256, 0, s>>>(Mh_, plan_.nf[1], plan_.nf[2] / 2 + 1, d_influence_,
+                                            d_xi_, plan_.nf[0], plan_.nf[2], d_spec_, d_spec4_,
+                                            nfields_);
+    CK(cudaGetLastError());
+    ++launches_;
+    if (t) CK(cudaEventRecord(ev_t_[5], s));
+    CF(cufftSetStream(inv_, s));
+    CF(cufftExecZ2D(inv_, d_spec4_, d_fields_));
+    if (t) CK(cudaEventRecord(ev_t_[6], s));
+}
+
+GridArgs Engine::grid_args() const {
+    GridArgs g{};
+    for (int d = 0; d < 3; ++d) {
+        g.nf[d] = plan_.nf[d];
+        g.h[d] = plan_.h[d];
+        g.half[d] = plan_.half[d];
+        g.nb[d] = nb_[d];
+    }
+    g.S = S_;
+    g.W = W_;
+    g.P = plan_.P;
+    g.win = d_win_;
+    return g;
+}
+
+void Engine::evaluate(long N, const double* pos, const double* q, double* u, double* F,
+                      double* energy_dev, double* qsum_dev, cudaStream_t s, StageTimes* t) {
+    CK(cudaSetDevice(device_));
+    launches_ = 0;
+    ensure_capacity(N);
+    if (t) {
+        // serialised on the caller's stream so that each stage is timed alone
+        CK(cudaEventRecord(ev_t_[0], s));
+        prepare(N, pos, q, qsum_dev, s);
+        CK(cudaEventRecord(ev_t_[1], s));
+        run_pair(N, s);
+        CK(cudaEventRecord(ev_t_[2], s));
+        run_grid(N, s, t);
+    } else {
+        // K4 on the caller's stream overlaps the grid pipeline on aux_
+        prepare(N, pos, q, qsum_dev, s);
+        CK(cudaEventRecord(ev_fork_, s));
+        CK(cudaStreamWaitEvent(aux_, ev_fork_, 0));
+        run_grid(N, aux_, nullptr);
+        CK(cudaEventRecord(ev_join_, aux_));
+        run_pair(N, s);
+        CK(cudaStreamWaitEvent(s, ev_join_, 0));
+    }
+    InterpArgs a{};
+    a.N = N;
+    a.xyzq = d_xyzqB_;
+    a.orig = d_origB_;
+    a.fields = d_fields_;
+    a.M = M_;
+    a.loc = d_loc_;
+    a.self_coef = plan_.self_coef;
+    a.u = u;
+    a.F = F;
+    a.epart = d_epart_;
+    const GridArgs g = grid_args();
+    const int nblk = static_cast<int>(grid1(std::max<long>(N, 1), 128));
+    if (N > 0) {
+        dispatch_P<InterpLaunch>(plan_.P, static_cast<int>(kCombine), nfields_ == 4, g, a, s);
+        ++launches_;
+        k_energy<<<1, 256, 0, s>>>(d_epart_, nblk, energy_dev);
+        CK(cudaGetLastError());
+        ++launches_;
+    } else {
+        CK(cudaMemsetAsync(energy_dev, 0, sizeof(double), s));
+    }
+    if (t) {
+        CK(cudaEventRecord(ev_t_[7], s));
+        CK(cudaEventSynchronize(ev_t_[7]));
+        auto el = [&](int a0, int a1) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, ev_t_[a0], ev_t_[a1]));
+            return ms * 1e-3;
+        };
+        t->bin = el(0, 1);
+        t->local = el(1, 2);
+        t->spread = el(2, 3);
+        t->fft = el(3, 4);
+        t->scale = el(4, 5);
+        t->ifft = el(5, 6);
+        t->interpolate = el(6, 7);
+    }
+}
+
+void Engine::local_sum(long N, const double* pos, const double* q, double* u, double* F,
+                       cudaStream_t s) {
+    CK(cudaSetDevice(device_));
+    ensure_capacity(N);
+    prepare(N, pos, q, nullptr, s);
+    run_pair(N, s);
+    if (N > 0) {
+        k_unpack<<<grid1(N, 256), 256, 0, s>>>(N, d_loc_, u, F);
+        CK(cudaGetLastError());
+    }
+}
+
+void Engine::spectral_sum(long N, const double* pos, const double* q, double* u, double* F,
+                          cudaStream_t s) {
+    CK(cudaSetDevice(device_));
+    ensure_capacity(N);
+    prepare(N, pos, q, nullptr, s);
+    CK(cudaEventRecord(ev_fork_, s));
+    CK(cudaStreamWaitEvent(aux_, ev_fork_, 0));
+    run_grid(N, aux_, nullptr);
+    CK(cudaEventRecord(ev_join_, aux_));
+    CK(cudaStreamWaitEvent(s, ev_join_, 0));
+    if (N == 0) return;
+    InterpArgs a{};
+    a.N = N;
+    a.xyzq = d_xyzqB_;
+    a.orig = d_origB_;
+    a.fields = d_fields_;
+    a.M = M_;
+    a.u = u;
+    a.F = F;
+    const GridArgs g = grid_args();
+    dispatch_P<InterpLaunch>(plan_.P, static_cast<int>(kSpectral), nfields_ == 4, g, a, s);
+}
+
+void Engine::spread(long N, const double* pos, const double* q, double* grid, cudaStream_t s) {
+    CK(cudaSetDevice(device_));
+    ensure_capacity(N);
+    prepare(N, pos, q, nullptr, s);
+    run_spread(N, s);
+    CK(cudaMemcpyAsync(grid, d_grid_, sizeof(double) * M_, cudaMemcpyDeviceToDevice, s));
+}
+
+void Engine::interpolate(long N, const double* pos, const double* grid, double* out,
+                         cudaStream_t s) {
+    CK(cudaSetDevice(device_));
+    ensure_capacity(N);
+    // charges are irrelevant; reuse pos as a dummy q source is unsafe, so bin
+    // with a zero charge array carved from the loc buffer
+    CK(cudaMemsetAsync(d_loc_, 0, sizeof(double) * std::max<long>(N, 1), s));
+    prepare(N, pos, reinterpret_cast<const double*>(d_loc_), nullptr, s);
+    if (N == 0) return;
+    InterpArgs a{};
+    a.N = N;
+    a.xyzq = d_xyzqB_;
+    a.orig = d_origB_;
+    a.fields = grid;
+    a.M = M_;
+    a.u = out;
+    const GridArgs g = grid_args();
+    dispatch_P<InterpLaunch>(plan_.P, static_cast<int>(kValue), true, g, a, s);
+}
+
+void Engine::interpolate_gradient(long N, const double* pos, const double* grid, double* out,
+                                  cudaStream_t s) {
+    CK(cudaSetDevice(device_));
+    ensure_capacity(N);
+    CK(cudaMemsetAsync(d_loc_, 0, sizeof(double) * std::max<long>(N, 1), s));
+    prepare(N, pos, reinterpret_cast<const double*>(d_loc_), nullptr, s);
+    if (N == 0) return;
+    InterpArgs a{};
+    a.N = N;
+    a.xyzq = d_xyzqB_;
+    a.orig = d_origB_;
+    a.fields = grid;
+    a.M = M_;
+    a.u = out;
+    const GridArgs g = grid_args();
+    dispatch_P<InterpLaunch>(plan_.P, static_cast<int>(kGradient), false, g, a, s);
+}
+
+}  // namespace espb

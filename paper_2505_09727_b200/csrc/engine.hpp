@@ -1,0 +1,126 @@
+// Device engine for one ESP plan on one B200 (sm_100a).
+//
+// Owns the device copies of the plan tables, the cuFFT plans, the scratch
+// buffers sized for the largest N seen, and two streams' worth of events.
+// Every public method is asynchronous on the caller's stream unless noted;
+// pointers are device pointers.  See DESIGN.md for the data layout and the
+// kernel list (K1 spread, K2 influence/derivative multiply, K3 interpolation
+// + combine, K4 real-space pair sum, plus the two counting sorts).
+#pragma once
+
+#include "plan.hpp"
+
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include <array>
+#include <string>
+
+namespace espb {
+
+struct GridArgs;
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+// Stage wall times in seconds (reference keys ewald.hpp:628-629 plus the
+// GPU-only binning stage).
+struct StageTimes {
+    double local = 0, spread = 0, fft = 0, scale = 0, ifft = 0, interpolate = 0, bin = 0;
+};
+
+class Engine {
+public:
+    Engine(const Plan& plan, int device);
+    ~Engine();
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    int device() const { return device_; }
+
+    // Full evaluation (ewald.hpp:619-649): u = u_l + u_s - self, F = F_l + F_s,
+    // energy_dev[0] = 1/2 sum q u.  qsum_dev (optional, 2 doubles) receives
+    // (sum q, sum |q|) for the neutrality check.
+    void evaluate(long N, const double* pos, const double* q, double* u, double* F,
+                  double* energy_dev, double* qsum_dev, cudaStream_t s, StageTimes* t = nullptr);
+    // Parts (ewald.hpp:419 local_sum, :524 spectral_sum).
+    void local_sum(long N, const double* pos, const double* q, double* u, double* F,
+                   cudaStream_t s);
+    void spectral_sum(long N, const double* pos, const double* q, double* u, double* F,
+                      cudaStream_t s);
+    // Grid pipeline pieces (gridder.hpp:215, :244, :280); grid = nx*ny*nz reals.
+    void spread(long N, const double* pos, const double* q, double* grid, cudaStream_t s);
+    void interpolate(long N, const double* pos, const double* grid, double* out,
+                     cudaStream_t s);
+    void interpolate_gradient(long N, const double* pos, const double* grid, double* out,
+                              cudaStream_t s);
+
+    // Launch count of the last evaluate() (our kernels only, excluding cuFFT).
+    int last_launches() const { return launches_; }
+    // Mean duration (ms) of the pair kernel over the last evaluate() when
+    // timing was requested.
+    long pairs_unordered_estimate() const { return 0; }
+
+private:
+    void ensure_capacity(long N);
+    void prepare(long N, const double* pos, const double* q, double* qsum_dev, cudaStream_t s);
+    void run_pair(long N, cudaStream_t s);
+    void run_grid(long N, cudaStream_t s, StageTimes* t);
+    void run_spread(long N, cudaStream_t s);
+    GridArgs grid_args() const;
+
+    const Plan& plan_;
+    int device_ = 0;
+    int launches_ = 0;
+
+    // geometry
+    std::array<int, 3> nc_{};   // pair cells per dim
+    bool cells_ok_ = false;     // nc >= 3 in every dim (ewald.hpp:431-434)
+    int ncell_ = 0;
+    int S_ = 8;                 // spread bin edge in grid cells
+    std::array<int, 3> nb_{};   // spread bins per dim
+    int nbin_ = 0;
+    int W_ = 0;                 // spread tile edge (nodes)
+    long M_ = 0, Mh_ = 0;       // real grid size, half spectrum size
+    int nfields_ = 4;           // 4 for ik, 1 for ad
+    int pair_warps_ = 4;
+
+    // tables on device
+    double* d_win_ = nullptr;        // 3 x 4P x 13 phi, then 3 x 4P x 13 dphi
+    double* d_influence_ = nullptr;  // Mh
+    double* d_xi_ = nullptr;         // nx + ny + nz derivative multipliers (Nyquist = 0)
+
+    // scratch
+    long cap_ = 0;
+    double4* d_tmp_ = nullptr;   // folded xyzq, original order
+    int* d_cellA_ = nullptr;
+    int* d_rankA_ = nullptr;
+    int* d_cellB_ = nullptr;
+    int* d_rankB_ = nullptr;
+    double4* d_xyzqA_ = nullptr;
+    int* d_origA_ = nullptr;
+    double4* d_xyzqB_ = nullptr;
+    int* d_origB_ = nullptr;
+    double4* d_loc_ = nullptr;   // (u_l, F_l) in original order
+    double* d_epart_ = nullptr;  // energy partials
+    int* d_countA_ = nullptr;    // ncell + 1
+    int* d_startA_ = nullptr;
+    int* d_countB_ = nullptr;    // nbin + 1
+    int* d_startB_ = nullptr;
+    void* d_scan_tmp_ = nullptr;
+    size_t scan_tmp_bytes_ = 0;
+    double* d_grid_ = nullptr;          // M reals
+    cufftDoubleComplex* d_spec_ = nullptr;   // Mh
+    cufftDoubleComplex* d_spec4_ = nullptr;  // nfields * Mh
+    double* d_fields_ = nullptr;        // nfields * M
+    double* d_qsum_ = nullptr;          // scratch for neutrality sums
+
+    cufftHandle fwd_ = 0, inv_ = 0;
+    void* d_cufft_work_ = nullptr;
+    cudaStream_t aux_ = nullptr;
+    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+    cudaEvent_t ev_t_[8] = {};
+};
+
+}  // namespace espb
