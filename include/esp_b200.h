@@ -142,6 +142,15 @@ int esp_interpolate_gradient(esp_plan* plan, long N, const double* pos, const do
  * cuFFT and CUB scans). */
 int esp_last_launch_count(const esp_plan* plan);
 
+/* Ordered in-range pairs (0 < r < r_c) counted on the device by the last
+ * pair-sum launch; the algorithmic work unit of the pair kernel
+ * (96 flops per unordered pair).  Synchronises. */
+int esp_last_pair_count(esp_plan* plan, unsigned long long* ordered_pairs);
+
+/* Measured fp64 FMA-pipe throughput of a device in TFLOP/s (DFMA
+ * microbenchmark; the fp64 roofline denominator). */
+int esp_fp64_peak(int device, double* tflops);
+
 #ifdef __cplusplus
 }
 #endif

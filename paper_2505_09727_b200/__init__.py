@@ -109,6 +109,8 @@ _sig("esp_spread", [_vp, C.c_long, _dp, _dp, _dp])
 _sig("esp_interpolate", [_vp, C.c_long, _dp, _dp, _dp])
 _sig("esp_interpolate_gradient", [_vp, C.c_long, _dp, _dp, _dp])
 _sig("esp_last_launch_count", [_vp])
+_sig("esp_last_pair_count", [_vp, C.POINTER(C.c_ulonglong)])
+_sig("esp_fp64_peak", [C.c_int, C.POINTER(C.c_double)])
 
 
 def _check(rc: int):
@@ -236,6 +238,19 @@ class EwaldPlan:
     def last_launch_count(self) -> int:
         return int(_lib.esp_last_launch_count(self._h))
 
+    def last_pair_count(self) -> int:
+        """Ordered in-range pairs evaluated by the last pair-sum launch."""
+        v = C.c_ulonglong()
+        _check(_lib.esp_last_pair_count(self._h, C.byref(v)))
+        return int(v.value)
+
+
+def fp64_peak_tflops(device: int = 0) -> float:
+    """Measured DFMA throughput of `device` (TFLOP/s)."""
+    v = C.c_double()
+    _check(_lib.esp_fp64_peak(int(device), C.byref(v)))
+    return float(v.value)
+
 
 @dataclass
 class ParticleSystem:
@@ -307,14 +322,21 @@ def require_neutral(system: ParticleSystem) -> None:
     _check(_lib.esp_check_neutral(system.size(), system.q))
 
 
-def evaluate(plan: EwaldPlan, system: ParticleSystem, timings: bool = False) -> EnergyForces:
+def evaluate(plan: EwaldPlan, system: ParticleSystem, timings: bool = False,
+             out: tuple | None = None) -> EnergyForces:
     """ewald.hpp:619-649 on host arrays (H2D, GPU evaluation, D2H).
 
     timings=True serialises the stages and reports them under the
-    reference's keys (seconds) plus 'bin'."""
+    reference's keys (seconds) plus 'bin'.  out=(u, F) supplies
+    preallocated (e.g. pinned) float64 output arrays."""
     N = system.size()
-    u = np.empty(N)
-    F = np.empty((N, 3))
+    if out is not None:
+        u, F = out
+        if u.shape != (N,) or F.shape != (N, 3) or u.dtype != np.float64 or F.dtype != np.float64:
+            raise InvalidArgument("out arrays must be float64 (N,) and (N, 3)")
+    else:
+        u = np.empty(N)
+        F = np.empty((N, 3))
     e = C.c_double()
     t = _Timings() if timings else None
     _check(_lib.esp_evaluate(plan._h, _f64(system.box, (3,)), N, system.pos, system.q, u, F,

@@ -418,4 +418,17 @@ int esp_interpolate_gradient(esp_plan* p, long N, const double* pos, const doubl
 
 int esp_last_launch_count(const esp_plan* p) { return p && p->eng ? p->eng->last_launches() : 0; }
 
+int esp_last_pair_count(esp_plan* p, unsigned long long* ordered_pairs) {
+    return guarded([&] {
+        espb::Engine& e = engine(p);
+        if (p->stream) cuda_ok(cudaStreamSynchronize(p->stream), "synchronize");
+        cuda_ok(cudaDeviceSynchronize(), "synchronize");
+        *ordered_pairs = e.last_pair_count();
+    });
+}
+
+int esp_fp64_peak(int device, double* tflops) {
+    return guarded([&] { *tflops = espb::fp64_peak_tflops(device); });
+}
+
 }  // extern "C"

@@ -228,6 +228,7 @@ struct PairArgs {
     const int* orig;
     const int* start;     // ncell + 1
     double4* loc;         // original order: (u_l, F_l)
+    unsigned long long* npairs;  // ordered in-range pairs evaluated (r < r_c, r > 0)
     int nc[3];
     double cw[3];
     double box[3];
@@ -236,10 +237,11 @@ struct PairArgs {
 template <int ND>
 __device__ __forceinline__ void pair_eval(const PairConsts& k, double4 pj, double xi, double yi,
                                           double zi, double& u, double& fx, double& fy,
-                                          double& fz) {
+                                          double& fz, int& npair) {
     const double dx = pj.x - xi, dy = pj.y - yi, dz = pj.z - zi;
     const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
     if (r2 < k.rc2 && r2 > 0.0) {
+        ++npair;
         const double rinv = rsqrt(r2);
         const double z = fma(r2, k.two_irc2, -1.0);
         double G = k.G[ND - 1], H = k.H[ND - 1];
@@ -324,7 +326,7 @@ __global__ void __launch_bounds__(256) k_pair(PairArgs a, const __grid_constant_
         const float yf = static_cast<float>(pi.y - oy);
         const float zf = static_cast<float>(pi.z - oz);
         double u = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
-        int head = 0, tail = 0;
+        int head = 0, tail = 0, npair = 0;
 
         for (int base = 0; base < total; base += kPairCap) {
             const int nk = min(kPairCap, total - base);
@@ -356,13 +358,13 @@ __global__ void __launch_bounds__(256) k_pair(PairArgs a, const __grid_constant_
                     const int n = __reduce_min_sync(0xffffffffu, backlog);
                     for (int r = 0; r < n; ++r) {
                         const int kk = valid ? qw[((head + r) & (kQcap - 1)) * 32 + lane] : 0;
-                        pair_eval<ND>(k, cd[kk], pi.x, pi.y, pi.z, u, fx, fy, fz);
+                        pair_eval<ND>(k, cd[kk], pi.x, pi.y, pi.z, u, fx, fy, fz, npair);
                     }
                     head += n;
                     while (__any_sync(0xffffffffu, valid && tail - head > kQcap - 32)) {
                         if (valid && tail - head > kQcap - 32) {
                             const int kk = qw[(head & (kQcap - 1)) * 32 + lane];
-                            pair_eval<ND>(k, cd[kk], pi.x, pi.y, pi.z, u, fx, fy, fz);
+                            pair_eval<ND>(k, cd[kk], pi.x, pi.y, pi.z, u, fx, fy, fz, npair);
                             ++head;
                         }
                     }
@@ -372,7 +374,7 @@ __global__ void __launch_bounds__(256) k_pair(PairArgs a, const __grid_constant_
             while (__any_sync(0xffffffffu, valid && tail > head)) {
                 if (valid && tail > head) {
                     const int kk = qw[(head & (kQcap - 1)) * 32 + lane];
-                    pair_eval<ND>(k, cd[kk], pi.x, pi.y, pi.z, u, fx, fy, fz);
+                    pair_eval<ND>(k, cd[kk], pi.x, pi.y, pi.z, u, fx, fy, fz, npair);
                     ++head;
                 }
             }
@@ -380,6 +382,10 @@ __global__ void __launch_bounds__(256) k_pair(PairArgs a, const __grid_constant_
         if (valid) {
             const double qi = pi.w;
             a.loc[a.orig[i]] = make_double4(u, -qi * fx, -qi * fy, -qi * fz);
+        }
+        if (warp_live) {
+            const int tot = __reduce_add_sync(0xffffffffu, npair);
+            if (lane == 0 && a.npairs) atomicAdd(a.npairs, static_cast<unsigned long long>(tot));
         }
     }
 }
@@ -390,11 +396,13 @@ template <int ND>
 __global__ void __launch_bounds__(128) k_pair_allpairs(long N, const double4* __restrict__ xyzq,
                                                        double4* __restrict__ loc, double bx,
                                                        double by, double bz,
+                                                       unsigned long long* npairs,
                                                        const __grid_constant__ PairConsts k) {
     long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
     if (i >= N) return;
     const double4 pi = xyzq[i];
     double u = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
+    int npair = 0;
     for (long j = 0; j < N; ++j) {
         if (j == i) continue;
         double4 pj = xyzq[j];
@@ -405,9 +413,10 @@ __global__ void __launch_bounds__(128) k_pair_allpairs(long N, const double4* __
         pj.x = pi.x + dx;
         pj.y = pi.y + dy;
         pj.z = pi.z + dz;
-        pair_eval<ND>(k, pj, pi.x, pi.y, pi.z, u, fx, fy, fz);
+        pair_eval<ND>(k, pj, pi.x, pi.y, pi.z, u, fx, fy, fz, npair);
     }
     loc[i] = make_double4(u, -pi.w * fx, -pi.w * fy, -pi.w * fz);
+    if (npairs) atomicAdd(npairs, static_cast<unsigned long long>(npair));
 }
 
 // ----------------------------------------------------------------------------
@@ -692,6 +701,21 @@ __global__ void k_energy(const double* __restrict__ part, int n, double* out) {
     }
 }
 
+// fp64 FMA-pipe peak microbenchmark: 8 independent DFMA chains per thread.
+__global__ void __launch_bounds__(256) k_dfma_peak(double* out, int iters, double a, double b) {
+    double x0 = threadIdx.x * 1e-3, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4,
+           x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+            x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+        }
+    }
+    double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+    if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
+
 // Unpack (u_l, F_l) to the caller's layout (local_sum only).
 __global__ void k_unpack(long N, const double4* __restrict__ loc, double* u, double* F) {
     long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
@@ -836,6 +860,7 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
     dalloc(d_spec4_, nfields_ * Mh_);
     dalloc(d_fields_, nfields_ * M_);
     dalloc(d_qsum_, 2);
+    dalloc(d_npairs_, 1);
 
     // cuFFT: forward D2Z, batched inverse Z2D
     CF(cufftCreate(&fwd_));
@@ -893,6 +918,7 @@ Engine::~Engine() {
     dfree(d_spec4_);
     dfree(d_fields_);
     dfree(d_qsum_);
+    dfree(d_npairs_);
     if (aux_) cudaStreamDestroy(aux_);
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_join_) cudaEventDestroy(ev_join_);
@@ -921,6 +947,7 @@ void Engine::prepare(long N, const double* pos, const double* q, double* qsum_de
                      cudaStream_t s) {
     const Plan& p = plan_;
     CK(cudaMemsetAsync(d_countA_, 0, sizeof(int) * (ncell_ + 1), s));
+    CK(cudaMemsetAsync(d_npairs_, 0, sizeof(unsigned long long), s));
     CK(cudaMemsetAsync(d_countB_, 0, sizeof(int) * (nbin_ + 1), s));
     if (qsum_dev) CK(cudaMemsetAsync(qsum_dev, 0, sizeof(double) * 2, s));
     BinArgs a{};
@@ -970,7 +997,8 @@ void Engine::run_pair(long N, cudaStream_t s) {
     if (!cells_ok_) {
         // all-pairs path works on the folded, original-order copy
         auto go = [&](auto kern) {
-            kern<<<grid1(N, 128), 128, 0, s>>>(N, d_tmp_, d_loc_, p.box[0], p.box[1], p.box[2], k);
+            kern<<<grid1(N, 128), 128, 0, s>>>(N, d_tmp_, d_loc_, p.box[0], p.box[1], p.box[2],
+                                               d_npairs_, k);
         };
         if (nd == 20) go(k_pair_allpairs<20>);
         else if (nd == 28) go(k_pair_allpairs<28>);
@@ -984,6 +1012,7 @@ void Engine::run_pair(long N, cudaStream_t s) {
     a.orig = d_origA_;
     a.start = d_startA_;
     a.loc = d_loc_;
+    a.npairs = d_npairs_;
     for (int d = 0; d < 3; ++d) {
         a.nc[d] = nc_[d];
         a.cw[d] = p.box[d] / nc_[d];
@@ -1189,6 +1218,37 @@ void Engine::interpolate_gradient(long N, const double* pos, const double* grid,
     a.u = out;
     const GridArgs g = grid_args();
     dispatch_P<InterpLaunch>(plan_.P, static_cast<int>(kGradient), false, g, a, s);
+}
+
+unsigned long long Engine::last_pair_count() const {
+    unsigned long long v = 0;
+    CK(cudaMemcpy(&v, d_npairs_, sizeof(v), cudaMemcpyDeviceToHost));
+    return v;
+}
+
+double fp64_peak_tflops(int device) {
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    CK(cudaGetDeviceProperties(&prop, device));
+    double* out = nullptr;
+    CK(cudaMalloc(&out, sizeof(double)));
+    const int blocks = prop.multiProcessorCount * 8, threads = 256, iters = 4096;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    k_dfma_peak<<<blocks, threads>>>(out, 64, 1.0000001, 1e-9);  // warm-up / clocks up
+    k_dfma_peak<<<blocks, threads>>>(out, iters, 1.0000001, 1e-9);
+    CK(cudaEventRecord(e0));
+    k_dfma_peak<<<blocks, threads>>>(out, iters, 1.0000001, 1e-9);
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    const double flops = 2.0 * 8.0 * 16.0 * iters * static_cast<double>(blocks) * threads;
+    return flops / (ms * 1e-3) / 1e12;
 }
 
 }  // namespace espb

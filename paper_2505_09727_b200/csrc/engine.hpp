@@ -30,6 +30,9 @@ struct StageTimes {
     double local = 0, spread = 0, fft = 0, scale = 0, ifft = 0, interpolate = 0, bin = 0;
 };
 
+// Measured fp64 FMA throughput of the device (TFLOP/s), for the roofline.
+double fp64_peak_tflops(int device);
+
 class Engine {
 public:
     Engine(const Plan& plan, int device);
@@ -58,9 +61,9 @@ public:
 
     // Launch count of the last evaluate() (our kernels only, excluding cuFFT).
     int last_launches() const { return launches_; }
-    // Mean duration (ms) of the pair kernel over the last evaluate() when
-    // timing was requested.
-    long pairs_unordered_estimate() const { return 0; }
+    // Ordered in-range pairs (0 < r < r_c) evaluated by the last pair-kernel
+    // launch, counted on the device (synchronous read).
+    unsigned long long last_pair_count() const;
 
 private:
     void ensure_capacity(long N);
@@ -115,6 +118,7 @@ private:
     cufftDoubleComplex* d_spec4_ = nullptr;  // nfields * Mh
     double* d_fields_ = nullptr;        // nfields * M
     double* d_qsum_ = nullptr;          // scratch for neutrality sums
+    unsigned long long* d_npairs_ = nullptr;
 
     cufftHandle fwd_ = 0, inv_ = 0;
     void* d_cufft_work_ = nullptr;
