@@ -57,8 +57,6 @@ namespace {
 
 constexpr double kPi = 3.14159265358979323846;
 constexpr int kNc = 13;        // coefficients per window piece (degree 12)
-constexpr int kPairCap = 1024; // candidates staged per pair-kernel chunk
-constexpr int kQcap = 64;      // per-lane pair queue depth (power of two)
 constexpr int kMaxPoly = 40;   // max pair-polynomial coefficients
 
 // ----------------------------------------------------------------------------
@@ -229,6 +227,8 @@ struct PairArgs {
     const int* start;     // ncell + 1
     double4* loc;         // original order: (u_l, F_l)
     unsigned long long* npairs;  // ordered in-range pairs evaluated (r < r_c, r > 0)
+    int cap;                     // candidates staged per chunk (multiple of 32)
+    int nsplit;                  // CTAs per cell (blockIdx.y) sharing its targets
     int nc[3];
     double cw[3];
     double box[3];
@@ -242,7 +242,16 @@ __device__ __forceinline__ void pair_eval(const PairConsts& k, double4 pj, doubl
     const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
     if (r2 < k.rc2 && r2 > 0.0) {
         ++npair;
-        const double rinv = rsqrt(r2);
+        // 1/sqrt(r2): MUFU seed + two Newton steps (r2 is a positive normal here)
+        double rinv;
+        asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rinv) : "d"(r2));
+        {
+            const double hr = 0.5 * r2;
+            double e = fma(-hr * rinv, rinv, 0.5);
+            rinv = fma(rinv, e, rinv);
+            e = fma(-hr * rinv, rinv, 0.5);
+            rinv = fma(rinv, e, rinv);
+        }
         const double z = fma(r2, k.two_irc2, -1.0);
         double G = k.G[ND - 1], H = k.H[ND - 1];
 #pragma unroll
@@ -262,23 +271,28 @@ __device__ __forceinline__ void pair_eval(const PairConsts& k, double4 pj, doubl
     }
 }
 
-// One CTA per pair cell; lane = target atom i; the 27 neighbour cells are
-// staged in shared memory (fp64 positions with the periodic image shift
-// applied, plus an fp32 copy for screening).  Each lane screens every staged
-// candidate in fp32 and queues the ones inside r_c; whenever every lane has
-// k queued pairs the warp evaluates k rounds fully converged in fp64.
+// One CTA per pair cell, one warp per target atom i (round-robin over the
+// cell's atoms).  The 27 neighbour cells are staged once per CTA in shared
+// memory as fp32 coordinates relative to the cell origin plus a 32-bit code
+// (source index | neighbour slot << 27).  For its i, a warp screens 32
+// candidates per step in fp32 (lane = candidate), compacts the survivors
+// with a ballot into a per-warp queue, and evaluates full 32-lane rounds in
+// fp64 (exact min-image geometry from the global copy + the slot's periodic
+// shift).  Per-i sums are warp-reduced once.  Candidate sets larger than the
+// staging capacity are processed in chunks (per-i partial sums accumulated
+// into loc by the owning lane).
 template <int ND>
-__global__ void __launch_bounds__(256) k_pair(PairArgs a, const __grid_constant__ PairConsts k) {
+__global__ void __launch_bounds__(128) k_pair(PairArgs a, const __grid_constant__ PairConsts k) {
     extern __shared__ __align__(16) unsigned char smem[];
-    double4* cd = reinterpret_cast<double4*>(smem);
-    float4* cf = reinterpret_cast<float4*>(cd + kPairCap);
-    unsigned short* qall = reinterpret_cast<unsigned short*>(cf + kPairCap);
-    __shared__ int nstart[27], ncount[27], npre[28];
+    float4* cand = reinterpret_cast<float4*>(smem);                 // a.cap entries
+    int* qall = reinterpret_cast<int*>(cand + a.cap);               // 64 per warp
+    __shared__ int nstart[27], npre[28];
     __shared__ double nshift[27][3];
 
     const int nw = blockDim.x >> 5;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    unsigned short* qw = qall + warp * kQcap * 32;
+    int* qw = qall + warp * 64;
+    const unsigned lt_mask = (1u << lane) - 1u;
 
     const int cell = blockIdx.x;
     const int cz = cell % a.nc[2];
@@ -288,104 +302,123 @@ __global__ void __launch_bounds__(256) k_pair(PairArgs a, const __grid_constant_
     if (ib == ie) return;
     const double ox = cx * a.cw[0], oy = cy * a.cw[1], oz = cz * a.cw[2];
 
-    if (threadIdx.x < 27) {
-        int t = threadIdx.x;
-        int dx = t / 9 - 1, dy = (t / 3) % 3 - 1, dz = t % 3 - 1;
-        int nx = cx + dx, ny = cy + dy, nz = cz + dz;
-        double sx = nx < 0 ? -a.box[0] : (nx >= a.nc[0] ? a.box[0] : 0.0);
-        double sy = ny < 0 ? -a.box[1] : (ny >= a.nc[1] ? a.box[1] : 0.0);
-        double sz = nz < 0 ? -a.box[2] : (nz >= a.nc[2] ? a.box[2] : 0.0);
-        nx = (nx + a.nc[0]) % a.nc[0];
-        ny = (ny + a.nc[1]) % a.nc[1];
-        nz = (nz + a.nc[2]) % a.nc[2];
-        int c = (nx * a.nc[1] + ny) * a.nc[2] + nz;
-        nstart[t] = a.start[c];
-        ncount[t] = a.start[c + 1] - a.start[c];
-        nshift[t][0] = sx;
-        nshift[t][1] = sy;
-        nshift[t][2] = sz;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int s = 0;
-        for (int t = 0; t < 27; ++t) {
-            npre[t] = s;
-            s += ncount[t];
+    if (threadIdx.x < 32) {
+        const int t = lane;
+        int cnt = 0;
+        if (t < 27) {
+            const int dx = t / 9 - 1, dy = (t / 3) % 3 - 1, dz = t % 3 - 1;
+            int nx = cx + dx, ny = cy + dy, nz = cz + dz;
+            nshift[t][0] = nx < 0 ? -a.box[0] : (nx >= a.nc[0] ? a.box[0] : 0.0);
+            nshift[t][1] = ny < 0 ? -a.box[1] : (ny >= a.nc[1] ? a.box[1] : 0.0);
+            nshift[t][2] = nz < 0 ? -a.box[2] : (nz >= a.nc[2] ? a.box[2] : 0.0);
+            nx = (nx + a.nc[0]) % a.nc[0];
+            ny = (ny + a.nc[1]) % a.nc[1];
+            nz = (nz + a.nc[2]) % a.nc[2];
+            const int c = (nx * a.nc[1] + ny) * a.nc[2] + nz;
+            nstart[t] = a.start[c];
+            cnt = a.start[c + 1] - a.start[c];
         }
-        npre[27] = s;
+        // exclusive warp scan of the 27 counts
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        if (t < 27) npre[t] = incl - cnt;
+        if (t == 26) npre[27] = incl;
     }
     __syncthreads();
     const int total = npre[27];
 
-    for (int i0 = ib; i0 < ie; i0 += nw * 32) {
-        const int i = i0 + warp * 32 + lane;
-        const bool valid = i < ie;
-        const bool warp_live = __any_sync(0xffffffffu, valid);
-        double4 pi = valid ? a.xyzq[i] : make_double4(0.0, 0.0, 0.0, 0.0);
-        const float xf = static_cast<float>(pi.x - ox);
-        const float yf = static_cast<float>(pi.y - oy);
-        const float zf = static_cast<float>(pi.z - oz);
-        double u = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
-        int head = 0, tail = 0, npair = 0;
-
-        for (int base = 0; base < total; base += kPairCap) {
-            const int nk = min(kPairCap, total - base);
-            __syncthreads();
-            for (int c = threadIdx.x; c < nk; c += blockDim.x) {
+    for (int base = 0; base < total; base += a.cap) {
+        const int nk = min(a.cap, total - base);
+        const int nk32 = (nk + 31) & ~31;
+        if (base > 0) __syncthreads();
+        {
+            int t = 0;
+            for (int c = threadIdx.x; c < nk32; c += blockDim.x) {
                 const int g = base + c;
-                int t = 0;
-                while (npre[t + 1] <= g) ++t;
-                double4 v = a.xyzq[nstart[t] + (g - npre[t])];
-                v.x += nshift[t][0];
-                v.y += nshift[t][1];
-                v.z += nshift[t][2];
-                cd[c] = v;
-                cf[c] = make_float4(static_cast<float>(v.x - ox), static_cast<float>(v.y - oy),
-                                    static_cast<float>(v.z - oz), 0.0f);
-            }
-            __syncthreads();
-            if (!warp_live) continue;
-            for (int c = 0; c < nk; ++c) {
-                const float4 v = cf[c];
-                const float ddx = v.x - xf, ddy = v.y - yf, ddz = v.z - zf;
-                const float r2 = fmaf(ddz, ddz, fmaf(ddy, ddy, ddx * ddx));
-                if (valid && r2 < k.rc2_test) {
-                    qw[(tail & (kQcap - 1)) * 32 + lane] = static_cast<unsigned short>(c);
-                    ++tail;
-                }
-                if ((c & 31) == 31) {
-                    const int backlog = valid ? tail - head : 0x7fffffff;
-                    const int n = __reduce_min_sync(0xffffffffu, backlog);
-                    for (int r = 0; r < n; ++r) {
-                        const int kk = valid ? qw[((head + r) & (kQcap - 1)) * 32 + lane] : 0;
-                        pair_eval<ND>(k, cd[kk], pi.x, pi.y, pi.z, u, fx, fy, fz, npair);
-                    }
-                    head += n;
-                    while (__any_sync(0xffffffffu, valid && tail - head > kQcap - 32)) {
-                        if (valid && tail - head > kQcap - 32) {
-                            const int kk = qw[(head & (kQcap - 1)) * 32 + lane];
-                            pair_eval<ND>(k, cd[kk], pi.x, pi.y, pi.z, u, fx, fy, fz, npair);
-                            ++head;
-                        }
-                    }
-                }
-            }
-            // drain this chunk's queue (divergent tail)
-            while (__any_sync(0xffffffffu, valid && tail > head)) {
-                if (valid && tail > head) {
-                    const int kk = qw[(head & (kQcap - 1)) * 32 + lane];
-                    pair_eval<ND>(k, cd[kk], pi.x, pi.y, pi.z, u, fx, fy, fz, npair);
-                    ++head;
+                if (c < nk) {
+                    while (npre[t + 1] <= g) ++t;
+                    const int src = nstart[t] + (g - npre[t]);
+                    const double4 v = a.xyzq[src];
+                    cand[c] = make_float4(static_cast<float>(v.x + nshift[t][0] - ox),
+                                          static_cast<float>(v.y + nshift[t][1] - oy),
+                                          static_cast<float>(v.z + nshift[t][2] - oz),
+                                          __int_as_float(src | (t << 27)));
+                } else {
+                    // padding sentinel: never within r_c
+                    cand[c] = make_float4(1e30f, 1e30f, 1e30f, __int_as_float(0));
                 }
             }
         }
-        if (valid) {
-            const double qi = pi.w;
-            a.loc[a.orig[i]] = make_double4(u, -qi * fx, -qi * fy, -qi * fz);
-        }
-        if (warp_live) {
-            const int tot = __reduce_add_sync(0xffffffffu, npair);
-            if (lane == 0 && a.npairs) atomicAdd(a.npairs, static_cast<unsigned long long>(tot));
+        __syncthreads();
+        // CTA part p handles targets ib + p*nw + warp, stepping by nsplit*nw
+        const int stride = nw * a.nsplit;
+        for (int i = ib + blockIdx.y * nw + warp; i < ie; i += stride) {
+            const double4 pi = a.xyzq[i];
+            const float xf = static_cast<float>(pi.x - ox);
+            const float yf = static_cast<float>(pi.y - oy);
+            const float zf = static_cast<float>(pi.z - oz);
+            double u = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
+            int npair = 0, qn = 0;
+#pragma unroll 2
+            for (int kb = lane; kb < nk32; kb += 32) {
+                const float4 c4 = cand[kb];
+                const float dx = c4.x - xf, dy = c4.y - yf, dz = c4.z - zf;
+                const bool in = fmaf(dz, dz, fmaf(dy, dy, dx * dx)) < k.rc2_test;
+                const unsigned m = __ballot_sync(0xffffffffu, in);
+                if (in) qw[qn + __popc(m & lt_mask)] = __float_as_int(c4.w);
+                qn += __popc(m);
+                if (qn >= 32) {
+                    __syncwarp();
+                    const int code = qw[lane];
+                    const int extra = qw[32 + lane];
+                    __syncwarp();
+                    qw[lane] = extra;
+                    qn -= 32;
+                    double4 pj = a.xyzq[code & 0x7ffffff];
+                    const int t = static_cast<unsigned>(code) >> 27;
+                    pj.x += nshift[t][0];
+                    pj.y += nshift[t][1];
+                    pj.z += nshift[t][2];
+                    pair_eval<ND>(k, pj, pi.x, pi.y, pi.z, u, fx, fy, fz, npair);
+                }
+            }
+            __syncwarp();
+            if (lane < qn) {
+                const int code = qw[lane];
+                double4 pj = a.xyzq[code & 0x7ffffff];
+                const int t = static_cast<unsigned>(code) >> 27;
+                pj.x += nshift[t][0];
+                pj.y += nshift[t][1];
+                pj.z += nshift[t][2];
+                pair_eval<ND>(k, pj, pi.x, pi.y, pi.z, u, fx, fy, fz, npair);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                u += __shfl_xor_sync(0xffffffffu, u, o);
+                fx += __shfl_xor_sync(0xffffffffu, fx, o);
+                fy += __shfl_xor_sync(0xffffffffu, fy, o);
+                fz += __shfl_xor_sync(0xffffffffu, fz, o);
+            }
+            npair = __reduce_add_sync(0xffffffffu, npair);
+            if (lane == 0) {
+                const double qi = pi.w;
+                const int o = a.orig[i];
+                double4 r = make_double4(u, -qi * fx, -qi * fy, -qi * fz);
+                if (base > 0) {
+                    const double4 p = a.loc[o];
+                    r.x += p.x;
+                    r.y += p.y;
+                    r.z += p.z;
+                    r.w += p.w;
+                }
+                a.loc[o] = r;
+                if (a.npairs) atomicAdd(a.npairs, static_cast<unsigned long long>(npair));
+            }
         }
     }
 }
@@ -1018,15 +1051,23 @@ void Engine::run_pair(long N, cudaStream_t s) {
         a.cw[d] = p.box[d] / nc_[d];
         a.box[d] = p.box[d];
     }
-    const double mean = static_cast<double>(N) / ncell_;
-    int nw = static_cast<int>(std::ceil(1.15 * mean / 32.0));
-    nw = std::max(1, std::min(8, nw));
+    const int nw = 4;
     pair_warps_ = nw;
-    size_t sm = kPairCap * (sizeof(double4) + sizeof(float4)) + nw * kQcap * 32 * sizeof(unsigned short);
+    a.cap = 2048;
+    // split crowded cells over several CTAs when there are too few cells to
+    // fill the GPU (small systems such as cfg2: 216 cells of ~150 atoms)
+    const double mean = static_cast<double>(N) / ncell_;
+    const long want_warps = 148L * 24;
+    int nsplit = static_cast<int>((want_warps + static_cast<long>(ncell_) * nw - 1) /
+                                  (static_cast<long>(ncell_) * nw));
+    nsplit = std::max(1, std::min(nsplit, static_cast<int>(std::ceil(mean / (2.0 * nw)))));
+    a.nsplit = nsplit;
+    if (N >= (1L << 27)) throw InvalidArgument("pair kernel: N must be < 2^27");
+    size_t sm = a.cap * sizeof(float4) + nw * 64 * sizeof(int);
     auto go = [&](auto kern) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(sm)));
-        kern<<<ncell_, nw * 32, sm, s>>>(a, k);
+        kern<<<dim3(ncell_, nsplit), nw * 32, sm, s>>>(a, k);
     };
     if (nd == 20) go(k_pair<20>);
     else if (nd == 28) go(k_pair<28>);
