@@ -33,6 +33,7 @@ struct GridArgs {
     int nb[3];
     int S;
     int W;
+    int RS, PS;         // padded row / plane strides of the spread tile (doubles)
     int P;
     const double* win;  // 3 x 4P x 13 (phi) then 3 x 4P x 13 (dphi)
 };
@@ -456,67 +457,85 @@ __global__ void __launch_bounds__(128) k_pair_allpairs(long N, const double4* __
 // K1: spread (gridder.hpp:215-241)
 // ----------------------------------------------------------------------------
 
-// One warp per spread bin (S^3 grid cells): the bin's atoms are accumulated
-// into a shared-memory tile of W^3 nodes (W = S + P + 2 covers every
-// footprint), one atom at a time with lanes over the P^3 footprint nodes, so
-// no two lanes ever touch the same node (no shared atomics -- fp64 shared
-// atomics are CAS loops on sm_100a).  The tile is then added to the global
-// grid with REDG.F64 (nonzero nodes only).  PT > 0 fixes P at compile time;
-// PT == 0 reads it from g.P (max 16).
+// One CTA per spread bin (S^3 grid cells).  The bin's atoms are accumulated
+// into a shared-memory tile covering every footprint (W = S + P + 2 nodes
+// per side), with one THREAD PER FOOTPRINT NODE: all threads of the CTA add
+// the same atom at the same time (no two threads touch one node, so no
+// shared atomics -- fp64 shared atomics are CAS loops on sm_100a) and one
+// barrier separates consecutive atoms.  Atom positions and their 3P window
+// weights are prepared a chunk at a time by all threads in parallel.  The
+// tile strides are padded (row = P, plane = P^2 mod 16 doubles) so that a
+// warp's 32 consecutive footprint nodes hit 32 distinct banks pairs.  The
+// tile is then added to the global grid with REDG.F64 (nonzero nodes).
+// PT > 0 fixes P at compile time; PT == 0 reads it from g.P (max 16).
+constexpr int kSpreadChunk = 64;
+
 template <int PT>
-__global__ void __launch_bounds__(32) k_spread(GridArgs g, const double4* __restrict__ xyzq,
-                                               const int* __restrict__ start,
-                                               double* __restrict__ grid) {
+__global__ void __launch_bounds__(512) k_spread(GridArgs g, const double4* __restrict__ xyzq,
+                                                const int* __restrict__ start,
+                                                double* __restrict__ grid) {
     extern __shared__ __align__(16) unsigned char smem[];
-    double* tile = reinterpret_cast<double*>(smem);
     constexpr int MP = PT > 0 ? PT : 16;
-    __shared__ double wb[3 * MP];
     const int P = PT > 0 ? PT : g.P;
-    const int P2 = P * P, P3 = P2 * P;
-    const int W = g.W;
-    const int lane = threadIdx.x;
+    double* wch = reinterpret_cast<double*>(smem);             // [chunk][3][MP]
+    int* fch = reinterpret_cast<int*>(wch + kSpreadChunk * 3 * MP);  // [chunk][3]
+    double* tile = reinterpret_cast<double*>(smem) + kSpreadChunk * 3 * MP + kSpreadChunk * 2;
+    const int W = g.W, RS = g.RS, PS = g.PS;
+    const int nt = blockDim.x;
     const int bin = blockIdx.x;
     const int bz = bin % g.nb[2], by = (bin / g.nb[2]) % g.nb[1], bx = bin / (g.nb[1] * g.nb[2]);
     const int ib = start[bin], ie = start[bin + 1];
     if (ib == ie) return;
-    const int lox = bx * g.S - P / 2, loy = by * g.S - P / 2, loz = bz * g.S - P / 2;
-    const int W3 = W * W * W;
-    for (int t = lane; t < W3; t += 32) tile[t] = 0.0;
-    __syncwarp();
-    for (int i = ib; i < ie; ++i) {
-        const double4 v = xyzq[i];
-        const Foot fx = footprint(P, v.x, g.h[0], g.half[0]);
-        const Foot fy = footprint(P, v.y, g.h[1], g.half[1]);
-        const Foot fz = footprint(P, v.z, g.h[2], g.half[2]);
-        if (lane < 3 * P) {
-            const int d = lane / P, j = lane - d * P;
-            const Foot& f = d == 0 ? fx : (d == 1 ? fy : fz);
+    const int lo[3] = {bx * g.S - P / 2, by * g.S - P / 2, bz * g.S - P / 2};
+    const int tsize = PS * W;
+    for (int t = threadIdx.x; t < tsize; t += nt) tile[t] = 0.0;
+
+    const int P2 = P * P, P3 = P2 * P;
+    for (int c0 = ib; c0 < ie; c0 += kSpreadChunk) {
+        const int nc = min(kSpreadChunk, ie - c0);
+        __syncthreads();  // previous chunk's last atom done with wch/fch
+        for (int task = threadIdx.x; task < 3 * nc; task += nt) {
+            const int ai = task / 3, d = task - 3 * ai;
+            const double4 v = xyzq[c0 + ai];
+            const double x = d == 0 ? v.x : (d == 1 ? v.y : v.z);
+            const Foot f = footprint(P, x, g.h[d], g.half[d]);
             const double* tab = g.win + static_cast<long>(d) * 4 * P * kNc;
-            double w = horner13(tab + (4 * (P - 1 - j) + f.s) * kNc, f.t);
-            if ((j == 0 && f.zero_lo) || (j == P - 1 && f.zero_hi)) w = 0.0;
-            if (d == 0) w *= v.w;
-            wb[d * MP + j] = w;
+            double* w = wch + (ai * 3 + d) * MP;
+            const double scale = d == 0 ? v.w : 1.0;
+#pragma unroll
+            for (int j = 0; j < MP; ++j) {
+                if (j < P) {
+                    double wj = horner13(tab + (4 * (P - 1 - j) + f.s) * kNc, f.t);
+                    if ((j == 0 && f.zero_lo) || (j == P - 1 && f.zero_hi)) wj = 0.0;
+                    w[j] = wj * scale;
+                }
+            }
+            // offsets are in [0, W-P] by construction; clamp for non-finite input
+            fch[ai * 3 + d] = clampi(f.first - lo[d], 0, W - P);
         }
-        __syncwarp();
-        // offsets are in [0, W-P] by construction; clamp for non-finite input
-        const int ox = clampi(fx.first - lox, 0, W - P);
-        const int oy = clampi(fy.first - loy, 0, W - P);
-        const int oz = clampi(fz.first - loz, 0, W - P);
-        for (int p = lane; p < P3; p += 32) {
-            const int jx = p / P2, r = p - jx * P2;
-            const int jy = r / P, jz = r - jy * P;
-            const int off = ((ox + jx) * W + (oy + jy)) * W + (oz + jz);
-            tile[off] += wb[jx] * wb[MP + jy] * wb[2 * MP + jz];
+        __syncthreads();
+        for (int ai = 0; ai < nc; ++ai) {
+            const int* fo = fch + ai * 3;
+            const double* w = wch + ai * 3 * MP;
+            const int base = fo[0] * PS + fo[1] * RS + fo[2];
+            for (int p = threadIdx.x; p < P3; p += nt) {
+                const int jx = p / P2, r = p - jx * P2;
+                const int jy = r / P, jz = r - jy * P;
+                const int off = base + jx * PS + jy * RS + jz;
+                tile[off] += w[jx] * w[MP + jy] * w[2 * MP + jz];
+            }
+            __syncthreads();
         }
-        __syncwarp();
     }
-    for (int t = lane; t < W3; t += 32) {
+    for (int t = threadIdx.x; t < tsize; t += nt) {
         const double val = tile[t];
         if (val != 0.0) {
-            const int ix = t / (W * W), iy = (t / W) % W, iz = t % W;
-            const int gx = wrapi(lox + ix, g.nf[0]);
-            const int gy = wrapi(loy + iy, g.nf[1]);
-            const int gz = wrapi(loz + iz, g.nf[2]);
+            const int ix = t / PS, rem = t - ix * PS;
+            const int iy = rem / RS, iz = rem - iy * RS;
+            if (iy >= W || iz >= W) continue;  // padding
+            const int gx = wrapi(lo[0] + ix, g.nf[0]);
+            const int gy = wrapi(lo[1] + iy, g.nf[1]);
+            const int gz = wrapi(lo[2] + iz, g.nf[2]);
             atomicAdd(&grid[(static_cast<long>(gx) * g.nf[1] + gy) * g.nf[2] + gz], val);
         }
     }
@@ -794,11 +813,14 @@ template <int P>
 struct SpreadLaunch {
     static void run(const GridArgs& g, int nbin, const double4* xyzq, const int* start,
                     double* grid, cudaStream_t s) {
-        size_t sm = sizeof(double) * g.W * g.W * g.W;
-        if (sm > 48 * 1024)
-            CK(cudaFuncSetAttribute(k_spread<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(sm)));
-        k_spread<P><<<nbin, 32, sm, s>>>(g, xyzq, start, grid);
+        const int Pr = P > 0 ? P : g.P;
+        const int MP = P > 0 ? P : 16;
+        const int nt = std::min(512, (Pr * Pr * Pr + 31) / 32 * 32);
+        size_t sm = sizeof(double) * (kSpreadChunk * 3 * MP + kSpreadChunk * 2) +
+                    sizeof(double) * static_cast<size_t>(g.PS) * g.W;
+        CK(cudaFuncSetAttribute(k_spread<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(sm)));
+        k_spread<P><<<nbin, nt, sm, s>>>(g, xyzq, start, grid);
         CK(cudaGetLastError());
     }
 };
@@ -855,10 +877,24 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
     for (int d = 0; d < 3; ++d) nc_[d] = std::max(1, static_cast<int>(std::floor(p.box[d] / p.r_c)));
     cells_ok_ = nc_[0] >= 3 && nc_[1] >= 3 && nc_[2] >= 3;
     ncell_ = nc_[0] * nc_[1] * nc_[2];
-    S_ = 8;
+    // spread bins: the largest S in {8, 6, 4} that still gives >= 4 CTAs per SM
+    S_ = 4;
+    for (int cand : {8, 6}) {
+        long nb = 1;
+        for (int d = 0; d < 3; ++d) nb *= (p.nf[d] + cand - 1) / cand;
+        if (nb >= 4 * 148) {
+            S_ = cand;
+            break;
+        }
+    }
     for (int d = 0; d < 3; ++d) nb_[d] = (p.nf[d] + S_ - 1) / S_;
     nbin_ = nb_[0] * nb_[1] * nb_[2];
     W_ = S_ + p.P + 2;
+    // padded strides: consecutive footprint nodes -> consecutive banks
+    RS_ = W_;
+    while (RS_ % 16 != p.P % 16) ++RS_;
+    PS_ = RS_ * W_;
+    while (PS_ % 16 != (p.P * p.P) % 16) ++PS_;
     M_ = static_cast<long>(p.nf[0]) * p.nf[1] * p.nf[2];
     Mh_ = static_cast<long>(p.nf[0]) * p.nf[1] * (p.nf[2] / 2 + 1);
     nfields_ = p.force_method == ForceMethod::ik ? 4 : 1;
@@ -1112,6 +1148,8 @@ GridArgs Engine::grid_args() const {
     }
     g.S = S_;
     g.W = W_;
+    g.RS = RS_;
+    g.PS = PS_;
     g.P = plan_.P;
     g.win = d_win_;
     return g;

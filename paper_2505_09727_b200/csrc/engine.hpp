@@ -85,6 +85,7 @@ private:
     std::array<int, 3> nb_{};   // spread bins per dim
     int nbin_ = 0;
     int W_ = 0;                 // spread tile edge (nodes)
+    int RS_ = 0, PS_ = 0;       // padded tile strides
     long M_ = 0, Mh_ = 0;       // real grid size, half spectrum size
     int nfields_ = 4;           // 4 for ik, 1 for ad
     int pair_warps_ = 4;
