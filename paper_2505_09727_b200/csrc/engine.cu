@@ -109,6 +109,14 @@ __device__ __forceinline__ Foot footprint(int P, double x, double h, double half
     return f;
 }
 
+// 256-bit read-only global load of 4 consecutive doubles (LDG.E.ENL2.256);
+// p must be 32-byte aligned.
+__device__ __forceinline__ void ldg4(const double* p, double& a, double& b, double& c, double& d) {
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+        : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
+        : "l"(p));
+}
+
 __device__ __forceinline__ double horner13(const double* __restrict__ c, double t) {
     double r = c[12];
 #pragma unroll
@@ -555,17 +563,19 @@ __global__ void __launch_bounds__(256) k_scale(long Mh, int ny, int nzh, const d
     const double pk = p[m];
     const cufftDoubleComplex b = in[m];
     const double cr = b.x * pk, ci = b.y * pk;
-    out[m] = make_cuDoubleComplex(cr, ci);
     if (nfields == 4) {
+        // interleaved spectra [m][4] -> the batched inverse writes [node][4]
         const int iz = static_cast<int>(m % nzh);
         const long r = m / nzh;
         const int iy = static_cast<int>(r % ny);
         const int ix = static_cast<int>(r / ny);
         const double fx = xi[ix], fy = xi[nx + iy], fz = xi[nx + ny + iz];
         // (a + ib) * i xi = (-b xi, a xi)
-        out[Mh + m] = make_cuDoubleComplex(-ci * fx, cr * fx);
-        out[2 * Mh + m] = make_cuDoubleComplex(-ci * fy, cr * fy);
-        out[3 * Mh + m] = make_cuDoubleComplex(-ci * fz, cr * fz);
+        double4* o = reinterpret_cast<double4*>(out + 4 * m);
+        o[0] = make_double4(cr, ci, -ci * fx, cr * fx);
+        o[1] = make_double4(-ci * fy, cr * fy, -ci * fz, cr * fz);
+    } else {
+        out[m] = make_cuDoubleComplex(cr, ci);
     }
 }
 
@@ -628,38 +638,57 @@ __global__ void __launch_bounds__(128) k_interp(GridArgs g, InterpArgs a) {
         const long ny = g.nf[1], nz = g.nf[2];
         double qi = v.w;
         double us = 0.0, Fx = 0.0, Fy = 0.0, Fz = 0.0;
-        if (MODE == kValue || (IK && MODE != kGradient)) {
-            constexpr int NFLD = (MODE == kValue) ? 1 : 4;
-            double acc[NFLD];
-#pragma unroll
-            for (int c = 0; c < NFLD; ++c) acc[c] = 0.0;
+        if (MODE == kValue) {
+            double acc = 0.0;
 #pragma unroll 1
             for (int jx = 0; jx < P; ++jx) {
 #pragma unroll
                 for (int jy = 0; jy < MP; ++jy) {
                     if (jy < P) {
-                        const long row = (idx[0][jx] * ny + idx[1][jy]) * nz;
-                        const double wxy = w[0][jx] * w[1][jy];
+                        const double* fld = a.fields + (idx[0][jx] * ny + idx[1][jy]) * nz;
+                        double sz = 0.0;
 #pragma unroll
-                        for (int c = 0; c < NFLD; ++c) {
-                            const double* fld = a.fields + c * a.M + row;
-                            double sz = 0.0;
-#pragma unroll
-                            for (int jz = 0; jz < MP; ++jz)
-                                if (jz < P) sz = fma(w[2][jz], __ldg(fld + idx[2][jz]), sz);
-                            acc[c] = fma(wxy, sz, acc[c]);
-                        }
+                        for (int jz = 0; jz < MP; ++jz)
+                            if (jz < P) sz = fma(w[2][jz], __ldg(fld + idx[2][jz]), sz);
+                        acc = fma(w[0][jx] * w[1][jy], sz, acc);
                     }
                 }
             }
-            if (MODE == kValue) {
-                a.u[o] = acc[0];
-            } else {
-                us = acc[0];
-                Fx = -qi * acc[NFLD > 1 ? 1 : 0];
-                Fy = -qi * acc[NFLD > 2 ? 2 : 0];
-                Fz = -qi * acc[NFLD > 3 ? 3 : 0];
+            a.u[o] = acc;
+        } else if (IK && MODE != kGradient) {
+            // four fields interleaved per node: one 256-bit load per node
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll 1
+            for (int jx = 0; jx < P; ++jx) {
+#pragma unroll
+                for (int jy = 0; jy < MP; ++jy) {
+                    if (jy < P) {
+                        const double* fld = a.fields + 4 * ((idx[0][jx] * ny + idx[1][jy]) * nz);
+                        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+                        for (int jz = 0; jz < MP; ++jz) {
+                            if (jz < P) {
+                                double f0, f1, f2, f3;
+                                ldg4(fld + 4 * idx[2][jz], f0, f1, f2, f3);
+                                const double wz = w[2][jz];
+                                s0 = fma(wz, f0, s0);
+                                s1 = fma(wz, f1, s1);
+                                s2 = fma(wz, f2, s2);
+                                s3 = fma(wz, f3, s3);
+                            }
+                        }
+                        const double wxy = w[0][jx] * w[1][jy];
+                        a0 = fma(wxy, s0, a0);
+                        a1 = fma(wxy, s1, a1);
+                        a2 = fma(wxy, s2, a2);
+                        a3 = fma(wxy, s3, a3);
+                    }
+                }
             }
+            us = a0;
+            Fx = -qi * a1;
+            Fy = -qi * a2;
+            Fz = -qi * a3;
         } else {
             // value + gradient from one field with derivative weights
             double dw[3][MP];
@@ -941,8 +970,13 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
     int n3[3] = {p.nf[0], p.nf[1], p.nf[2]};
     int inembed[3] = {p.nf[0], p.nf[1], p.nf[2] / 2 + 1};
     int onembed[3] = {p.nf[0], p.nf[1], p.nf[2]};
-    CF(cufftMakePlanMany(inv_, 3, n3, inembed, 1, static_cast<int>(Mh_), onembed, 1,
-                         static_cast<int>(M_), CUFFT_Z2D, nfields_, &w2));
+    if (nfields_ == 4) {
+        // interleaved batch: spectra [m][4] -> fields [node][4] (one 256-bit load per node in K3)
+        CF(cufftMakePlanMany(inv_, 3, n3, inembed, 4, 1, onembed, 4, 1, CUFFT_Z2D, 4, &w2));
+    } else {
+        CF(cufftMakePlanMany(inv_, 3, n3, inembed, 1, static_cast<int>(Mh_), onembed, 1,
+                             static_cast<int>(M_), CUFFT_Z2D, 1, &w2));
+    }
     CK(cudaMalloc(&d_cufft_work_, std::max<size_t>(std::max(w1, w2), 16)));
     CF(cufftSetWorkArea(fwd_, d_cufft_work_));
     CF(cufftSetWorkArea(inv_, d_cufft_work_));
