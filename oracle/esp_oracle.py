@@ -1,0 +1,573 @@
+"""CPU restatement of the reference ESP algorithm in numpy/scipy.
+
+TEST INFRASTRUCTURE ONLY -- the checker, never the product.  Only tests/,
+__graft_entry__.smoke() and bench.py's cpu_baseline leg may use anything
+under oracle/.  The product (paper_2505_09727_b200/) never imports it.
+
+Pinned against the reference: tests/test_oracle.py checks this module
+against the golden fixtures produced by the unmodified reference
+(tests/golden/make_golden.py, oracle/_ref) -- plan parameters exactly,
+energies/forces to 1e-10.
+
+Every function cites the reference routine it restates (file:line under
+/root/reference/proj/include/esp).  Where the reference evaluates a kernel
+through its compiled piecewise-Chebyshev tables, this module evaluates the
+exact series the tables approximate (differences ~1e-14 relative).
+Independent numerics on purpose: scipy eigh_tridiagonal for the prolate
+ground state (reference: QL), brentq for the bandwidth (reference: its own
+Brent), scipy spherical_jn for the cosine transform (reference: Miller
+recurrence), numpy.fft (pocketfft) for the transforms (reference: FFTW).
+Sizes: plan selection up to nf ~ 100; evaluation O(N^2) in the real-space
+part, meant for N up to a few thousand.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+from numpy.polynomial import legendre as npleg
+from scipy.linalg import eigh_tridiagonal
+from scipy.optimize import brentq
+from scipy.special import erf, erfc, spherical_jn
+
+INV4PI = 1.0 / (4.0 * math.pi)
+
+
+# ---------------------------------------------------------------------------
+# prolate spheroidal wave function psi_0^c (prolate.hpp:137-263)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class Prolate:
+    c: float
+    a: np.ndarray        # psi(x) = sum_k a[k] P_2k(x), psi(0) = 1
+    C0: float
+    psi1: float
+    l2: float
+
+
+def build_prolate(c: float, tol: float = 1e-15) -> Prolate:
+    """prolate.hpp:137-237: even-Legendre tridiagonal operator, ground state."""
+    n = 2 * int(math.ceil(c)) + 30
+    while True:
+        k = np.arange(n, dtype=np.float64)
+        m = 2.0 * k
+        x2 = (m + 1) ** 2 / ((2 * m + 1) * (2 * m + 3))
+        x2[1:] += m[1:] ** 2 / ((2 * m[1:] + 1) * (2 * m[1:] - 1))
+        d = m * (m + 1) + c * c * x2
+        kk = k[:-1]
+        e = c * c * (2 * kk + 1) * (2 * kk + 2) / ((4 * kk + 3) * np.sqrt((4 * kk + 1) * (4 * kk + 5)))
+        _, v = eigh_tridiagonal(d, e, select="i", select_range=(0, 0))
+        a = v[:, 0] * np.sqrt((4 * k + 1) / 2.0)
+        amax = np.abs(a).max()
+        if abs(a[-1]) < tol * amax and abs(a[-2]) < tol * amax:
+            break
+        n += 16
+        if n > 600:
+            raise RuntimeError("build_prolate: order cap exceeded")
+    # sup normalisation psi(0) = 1: P_2k(0) = (-1)^k (2k-1)!!/(2k)!!
+    p0 = np.ones(n)
+    for j in range(1, n):
+        p0[j] = -p0[j - 1] * (2 * j - 1) / (2 * j)
+    a = a / float(np.dot(a, p0))
+    if a[0] < 0:
+        a = -a
+    amax = np.abs(a).max()
+    keep = a.size
+    while keep > 2 and abs(a[keep - 2]) < tol * amax:
+        keep -= 1
+    a = a[:keep].copy()
+    l2 = math.sqrt(float(np.sum(a * a * 2.0 / (4 * np.arange(keep) + 1))))
+    return Prolate(c, a, float(a[0]), float(a.sum()), l2)
+
+
+def solve_c(eps: float) -> float:
+    """prolate.hpp:254-263: psi(1)/||psi||_2 = eps."""
+    def f(c):
+        p = build_prolate(c)
+        return math.log(max(p.psi1 / p.l2, 1e-300)) - math.log(eps)
+    return brentq(f, 2.0, 28.0, xtol=1e-14, rtol=1e-15)
+
+
+def prolate_cos(a: np.ndarray, nu) -> np.ndarray:
+    """prolate.hpp:75-87: B(nu) = int_0^1 psi cos(nu t) dt = sum_k a_k (-1)^k j_2k(nu)."""
+    nu = np.abs(np.asarray(nu, dtype=np.float64))
+    out = np.zeros_like(nu)
+    for k, ak in enumerate(a):
+        out += (ak if k % 2 == 0 else -ak) * spherical_jn(2 * k, nu)
+    return out
+
+
+def _even_leg(a):
+    c = np.zeros(2 * a.size - 1)
+    c[0::2] = a
+    return c
+
+
+# ---------------------------------------------------------------------------
+# split and window kernels (kernels.hpp:63-273)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class Split:
+    family: str
+    eps: float
+    r_c: float
+    shape: float
+    chi0: float
+    pro: Prolate | None = None
+
+    def chi(self, y):
+        y = np.asarray(y, dtype=np.float64)
+        if self.family == "gaussian":
+            return 2.0 * math.sqrt(self.shape / math.pi) * np.exp(-self.shape * y * y)
+        v = npleg.legval(y, _even_leg(self.pro.a)) / self.pro.C0
+        return np.where((y < 0) | (y > 1), 0.0, v)
+
+    def Psi(self, y):
+        y = np.asarray(y, dtype=np.float64)
+        if self.family == "gaussian":
+            v = erf(math.sqrt(self.shape) * y)
+        else:
+            v = npleg.legval(y, npleg.legint(_even_leg(self.pro.a), lbnd=0)) / self.pro.C0
+        return np.where(y <= 0, 0.0, np.where(y >= 1, 1.0, v))
+
+    def chihat_n(self, nu):
+        if self.family == "gaussian":
+            return np.exp(-np.asarray(nu) ** 2 / (4.0 * self.shape))
+        return prolate_cos(self.pro.a, nu) / self.pro.C0
+
+
+def build_split(family: str, eps: float, r_c: float) -> Split:
+    """kernels.hpp:105-138."""
+    if family == "gaussian":
+        alpha = math.log(1.0 / eps)
+        return Split(family, eps, r_c, alpha, 2.0 * math.sqrt(alpha / math.pi))
+    c = solve_c(eps)
+    pro = build_prolate(c)
+    return Split(family, eps, r_c, c, 1.0 / pro.C0, pro)
+
+
+def local_kernel(sp: Split, r):
+    """kernels.hpp:143-163 -> (pot, fr) with fr = -dS/dr."""
+    r = np.asarray(r, dtype=np.float64)
+    y = r / sp.r_c
+    if sp.family == "gaussian":
+        one_minus = erfc(math.sqrt(sp.shape) * y)
+    else:
+        one_minus = 1.0 - sp.Psi(y)
+    pot = one_minus * INV4PI / r
+    fr = pot / r + sp.chi(y) * INV4PI / (r * sp.r_c)
+    inside = r < sp.r_c
+    return np.where(inside, pot, 0.0), np.where(inside, fr, 0.0)
+
+
+def _bspline(P, v):
+    """Cardinal B-spline M_P on [0, P] (kernels.hpp:40-55), vectorised."""
+    v = np.asarray(v, dtype=np.float64)
+    out = np.zeros_like(v)
+    # explicit formula M_P(v) = 1/(P-1)! sum_k (-1)^k C(P,k) (v-k)_+^(P-1)
+    for k in range(P + 1):
+        out += (-1) ** k * math.comb(P, k) * np.maximum(v - k, 0.0) ** (P - 1)
+    out /= math.factorial(P - 1)
+    return np.where((v <= 0) | (v >= P), 0.0, out)
+
+
+@dataclass
+class Window:
+    family: str
+    P: int
+    h: float
+    c1: float
+    half: float
+    pro: Prolate | None = None
+
+    def phi(self, x):
+        x = np.asarray(x, dtype=np.float64)
+        if self.family == "bspline":
+            v = _bspline(self.P, x / self.h + self.P / 2.0) / self.h
+        else:
+            t = x / self.half
+            v = npleg.legval(t, _even_leg(self.pro.a)) / (2.0 * self.half * self.pro.C0)
+        return np.where(np.abs(x) >= self.half, 0.0, v)
+
+    def dphi(self, x):
+        x = np.asarray(x, dtype=np.float64)
+        if self.family == "bspline":
+            u = x / self.h + self.P / 2.0
+            v = (_bspline(self.P - 1, u) - _bspline(self.P - 1, u - 1.0)) / (self.h * self.h)
+        else:
+            t = x / self.half
+            v = npleg.legval(t, npleg.legder(_even_leg(self.pro.a))) / (
+                2.0 * self.half * self.half * self.pro.C0)
+        return np.where(np.abs(x) >= self.half, 0.0, v)
+
+    def phi_hat(self, xi):
+        nu = np.abs(np.asarray(xi, dtype=np.float64))
+        if self.family == "bspline":
+            t = nu * self.h / 2.0
+            s = np.where(t == 0, 1.0, np.sin(t) / np.where(t == 0, 1.0, t))
+            return s ** self.P
+        return prolate_cos(self.pro.a, nu * self.half) / self.pro.C0
+
+
+# ---------------------------------------------------------------------------
+# parameter selection and plan (ewald.hpp:110-405)
+# ---------------------------------------------------------------------------
+
+def signed_mode(n):
+    """gridder.hpp:76 for all storage indices of an n-point dimension."""
+    i = np.arange(n)
+    return np.where(i < (n + 1) // 2, i, i - n)
+
+
+def next_even_5smooth(x: float) -> int:
+    """numerics.hpp:289-293."""
+    m = max(2, int(math.ceil(x - 1e-9)))
+
+    def smooth(n):
+        for p in (2, 3, 5):
+            while n % p == 0:
+                n //= p
+        return n == 1
+
+    while not (m % 2 == 0 and smooth(m)):
+        m += 1
+    return m
+
+
+def pswf_order_default(eps: float) -> int:
+    """ewald.hpp:206-212."""
+    s = 1.0 - 1e-9
+    return 5 if eps >= 5e-4 * s else 6 if eps >= 1e-4 * s else 7 if eps >= 5e-5 * s else 8
+
+
+def _alias_slabs(sp: Split, nf, box):
+    """ewald.hpp:110-143: slab marginals of g = |chihat_n(r_c|xi|)|/|xi|^2."""
+    f2 = [(2 * math.pi * signed_mode(n) / L) ** 2 for n, L in zip(nf, box)]
+    xi2 = f2[0][:, None, None] + f2[1][None, :, None] + f2[2][None, None, :]
+    g = np.zeros_like(xi2)
+    nz = xi2 != 0
+    g[nz] = np.abs(sp.chihat_n(sp.r_c * np.sqrt(xi2[nz]))) / xi2[nz]
+    return [g.sum(axis=(1, 2)), g.sum(axis=(0, 2)), g.sum(axis=(0, 1))], g.sum()
+
+
+@dataclass
+class Plan:
+    family: str
+    eps: float
+    r_c: float
+    box: tuple
+    nf: tuple
+    base_nf: tuple
+    P: int
+    shape: float
+    c1: float
+    E_A: float
+    E_T: float
+    E_SI: float
+    h: tuple
+    split: Split
+    win: list
+    influence: np.ndarray
+    force_method: str = "ik"
+    demand: tuple = field(default_factory=tuple)
+
+
+def build_plan(box, family="pswf", eps=1e-4, r_c=1.0, nf_ov=0, P_ov=0, c1_ov=0.0,
+               force_method="ik", allow_degraded=False) -> Plan:
+    """ewald.hpp:236-405 (select_with_split + build_plan + influence)."""
+    box = tuple(float(b) for b in box)
+    if not (1e-5 <= eps <= 1e-3):
+        raise ValueError("build_plan: eps out of supported range [1e-5, 1e-3]")
+    if not min(box) > 0:
+        raise ValueError("build_plan: invalid box")
+    if not (r_c > 0 and r_c < min(box) / 2):
+        raise ValueError("build_plan: require 0 < r_c < min(L)/2")
+    sp = build_split(family, eps, r_c)
+    gauss = family == "gaussian"
+    P = P_ov if P_ov > 0 else (5 if gauss else pswf_order_default(eps))
+    if not 3 <= P <= 16:
+        raise ValueError("select_parameters: P out of range [3,16]")
+    demand, nf = [], []
+    for L in box:
+        if gauss:
+            demand.append(max(2 * sp.shape * L / (math.pi * r_c),
+                              L * math.sqrt(sp.shape) * eps ** (-1.0 / P) / (2 * r_c)))
+        else:
+            demand.append(sp.shape * L / (math.pi * r_c))
+        if nf_ov > 0:
+            if nf_ov % 2:
+                raise ValueError("select_parameters: overridden n_f must be even")
+            nf.append(nf_ov)
+        elif gauss:
+            nf.append(next_even_5smooth(2.0 * math.ceil(sp.shape * L / (math.pi * r_c))))
+        else:
+            nf.append(next_even_5smooth(math.ceil(sp.shape * L / (math.pi * r_c))))
+    base_nf = tuple(nf)
+    cands = [] if gauss else ([c1_ov] if c1_ov > 0 else
+                              [sp.shape * (1.0 + 0.5 * i / 24) for i in range(25)])
+    cexp = [build_prolate(c) for c in cands]
+    for step in range(61):
+        slabs, den = _alias_slabs(sp, nf, box)
+        esi, c1 = 0.0, float("nan")
+        if gauss:
+            num = 0.0
+            for d in range(3):
+                k = signed_mode(nf[d]).astype(np.float64)
+                num += np.sum(2 * slabs[d] * np.abs(k / (k + nf[d])) ** P)
+            ea = num / den
+            hmax = max(L / n for L, n in zip(box, nf))
+            esi = (math.sqrt(sp.shape) * hmax / (2 * r_c)) ** P
+        else:
+            ea = float("inf")
+            for c, pe in zip(cands, cexp):
+                num = 0.0
+                for d in range(3):
+                    k = signed_mode(nf[d]).astype(np.float64)
+                    lo = prolate_cos(pe.a, math.pi * P * k / nf[d])
+                    hi = prolate_cos(pe.a, math.pi * P * (k + nf[d]) / nf[d])
+                    num += np.sum(2 * slabs[d] * np.abs(hi / lo))
+                e = num / den
+                if e < ea:
+                    ea, c1 = e, c
+        if nf_ov > 0 or max(ea, esi) <= eps:
+            break
+        if step >= 60:
+            raise RuntimeError("select_parameters: grid inflation did not reach the target")
+        hmax = max(L / n for L, n in zip(box, nf))
+        nf = [next_even_5smooth(n + 1.0) if L / n >= hmax * (1 - 1e-12) else n
+              for L, n in zip(box, nf)]
+    h = tuple(L / n for L, n in zip(box, nf))
+    if gauss:
+        win = [Window("bspline", P, hd, float("nan"), P * hd / 2.0) for hd in h]
+    else:
+        wp = build_prolate(c1)
+        win = [Window("pswf", P, hd, c1, P * hd / 2.0, wp) for hd in h]
+    for hd in h:
+        if P * hd / 2.0 > (r_c + hd) * (1 + 1e-9):
+            raise RuntimeError("build_plan: window footprint exceeds the split support")
+    E_T = max(abs(float(sp.chihat_n(r_c * math.pi * n / L))) for n, L in zip(nf, box))
+    if not allow_degraded and (ea > eps or E_T > eps or esi > eps):
+        raise RuntimeError("build_plan: predicted error exceeds eps")
+    infl = influence_coefficients(sp, win, nf, box)
+    return Plan(family, eps, r_c, box, tuple(nf), base_nf, P, sp.shape, c1, ea, E_T, esi, h, sp,
+                win, infl, force_method, tuple(demand))
+
+
+def influence_coefficients(sp: Split, win, nf, box) -> np.ndarray:
+    """gridder.hpp:162-210: p_k = (hx hy hz)^2/V chihat_n(r_c|xi|)/|xi|^2 / prod phihat^2."""
+    freq = [2 * math.pi * signed_mode(n) / L for n, L in zip(nf, box)]
+    ph = [w.phi_hat(f) for w, f in zip(win, freq)]
+    V = box[0] * box[1] * box[2]
+    hh = np.prod([L / n for L, n in zip(box, nf)])
+    pref = hh * hh / V
+    xi2 = (freq[0][:, None, None] ** 2 + freq[1][None, :, None] ** 2) + freq[2][None, None, :] ** 2
+    w = (ph[0][:, None, None] ** 2 * ph[1][None, :, None] ** 2) * ph[2][None, None, :] ** 2
+    p = np.zeros_like(xi2)
+    nz = xi2 != 0
+    p[nz] = pref * (sp.chihat_n(sp.r_c * np.sqrt(xi2[nz])) / xi2[nz]) / w[nz]
+    return p
+
+
+# ---------------------------------------------------------------------------
+# grid pipeline (gridder.hpp:102-314) and solver (ewald.hpp:419-649)
+# ---------------------------------------------------------------------------
+
+def fold(pos, box):
+    """system.hpp:29-36."""
+    L = np.asarray(box, dtype=np.float64)
+    p = pos - L * np.floor(pos / L)
+    return np.where(p >= L, 0.0, p)
+
+
+def _footprint(win: Window, x, deriv=False):
+    """gridder.hpp:108-139: first node and P weights per particle."""
+    P, h = win.P, win.h
+    if P % 2 == 0:
+        first = np.floor(x / h).astype(np.int64) - (P // 2 - 1)
+    else:
+        first = np.floor(x / h + 0.5).astype(np.int64) - (P - 1) // 2
+    j = np.arange(P)
+    arg = x[:, None] - h * (first[:, None] + j[None, :])
+    w = win.dphi(arg) if deriv else win.phi(arg)
+    return first, w
+
+
+def spread(plan: Plan, pos, q) -> np.ndarray:
+    """gridder.hpp:215-241 (real part)."""
+    nf = plan.nf
+    g = np.zeros(nf)
+    fps = [_footprint(plan.win[d], pos[:, d]) for d in range(3)]
+    P = plan.P
+    for jx in range(P):
+        ix = (fps[0][0] + jx) % nf[0]
+        wx = q * fps[0][1][:, jx]
+        for jy in range(P):
+            iy = (fps[1][0] + jy) % nf[1]
+            wxy = wx * fps[1][1][:, jy]
+            for jz in range(P):
+                iz = (fps[2][0] + jz) % nf[2]
+                np.add.at(g, (ix, iy, iz), wxy * fps[2][1][:, jz])
+    return g
+
+
+def interpolate(plan: Plan, grid, pos, deriv_dim: int = -1) -> np.ndarray:
+    """gridder.hpp:244-277; deriv_dim >= 0 gives that component of
+    interpolate_gradient (gridder.hpp:280-314)."""
+    nf = plan.nf
+    fps = [_footprint(plan.win[d], pos[:, d], deriv=(d == deriv_dim)) for d in range(3)]
+    out = np.zeros(pos.shape[0])
+    P = plan.P
+    for jx in range(P):
+        ix = (fps[0][0] + jx) % nf[0]
+        for jy in range(P):
+            iy = (fps[1][0] + jy) % nf[1]
+            wxy = fps[0][1][:, jx] * fps[1][1][:, jy]
+            for jz in range(P):
+                iz = (fps[2][0] + jz) % nf[2]
+                out += wxy * fps[2][1][:, jz] * grid[ix, iy, iz]
+    return out
+
+
+def local_sum(plan: Plan, pos, q, chunk: int = 256):
+    """ewald.hpp:419-515 (all ordered pairs, min image; O(N^2) restatement)."""
+    L = np.asarray(plan.box)
+    pos = fold(pos, plan.box)
+    N = q.size
+    u = np.zeros(N)
+    F = np.zeros((N, 3))
+    rc2 = plan.r_c ** 2
+    for s in range(0, N, chunk):
+        d = pos[None, :, :] - pos[s:s + chunk, None, :]           # r_j - r_i
+        d -= L * np.round(d / L)
+        r2 = np.einsum("ijk,ijk->ij", d, d)
+        m = (r2 < rc2) & (r2 > 0)
+        r = np.sqrt(np.where(m, r2, 1.0))
+        pot, fr = local_kernel(plan.split, r)
+        pot = np.where(m, pot, 0.0)
+        fr = np.where(m, fr, 0.0)
+        u[s:s + chunk] = pot @ q
+        coef = -(q[s:s + chunk, None] * q[None, :]) * fr / r
+        F[s:s + chunk] = np.einsum("ij,ijk->ik", coef, d)
+    return u, F
+
+
+def spectral_sum(plan: Plan, pos, q):
+    """ewald.hpp:524-604 (ik and ad)."""
+    pos = fold(pos, plan.box)
+    g = np.fft.fftn(spread(plan, pos, q))          # forward, e^{-i}
+    c = g * plan.influence
+    if plan.force_method == "ad":
+        grid = np.fft.ifftn(c).real * np.prod(plan.nf)   # unnormalised inverse
+        u = interpolate(plan, grid, pos)
+        F = np.stack([-q * interpolate(plan, grid, pos, d) for d in range(3)], axis=1)
+        return u, F
+    grid = np.fft.ifftn(c).real * np.prod(plan.nf)
+    u = interpolate(plan, grid, pos)
+    F = np.zeros((q.size, 3))
+    for d in range(3):
+        n = plan.nf[d]
+        xi = np.where(2 * np.arange(n) == n, 0.0, 2 * math.pi * signed_mode(n) / plan.box[d])
+        shape = [1, 1, 1]
+        shape[d] = n
+        work = c * (1j * xi.reshape(shape))
+        gd = np.fft.ifftn(work).real * np.prod(plan.nf)
+        F[:, d] = -q * interpolate(plan, gd, pos)
+    return u, F
+
+
+def self_correction(plan: Plan, q):
+    """ewald.hpp:609-615."""
+    return q * plan.split.chi0 / (4.0 * math.pi * plan.r_c)
+
+
+def evaluate(plan: Plan, pos, q):
+    """ewald.hpp:619-649 -> (energy, u, F)."""
+    q = np.asarray(q, dtype=np.float64)
+    if abs(q.sum()) > 1e-12 * max(np.abs(q).sum(), 1.0):
+        raise RuntimeError("system is not charge neutral")
+    ul, Fl = local_sum(plan, pos, q)
+    us, Fs = spectral_sum(plan, pos, q)
+    u = ul + us - self_correction(plan, q)
+    F = Fl + Fs
+    return 0.5 * math.fsum(q * u), u, F
+
+
+def direct_ewald(pos, q, box, tol=1e-9, lam=None):
+    """reference.hpp:42-206 (one pass): explicit image shells + reciprocal
+    structure factors, lambda = min(L)/6 by default (reference.hpp:222)."""
+    box = np.asarray(box, dtype=np.float64)
+    pos = fold(pos, box)
+    N = q.size
+    V = float(np.prod(box))
+    lam = lam or float(box.min()) / 6.0
+    u = np.zeros(N)
+    F = np.zeros((N, 3))
+    for m in range(0, 17):
+        rng = np.arange(-m, m + 1)
+        off = np.array([(a, b, c) for a in rng for b in rng for c in rng
+                        if max(abs(a), abs(b), abs(c)) == m], dtype=np.float64) * box
+        du = np.zeros(N)
+        for o in off:
+            d = pos[:, None, :] - pos[None, :, :] + o          # r_i - r_j + n
+            r2 = np.einsum("ijk,ijk->ij", d, d)
+            if m == 0:
+                np.fill_diagonal(r2, np.inf)
+            r = np.sqrt(r2)
+            a = r / lam
+            ok = a <= 27.0
+            er = np.where(ok, erfc(np.where(ok, a, 0.0)), 0.0)
+            contrib = np.where(ok, er * INV4PI / r, 0.0)
+            du += contrib @ q
+            fp = -(er / r2 + (2.0 / (lam * math.sqrt(math.pi))) * np.exp(-a * a) / r) * INV4PI
+            coef = -(q[:, None] * q[None, :]) * np.where(ok, fp / r, 0.0)
+            F += np.einsum("ij,ijk->ik", coef, d)
+        u += du
+        if m >= 1 and np.abs(du).max() < tol / 10.0:
+            break
+    qabs = np.abs(q).sum()
+    Lmax = float(box.max())
+    kmax = 1
+    while True:
+        ximin = 2 * math.pi * kmax / Lmax
+        if (qabs / V) * math.exp(-lam * lam * ximin * ximin / 4) / (ximin * ximin) < tol / 10:
+            break
+        kmax += 1
+    k = np.arange(-kmax, kmax + 1)
+    KX, KY, KZ = np.meshgrid(k, k, k, indexing="ij")
+    sel = np.maximum(np.maximum(abs(KX), abs(KY)), abs(KZ)) > 0
+    kv = np.stack([KX[sel], KY[sel], KZ[sel]], axis=1).astype(np.float64)
+    xi = 2 * math.pi * kv / box
+    xi2 = np.einsum("ij,ij->i", xi, xi)
+    w = np.exp(-lam * lam * xi2 / 4) / (xi2 * V)
+    for s in range(0, xi.shape[0], 512):
+        ph = pos @ xi[s:s + 512].T                       # N x K
+        c, sn = np.cos(ph), np.sin(ph)
+        rho_r, rho_i = q @ c, -(q @ sn)                    # sum q e^{-i xi r}
+        tr = c * rho_r - sn * rho_i                        # Re(e^{+i xi r_i} rho)
+        ti = sn * rho_r + c * rho_i                        # Im
+        u += tr @ w[s:s + 512]
+        F += (q[:, None] * ti * w[s:s + 512]) @ xi[s:s + 512]
+    u -= q / (2.0 * math.pi ** 1.5 * lam)
+    return 0.5 * math.fsum(q * u), u, F
+
+
+def splitmix64_uniform(seed: int, start: int, count: int) -> np.ndarray:
+    """io.hpp:33-44, vectorised over the counter."""
+    with np.errstate(over="ignore"):
+        k = np.arange(start + 1, start + count + 1, dtype=np.uint64)
+        z = np.uint64(seed) + k * np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    return (z >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+
+
+def random_system(N: int, box, seed: int = 1):
+    """io.hpp:92-104: +-1 alternating, positions L * uniform (i-major)."""
+    box = np.asarray(box, dtype=np.float64)
+    pos = box * splitmix64_uniform(seed, 0, 3 * N).reshape(N, 3)
+    q = np.where(np.arange(N) % 2 == 0, 1.0, -1.0)
+    return fold(pos, box), q

@@ -1,0 +1,90 @@
+"""The numpy restatement (oracle/esp_oracle.py) pinned against the reference's
+own outputs (golden fixtures from the compiled reference, tests/golden/)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, golden, max_rel, rel_rms
+from oracle import esp_oracle as O
+
+PLANS = json.load(open(os.path.join(GOLDEN, "plans.json")))
+
+
+@pytest.mark.parametrize("name", ["row_1e-3", "row_5e-4", "row_1e-4", "row_5e-5", "row_1e-5",
+                                  "box_10_10_15", "cfg1", "cfg2", "gauss_0.001"])
+def test_oracle_plan_matches_reference(name):
+    g = PLANS[name]
+    p = O.build_plan(g["box"], g.get("family", "pswf"), g["eps"], g["r_c"])
+    assert list(p.nf) == g["nf"] and list(p.base_nf) == g["base_nf"] and p.P == g["P"]
+    assert abs(p.shape - g["shape"]) <= 1e-10 * g["shape"]
+    if g.get("family", "pswf") == "pswf":
+        assert abs(p.c1 - g["c1"]) <= 1e-10 * g["c1"]
+    assert abs(p.E_A - g["E_A"]) <= 1e-9 * g["E_A"]
+    assert abs(p.E_T - g["E_T"]) <= 1e-9 * max(g["E_T"], 1e-300)
+
+
+def test_oracle_cfg1_matches_reference():
+    g = golden("cfg1.npz")
+    p = O.build_plan((10.0, 10.0, 10.0), "pswf", 1e-4, 1.0)
+    pos, q = O.random_system(1000, (10.0, 10.0, 10.0), 1)
+    E, u, F = O.evaluate(p, pos, q)
+    assert abs(E - g["energy"]) <= 1e-11 * abs(g["energy"])
+    assert rel_rms(F, g["F"]) <= 1e-10
+    assert max_rel(u, g["u"]) <= 1e-10
+    ul, Fl = O.local_sum(p, pos, q)
+    assert max_rel(ul, g["u_local"]) <= 1e-12 and rel_rms(Fl, g["F_local"]) <= 1e-12
+    pa = O.build_plan((10.0, 10.0, 10.0), "pswf", 1e-4, 1.0, force_method="ad")
+    Ea, ua, Fa = O.evaluate(pa, pos, q)
+    assert abs(Ea - g["ad_energy"]) <= 1e-11 * abs(g["ad_energy"])
+    assert rel_rms(Fa, g["ad_F"]) <= 1e-10
+
+
+@pytest.mark.parametrize("name", ["small_n16", "small_n128", "small_n64_rc34"])
+def test_oracle_small_systems(name):
+    g = golden(name + ".npz")
+    L = float(g["L"])
+    pos, q = O.random_system(int(g["N"]), (L, L, L), int(g["seed"]))
+    p = O.build_plan((L, L, L), "pswf", float(g["eps"]), float(g["r_c"]))
+    E, u, F = O.evaluate(p, pos, q)
+    assert abs(E - g["energy"]) <= 1e-11 * abs(g["energy"])
+    assert rel_rms(F, g["F"]) <= 1e-10
+
+
+def test_oracle_direct_ewald_matches_reference():
+    g = golden("small_n128.npz")
+    L = float(g["L"])
+    pos, q = O.random_system(128, (L, L, L), 128)
+    E, u, F = O.direct_ewald(pos, q, (L, L, L), 1e-9)
+    assert abs(E - g["d_energy"]) <= 1e-10 * abs(g["d_energy"])
+    assert rel_rms(F, g["d_F"]) <= 1e-9
+
+
+def test_oracle_grid_pipeline_matches_reference():
+    g = golden("grid_cfg1.npz")
+    p = O.build_plan((10.0, 10.0, 10.0), "pswf", 1e-4, 1.0)
+    pos, q = O.random_system(1000, (10.0, 10.0, 10.0), 1)
+    assert max_rel(O.spread(p, pos[:200], q[:200]), g["spread"]) <= 1e-12
+    field = np.random.default_rng(8).uniform(-1.0, 1.0, p.nf)
+    assert max_rel(O.interpolate(p, field, pos[:200]), g["interp"]) <= 1e-12
+    grad = np.stack([O.interpolate(p, field, pos[:200], d) for d in range(3)], axis=1)
+    assert max_rel(grad, g["interp_grad"]) <= 1e-11
+
+
+def test_fftw_shim_and_reference_if_built():
+    """oracle/_ref (the compiled reference with the FFTW3 shim) honours the
+    FFT contract of test_gridder.cpp:44-76 and reproduces the fixtures."""
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("oracle/_ref not built (needs /root/reference)")
+    rng = np.random.default_rng(1)
+    a = rng.uniform(-1, 1, (8, 12, 10)) + 1j * rng.uniform(-1, 1, (8, 12, 10))
+    f = ref.fft3(a, -1)
+    assert np.abs(f - np.fft.fftn(a)).max() <= 1e-12
+    assert np.abs(ref.fft3(f, +1) / a.size - a).max() <= 1e-13
+    g = golden("cfg1.npz")
+    pos, q = O.random_system(1000, (10.0, 10.0, 10.0), 1)
+    rp = ref.RefPlan((10.0, 10.0, 10.0), "pswf", 1e-4, 1.0)
+    r = rp.evaluate(pos, q)
+    assert r.energy == float(g["energy"]) or abs(r.energy - g["energy"]) <= 1e-14 * abs(r.energy)
