@@ -1,0 +1,196 @@
+// Drop-in check: reference-style unit tests (test_ewald.cpp) written against
+// include/esp/esp.hpp and run on the GPU through libesp_b200.so.  Plain main,
+// one line per check, nonzero exit on failure (the reference's acceptance
+// harness style).  Bitwise gates of the reference are tolerances here where
+// GPU atomics reorder sums.
+#include "esp/esp.hpp"
+
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+
+static int failures = 0;
+#define CHECK(cond)                                                                  \
+    do {                                                                             \
+        bool ok_ = (cond);                                                           \
+        std::printf("%s  %s:%d  %s\n", ok_ ? "ok  " : "FAIL", __FILE__, __LINE__, #cond); \
+        if (!ok_) ++failures;                                                        \
+    } while (0)
+
+template <class E, class F>
+bool throws(F&& f) {
+    try {
+        f();
+    } catch (const E&) {
+        return true;
+    } catch (...) {
+        return false;
+    }
+    return false;
+}
+
+// splitmix64 random +-1 system (io.hpp:33-44, 92-104)
+static esp::ParticleSystem random_system(std::size_t N, esp::Vec3 box, std::uint64_t seed) {
+    esp::ParticleSystem s;
+    s.box = box;
+    std::uint64_t st = seed;
+    auto uni = [&st] {
+        st += 0x9E3779B97F4A7C15ull;
+        std::uint64_t z = st;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        return static_cast<double>((z ^ (z >> 31)) >> 11) * 0x1.0p-53;
+    };
+    for (std::size_t i = 0; i < N; ++i) {
+        esp::Vec3 p;
+        for (int d = 0; d < 3; ++d) p[d] = box[d] * uni();
+        s.pos.push_back(p);
+        s.q.push_back(i % 2 == 0 ? 1.0 : -1.0);
+    }
+    return s;
+}
+
+int main() {
+    const esp::Vec3 box{10.0, 10.0, 10.0};
+
+    // parameter rows (test_ewald.cpp:26-43)
+    {
+        const double eps[5] = {1e-3, 5e-4, 1e-4, 5e-5, 1e-5};
+        const int nf[5] = {32, 36, 40, 48, 48}, P[5] = {5, 5, 6, 7, 8};
+        for (int r = 0; r < 5; ++r) {
+            esp::EwaldPlan p = esp::build_plan(box, esp::SplitFamily::pswf, eps[r], 1.0);
+            CHECK(p.nf[0] == nf[r] && p.nf[1] == nf[r] && p.nf[2] == nf[r] && p.P == P[r]);
+            CHECK(p.stats.E_A <= eps[r]);
+        }
+    }
+    // input rejection (test_ewald.cpp:151-190)
+    CHECK(throws<std::invalid_argument>([&] { esp::build_plan(box, esp::SplitFamily::pswf, 1e-6, 1.0); }));
+    CHECK(throws<std::invalid_argument>([&] { esp::build_plan(box, esp::SplitFamily::pswf, 1e-4, 5.0); }));
+    {
+        esp::Overrides odd;
+        odd.nf = 15;
+        CHECK(throws<std::invalid_argument>([&] { esp::build_plan(box, esp::SplitFamily::pswf, 1e-4, 1.0, odd); }));
+        esp::Overrides low;
+        low.nf = 20;
+        CHECK(throws<esp::NumericalError>([&] { esp::build_plan(box, esp::SplitFamily::pswf, 1e-3, 1.0, low); }));
+    }
+    // isolated pair (test_ewald.cpp:192-227)
+    {
+        esp::EwaldPlan plan = esp::build_plan(box, esp::SplitFamily::pswf, 1e-3, 1.0);
+        esp::ParticleSystem s;
+        s.box = box;
+        s.q = {1.0, -1.0};
+        s.pos = {{1.0, 1.0, 1.0}, {1.3, 1.0, 1.0}};
+        esp::PartialField f = esp::local_sum(plan, s);
+        CHECK(f.u[0] == -f.u[1] && f.u[1] > 0.0);
+        CHECK(f.F[0][0] == -f.F[1][0] && f.F[0][0] > 0.0 && f.F[0][1] == 0.0 && f.F[0][2] == 0.0);
+        s.pos = {{1.0, 1.0, 1.0}, {3.5, 1.0, 1.0}};
+        f = esp::local_sum(plan, s);
+        CHECK(f.u[0] == 0.0 && f.u[1] == 0.0 && f.F[0][0] == 0.0);
+        s.pos = {{0.1, 5.0, 5.0}, {9.8, 5.0, 5.0}};
+        f = esp::local_sum(plan, s);
+        CHECK(f.u[0] != 0.0 && f.F[0][0] < 0.0 && f.F[0][0] == -f.F[1][0]);
+    }
+    // contracts (test_ewald.cpp:364-381)
+    {
+        esp::EwaldPlan plan = esp::build_plan(box, esp::SplitFamily::pswf, 1e-3, 1.0);
+        esp::ParticleSystem wrong = random_system(8, {8.0, 8.0, 8.0}, 1);
+        CHECK(throws<std::invalid_argument>([&] { esp::evaluate(plan, wrong); }));
+        esp::ParticleSystem charged = random_system(8, box, 1);
+        charged.q[0] = 2.0;
+        CHECK(throws<esp::NumericalError>([&] { esp::evaluate(plan, charged); }));
+        esp::EnergyForces ef = esp::evaluate(plan, random_system(8, box, 1));
+        CHECK(ef.timings.size() == 6);
+    }
+    // translation invariance (test_ewald.cpp:383-409)
+    {
+        const double eps = 1e-4;
+        esp::EwaldPlan plan = esp::build_plan(box, esp::SplitFamily::pswf, eps, 1.0);
+        esp::ParticleSystem s = random_system(64, box, 21);
+        esp::EnergyForces a = esp::evaluate(plan, s);
+        esp::ParticleSystem t = s;
+        for (auto& r : t.pos) {
+            r[0] += 0.37;
+            r[1] += -1.2;
+            r[2] += 2.05;
+        }
+        esp::EnergyForces b = esp::evaluate(plan, t);
+        double fs = 0, us = 0, df = 0, du = 0;
+        for (std::size_t i = 0; i < s.size(); ++i) {
+            us = std::max(us, std::fabs(a.u[i]));
+            du = std::max(du, std::fabs(a.u[i] - b.u[i]));
+            for (int d = 0; d < 3; ++d) {
+                fs = std::max(fs, std::fabs(a.F[i][d]));
+                df = std::max(df, std::fabs(a.F[i][d] - b.F[i][d]));
+            }
+        }
+        CHECK(du <= 10 * eps * us && df <= 10 * eps * fs);
+        CHECK(std::fabs(a.energy - b.energy) <= 10 * eps * std::fabs(a.energy));
+    }
+    // charge scaling (test_ewald.cpp:411-438), bitwise gate -> 1e-14
+    {
+        esp::EwaldPlan plan = esp::build_plan(box, esp::SplitFamily::pswf, 1e-3, 1.0);
+        esp::ParticleSystem s = random_system(32, box, 29);
+        esp::EnergyForces a = esp::evaluate(plan, s);
+        for (auto& q : s.q) q *= 2.0;
+        esp::EnergyForces b = esp::evaluate(plan, s);
+        double worst = 0, scale = 0;
+        for (std::size_t i = 0; i < s.size(); ++i) {
+            scale = std::max(scale, std::fabs(a.u[i]));
+            worst = std::max(worst, std::fabs(b.u[i] - 2.0 * a.u[i]));
+        }
+        CHECK(worst <= 1e-14 * 2.0 * scale);
+        CHECK(std::fabs(b.energy - 4.0 * a.energy) <= 1e-13 * std::fabs(4.0 * a.energy));
+    }
+    // ik vs ad (test_ewald.cpp:340-351)
+    {
+        esp::ParticleSystem s = random_system(100, box, 23);
+        esp::Overrides ik, ad;
+        ad.force_method = esp::ForceMethod::ad;
+        esp::EnergyForces a = esp::evaluate(esp::build_plan(box, esp::SplitFamily::pswf, 1e-3, 1.0, ik), s);
+        esp::EnergyForces b = esp::evaluate(esp::build_plan(box, esp::SplitFamily::pswf, 1e-3, 1.0, ad), s);
+        CHECK(esp::relative_force_error(b.F, a.F) <= 10 * 1e-3);
+        CHECK(std::fabs(a.energy - b.energy) <= 1e-13 * std::fabs(a.energy));
+    }
+    // net force (test_ewald.cpp:463-476)
+    {
+        esp::EwaldPlan plan = esp::build_plan(box, esp::SplitFamily::pswf, 1e-4, 1.0);
+        esp::EnergyForces ef = esp::evaluate(plan, random_system(128, box, 41));
+        for (int d = 0; d < 3; ++d) {
+            double net = 0, mag = 0;
+            for (auto& F : ef.F) {
+                net += F[d];
+                mag += std::fabs(F[d]);
+            }
+            CHECK(std::fabs(net) <= 1e-8 * mag);
+        }
+    }
+    // Madelung (test_ewald.cpp:493-508)
+    {
+        esp::ParticleSystem s;
+        s.box = {2.0, 2.0, 2.0};
+        for (int i = 0; i < 2; ++i)
+            for (int j = 0; j < 2; ++j)
+                for (int k = 0; k < 2; ++k) {
+                    s.pos.push_back({1.0 * i, 1.0 * j, 1.0 * k});
+                    s.q.push_back((i + j + k) % 2 == 0 ? 1.0 : -1.0);
+                }
+        esp::EnergyForces ef = esp::evaluate(esp::build_plan(s.box, esp::SplitFamily::pswf, 1e-5, 0.5), s);
+        const double expect = -1.7475645946331822 / M_PI;
+        CHECK(std::fabs(ef.energy - expect) <= 1e-4 * std::fabs(expect));
+        double fs = 0;
+        for (auto& F : ef.F)
+            for (double c : F) fs = std::max(fs, std::fabs(c));
+        CHECK(fs <= 1e-6);
+    }
+    // plan metadata (test_ewald.cpp:510-516)
+    {
+        esp::EwaldPlan plan = esp::build_plan(box, esp::SplitFamily::pswf, 1e-4, 1.0);
+        CHECK(plan.total_modes() == 40ull * 40ull * 40ull);
+        CHECK(std::fabs(plan.avg_neighbors(512) - 4.0 * M_PI / 3.0 * 512.0 / 1000.0) <= 1e-12);
+        CHECK(plan.influence()[0] == 0.0);
+    }
+    std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "PASSED", failures);
+    return failures ? 1 : 0;
+}
