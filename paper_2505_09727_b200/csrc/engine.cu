@@ -243,11 +243,13 @@ struct PairArgs {
     double box[3];
 };
 
+// d = (r_j - r_i) + image shift, in that order: the reference's min-image
+// displacement (ewald.hpp:436-443) bit for bit, hence F_ij = -F_ji exactly.
 template <int ND>
-__device__ __forceinline__ void pair_eval(const PairConsts& k, double4 pj, double xi, double yi,
-                                          double zi, double& u, double& fx, double& fy,
-                                          double& fz, int& npair) {
-    const double dx = pj.x - xi, dy = pj.y - yi, dz = pj.z - zi;
+__device__ __forceinline__ void pair_eval(const PairConsts& k, double4 pj, double sx, double sy,
+                                          double sz, double xi, double yi, double zi, double& u,
+                                          double& fx, double& fy, double& fz, int& npair) {
+    const double dx = (pj.x - xi) + sx, dy = (pj.y - yi) + sy, dz = (pj.z - zi) + sz;
     const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
     if (r2 < k.rc2 && r2 > 0.0) {
         ++npair;
@@ -387,23 +389,19 @@ __global__ void __launch_bounds__(128) k_pair(PairArgs a, const __grid_constant_
                     __syncwarp();
                     qw[lane] = extra;
                     qn -= 32;
-                    double4 pj = a.xyzq[code & 0x7ffffff];
+                    const double4 pj = a.xyzq[code & 0x7ffffff];
                     const int t = static_cast<unsigned>(code) >> 27;
-                    pj.x += nshift[t][0];
-                    pj.y += nshift[t][1];
-                    pj.z += nshift[t][2];
-                    pair_eval<ND>(k, pj, pi.x, pi.y, pi.z, u, fx, fy, fz, npair);
+                    pair_eval<ND>(k, pj, nshift[t][0], nshift[t][1], nshift[t][2], pi.x, pi.y,
+                                  pi.z, u, fx, fy, fz, npair);
                 }
             }
             __syncwarp();
             if (lane < qn) {
                 const int code = qw[lane];
-                double4 pj = a.xyzq[code & 0x7ffffff];
+                const double4 pj = a.xyzq[code & 0x7ffffff];
                 const int t = static_cast<unsigned>(code) >> 27;
-                pj.x += nshift[t][0];
-                pj.y += nshift[t][1];
-                pj.z += nshift[t][2];
-                pair_eval<ND>(k, pj, pi.x, pi.y, pi.z, u, fx, fy, fz, npair);
+                pair_eval<ND>(k, pj, nshift[t][0], nshift[t][1], nshift[t][2], pi.x, pi.y, pi.z,
+                              u, fx, fy, fz, npair);
             }
             __syncwarp();
 #pragma unroll
@@ -447,15 +445,12 @@ __global__ void __launch_bounds__(128) k_pair_allpairs(long N, const double4* __
     int npair = 0;
     for (long j = 0; j < N; ++j) {
         if (j == i) continue;
-        double4 pj = xyzq[j];
-        double dx = pj.x - pi.x, dy = pj.y - pi.y, dz = pj.z - pi.z;
-        dx -= bx * round(dx / bx);
-        dy -= by * round(dy / by);
-        dz -= bz * round(dz / bz);
-        pj.x = pi.x + dx;
-        pj.y = pi.y + dy;
-        pj.z = pi.z + dz;
-        pair_eval<ND>(k, pj, pi.x, pi.y, pi.z, u, fx, fy, fz, npair);
+        const double4 pj = xyzq[j];
+        // ewald.hpp:436-443: d = (r_j - r_i) - L round((r_j - r_i)/L)
+        const double sx = -bx * round((pj.x - pi.x) / bx);
+        const double sy = -by * round((pj.y - pi.y) / by);
+        const double sz = -bz * round((pj.z - pi.z) / bz);
+        pair_eval<ND>(k, pj, sx, sy, sz, pi.x, pi.y, pi.z, u, fx, fy, fz, npair);
     }
     loc[i] = make_double4(u, -pi.w * fx, -pi.w * fy, -pi.w * fz);
     if (npairs) atomicAdd(npairs, static_cast<unsigned long long>(npair));
