@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -167,7 +168,8 @@ __global__ void __launch_bounds__(256) k_fold_bin(BinArgs a) {
         double z = fold1(a.pos[3 * i + 2], a.box[2]);
         qi = a.q[i];
         a.tmp[i] = make_double4(x, y, z, qi);
-        // pair cell (ewald.hpp:479-482)
+        // fine pair cell (the reference's coarse cell ewald.hpp:479-482 split
+        // kFS x kFS x kFZ); nc = fine cells per dim here
         int cx = clampi(static_cast<int>(x / a.cw[0]), 0, a.nc[0] - 1);
         int cy = clampi(static_cast<int>(y / a.cw[1]), 0, a.nc[1] - 1);
         int cz = clampi(static_cast<int>(z / a.cw[2]), 0, a.nc[2] - 1);
@@ -236,10 +238,12 @@ struct PairArgs {
     const int* start;     // ncell + 1
     double4* loc;         // original order: (u_l, F_l)
     unsigned long long* npairs;  // ordered in-range pairs evaluated (r < r_c, r > 0)
-    int cap;                     // candidates staged per chunk (multiple of 32)
+    int cap;                     // candidates staged per chunk
     int nsplit;                  // CTAs per cell (blockIdx.y) sharing its targets
-    int nc[3];
-    double cw[3];
+    int nc[3];                   // coarse cells per dim
+    int F[3];                    // fine cells per dim (nc*kFS, nc*kFS, nc*kFZ)
+    double cw[3];                // coarse cell edge
+    double fw[3];                // fine cell edge
     double box[3];
 };
 
@@ -282,125 +286,238 @@ __device__ __forceinline__ void pair_eval(const PairConsts& k, double4 pj, doubl
     }
 }
 
-// One CTA per pair cell, one warp per target atom i (round-robin over the
-// cell's atoms).  The 27 neighbour cells are staged once per CTA in shared
-// memory as fp32 coordinates relative to the cell origin plus a 32-bit code
-// (source index | neighbour slot << 27).  For its i, a warp screens 32
-// candidates per step in fp32 (lane = candidate), compacts the survivors
-// with a ballot into a per-warp queue, and evaluates full 32-lane rounds in
-// fp64 (exact min-image geometry from the global copy + the slot's periodic
-// shift).  Per-i sums are warp-reduced once.  Candidate sets larger than the
-// staging capacity are processed in chunks (per-i partial sums accumulated
-// into loc by the owning lane).
+// Fine cell-list geometry of K4: every coarse cell (edge cw >= r_c, the
+// reference's cell, ewald.hpp:431-434) is split into kFS x kFS columns in
+// (x, y) and kFZ slices in z; atoms are sorted by fine cell with z fastest, so
+// a fine column's slices are contiguous in memory.
+constexpr int kFS = 2;
+constexpr int kFZ = 4;
+constexpr int kNCol = (3 * kFS) * (3 * kFS);  // 36 neighbour columns
+constexpr int kNSl = 3 * kFZ;                 // 12 slices per neighbour column
+constexpr int kNEnt = kNCol * kNSl;           // 432 (column, slice) entries
+
+// One CTA per coarse cell (x nsplit for small systems), one warp per target
+// atom i.  The CTA stages its 3x3x3-coarse-cell neighbourhood in shared
+// memory, ordered by (column, slice), as fp32 coordinates relative to the
+// cell origin plus a 32-bit code (source index | periodic-image slot << 27).
+// For its i, a warp keeps only the columns whose xy distance is below r_c
+// and, in each, only the z slices the sphere reaches (~2.2-2.6 candidates per
+// in-range pair instead of 6.4-9.5 for the 27-cell stencil).  Lanes walk
+// contiguous pieces of that candidate stream, screen in fp32, compact the
+// survivors with a ballot into a per-warp queue and evaluate full 32-lane
+// rounds in fp64.  Per-i sums are warp-reduced once.  Neighbourhoods larger
+// than the staging capacity are processed in chunks.
 template <int ND>
-__global__ void __launch_bounds__(128) k_pair(PairArgs a, const __grid_constant__ PairConsts k) {
+__global__ void __launch_bounds__(128, 7) k_pair(PairArgs a, const __grid_constant__ PairConsts k) {
     extern __shared__ __align__(16) unsigned char smem[];
-    float4* cand = reinterpret_cast<float4*>(smem);                 // a.cap entries
-    int* qall = reinterpret_cast<int*>(cand + a.cap);               // 64 per warp
-    __shared__ int nstart[27], npre[28];
-    __shared__ double nshift[27][3];
+    float4* cand = reinterpret_cast<float4*>(smem);   // a.cap + 1 (sentinel)
+    int* qall = reinterpret_cast<int*>(cand + a.cap + 1); // 64 per warp
+    int* cball = qall + 4 * 64;                       // column begin, 36 per warp
+    unsigned short* lall = reinterpret_cast<unsigned short*>(cball + 4 * kNCol);  // a.cap+32 per warp
+    __shared__ int ent_src[kNEnt], ent_off[kNEnt + 1];
+    __shared__ unsigned char ent_slot[kNEnt];
+    __shared__ double shiftv[27][3];
+    __shared__ int isrc[kFS * kFS], ipre[kFS * kFS + 1];
 
     const int nw = blockDim.x >> 5;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int* qw = qall + warp * 64;
+    int* cb = cball + warp * kNCol;
+    unsigned short* lw = lall + warp * (a.cap + 32);
     const unsigned lt_mask = (1u << lane) - 1u;
 
     const int cell = blockIdx.x;
     const int cz = cell % a.nc[2];
     const int cy = (cell / a.nc[2]) % a.nc[1];
     const int cx = cell / (a.nc[1] * a.nc[2]);
-    const int ib = a.start[cell], ie = a.start[cell + 1];
-    if (ib == ie) return;
     const double ox = cx * a.cw[0], oy = cy * a.cw[1], oz = cz * a.cw[2];
 
-    if (threadIdx.x < 32) {
-        const int t = lane;
-        int cnt = 0;
-        if (t < 27) {
-            const int dx = t / 9 - 1, dy = (t / 3) % 3 - 1, dz = t % 3 - 1;
-            int nx = cx + dx, ny = cy + dy, nz = cz + dz;
-            nshift[t][0] = nx < 0 ? -a.box[0] : (nx >= a.nc[0] ? a.box[0] : 0.0);
-            nshift[t][1] = ny < 0 ? -a.box[1] : (ny >= a.nc[1] ? a.box[1] : 0.0);
-            nshift[t][2] = nz < 0 ? -a.box[2] : (nz >= a.nc[2] ? a.box[2] : 0.0);
-            nx = (nx + a.nc[0]) % a.nc[0];
-            ny = (ny + a.nc[1]) % a.nc[1];
-            nz = (nz + a.nc[2]) % a.nc[2];
-            const int c = (nx * a.nc[1] + ny) * a.nc[2] + nz;
-            nstart[t] = a.start[c];
-            cnt = a.start[c + 1] - a.start[c];
+    if (threadIdx.x < 27) {
+        const int t = threadIdx.x;
+        shiftv[t][0] = (t / 9 - 1) * a.box[0];
+        shiftv[t][1] = ((t / 3) % 3 - 1) * a.box[1];
+        shiftv[t][2] = (t % 3 - 1) * a.box[2];
+    }
+    for (int e = threadIdx.x; e < kNEnt; e += blockDim.x) {
+        const int col = e / kNSl, sl = e - col * kNSl;
+        const int ca = col / (3 * kFS), cbb = col - ca * (3 * kFS);
+        int fx = cx * kFS - kFS + ca, fy = cy * kFS - kFS + cbb, fz = cz * kFZ - kFZ + sl;
+        const int ix = fx < 0 ? 0 : (fx >= a.F[0] ? 2 : 1);
+        const int iy = fy < 0 ? 0 : (fy >= a.F[1] ? 2 : 1);
+        const int iz = fz < 0 ? 0 : (fz >= a.F[2] ? 2 : 1);
+        fx += (1 - ix) * a.F[0];
+        fy += (1 - iy) * a.F[1];
+        fz += (1 - iz) * a.F[2];
+        const int f = (fx * a.F[1] + fy) * a.F[2] + fz;
+        const int s0 = a.start[f];
+        ent_src[e] = s0;
+        ent_off[e + 1] = a.start[f + 1] - s0;  // count, scanned below
+        ent_slot[e] = static_cast<unsigned char>((ix * 3 + iy) * 3 + iz);
+    }
+    __syncthreads();
+    if (warp == 0) {
+        // exclusive scan of the 432 counts: 14 per lane, then a warp scan
+        constexpr int per = (kNEnt + 31) / 32;
+        int loc[per];
+        int sum = 0;
+#pragma unroll
+        for (int j = 0; j < per; ++j) {
+            const int e = lane * per + j;
+            loc[j] = e < kNEnt ? ent_off[e + 1] : 0;
+            sum += loc[j];
         }
-        // exclusive warp scan of the 27 counts
-        int incl = cnt;
+        int incl = sum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int v = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += v;
         }
-        if (t < 27) npre[t] = incl - cnt;
-        if (t == 26) npre[27] = incl;
+        int run = incl - sum;
+#pragma unroll
+        for (int j = 0; j < per; ++j) {
+            const int e = lane * per + j;
+            if (e < kNEnt) ent_off[e] = run;
+            run += loc[j];
+        }
+        if (lane == 31) ent_off[kNEnt] = incl;
     }
     __syncthreads();
-    const int total = npre[27];
+    if (threadIdx.x == 0) {
+        // this cell's own atoms: inner columns, inner slices (never wrapped)
+        int acc = 0;
+        for (int c = 0; c < kFS * kFS; ++c) {
+            const int col = (kFS + c / kFS) * (3 * kFS) + (kFS + c % kFS);
+            const int e0 = col * kNSl + kFZ, e1 = col * kNSl + 2 * kFZ;
+            isrc[c] = ent_src[e0];
+            ipre[c] = acc;
+            acc += ent_off[e1] - ent_off[e0];
+        }
+        ipre[kFS * kFS] = acc;
+    }
+    __syncthreads();
+    const int total = ent_off[kNEnt];
+    const int ni = ipre[kFS * kFS];
+    if (ni == 0) return;
+    const float R2 = k.rc2_test;
+    const float fwx = static_cast<float>(a.fw[0]), fwy = static_cast<float>(a.fw[1]);
+    const float fwz = static_cast<float>(a.fw[2]);
 
     for (int base = 0; base < total; base += a.cap) {
         const int nk = min(a.cap, total - base);
-        const int nk32 = (nk + 31) & ~31;
         if (base > 0) __syncthreads();
-        {
-            int t = 0;
-            for (int c = threadIdx.x; c < nk32; c += blockDim.x) {
-                const int g = base + c;
-                if (c < nk) {
-                    while (npre[t + 1] <= g) ++t;
-                    const int src = nstart[t] + (g - npre[t]);
-                    const double4 v = a.xyzq[src];
-                    cand[c] = make_float4(static_cast<float>(v.x + nshift[t][0] - ox),
-                                          static_cast<float>(v.y + nshift[t][1] - oy),
-                                          static_cast<float>(v.z + nshift[t][2] - oz),
-                                          __int_as_float(src | (t << 27)));
-                } else {
-                    // padding sentinel: never within r_c
-                    cand[c] = make_float4(1e30f, 1e30f, 1e30f, __int_as_float(0));
-                }
+        for (int c = threadIdx.x; c < nk; c += blockDim.x) {
+            const int g = base + c;
+            int lo = 0, hi = kNEnt - 1;  // last entry with ent_off[e] <= g
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (ent_off[mid] <= g) lo = mid;
+                else hi = mid - 1;
             }
+            const int src = ent_src[lo] + (g - ent_off[lo]);
+            const int sl = ent_slot[lo];
+            const double4 v = a.xyzq[src];
+            cand[c] = make_float4(static_cast<float>(v.x + shiftv[sl][0] - ox),
+                                  static_cast<float>(v.y + shiftv[sl][1] - oy),
+                                  static_cast<float>(v.z + shiftv[sl][2] - oz),
+                                  __int_as_float(src | (sl << 27)));
         }
+        if (threadIdx.x == 0) cand[a.cap] = make_float4(1e30f, 1e30f, 1e30f, __int_as_float(0));
         __syncthreads();
-        // CTA part p handles targets ib + p*nw + warp, stepping by nsplit*nw
         const int stride = nw * a.nsplit;
-        for (int i = ib + blockIdx.y * nw + warp; i < ie; i += stride) {
+        for (int ii = blockIdx.y * nw + warp; ii < ni; ii += stride) {
+            const int ic = (ii >= ipre[1]) + (ii >= ipre[2]) + (ii >= ipre[3]);
+            const int i = isrc[ic] + (ii - ipre[ic]);
             const double4 pi = a.xyzq[i];
             const float xf = static_cast<float>(pi.x - ox);
             const float yf = static_cast<float>(pi.y - oy);
             const float zf = static_cast<float>(pi.z - oz);
+            // candidate ranges per neighbour column (lanes 0..31, then 32..35)
+            int cnt0 = 0, cnt1 = 0;
+#pragma unroll
+            for (int pass = 0; pass < 2; ++pass) {
+                const int col = lane + 32 * pass;
+                int beg = 0, cnt = 0;
+                if (col < kNCol) {
+                    const int ca = col / (3 * kFS), cbb = col - ca * (3 * kFS);
+                    const float x0 = (ca - kFS) * fwx, y0 = (cbb - kFS) * fwy;
+                    const float gx = fmaxf(0.f, fmaxf(x0 - xf, xf - (x0 + fwx)));
+                    const float gy = fmaxf(0.f, fmaxf(y0 - yf, yf - (y0 + fwy)));
+                    const float g2 = fmaf(gx, gx, gy * gy);
+                    if (g2 < R2) {
+                        const float zm = sqrtf(R2 - g2);
+                        int klo = static_cast<int>(floorf((zf - zm) / fwz)) + kFZ;
+                        int khi = static_cast<int>(floorf((zf + zm) / fwz)) + kFZ;
+                        klo = max(0, min(kNSl - 1, klo));
+                        khi = max(0, min(kNSl - 1, khi));
+                        int lo = ent_off[col * kNSl + klo], hi = ent_off[col * kNSl + khi + 1];
+                        lo = max(lo, base);
+                        hi = min(hi, base + nk);
+                        if (hi > lo) {
+                            beg = lo - base;
+                            cnt = hi - lo;
+                        }
+                    }
+                    cb[col] = beg;
+                }
+                if (pass == 0) cnt0 = cnt;
+                else cnt1 = cnt;
+            }
+            int inc0 = cnt0, inc1 = cnt1;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v0 = __shfl_up_sync(0xffffffffu, inc0, o);
+                const int v1 = __shfl_up_sync(0xffffffffu, inc1, o);
+                if (lane >= o) {
+                    inc0 += v0;
+                    inc1 += v1;
+                }
+            }
+            const int tot0 = __shfl_sync(0xffffffffu, inc0, 31);
+            const int T = __shfl_sync(0xffffffffu, tot0 + inc1, kNCol - 33);
+            // materialise this i's candidate list (staged indices), padded to
+            // a multiple of 32 with the far-away sentinel a.cap
+            {
+                const int b0 = cb[lane], p0 = inc0 - cnt0;
+#pragma unroll 4
+                for (int j = 0; j < cnt0; ++j) lw[p0 + j] = static_cast<unsigned short>(b0 + j);
+                if (lane + 32 < kNCol) {
+                    const int b1 = cb[lane + 32], p1 = tot0 + inc1 - cnt1;
+#pragma unroll 4
+                    for (int j = 0; j < cnt1; ++j) lw[p1 + j] = static_cast<unsigned short>(b1 + j);
+                }
+            }
+            const int T32 = (T + 31) & ~31;
+            if (T + lane < T32) lw[T + lane] = static_cast<unsigned short>(a.cap);
+            __syncwarp();
             double u = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
             int npair = 0, qn = 0;
-#pragma unroll 2
-            for (int kb = lane; kb < nk32; kb += 32) {
-                const float4 c4 = cand[kb];
+            for (int kb = lane; kb < T32; kb += 32) {
+                const float4 c4 = cand[lw[kb]];
                 const float dx = c4.x - xf, dy = c4.y - yf, dz = c4.z - zf;
-                const bool in = fmaf(dz, dz, fmaf(dy, dy, dx * dx)) < k.rc2_test;
+                const bool in = fmaf(dz, dz, fmaf(dy, dy, dx * dx)) < R2;
+                const int code = __float_as_int(c4.w);
                 const unsigned m = __ballot_sync(0xffffffffu, in);
-                if (in) qw[qn + __popc(m & lt_mask)] = __float_as_int(c4.w);
+                if (in) qw[qn + __popc(m & lt_mask)] = code;
                 qn += __popc(m);
                 if (qn >= 32) {
                     __syncwarp();
-                    const int code = qw[lane];
+                    const int cd = qw[lane];
                     const int extra = qw[32 + lane];
                     __syncwarp();
                     qw[lane] = extra;
                     qn -= 32;
-                    const double4 pj = a.xyzq[code & 0x7ffffff];
-                    const int t = static_cast<unsigned>(code) >> 27;
-                    pair_eval<ND>(k, pj, nshift[t][0], nshift[t][1], nshift[t][2], pi.x, pi.y,
+                    const double4 pj = a.xyzq[cd & 0x7ffffff];
+                    const int t = static_cast<unsigned>(cd) >> 27;
+                    pair_eval<ND>(k, pj, shiftv[t][0], shiftv[t][1], shiftv[t][2], pi.x, pi.y,
                                   pi.z, u, fx, fy, fz, npair);
                 }
             }
             __syncwarp();
             if (lane < qn) {
-                const int code = qw[lane];
-                const double4 pj = a.xyzq[code & 0x7ffffff];
-                const int t = static_cast<unsigned>(code) >> 27;
-                pair_eval<ND>(k, pj, nshift[t][0], nshift[t][1], nshift[t][2], pi.x, pi.y, pi.z,
+                const int cd = qw[lane];
+                const double4 pj = a.xyzq[cd & 0x7ffffff];
+                const int t = static_cast<unsigned>(cd) >> 27;
+                pair_eval<ND>(k, pj, shiftv[t][0], shiftv[t][1], shiftv[t][2], pi.x, pi.y, pi.z,
                               u, fx, fy, fz, npair);
             }
             __syncwarp();
@@ -881,7 +998,7 @@ PairConsts make_pair_consts(const Plan& p, int& nd) {
     k.rc2_test = static_cast<float>(k.rc2 * (1.0 + 2e-4));
     const int n = static_cast<int>(std::max(p.pair_G.size(), p.pair_H.size()));
     if (n > kMaxPoly) throw NumericalError("pair kernel polynomial too long");
-    nd = n <= 20 ? 20 : (n <= 28 ? 28 : kMaxPoly);
+    nd = n <= 17 ? 17 : n <= 18 ? 18 : n <= 19 ? 19 : n <= 20 ? 20 : n <= 28 ? 28 : kMaxPoly;
     for (int i = 0; i < kMaxPoly; ++i) {
         k.G[i] = i < static_cast<int>(p.pair_G.size()) ? p.pair_G[i] : 0.0;
         k.H[i] = i < static_cast<int>(p.pair_H.size()) ? p.pair_H[i] : 0.0;
@@ -901,6 +1018,9 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
     for (int d = 0; d < 3; ++d) nc_[d] = std::max(1, static_cast<int>(std::floor(p.box[d] / p.r_c)));
     cells_ok_ = nc_[0] >= 3 && nc_[1] >= 3 && nc_[2] >= 3;
     ncell_ = nc_[0] * nc_[1] * nc_[2];
+    F_ = {nc_[0] * kFS, nc_[1] * kFS, nc_[2] * kFZ};
+    ncellF_ = static_cast<long>(F_[0]) * F_[1] * F_[2];
+    if (ncellF_ >= (1L << 30)) throw InvalidArgument("cell list too fine for this box / r_c");
     // spread bins: the largest S in {8, 6, 4} that still gives >= 4 CTAs per SM
     S_ = 4;
     for (int cand : {8, 6}) {
@@ -939,12 +1059,13 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
     dalloc(d_xi_, xi.size());
     CK(cudaMemcpy(d_xi_, xi.data(), sizeof(double) * xi.size(), cudaMemcpyHostToDevice));
 
-    dalloc(d_countA_, ncell_ + 1);
-    dalloc(d_startA_, ncell_ + 1);
+    dalloc(d_countA_, ncellF_ + 1);
+    dalloc(d_startA_, ncellF_ + 1);
     dalloc(d_countB_, nbin_ + 1);
     dalloc(d_startB_, nbin_ + 1);
     size_t t1 = 0, t2 = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, t1, d_countA_, d_startA_, ncell_ + 1));
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, t1, d_countA_, d_startA_,
+                                     static_cast<int>(ncellF_ + 1)));
     CK(cub::DeviceScan::ExclusiveSum(nullptr, t2, d_countB_, d_startB_, nbin_ + 1));
     scan_tmp_bytes_ = std::max(t1, t2);
     CK(cudaMalloc(&d_scan_tmp_, std::max<size_t>(scan_tmp_bytes_, 16)));
@@ -983,8 +1104,10 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
     CF(cufftSetStream(fwd_, aux_));
     CF(cufftSetStream(inv_, aux_));
 
-    // pair kernel occupancy: warps per CTA from the mean cell population
+    // pair kernel staging capacity (candidates per chunk); ESP_PAIR_CAP overrides
     pair_warps_ = 4;
+    pair_cap_ = 1536;
+    if (const char* e = std::getenv("ESP_PAIR_CAP")) pair_cap_ = std::max(256, std::min(4096, std::atoi(e)));
 }
 
 Engine::~Engine() {
@@ -1044,7 +1167,7 @@ void Engine::ensure_capacity(long N) {
 void Engine::prepare(long N, const double* pos, const double* q, double* qsum_dev,
                      cudaStream_t s) {
     const Plan& p = plan_;
-    CK(cudaMemsetAsync(d_countA_, 0, sizeof(int) * (ncell_ + 1), s));
+    CK(cudaMemsetAsync(d_countA_, 0, sizeof(int) * (ncellF_ + 1), s));
     CK(cudaMemsetAsync(d_npairs_, 0, sizeof(unsigned long long), s));
     CK(cudaMemsetAsync(d_countB_, 0, sizeof(int) * (nbin_ + 1), s));
     if (qsum_dev) CK(cudaMemsetAsync(qsum_dev, 0, sizeof(double) * 2, s));
@@ -1054,8 +1177,8 @@ void Engine::prepare(long N, const double* pos, const double* q, double* qsum_de
     a.q = q;
     for (int d = 0; d < 3; ++d) {
         a.box[d] = p.box[d];
-        a.nc[d] = nc_[d];
-        a.cw[d] = p.box[d] / nc_[d];
+        a.nc[d] = F_[d];               // fine pair cells
+        a.cw[d] = p.box[d] / F_[d];
         a.nb[d] = nb_[d];
         a.h[d] = p.h[d];
     }
@@ -1074,7 +1197,8 @@ void Engine::prepare(long N, const double* pos, const double* q, double* qsum_de
         ++launches_;
     }
     size_t tb = scan_tmp_bytes_;
-    CK(cub::DeviceScan::ExclusiveSum(d_scan_tmp_, tb, d_countA_, d_startA_, ncell_ + 1, s));
+    CK(cub::DeviceScan::ExclusiveSum(d_scan_tmp_, tb, d_countA_, d_startA_,
+                                     static_cast<int>(ncellF_ + 1), s));
     tb = scan_tmp_bytes_;
     CK(cub::DeviceScan::ExclusiveSum(d_scan_tmp_, tb, d_countB_, d_startB_, nbin_ + 1, s));
     launches_ += 2;
@@ -1113,12 +1237,14 @@ void Engine::run_pair(long N, cudaStream_t s) {
     a.npairs = d_npairs_;
     for (int d = 0; d < 3; ++d) {
         a.nc[d] = nc_[d];
+        a.F[d] = F_[d];
         a.cw[d] = p.box[d] / nc_[d];
+        a.fw[d] = p.box[d] / F_[d];
         a.box[d] = p.box[d];
     }
     const int nw = 4;
     pair_warps_ = nw;
-    a.cap = 2048;
+    a.cap = pair_cap_;
     // split crowded cells over several CTAs when there are too few cells to
     // fill the GPU (small systems such as cfg2: 216 cells of ~150 atoms)
     const double mean = static_cast<double>(N) / ncell_;
@@ -1128,15 +1254,21 @@ void Engine::run_pair(long N, cudaStream_t s) {
     nsplit = std::max(1, std::min(nsplit, static_cast<int>(std::ceil(mean / (2.0 * nw)))));
     a.nsplit = nsplit;
     if (N >= (1L << 27)) throw InvalidArgument("pair kernel: N must be < 2^27");
-    size_t sm = a.cap * sizeof(float4) + nw * 64 * sizeof(int);
+    size_t sm = (a.cap + 1) * sizeof(float4) + 4 * (64 + kNCol) * sizeof(int) +
+                4 * (a.cap + 32) * sizeof(unsigned short);
     auto go = [&](auto kern) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(sm)));
         kern<<<dim3(ncell_, nsplit), nw * 32, sm, s>>>(a, k);
     };
-    if (nd == 20) go(k_pair<20>);
-    else if (nd == 28) go(k_pair<28>);
-    else go(k_pair<kMaxPoly>);
+    switch (nd) {
+        case 17: go(k_pair<17>); break;
+        case 18: go(k_pair<18>); break;
+        case 19: go(k_pair<19>); break;
+        case 20: go(k_pair<20>); break;
+        case 28: go(k_pair<28>); break;
+        default: go(k_pair<kMaxPoly>); break;
+    }
     CK(cudaGetLastError());
     ++launches_;
 }

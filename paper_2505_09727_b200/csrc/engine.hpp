@@ -80,7 +80,9 @@ private:
     // geometry
     std::array<int, 3> nc_{};   // pair cells per dim
     bool cells_ok_ = false;     // nc >= 3 in every dim (ewald.hpp:431-434)
-    int ncell_ = 0;
+    int ncell_ = 0;             // coarse cells (CTAs of the pair kernel)
+    std::array<int, 3> F_{};    // fine cells per dim (sort key of the pair path)
+    long ncellF_ = 0;
     int S_ = 8;                 // spread bin edge in grid cells
     std::array<int, 3> nb_{};   // spread bins per dim
     int nbin_ = 0;
@@ -89,6 +91,7 @@ private:
     long M_ = 0, Mh_ = 0;       // real grid size, half spectrum size
     int nfields_ = 4;           // 4 for ik, 1 for ad
     int pair_warps_ = 4;
+    int pair_cap_ = 1536;
 
     // tables on device
     double* d_win_ = nullptr;        // 3 x 4P x 13 phi, then 3 x 4P x 13 dphi
