@@ -209,7 +209,7 @@ int esp_plan_get_info(const esp_plan* p, esp_plan_info* o) {
         o->self_coef = P.self_coef;
         o->n_split_coef = static_cast<int>(P.split.a.size());
         o->n_window_coef = static_cast<int>(P.window.a.size());
-        o->pair_poly_degree = static_cast<int>(P.pair_G.size()) - 1;
+        o->pair_poly_degree = static_cast<int>(P.pair_H.size()) - 1;
         o->pair_fit_err = P.pair_fit_err;
         o->device = p->device;
     });

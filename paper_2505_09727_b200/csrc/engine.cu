@@ -228,8 +228,7 @@ struct PairConsts {
     double inv4pi;
     float rc2_test;    // fp32 screening radius^2 (superset of the exact test)
     int pad;
-    double G[kMaxPoly];  // chi(y)   = sum G_k z^k,   z = 2y^2 - 1
-    double H[kMaxPoly];  // Psi(y)/y = sum H_k z^k
+    double H[kMaxPoly];  // Psi(y)/y = sum H_k z^k, z = 2y^2 - 1 (chi from dH/dz)
 };
 
 struct PairArgs {
@@ -268,12 +267,14 @@ __device__ __forceinline__ void pair_eval(const PairConsts& k, double4 pj, doubl
             rinv = fma(rinv, e, rinv);
         }
         const double z = fma(r2, k.two_irc2, -1.0);
-        double G = k.G[ND - 1], H = k.H[ND - 1];
+        // Psi(y) = y H(z); chi(y) = H + 2 (z+1) dH/dz, from one Horner pass
+        double H = k.H[ND - 1], dH = 0.0;
 #pragma unroll
         for (int m = ND - 2; m >= 0; --m) {
-            G = fma(G, z, k.G[m]);
+            dH = fma(dH, z, H);
             H = fma(H, z, k.H[m]);
         }
+        const double G = fma(2.0 * (z + 1.0), dH, H);
         const double y = r2 * rinv * k.irc;        // r / r_c
         const double w = k.inv4pi * rinv;          // 1 / (4 pi r)
         const double pot = (1.0 - y * H) * w;      // (1 - Psi(y)) / (4 pi r)
@@ -996,13 +997,13 @@ PairConsts make_pair_consts(const Plan& p, int& nd) {
     k.irc = 1.0 / p.r_c;
     k.inv4pi = 1.0 / (4.0 * kPi);
     k.rc2_test = static_cast<float>(k.rc2 * (1.0 + 2e-4));
-    const int n = static_cast<int>(std::max(p.pair_G.size(), p.pair_H.size()));
+    const int n = static_cast<int>(p.pair_H.size());
     if (n > kMaxPoly) throw NumericalError("pair kernel polynomial too long");
-    nd = n <= 17 ? 17 : n <= 18 ? 18 : n <= 19 ? 19 : n <= 20 ? 20 : n <= 28 ? 28 : kMaxPoly;
-    for (int i = 0; i < kMaxPoly; ++i) {
-        k.G[i] = i < static_cast<int>(p.pair_G.size()) ? p.pair_G[i] : 0.0;
-        k.H[i] = i < static_cast<int>(p.pair_H.size()) ? p.pair_H[i] : 0.0;
-    }
+    nd = n <= 14 ? 14 : n <= 15 ? 15 : n <= 16 ? 16 : n <= 17 ? 17 : n <= 18 ? 18 : n <= 20 ? 20
+                                                                                   : n <= 28 ? 28
+                                                                                             : kMaxPoly;
+    for (int i = 0; i < kMaxPoly; ++i)
+        k.H[i] = i < n ? p.pair_H[i] : 0.0;
     return k;
 }
 
@@ -1262,9 +1263,11 @@ void Engine::run_pair(long N, cudaStream_t s) {
         kern<<<dim3(ncell_, nsplit), nw * 32, sm, s>>>(a, k);
     };
     switch (nd) {
+        case 14: go(k_pair<14>); break;
+        case 15: go(k_pair<15>); break;
+        case 16: go(k_pair<16>); break;
         case 17: go(k_pair<17>); break;
         case 18: go(k_pair<18>); break;
-        case 19: go(k_pair<19>); break;
         case 20: go(k_pair<20>); break;
         case 28: go(k_pair<28>); break;
         default: go(k_pair<kMaxPoly>); break;

@@ -77,6 +77,35 @@ double even_legendre_integral(const std::vector<double>& a, double y) {
     return acc;
 }
 
+// Extended-precision versions for the pair-kernel fit (the polynomial and its
+// derivative must be accurate to ~1e-17 before rounding to double).
+long double even_legendre_ld(const std::vector<double>& a, long double x) {
+    long double pm = 1.0L, p = x, v = a[0];
+    const int top = 2 * (static_cast<int>(a.size()) - 1);
+    for (int n = 1; n < top; ++n) {
+        long double pn = ((2 * n + 1) * x * p - n * pm) / (n + 1);
+        pm = p;
+        p = pn;
+        if (((n + 1) & 1) == 0) v += a[(n + 1) / 2] * p;
+    }
+    return v;
+}
+
+long double even_legendre_integral_ld(const std::vector<double>& a, long double y) {
+    const int K = static_cast<int>(a.size()) - 1;
+    std::vector<long double> P(2 * K + 2);
+    P[0] = 1.0L;
+    P[1] = y;
+    for (int n = 1; n + 1 < static_cast<int>(P.size()); ++n)
+        P[n + 1] = ((2 * n + 1) * y * P[n] - n * P[n - 1]) / (n + 1);
+    long double acc = 0.0L;
+    for (int k = 0; k <= K; ++k) {
+        const int n = 2 * k;
+        acc += a[k] * (P[n + 1] - (n >= 1 ? P[n - 1] : 0.0L)) / (2.0L * n + 1.0L);
+    }
+    return acc;
+}
+
 // ----------------------------------------------------------------------------
 // Spherical Bessel j_0..j_nmax by Miller's downward recurrence
 // (restates numerics.hpp:174-203).
@@ -308,6 +337,32 @@ std::vector<double> fit_z_poly(const std::function<double(double)>& f, int deg) 
     for (int p = 0; p < n; ++p) {
         long double s = 0.0L;
         for (int j = 0; j < n; ++j) s += static_cast<long double>(cheb[j]) * T[j][p];
+        mono[p] = static_cast<double>(s);
+    }
+    return mono;
+}
+
+// Same fit with the samples, transform and basis change in long double.
+std::vector<double> fit_z_poly_ld(const std::function<long double(long double)>& f, int deg) {
+    const int n = deg + 1;
+    const long double pi = 3.141592653589793238462643383279502884L;
+    std::vector<long double> fv(n), cheb(n);
+    for (int k = 0; k < n; ++k) fv[k] = f(std::cos(pi * (k + 0.5L) / n));
+    for (int j = 0; j < n; ++j) {
+        long double s = 0.0L;
+        for (int k = 0; k < n; ++k) s += fv[k] * std::cos(pi * j * (k + 0.5L) / n);
+        cheb[j] = 2.0L * s / n;
+    }
+    cheb[0] *= 0.5L;
+    std::vector<std::vector<long double>> T(n, std::vector<long double>(n, 0.0L));
+    T[0][0] = 1.0L;
+    if (n > 1) T[1][1] = 1.0L;
+    for (int j = 2; j < n; ++j)
+        for (int p = 0; p < n; ++p) T[j][p] = (p > 0 ? 2.0L * T[j - 1][p - 1] : 0.0L) - T[j - 2][p];
+    std::vector<double> mono(n);
+    for (int p = 0; p < n; ++p) {
+        long double s = 0.0L;
+        for (int j = 0; j < n; ++j) s += cheb[j] * T[j][p];
         mono[p] = static_cast<double>(s);
     }
     return mono;
@@ -692,21 +747,45 @@ Plan build_plan(const std::array<double, 3>& box, Family family, double eps, dou
         }
         auto Gz = [&G](double z) { return G(std::sqrt(std::max(0.0, 0.5 * (z + 1.0)))); };
         auto Hz = [&H](double z) { return H(std::sqrt(std::max(0.0, 0.5 * (z + 1.0)))); };
-        int deg0 = gauss ? 10 : static_cast<int>(p.split.a.size()) - 1;
+        std::function<long double(long double)> Hld;  // Psi(y)/y in long double
+        if (gauss) {
+            const long double alpha = p.shape, sa = std::sqrt(alpha);
+            Hld = [sa, alpha](long double y) {
+                return y < 1e-10L ? 2.0L * std::sqrt(alpha / 3.141592653589793238462643383279502884L)
+                                  : std::erf(sa * y) / y;
+            };
+        } else {
+            const Prolate& sp = p.split;
+            Hld = [&sp](long double y) {
+                if (y < 1e-10L) return even_legendre_ld(sp.a, 0.0L) / sp.C0;
+                return even_legendre_integral_ld(sp.a, y) / (sp.C0 * y);
+            };
+        }
+        auto Hzl = [&Hld](long double z) {
+            return Hld(std::sqrt(std::max(0.0L, 0.5L * (z + 1.0L))));
+        };
+        // Only H is tabulated; the kernel recovers chi = dPsi/dy from H and its
+        // z-derivative: chi = H + 2 (z + 1) dH/dz (one coefficient stream).
+        // Smallest degree meeting 2e-15 on Psi and 2e-14 * max|chi| on chi.
         double gmax = 0.0;
         for (int i = 0; i <= 400; ++i) gmax = std::max(gmax, std::fabs(G(i / 400.0)));
-        for (int deg = deg0;; ++deg) {
-            p.pair_G = fit_z_poly(Gz, deg);
-            p.pair_H = fit_z_poly(Hz, deg);
-            double err = 0.0;
+        for (int deg = 6;; ++deg) {
+            p.pair_H = fit_z_poly_ld(Hzl, deg);
+            double epsi = 0.0, echi = 0.0;
             for (int i = 0; i <= 2000; ++i) {
-                double y = i / 2000.0, z = 2.0 * y * y - 1.0;
-                err = std::max(err, std::fabs(horner(p.pair_G, z) - G(y)));
-                err = std::max(err, std::fabs(y * horner(p.pair_H, z) - y * H(y)));
+                const double y = i / 2000.0, z = 2.0 * y * y - 1.0;
+                double hv = p.pair_H.back(), dh = 0.0;
+                for (int m = static_cast<int>(p.pair_H.size()) - 2; m >= 0; --m) {
+                    dh = dh * z + hv;
+                    hv = hv * z + p.pair_H[m];
+                }
+                epsi = std::max(epsi, std::fabs(y * hv - y * H(y)));
+                echi = std::max(echi, std::fabs(hv + 2.0 * (z + 1.0) * dh - G(y)));
             }
-            p.pair_fit_err = err;
-            if (err <= 8e-15 * std::max(1.0, gmax) || deg >= 40) break;
+            p.pair_fit_err = std::max(epsi, echi / std::max(1.0, gmax));
+            if ((epsi <= 2e-15 && echi <= 2e-14 * std::max(1.0, gmax)) || deg >= 39) break;
         }
+        p.pair_G.clear();
     }
 
     // --- parameter selection (ewald.hpp:236-330)

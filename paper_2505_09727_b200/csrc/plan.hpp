@@ -87,14 +87,15 @@ struct Plan {
     std::array<PiecewisePoly, 3> phi, dphi;  // on [-half, half], 4P segments
     std::array<double, 3> half{};        // P h / 2
     std::vector<double> influence_half;  // nx * ny * (nz/2+1)
-    // Pair-kernel form of the split (device K4): chi(y) = sum_k G[k] z^k and
-    // Psi(y) = y * sum_k H[k] z^k with z = 2 y^2 - 1 on y in [0,1].  For the
-    // PSWF split both are exact polynomials of degree K = nterms-1 in y^2
-    // (kernels.hpp:105-138), so this is a change of basis, not a new
-    // approximation; the monomial form is well conditioned in z (sum |coef|
-    // ~ 3).  The Gaussian split is fitted to 4e-15.
-    std::vector<double> pair_G, pair_H;
-    double pair_fit_err = 0.0;  // max abs deviation from the exact kernels
+    // Pair-kernel form of the split (device K4): Psi(y) = y * H(z) with
+    // z = 2 y^2 - 1 on y in [0,1], H a monomial polynomial in z, and
+    // chi(y) = H + 2 (z+1) dH/dz (so one coefficient stream serves both).
+    // For the PSWF split Psi(y)/y is an exact polynomial of degree
+    // K = nterms-1 in y^2 (kernels.hpp:105-138); the degree is reduced to the
+    // smallest meeting 2e-15 on Psi and 2e-14 (relative) on chi.  The
+    // monomial form is well conditioned in z (sum |coef| ~ 3).
+    std::vector<double> pair_G, pair_H;  // pair_G unused (kept empty)
+    double pair_fit_err = 0.0;  // max deviation from the exact kernels
 
     // Host-side evaluators (used for validation and by the C ABI getters).
     double Psi_at(double y) const;     // kernels.hpp:76-81
