@@ -492,6 +492,12 @@ __global__ void __launch_bounds__(128, 7) k_pair(PairArgs a, const __grid_consta
             __syncwarp();
             double u = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
             int npair = 0, qn = 0;
+            // software pipeline: a full round's fp64 operands are loaded when
+            // the round is formed and evaluated when the NEXT round is formed,
+            // so the global-load latency overlaps one round of fp64 work
+            bool have_pf = false;
+            double4 pf = make_double4(0.0, 0.0, 0.0, 0.0);
+            int tf = 13;
             for (int kb = lane; kb < T32; kb += 32) {
                 const float4 c4 = cand[lw[kb]];
                 const float dx = c4.x - xf, dy = c4.y - yf, dz = c4.z - zf;
@@ -507,13 +513,18 @@ __global__ void __launch_bounds__(128, 7) k_pair(PairArgs a, const __grid_consta
                     __syncwarp();
                     qw[lane] = extra;
                     qn -= 32;
-                    const double4 pj = a.xyzq[cd & 0x7ffffff];
-                    const int t = static_cast<unsigned>(cd) >> 27;
-                    pair_eval<ND>(k, pj, shiftv[t][0], shiftv[t][1], shiftv[t][2], pi.x, pi.y,
-                                  pi.z, u, fx, fy, fz, npair);
+                    if (have_pf)
+                        pair_eval<ND>(k, pf, shiftv[tf][0], shiftv[tf][1], shiftv[tf][2], pi.x,
+                                      pi.y, pi.z, u, fx, fy, fz, npair);
+                    pf = a.xyzq[cd & 0x7ffffff];
+                    tf = static_cast<unsigned>(cd) >> 27;
+                    have_pf = true;
                 }
             }
             __syncwarp();
+            if (have_pf)
+                pair_eval<ND>(k, pf, shiftv[tf][0], shiftv[tf][1], shiftv[tf][2], pi.x, pi.y,
+                              pi.z, u, fx, fy, fz, npair);
             if (lane < qn) {
                 const int cd = qw[lane];
                 const double4 pj = a.xyzq[cd & 0x7ffffff];
