@@ -881,6 +881,37 @@ __global__ void __launch_bounds__(128) k_interp(GridArgs g, InterpArgs a) {
     }
 }
 
+// Combine (ewald.hpp:639-647): u = u_l + u_s - q s0, F = F_l + F_s in the
+// caller's (original) order; u/F hold the spectral part on entry.  Block
+// partial sums of q u feed the energy.
+__global__ void __launch_bounds__(256) k_combine(long N, const double4* __restrict__ loc,
+                                                 const double4* __restrict__ xyzq_orig,
+                                                 double self_coef, double* __restrict__ u,
+                                                 double* __restrict__ F, double* __restrict__ epart) {
+    const long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+    double e = 0.0;
+    if (i < N) {
+        const double4 l = loc[i];
+        const double qi = xyzq_orig[i].w;
+        const double ui = (l.x + u[i]) - qi * self_coef;
+        u[i] = ui;
+        F[3 * i + 0] += l.y;
+        F[3 * i + 1] += l.z;
+        F[3 * i + 2] += l.w;
+        e = qi * ui;
+    }
+    __shared__ double red[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = e;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double sum = 0.0;
+        for (int w = 0; w < (blockDim.x >> 5); ++w) sum += red[w];
+        epart[blockIdx.x] = sum;
+    }
+}
+
 // Final energy: E = 1/2 sum of block partials, compensated (ewald.hpp:641-647).
 __global__ void k_energy(const double* __restrict__ part, int n, double* out) {
     __shared__ double ss[256], cc[256];
@@ -1335,6 +1366,15 @@ void Engine::evaluate(long N, const double* pos, const double* q, double* u, dou
     CK(cudaSetDevice(device_));
     launches_ = 0;
     ensure_capacity(N);
+    InterpArgs a{};
+    a.N = N;
+    a.xyzq = d_xyzqB_;
+    a.orig = d_origB_;
+    a.fields = d_fields_;
+    a.M = M_;
+    a.u = u;  // spectral part lands in the caller's arrays, combined below
+    a.F = F;
+    const GridArgs g = grid_args();
     if (t) {
         // serialised on the caller's stream so that each stage is timed alone
         CK(cudaEventRecord(ev_t_[0], s));
@@ -1343,31 +1383,30 @@ void Engine::evaluate(long N, const double* pos, const double* q, double* u, dou
         run_pair(N, s);
         CK(cudaEventRecord(ev_t_[2], s));
         run_grid(N, s, t);
+        if (N > 0) {
+            dispatch_P<InterpLaunch>(plan_.P, static_cast<int>(kSpectral), nfields_ == 4, g, a, s);
+            ++launches_;
+        }
     } else {
-        // K4 on the caller's stream overlaps the grid pipeline on aux_
+        // K4 on the caller's stream overlaps the whole grid pipeline (K1, FFT,
+        // K2, inverse FFT, K3) on aux_; the combine joins them
         prepare(N, pos, q, qsum_dev, s);
         CK(cudaEventRecord(ev_fork_, s));
         CK(cudaStreamWaitEvent(aux_, ev_fork_, 0));
         run_grid(N, aux_, nullptr);
+        if (N > 0) {
+            dispatch_P<InterpLaunch>(plan_.P, static_cast<int>(kSpectral), nfields_ == 4, g, a,
+                                     aux_);
+            ++launches_;
+        }
         CK(cudaEventRecord(ev_join_, aux_));
         run_pair(N, s);
         CK(cudaStreamWaitEvent(s, ev_join_, 0));
     }
-    InterpArgs a{};
-    a.N = N;
-    a.xyzq = d_xyzqB_;
-    a.orig = d_origB_;
-    a.fields = d_fields_;
-    a.M = M_;
-    a.loc = d_loc_;
-    a.self_coef = plan_.self_coef;
-    a.u = u;
-    a.F = F;
-    a.epart = d_epart_;
-    const GridArgs g = grid_args();
-    const int nblk = static_cast<int>(grid1(std::max<long>(N, 1), 128));
+    const int nblk = static_cast<int>(grid1(std::max<long>(N, 1), 256));
     if (N > 0) {
-        dispatch_P<InterpLaunch>(plan_.P, static_cast<int>(kCombine), nfields_ == 4, g, a, s);
+        k_combine<<<nblk, 256, 0, s>>>(N, d_loc_, d_tmp_, plan_.self_coef, u, F, d_epart_);
+        CK(cudaGetLastError());
         ++launches_;
         k_energy<<<1, 256, 0, s>>>(d_epart_, nblk, energy_dev);
         CK(cudaGetLastError());
