@@ -238,11 +238,12 @@ struct PairArgs {
     double4* loc;         // original order: (u_l, F_l)
     unsigned long long* npairs;  // ordered in-range pairs evaluated (r < r_c, r > 0)
     int cap;                     // candidates staged per chunk
-    int nsplit;                  // CTAs per cell (blockIdx.y) sharing its targets
-    int nc[3];                   // coarse cells per dim
-    int F[3];                    // fine cells per dim (nc*kFS, nc*kFS, nc*kFZ)
-    double cw[3];                // coarse cell edge
-    double fw[3];                // fine cell edge
+    int lcap;                    // per-warp candidate-list capacity
+    int M, Mz;                   // neighbourhood reach in columns / slices
+    int bz;                      // target slices per CTA
+    int bx;                      // target columns per CTA edge (1 or 2)
+    int F[3];                    // fine cells per dim (columns x, y; slices z)
+    double fw[3];                // fine cell edges
     double box[3];
 };
 
@@ -287,51 +288,61 @@ __device__ __forceinline__ void pair_eval(const PairConsts& k, double4 pj, doubl
     }
 }
 
-// Fine cell-list geometry of K4: every coarse cell (edge cw >= r_c, the
-// reference's cell, ewald.hpp:431-434) is split into kFS x kFS columns in
-// (x, y) and kFZ slices in z; atoms are sorted by fine cell with z fastest, so
-// a fine column's slices are contiguous in memory.
-constexpr int kFS = 2;
-constexpr int kFZ = 4;
-constexpr int kNCol = (3 * kFS) * (3 * kFS);  // 36 neighbour columns
-constexpr int kNSl = 3 * kFZ;                 // 12 slices per neighbour column
-constexpr int kNEnt = kNCol * kNSl;           // 432 (column, slice) entries
+// Fine cell-list geometry of K4.  Atoms are sorted into fine cells: columns
+// of edge fw >= r_c/2 in x and y, slices of edge fz >= r_c/4 in z, z fastest,
+// so every column is contiguous in memory.  A CTA owns the targets of one
+// column and kBZ consecutive slices; its neighbourhood is the (2M+1)^2 columns
+// and kBZ + 2Mz slices around them (M = ceil(r_c/fw) <= 2, Mz = ceil(r_c/fz)
+// <= 4).  Valid when there are >= 2M+1 columns and >= kBZ + 2Mz slices per
+// period (otherwise the all-pairs path runs, as in the reference for
+// nc < 3, ewald.hpp:457-470).
+constexpr int kMaxBZ = 8;     // target slices per CTA (runtime a.bz <= kMaxBZ)
+constexpr int kMaxCol = 36;   // (BX+2M)^2 with BX <= 2, M <= 2
+constexpr int kMaxSl = kMaxBZ + 8;  // bz + 2 Mz with Mz <= 4
+constexpr int kMaxEnt = kMaxCol * kMaxSl;
 
-// One CTA per coarse cell (x nsplit for small systems), one warp per target
-// atom i.  The CTA stages its 3x3x3-coarse-cell neighbourhood in shared
-// memory, ordered by (column, slice), as fp32 coordinates relative to the
-// cell origin plus a 32-bit code (source index | periodic-image slot << 27).
-// For its i, a warp keeps only the columns whose xy distance is below r_c
-// and, in each, only the z slices the sphere reaches (~2.2-2.6 candidates per
-// in-range pair instead of 6.4-9.5 for the 27-cell stencil).  Lanes walk
-// contiguous pieces of that candidate stream, screen in fp32, compact the
-// survivors with a ballot into a per-warp queue and evaluate full 32-lane
-// rounds in fp64.  Per-i sums are warp-reduced once.  Neighbourhoods larger
-// than the staging capacity are processed in chunks.
+// One CTA per (column, slice block), one warp per target atom i.  The CTA
+// stages its neighbourhood in shared memory, ordered by (column, slice), as
+// fp32 coordinates relative to the block origin plus a 32-bit code (source
+// index | periodic-image slot << 27).  For its i, a warp keeps only the
+// columns whose xy distance is below r_c and, in each, only the slices the
+// sphere reaches (~2.2-2.6 candidates per in-range pair), materialises that
+// list, screens 32 candidates per step in fp32, compacts survivors with a
+// ballot into a per-warp queue and evaluates full 32-lane rounds in fp64
+// (operand loads software-pipelined by one round).  Per-i sums are
+// warp-reduced once.  Neighbourhoods larger than the staging capacity are
+// processed in chunks.
 template <int ND>
-__global__ void __launch_bounds__(128, 7) k_pair(PairArgs a, const __grid_constant__ PairConsts k) {
+__global__ void __launch_bounds__(128, 6) k_pair(PairArgs a, const __grid_constant__ PairConsts k) {
     extern __shared__ __align__(16) unsigned char smem[];
-    float4* cand = reinterpret_cast<float4*>(smem);   // a.cap + 1 (sentinel)
-    int* qall = reinterpret_cast<int*>(cand + a.cap + 1); // 64 per warp
-    int* cball = qall + 4 * 64;                       // column begin, 36 per warp
-    unsigned short* lall = reinterpret_cast<unsigned short*>(cball + 4 * kNCol);  // a.cap+32 per warp
-    __shared__ int ent_src[kNEnt], ent_off[kNEnt + 1];
-    __shared__ unsigned char ent_slot[kNEnt];
+    float4* cand = reinterpret_cast<float4*>(smem);       // a.cap + 1 (sentinel)
+    int* qall = reinterpret_cast<int*>(cand + a.cap + 1);  // 64 per warp
+    int* cball = qall + 4 * 64;                            // column begin, kMaxCol per warp
+    unsigned short* lall = reinterpret_cast<unsigned short*>(cball + 4 * kMaxCol);  // a.lcap per warp
+    __shared__ int ent_src[kMaxEnt], ent_off[kMaxEnt + 1];
+    __shared__ unsigned char ent_slot[kMaxEnt];
     __shared__ double shiftv[27][3];
-    __shared__ int isrc[kFS * kFS], ipre[kFS * kFS + 1];
+    __shared__ int isrc[4], ipre[5];
 
     const int nw = blockDim.x >> 5;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int* qw = qall + warp * 64;
-    int* cb = cball + warp * kNCol;
-    unsigned short* lw = lall + warp * (a.cap + 32);
+    int* cb = cball + warp * kMaxCol;
+    unsigned short* lw = lall + warp * a.lcap;
     const unsigned lt_mask = (1u << lane) - 1u;
 
-    const int cell = blockIdx.x;
-    const int cz = cell % a.nc[2];
-    const int cy = (cell / a.nc[2]) % a.nc[1];
-    const int cx = cell / (a.nc[1] * a.nc[2]);
-    const double ox = cx * a.cw[0], oy = cy * a.cw[1], oz = cz * a.cw[2];
+    const int M = a.M, Mz = a.Mz, BX = a.bx, W = BX + 2 * M;
+    const int ncol = W * W;
+    const int nzb = (a.F[2] + a.bz - 1) / a.bz;
+    const int nyb = (a.F[1] + BX - 1) / BX;
+    const int blk = blockIdx.x;
+    const int bzi = blk % nzb;
+    const int fy0 = ((blk / nzb) % nyb) * BX;
+    const int fx0 = (blk / (nzb * nyb)) * BX;
+    const int z0 = bzi * a.bz, z1 = min(a.F[2], z0 + a.bz);
+    const int nsl = (z1 - z0) + 2 * Mz;
+    const int nent = ncol * nsl;
+    const double ox = fx0 * a.fw[0], oy = fy0 * a.fw[1], oz = z0 * a.fw[2];
 
     if (threadIdx.x < 27) {
         const int t = threadIdx.x;
@@ -339,10 +350,10 @@ __global__ void __launch_bounds__(128, 7) k_pair(PairArgs a, const __grid_consta
         shiftv[t][1] = ((t / 3) % 3 - 1) * a.box[1];
         shiftv[t][2] = (t % 3 - 1) * a.box[2];
     }
-    for (int e = threadIdx.x; e < kNEnt; e += blockDim.x) {
-        const int col = e / kNSl, sl = e - col * kNSl;
-        const int ca = col / (3 * kFS), cbb = col - ca * (3 * kFS);
-        int fx = cx * kFS - kFS + ca, fy = cy * kFS - kFS + cbb, fz = cz * kFZ - kFZ + sl;
+    for (int e = threadIdx.x; e < nent; e += blockDim.x) {
+        const int col = e / nsl, sl = e - col * nsl;
+        const int ca = col / W, cbb = col - ca * W;
+        int fx = fx0 - M + ca, fy = fy0 - M + cbb, fz = z0 - Mz + sl;
         const int ix = fx < 0 ? 0 : (fx >= a.F[0] ? 2 : 1);
         const int iy = fy < 0 ? 0 : (fy >= a.F[1] ? 2 : 1);
         const int iz = fz < 0 ? 0 : (fz >= a.F[2] ? 2 : 1);
@@ -355,16 +366,33 @@ __global__ void __launch_bounds__(128, 7) k_pair(PairArgs a, const __grid_consta
         ent_off[e + 1] = a.start[f + 1] - s0;  // count, scanned below
         ent_slot[e] = static_cast<unsigned char>((ix * 3 + iy) * 3 + iz);
     }
+    if (threadIdx.x == 32) {
+        // target columns of this block (edge columns may fall off the grid)
+        int acc = 0;
+        for (int c = 0; c < 4; ++c) {
+            const int cx = fx0 + c / 2, cy = fy0 + c % 2;
+            int b = 0, e = 0;
+            if (c / 2 < BX && c % 2 < BX && cx < a.F[0] && cy < a.F[1]) {
+                const int fc = (cx * a.F[1] + cy) * a.F[2];
+                b = a.start[fc + z0];
+                e = a.start[fc + z1];
+            }
+            isrc[c] = b;
+            ipre[c] = acc;
+            acc += e - b;
+        }
+        ipre[4] = acc;
+    }
     __syncthreads();
     if (warp == 0) {
-        // exclusive scan of the 432 counts: 14 per lane, then a warp scan
-        constexpr int per = (kNEnt + 31) / 32;
+        // exclusive scan of the entry counts
+        constexpr int per = (kMaxEnt + 31) / 32;
         int loc[per];
         int sum = 0;
 #pragma unroll
         for (int j = 0; j < per; ++j) {
             const int e = lane * per + j;
-            loc[j] = e < kNEnt ? ent_off[e + 1] : 0;
+            loc[j] = e < nent ? ent_off[e + 1] : 0;
             sum += loc[j];
         }
         int incl = sum;
@@ -377,27 +405,14 @@ __global__ void __launch_bounds__(128, 7) k_pair(PairArgs a, const __grid_consta
 #pragma unroll
         for (int j = 0; j < per; ++j) {
             const int e = lane * per + j;
-            if (e < kNEnt) ent_off[e] = run;
+            if (e < nent) ent_off[e] = run;
             run += loc[j];
         }
-        if (lane == 31) ent_off[kNEnt] = incl;
+        if (lane == 31) ent_off[nent] = incl;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        // this cell's own atoms: inner columns, inner slices (never wrapped)
-        int acc = 0;
-        for (int c = 0; c < kFS * kFS; ++c) {
-            const int col = (kFS + c / kFS) * (3 * kFS) + (kFS + c % kFS);
-            const int e0 = col * kNSl + kFZ, e1 = col * kNSl + 2 * kFZ;
-            isrc[c] = ent_src[e0];
-            ipre[c] = acc;
-            acc += ent_off[e1] - ent_off[e0];
-        }
-        ipre[kFS * kFS] = acc;
-    }
-    __syncthreads();
-    const int total = ent_off[kNEnt];
-    const int ni = ipre[kFS * kFS];
+    const int total = ent_off[nent];
+    const int ni = ipre[4];
     if (ni == 0) return;
     const float R2 = k.rc2_test;
     const float fwx = static_cast<float>(a.fw[0]), fwy = static_cast<float>(a.fw[1]);
@@ -408,7 +423,7 @@ __global__ void __launch_bounds__(128, 7) k_pair(PairArgs a, const __grid_consta
         if (base > 0) __syncthreads();
         for (int c = threadIdx.x; c < nk; c += blockDim.x) {
             const int g = base + c;
-            int lo = 0, hi = kNEnt - 1;  // last entry with ent_off[e] <= g
+            int lo = 0, hi = nent - 1;  // last entry with ent_off[e] <= g
             while (lo < hi) {
                 const int mid = (lo + hi + 1) >> 1;
                 if (ent_off[mid] <= g) lo = mid;
@@ -424,33 +439,32 @@ __global__ void __launch_bounds__(128, 7) k_pair(PairArgs a, const __grid_consta
         }
         if (threadIdx.x == 0) cand[a.cap] = make_float4(1e30f, 1e30f, 1e30f, __int_as_float(0));
         __syncthreads();
-        const int stride = nw * a.nsplit;
-        for (int ii = blockIdx.y * nw + warp; ii < ni; ii += stride) {
+        for (int ii = warp; ii < ni; ii += nw) {
             const int ic = (ii >= ipre[1]) + (ii >= ipre[2]) + (ii >= ipre[3]);
             const int i = isrc[ic] + (ii - ipre[ic]);
             const double4 pi = a.xyzq[i];
             const float xf = static_cast<float>(pi.x - ox);
             const float yf = static_cast<float>(pi.y - oy);
             const float zf = static_cast<float>(pi.z - oz);
-            // candidate ranges per neighbour column (lanes 0..31, then 32..35)
-            int cnt0 = 0, cnt1 = 0;
+            // candidate range per neighbour column (lanes 0..31, then 32..35)
+            int beg0 = 0, cnt0 = 0, beg1 = 0, cnt1 = 0;
 #pragma unroll
             for (int pass = 0; pass < 2; ++pass) {
                 const int col = lane + 32 * pass;
                 int beg = 0, cnt = 0;
-                if (col < kNCol) {
-                    const int ca = col / (3 * kFS), cbb = col - ca * (3 * kFS);
-                    const float x0 = (ca - kFS) * fwx, y0 = (cbb - kFS) * fwy;
+                if (col < ncol) {
+                    const int ca = col / W, cbb = col - ca * W;
+                    const float x0 = (ca - M) * fwx, y0 = (cbb - M) * fwy;
                     const float gx = fmaxf(0.f, fmaxf(x0 - xf, xf - (x0 + fwx)));
                     const float gy = fmaxf(0.f, fmaxf(y0 - yf, yf - (y0 + fwy)));
                     const float g2 = fmaf(gx, gx, gy * gy);
                     if (g2 < R2) {
                         const float zm = sqrtf(R2 - g2);
-                        int klo = static_cast<int>(floorf((zf - zm) / fwz)) + kFZ;
-                        int khi = static_cast<int>(floorf((zf + zm) / fwz)) + kFZ;
-                        klo = max(0, min(kNSl - 1, klo));
-                        khi = max(0, min(kNSl - 1, khi));
-                        int lo = ent_off[col * kNSl + klo], hi = ent_off[col * kNSl + khi + 1];
+                        int klo = static_cast<int>(floorf((zf - zm) / fwz)) + Mz;
+                        int khi = static_cast<int>(floorf((zf + zm) / fwz)) + Mz;
+                        klo = max(0, min(nsl - 1, klo));
+                        khi = max(0, min(nsl - 1, khi));
+                        int lo = ent_off[col * nsl + klo], hi = ent_off[col * nsl + khi + 1];
                         lo = max(lo, base);
                         hi = min(hi, base + nk);
                         if (hi > lo) {
@@ -458,10 +472,14 @@ __global__ void __launch_bounds__(128, 7) k_pair(PairArgs a, const __grid_consta
                             cnt = hi - lo;
                         }
                     }
-                    cb[col] = beg;
                 }
-                if (pass == 0) cnt0 = cnt;
-                else cnt1 = cnt;
+                if (pass == 0) {
+                    beg0 = beg;
+                    cnt0 = cnt;
+                } else {
+                    beg1 = beg;
+                    cnt1 = cnt;
+                }
             }
             int inc0 = cnt0, inc1 = cnt1;
 #pragma unroll
@@ -474,54 +492,59 @@ __global__ void __launch_bounds__(128, 7) k_pair(PairArgs a, const __grid_consta
                 }
             }
             const int tot0 = __shfl_sync(0xffffffffu, inc0, 31);
-            const int T = __shfl_sync(0xffffffffu, tot0 + inc1, kNCol - 33);
-            // materialise this i's candidate list (staged indices), padded to
-            // a multiple of 32 with the far-away sentinel a.cap
-            {
-                const int b0 = cb[lane], p0 = inc0 - cnt0;
-#pragma unroll 4
-                for (int j = 0; j < cnt0; ++j) lw[p0 + j] = static_cast<unsigned short>(b0 + j);
-                if (lane + 32 < kNCol) {
-                    const int b1 = cb[lane + 32], p1 = tot0 + inc1 - cnt1;
-#pragma unroll 4
-                    for (int j = 0; j < cnt1; ++j) lw[p1 + j] = static_cast<unsigned short>(b1 + j);
-                }
-            }
-            const int T32 = (T + 31) & ~31;
-            if (T + lane < T32) lw[T + lane] = static_cast<unsigned short>(a.cap);
-            __syncwarp();
+            inc1 += tot0;
+            const int T = __shfl_sync(0xffffffffu, inc1, 31);
             double u = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
             int npair = 0, qn = 0;
-            // software pipeline: a full round's fp64 operands are loaded when
-            // the round is formed and evaluated when the NEXT round is formed,
-            // so the global-load latency overlaps one round of fp64 work
             bool have_pf = false;
             double4 pf = make_double4(0.0, 0.0, 0.0, 0.0);
             int tf = 13;
-            for (int kb = lane; kb < T32; kb += 32) {
-                const float4 c4 = cand[lw[kb]];
-                const float dx = c4.x - xf, dy = c4.y - yf, dz = c4.z - zf;
-                const bool in = fmaf(dz, dz, fmaf(dy, dy, dx * dx)) < R2;
-                const int code = __float_as_int(c4.w);
-                const unsigned m = __ballot_sync(0xffffffffu, in);
-                if (in) qw[qn + __popc(m & lt_mask)] = code;
-                qn += __popc(m);
-                if (qn >= 32) {
-                    __syncwarp();
-                    const int cd = qw[lane];
-                    const int extra = qw[32 + lane];
-                    __syncwarp();
-                    qw[lane] = extra;
-                    qn -= 32;
-                    if (have_pf)
-                        pair_eval<ND>(k, pf, shiftv[tf][0], shiftv[tf][1], shiftv[tf][2], pi.x,
-                                      pi.y, pi.z, u, fx, fy, fz, npair);
-                    pf = a.xyzq[cd & 0x7ffffff];
-                    tf = static_cast<unsigned>(cd) >> 27;
-                    have_pf = true;
+            // the list holds at most a.lcap entries: walk it in pieces if needed
+            for (int lb = 0; lb < T; lb += a.lcap) {
+                const int le = min(T, lb + a.lcap);
+                {
+                    // this lane's columns cover stream positions [inc-cnt, inc)
+                    int p0 = max(inc0 - cnt0, lb), p1 = min(inc0, le);
+                    int off = beg0 - (inc0 - cnt0);
+#pragma unroll 4
+                    for (int p = p0; p < p1; ++p)
+                        lw[p - lb] = static_cast<unsigned short>(off + p);
+                    p0 = max(inc1 - cnt1, lb);
+                    p1 = min(inc1, le);
+                    off = beg1 - (inc1 - cnt1);
+#pragma unroll 4
+                    for (int p = p0; p < p1; ++p)
+                        lw[p - lb] = static_cast<unsigned short>(off + p);
                 }
+                const int n = le - lb;
+                const int n32 = (n + 31) & ~31;
+                if (n + lane < n32) lw[n + lane] = static_cast<unsigned short>(a.cap);
+                __syncwarp();
+                for (int kb = lane; kb < n32; kb += 32) {
+                    const float4 c4 = cand[lw[kb]];
+                    const float dx = c4.x - xf, dy = c4.y - yf, dz = c4.z - zf;
+                    const bool in = fmaf(dz, dz, fmaf(dy, dy, dx * dx)) < R2;
+                    const int code = __float_as_int(c4.w);
+                    const unsigned m = __ballot_sync(0xffffffffu, in);
+                    if (in) qw[qn + __popc(m & lt_mask)] = code;
+                    qn += __popc(m);
+                    if (qn >= 32) {
+                        __syncwarp();
+                        const int cd = qw[lane];
+                        const int extra = qw[32 + lane];
+                        __syncwarp();
+                        qw[lane] = extra;
+                        qn -= 32;
+                        if (have_pf)
+                            pair_eval<ND>(k, pf, shiftv[tf][0], shiftv[tf][1], shiftv[tf][2],
+                                          pi.x, pi.y, pi.z, u, fx, fy, fz, npair);
+                        pf = a.xyzq[cd & 0x7ffffff];
+                        tf = static_cast<unsigned>(cd) >> 27;
+                        have_pf = true;
+                    }
+                }
+                __syncwarp();
             }
-            __syncwarp();
             if (have_pf)
                 pair_eval<ND>(k, pf, shiftv[tf][0], shiftv[tf][1], shiftv[tf][2], pi.x, pi.y,
                               pi.z, u, fx, fy, fz, npair);
@@ -1059,9 +1082,18 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
     CK(cudaSetDevice(device_));
     const Plan& p = plan_;
     for (int d = 0; d < 3; ++d) nc_[d] = std::max(1, static_cast<int>(std::floor(p.box[d] / p.r_c)));
-    cells_ok_ = nc_[0] >= 3 && nc_[1] >= 3 && nc_[2] >= 3;
-    ncell_ = nc_[0] * nc_[1] * nc_[2];
-    F_ = {nc_[0] * kFS, nc_[1] * kFS, nc_[2] * kFZ};
+    // fine pair cells: columns >= r_c/2 in x, y; slices >= r_c/4 in z
+    F_[0] = std::max(1, static_cast<int>(std::floor(p.box[0] / (0.5 * p.r_c))));
+    F_[1] = std::max(1, static_cast<int>(std::floor(p.box[1] / (0.5 * p.r_c))));
+    F_[2] = std::max(1, static_cast<int>(std::floor(p.box[2] / (0.25 * p.r_c))));
+    pM_ = std::max(static_cast<int>(std::ceil(p.r_c / (p.box[0] / F_[0]) - 1e-12)),
+                   static_cast<int>(std::ceil(p.r_c / (p.box[1] / F_[1]) - 1e-12)));
+    pMz_ = static_cast<int>(std::ceil(p.r_c / (p.box[2] / F_[2]) - 1e-12));
+    // the fine stencil must not alias across the period; otherwise all pairs
+    cells_ok_ = pM_ <= 2 && pMz_ <= 4 && F_[0] >= 2 * pM_ + 1 && F_[1] >= 2 * pM_ + 1 &&
+                F_[2] >= 4 + 2 * pMz_;
+    pbz_ = 4;
+    ncell_ = F_[0] * F_[1] * ((F_[2] + pbz_ - 1) / pbz_);
     ncellF_ = static_cast<long>(F_[0]) * F_[1] * F_[2];
     if (ncellF_ >= (1L << 30)) throw InvalidArgument("cell list too fine for this box / r_c");
     // spread bins: the largest S in {8, 6, 4} that still gives >= 4 CTAs per SM
@@ -1149,7 +1181,7 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
 
     // pair kernel staging capacity (candidates per chunk); ESP_PAIR_CAP overrides
     pair_warps_ = 4;
-    pair_cap_ = 1536;
+    pair_cap_ = 2048;
     if (const char* e = std::getenv("ESP_PAIR_CAP")) pair_cap_ = std::max(256, std::min(4096, std::atoi(e)));
 }
 
@@ -1279,30 +1311,46 @@ void Engine::run_pair(long N, cudaStream_t s) {
     a.loc = d_loc_;
     a.npairs = d_npairs_;
     for (int d = 0; d < 3; ++d) {
-        a.nc[d] = nc_[d];
         a.F[d] = F_[d];
-        a.cw[d] = p.box[d] / nc_[d];
         a.fw[d] = p.box[d] / F_[d];
         a.box[d] = p.box[d];
     }
     const int nw = 4;
     pair_warps_ = nw;
     a.cap = pair_cap_;
-    // split crowded cells over several CTAs when there are too few cells to
-    // fill the GPU (small systems such as cfg2: 216 cells of ~150 atoms)
-    const double mean = static_cast<double>(N) / ncell_;
-    const long want_warps = 148L * 24;
-    int nsplit = static_cast<int>((want_warps + static_cast<long>(ncell_) * nw - 1) /
-                                  (static_cast<long>(ncell_) * nw));
-    nsplit = std::max(1, std::min(nsplit, static_cast<int>(std::ceil(mean / (2.0 * nw)))));
-    a.nsplit = nsplit;
+    a.lcap = std::min(pair_cap_, 1024) + 32;
+    a.M = pM_;
+    a.Mz = pMz_;
+    // target block (bx x bx columns, bz slices): the most targets per CTA
+    // (amortises the neighbourhood staging) whose expected neighbourhood still
+    // fits one staging chunk
+    {
+        const double per_cell = static_cast<double>(N) / ncellF_;
+        int best_bx = 1, best_bz = 4;
+        double best_t = -1.0;
+        for (int bx : {1, 2})
+            for (int bz : {4, 8}) {
+                if (F_[0] < bx + 2 * pM_ || F_[1] < bx + 2 * pM_ || F_[2] < bz + 2 * pMz_) continue;
+                const double nbr = per_cell * (bx + 2 * pM_) * (bx + 2 * pM_) * (bz + 2 * pMz_);
+                const double tgt = per_cell * bx * bx * bz;
+                if (nbr <= 0.9 * a.cap && tgt > best_t) {
+                    best_t = tgt;
+                    best_bx = bx;
+                    best_bz = bz;
+                }
+            }
+        a.bx = best_bx;
+        a.bz = best_bz;
+    }
+    const int nblocks = ((F_[0] + a.bx - 1) / a.bx) * ((F_[1] + a.bx - 1) / a.bx) *
+                        ((F_[2] + a.bz - 1) / a.bz);
     if (N >= (1L << 27)) throw InvalidArgument("pair kernel: N must be < 2^27");
-    size_t sm = (a.cap + 1) * sizeof(float4) + 4 * (64 + kNCol) * sizeof(int) +
-                4 * (a.cap + 32) * sizeof(unsigned short);
+    size_t sm = (a.cap + 1) * sizeof(float4) + 4 * (64 + kMaxCol) * sizeof(int) +
+                4 * a.lcap * sizeof(unsigned short);
     auto go = [&](auto kern) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(sm)));
-        kern<<<dim3(ncell_, nsplit), nw * 32, sm, s>>>(a, k);
+        kern<<<nblocks, nw * 32, sm, s>>>(a, k);
     };
     switch (nd) {
         case 14: go(k_pair<14>); break;

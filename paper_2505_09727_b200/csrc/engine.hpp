@@ -91,7 +91,9 @@ private:
     long M_ = 0, Mh_ = 0;       // real grid size, half spectrum size
     int nfields_ = 4;           // 4 for ik, 1 for ad
     int pair_warps_ = 4;
-    int pair_cap_ = 1536;
+    int pair_cap_ = 2048;
+    int pM_ = 2, pMz_ = 4;      // fine stencil reach (columns, slices)
+    int pbz_ = 4;
 
     // tables on device
     double* d_win_ = nullptr;        // 3 x 4P x 13 phi, then 3 x 4P x 13 dphi
