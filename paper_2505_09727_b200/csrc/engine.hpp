@@ -66,6 +66,8 @@ public:
     unsigned long long last_pair_count() const;
 
 private:
+    void enqueue(long N, const double* pos, const double* q, double* u, double* F,
+                 double* energy_dev, double* qsum_dev, cudaStream_t s, StageTimes* t);
     void ensure_capacity(long N);
     void prepare(long N, const double* pos, const double* q, double* qsum_dev, cudaStream_t s);
     void run_pair(long N, cudaStream_t s);
@@ -131,6 +133,23 @@ private:
     cudaStream_t aux_ = nullptr;
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
     cudaEvent_t ev_t_[8] = {};
+
+    // CUDA graph of a full evaluation, keyed by its arguments
+    struct GraphKey {
+        long N;
+        const void *pos, *q, *u, *F, *e, *qs;
+        bool operator==(const GraphKey& o) const {
+            return N == o.N && pos == o.pos && q == o.q && u == o.u && F == o.F && e == o.e &&
+                   qs == o.qs;
+        }
+    };
+    bool use_graph_ = true;
+    bool warm_ = false;
+    GraphKey gkey_{};
+    cudaGraphExec_t gexec_ = nullptr;
+    cudaStream_t gstream_ = nullptr;
+    cudaEvent_t ev_gin_ = nullptr, ev_gout_ = nullptr;
+    int graph_launches_ = 0;
 };
 
 }  // namespace espb
