@@ -52,10 +52,8 @@ def parse():
 
 
 def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    from paper_2505_09727_b200.dist import env
+    return env()
 
 
 class ClockSampler:
@@ -199,8 +197,10 @@ def run_ours(args):
     import paper_2505_09727_b200 as E
     from paper_2505_09727_b200 import systems as S
 
+    from paper_2505_09727_b200.dist import max_over_ranks, replica_seed, weak_scaling_value
     base = S.config(args.workload)
-    c = S.Config(base.name, base.kind, base.N, base.L, base.r_c, base.eps, seed=1 + rank)
+    c = S.Config(base.name, base.kind, base.N, base.L, base.r_c, base.eps,
+                 seed=replica_seed(base.seed, rank))
     pos, q, box = c.system()
     N = int(q.size)
     plan = E.build_plan(box, "pswf", c.eps, c.r_c, E.Overrides(force_method=args.force_method),
@@ -296,10 +296,7 @@ def run_ours(args):
         t_e2e.append(time.perf_counter() - t0)
     e2e_ms = statistics.mean(t_e2e) * 1e3
 
-    if dist:
-        t = torch.tensor([ms, e2e_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, e2e_ms = float(t[0]), float(t[1])
+    ms, e2e_ms = max_over_ranks([ms, e2e_ms], device=dev)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -309,7 +306,7 @@ def run_ours(args):
             cpu = {"error": str(exc)}
 
     if rank == 0:
-        value = N * world / (ms * 1e-3)
+        value = weak_scaling_value(N, world, ms)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -328,7 +325,7 @@ def run_ours(args):
             "stages_ms": stages_ms,
             "roofline": roofline,
             "cpu_baseline": cpu,
-            "e2e": {"value": N * world / (e2e_ms * 1e-3), "unit": UNIT,
+            "e2e": {"value": weak_scaling_value(N, world, e2e_ms), "unit": UNIT,
                     "h2d_bytes_per_step": int(N * 32), "d2h_bytes_per_step": int(N * 32 + 8),
                     "ms_per_step": e2e_ms},
         }

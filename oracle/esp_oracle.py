@@ -495,35 +495,43 @@ def evaluate(plan: Plan, pos, q):
     return 0.5 * math.fsum(q * u), u, F
 
 
-def direct_ewald(pos, q, box, tol=1e-9, lam=None):
+def direct_ewald(pos, q, box, tol=1e-9, lam=None, targets=None, chunk=64):
     """reference.hpp:42-206 (one pass): explicit image shells + reciprocal
-    structure factors, lambda = min(L)/6 by default (reference.hpp:222)."""
+    structure factors, lambda = min(L)/6 by default (reference.hpp:222).
+
+    targets (optional index array) restricts u and F to those atoms while
+    every source still contributes (the target-subset restatement SURVEY.md
+    8(c) asks for beyond the reference's N <= 1e4 cap); the energy is then
+    not available (returned as nan)."""
     box = np.asarray(box, dtype=np.float64)
     pos = fold(pos, box)
     N = q.size
+    tg = np.arange(N) if targets is None else np.asarray(targets)
     V = float(np.prod(box))
     lam = lam or float(box.min()) / 6.0
-    u = np.zeros(N)
-    F = np.zeros((N, 3))
+    u = np.zeros(tg.size)
+    F = np.zeros((tg.size, 3))
     for m in range(0, 17):
         rng = np.arange(-m, m + 1)
         off = np.array([(a, b, c) for a in rng for b in rng for c in rng
                         if max(abs(a), abs(b), abs(c)) == m], dtype=np.float64) * box
-        du = np.zeros(N)
-        for o in off:
-            d = pos[:, None, :] - pos[None, :, :] + o          # r_i - r_j + n
-            r2 = np.einsum("ijk,ijk->ij", d, d)
-            if m == 0:
-                np.fill_diagonal(r2, np.inf)
-            r = np.sqrt(r2)
-            a = r / lam
-            ok = a <= 27.0
-            er = np.where(ok, erfc(np.where(ok, a, 0.0)), 0.0)
-            contrib = np.where(ok, er * INV4PI / r, 0.0)
-            du += contrib @ q
-            fp = -(er / r2 + (2.0 / (lam * math.sqrt(math.pi))) * np.exp(-a * a) / r) * INV4PI
-            coef = -(q[:, None] * q[None, :]) * np.where(ok, fp / r, 0.0)
-            F += np.einsum("ij,ijk->ik", coef, d)
+        du = np.zeros(tg.size)
+        for s0 in range(0, tg.size, chunk):
+            ti = tg[s0:s0 + chunk]
+            for o in off:
+                d = pos[ti, None, :] - pos[None, :, :] + o      # r_i - r_j + n
+                r2 = np.einsum("ijk,ijk->ij", d, d)
+                if m == 0:
+                    r2[np.arange(ti.size), ti] = np.inf
+                r = np.sqrt(r2)
+                a = r / lam
+                ok = a <= 27.0
+                er = np.where(ok, erfc(np.where(ok, a, 0.0)), 0.0)
+                contrib = np.where(ok, er * INV4PI / r, 0.0)
+                du[s0:s0 + chunk] += contrib @ q
+                fp = -(er / r2 + (2.0 / (lam * math.sqrt(math.pi))) * np.exp(-a * a) / r) * INV4PI
+                coef = -(q[ti, None] * q[None, :]) * np.where(ok, fp / r, 0.0)
+                F[s0:s0 + chunk] += np.einsum("ij,ijk->ik", coef, d)
         u += du
         if m >= 1 and np.abs(du).max() < tol / 10.0:
             break
@@ -542,16 +550,19 @@ def direct_ewald(pos, q, box, tol=1e-9, lam=None):
     xi = 2 * math.pi * kv / box
     xi2 = np.einsum("ij,ij->i", xi, xi)
     w = np.exp(-lam * lam * xi2 / 4) / (xi2 * V)
-    for s in range(0, xi.shape[0], 512):
-        ph = pos @ xi[s:s + 512].T                       # N x K
-        c, sn = np.cos(ph), np.sin(ph)
-        rho_r, rho_i = q @ c, -(q @ sn)                    # sum q e^{-i xi r}
-        tr = c * rho_r - sn * rho_i                        # Re(e^{+i xi r_i} rho)
-        ti = sn * rho_r + c * rho_i                        # Im
-        u += tr @ w[s:s + 512]
-        F += (q[:, None] * ti * w[s:s + 512]) @ xi[s:s + 512]
-    u -= q / (2.0 * math.pi ** 1.5 * lam)
-    return 0.5 * math.fsum(q * u), u, F
+    kc = max(16, min(512, int(2e7 // max(N, 1))))
+    for s in range(0, xi.shape[0], kc):
+        ph = pos @ xi[s:s + kc].T                        # N x K
+        rho_r = q @ np.cos(ph)                           # sum_j q_j e^{-i xi r_j}
+        rho_i = -(q @ np.sin(ph))
+        c, sn = np.cos(ph[tg]), np.sin(ph[tg])
+        tr = c * rho_r - sn * rho_i                      # Re(e^{+i xi r_i} rho)
+        ti = sn * rho_r + c * rho_i                      # Im
+        u += tr @ w[s:s + kc]
+        F += (q[tg, None] * ti * w[s:s + kc]) @ xi[s:s + kc]
+    u -= q[tg] / (2.0 * math.pi ** 1.5 * lam)
+    E = 0.5 * math.fsum(q * u) if targets is None else float("nan")
+    return E, u, F
 
 
 def splitmix64_uniform(seed: int, start: int, count: int) -> np.ndarray:
