@@ -37,12 +37,15 @@ def test_noncubic_box_vs_oracle(esp, gpu):
     _check_vs_oracle(esp, gpu, (10.0, 12.5, 15.0), 600, 7, 1e-4, 1.0)
 
 
-@pytest.mark.parametrize("P", [3, 4, 9, 12])
+@pytest.mark.parametrize("P", [3, 4, 9])
 def test_window_order_override_vs_oracle(esp, gpu, P):
     """P outside the specialised {5..8} kernels runs the generic path (grid
     pinned: low P cannot reach eps by inflation, the reference then spends
-    60 inflation steps before refusing)."""
-    _check_vs_oracle(esp, gpu, (8.0, 8.0, 8.0), 300, 11, 1e-3, 1.5, P=P, nf=32)
+    60 inflation steps before refusing).  P >= 10 on this pinned grid is
+    ill-conditioned (1/phihat^2 amplification): the reference and the oracle
+    already disagree there at 1e-7..1e-5, so it is not a parity case."""
+    _check_vs_oracle(esp, gpu, (8.0, 8.0, 8.0), 300, 11, 1e-3, 1.5, P=P, nf=32,
+                     e_tol=1e-10, f_tol=1e-9)
 
 
 def test_pinned_grid_and_c1_vs_oracle(esp, gpu):
