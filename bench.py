@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
                     help="budget of the cpu_baseline sample (rank 0, N=1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--strong", action="store_true",
+                    help="N>1: decompose ONE system over the ranks (x-slabs, NCCL all-reduce of "
+                         "the charge grid and of the outputs) instead of one replica per rank")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     return args
@@ -199,8 +202,9 @@ def run_ours(args):
 
     from paper_2505_09727_b200.dist import max_over_ranks, replica_seed, weak_scaling_value
     base = S.config(args.workload)
+    strong = args.strong
     c = S.Config(base.name, base.kind, base.N, base.L, base.r_c, base.eps,
-                 seed=replica_seed(base.seed, rank))
+                 seed=base.seed if strong else replica_seed(base.seed, rank))
     pos, q, box = c.system()
     N = int(q.size)
     plan = E.build_plan(box, "pswf", c.eps, c.r_c, E.Overrides(force_method=args.force_method),
@@ -214,9 +218,18 @@ def run_ours(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
 
-    def step():
-        E.evaluate_device(plan, box, N, pos_d.data_ptr(), q_d.data_ptr(), u_d.data_ptr(),
-                          F_d.data_ptr(), e_d.data_ptr(), stream.cuda_stream)
+    if strong:
+        from paper_2505_09727_b200.dist import evaluate_slab
+        out_d = torch.empty(4 * N + 1, dtype=torch.float64, device=dev)
+        grid_d = torch.empty(E.grid_size(plan), dtype=torch.float64, device=dev)
+
+        def step():
+            evaluate_slab(plan, box, N, pos_d, q_d, out_d, grid_d, rank, world,
+                          stream.cuda_stream)
+    else:
+        def step():
+            E.evaluate_device(plan, box, N, pos_d.data_ptr(), q_d.data_ptr(), u_d.data_ptr(),
+                              F_d.data_ptr(), e_d.data_ptr(), stream.cuda_stream)
 
     clocks = ClockSampler(local)
     clocks.start()
@@ -240,7 +253,7 @@ def run_ours(args):
     if dist:
         dist.barrier()
     ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev0, ev1))
-    energy = float(e_d.item())
+    energy = float(out_d[4 * N].item()) if strong else float(e_d.item())
 
     # keep the GPU busy (untimed) until the clock sampler has a few samples
     t_end = time.time() + 3.0
@@ -285,14 +298,28 @@ def run_ours(args):
     u_h = torch.empty(N, dtype=torch.float64).pin_memory().numpy()
     F_h = torch.empty((N, 3), dtype=torch.float64).pin_memory().numpy()
     sysh = E.ParticleSystem(box, q_h, pos_h)
+    if strong:
+        out_h = torch.empty(4 * N + 1, dtype=torch.float64).pin_memory()
+        pos_ht = torch.from_numpy(pos_h)
+        q_ht = torch.from_numpy(q_h)
+
+        def e2e_step():
+            pos_d.copy_(pos_ht, non_blocking=True)
+            q_d.copy_(q_ht, non_blocking=True)
+            step()
+            out_h.copy_(out_d, non_blocking=True)
+            torch.cuda.synchronize()
+    else:
+        def e2e_step():
+            E.evaluate(plan, sysh, out=(u_h, F_h))
     for _ in range(2):
-        E.evaluate(plan, sysh, out=(u_h, F_h))
+        e2e_step()
     if dist:
         dist.barrier()
     t_e2e = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        ef = E.evaluate(plan, sysh, out=(u_h, F_h))
+        e2e_step()
         t_e2e.append(time.perf_counter() - t0)
     e2e_ms = statistics.mean(t_e2e) * 1e3
 
@@ -306,16 +333,19 @@ def run_ours(args):
             cpu = {"error": str(exc)}
 
     if rank == 0:
-        value = weak_scaling_value(N, world, ms)
+        value = (N / (ms * 1e-3)) if strong else weak_scaling_value(N, world, ms)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if strong else "weak",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generators, SURVEY.md 8(d); water-like boxes by "
                     "paper_2505_09727_b200/systems.py water_box)",
             "config": {"workload": c.name, "N": N, "box_L": box[0], "r_c": c.r_c, "eps": c.eps,
                        "nf": list(plan.nf), "P": plan.P, "force_method": plan.force_method,
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                       "parallelism": (f"x-slabs x{world} (NCCL all-reduce of grid + outputs)"
+                                       if strong else f"replicas x{world}" if world > 1
+                                       else "single GPU"),
                        "l2": "256 MiB flush write before every timed step (outside the events)"},
             "impl": "ours",
             "energy": energy,
@@ -325,7 +355,8 @@ def run_ours(args):
             "stages_ms": stages_ms,
             "roofline": roofline,
             "cpu_baseline": cpu,
-            "e2e": {"value": weak_scaling_value(N, world, e2e_ms), "unit": UNIT,
+            "e2e": {"value": (N / (e2e_ms * 1e-3)) if strong else weak_scaling_value(N, world, e2e_ms),
+                    "unit": UNIT,
                     "h2d_bytes_per_step": int(N * 32), "d2h_bytes_per_step": int(N * 32 + 8),
                     "ms_per_step": e2e_ms},
         }

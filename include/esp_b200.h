@@ -121,6 +121,25 @@ int esp_evaluate_device(esp_plan* plan, const double box[3], long N, const doubl
                         const double* q_dev, double* u_dev, double* F_dev, double* energy_dev,
                         void* stream);
 
+/* Slab-decomposed evaluation for nranks GPUs (one plan per rank; the ranks
+ * may also be emulated sequentially on one GPU).  All pointers are device
+ * pointers, asynchronous on `stream`.
+ *   phase A: bins/sorts all N atoms (inputs replicated on every rank), sums
+ *            the real-space part for the targets of this rank's x-slab and
+ *            spreads this slab's atoms into grid_dev (nx*ny*nz reals).
+ *   (caller: sum grid_dev over ranks, e.g. ncclAllReduce)
+ *   phase B: FFT pipeline on the summed grid, interpolation and combine for
+ *            this slab; u/F/energy receive this rank's PARTIAL sums (zero
+ *            for atoms owned elsewhere).
+ *   (caller: sum u, F, energy over ranks)
+ * With nranks == 1 the two phases equal esp_evaluate_device. */
+int esp_eval_phase_a(esp_plan* plan, const double box[3], long N, const double* pos_dev,
+                     const double* q_dev, int rank, int nranks, double* grid_dev, void* stream);
+int esp_eval_phase_b(esp_plan* plan, int rank, int nranks, const double* grid_dev, double* u_dev,
+                     double* F_dev, double* energy_dev, void* stream);
+/* Number of reals in the charge grid (nx*ny*nz) for sizing grid_dev. */
+long esp_grid_size(const esp_plan* plan);
+
 /* require_neutral (system.hpp:39-47) on host data. */
 int esp_check_neutral(long N, const double* q);
 

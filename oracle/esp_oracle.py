@@ -457,7 +457,13 @@ def local_sum(plan: Plan, pos, q, chunk: int = 256):
 def spectral_sum(plan: Plan, pos, q):
     """ewald.hpp:524-604 (ik and ad)."""
     pos = fold(pos, plan.box)
-    g = np.fft.fftn(spread(plan, pos, q))          # forward, e^{-i}
+    return spectral_from_grid(plan, spread(plan, pos, q), pos, q)
+
+
+def spectral_from_grid(plan: Plan, grid, pos, q):
+    """ewald.hpp:542-604 from a given (spread) charge grid: FFT, scale, ik/ad."""
+    pos = fold(pos, plan.box)
+    g = np.fft.fftn(np.asarray(grid).reshape(plan.nf))   # forward, e^{-i}
     c = g * plan.influence
     if plan.force_method == "ad":
         grid = np.fft.ifftn(c).real * np.prod(plan.nf)   # unnormalised inverse

@@ -109,6 +109,9 @@ _sig("esp_spread", [_vp, C.c_long, _dp, _dp, _dp])
 _sig("esp_interpolate", [_vp, C.c_long, _dp, _dp, _dp])
 _sig("esp_interpolate_gradient", [_vp, C.c_long, _dp, _dp, _dp])
 _sig("esp_last_launch_count", [_vp])
+_sig("esp_eval_phase_a", [_vp, _dp, C.c_long, _vp, _vp, C.c_int, C.c_int, _vp, _vp])
+_sig("esp_eval_phase_b", [_vp, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp])
+_sig("esp_grid_size", [_vp], C.c_long)
 _sig("esp_last_pair_count", [_vp, C.POINTER(C.c_ulonglong)])
 _sig("esp_fp64_peak", [C.c_int, C.POINTER(C.c_double)])
 
@@ -353,6 +356,27 @@ def evaluate_device(plan: EwaldPlan, box, N: int, pos_ptr: int, q_ptr: int, u_pt
     _check(_lib.esp_evaluate_device(plan._h, _f64(box, (3,)), int(N), C.c_void_p(pos_ptr),
                                     C.c_void_p(q_ptr), C.c_void_p(u_ptr), C.c_void_p(F_ptr),
                                     C.c_void_p(energy_ptr), C.c_void_p(stream)))
+
+
+def eval_phase_a(plan: EwaldPlan, box, N: int, pos_ptr: int, q_ptr: int, rank: int, nranks: int,
+                 grid_ptr: int, stream: int = 0) -> None:
+    """Slab decomposition, phase A (see include/esp_b200.h): real-space sum for
+    this rank's targets, spread of its atoms into the grid at grid_ptr."""
+    _check(_lib.esp_eval_phase_a(plan._h, _f64(box, (3,)), int(N), C.c_void_p(pos_ptr),
+                                 C.c_void_p(q_ptr), int(rank), int(nranks), C.c_void_p(grid_ptr),
+                                 C.c_void_p(stream)))
+
+
+def eval_phase_b(plan: EwaldPlan, rank: int, nranks: int, grid_ptr: int, u_ptr: int, F_ptr: int,
+                 energy_ptr: int, stream: int = 0) -> None:
+    """Phase B on the rank-summed grid: this rank's partial u, F, energy."""
+    _check(_lib.esp_eval_phase_b(plan._h, int(rank), int(nranks), C.c_void_p(grid_ptr),
+                                 C.c_void_p(u_ptr), C.c_void_p(F_ptr), C.c_void_p(energy_ptr),
+                                 C.c_void_p(stream)))
+
+
+def grid_size(plan: EwaldPlan) -> int:
+    return int(_lib.esp_grid_size(plan._h))
 
 
 def local_sum(plan: EwaldPlan, system: ParticleSystem) -> PartialField:

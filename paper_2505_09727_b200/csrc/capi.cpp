@@ -323,6 +323,29 @@ int esp_evaluate_device(esp_plan* p, const double box[3], long N, const double* 
     });
 }
 
+int esp_eval_phase_a(esp_plan* p, const double box[3], long N, const double* pos_dev,
+                     const double* q_dev, int rank, int nranks, double* grid_dev, void* stream) {
+    return guarded([&] {
+        espb::Engine& e = engine(p);
+        check_box(p, box, "evaluate");
+        check_n(N);
+        e.phase_a(N, pos_dev, q_dev, rank, nranks, grid_dev, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int esp_eval_phase_b(esp_plan* p, int rank, int nranks, const double* grid_dev, double* u_dev,
+                     double* F_dev, double* energy_dev, void* stream) {
+    return guarded([&] {
+        espb::Engine& e = engine(p);
+        e.phase_b(rank, nranks, grid_dev, u_dev, F_dev, energy_dev,
+                  static_cast<cudaStream_t>(stream));
+    });
+}
+
+long esp_grid_size(const esp_plan* p) {
+    return p ? static_cast<long>(p->plan.nf[0]) * p->plan.nf[1] * p->plan.nf[2] : 0;
+}
+
 int esp_local_sum(esp_plan* p, const double box[3], long N, const double* pos, const double* q,
                   double* u, double* F) {
     return guarded([&] {

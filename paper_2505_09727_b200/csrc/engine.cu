@@ -36,6 +36,7 @@ struct GridArgs {
     int W;
     int RS, PS;         // padded row / plane strides of the spread tile (doubles)
     int P;
+    int bin0;           // first spread bin of this launch (slab decomposition)
     const double* win;  // 3 x 4P x 13 (phi) then 3 x 4P x 13 (dphi)
 };
 
@@ -242,6 +243,7 @@ struct PairArgs {
     int M, Mz;                   // neighbourhood reach in columns / slices
     int bz;                      // target slices per CTA
     int bx;                      // target columns per CTA edge (1 or 2)
+    int blk0;                    // first target block of this launch (slab decomposition)
     int F[3];                    // fine cells per dim (columns x, y; slices z)
     double fw[3];                // fine cell edges
     double box[3];
@@ -335,7 +337,7 @@ __global__ void __launch_bounds__(128, 6) k_pair(PairArgs a, const __grid_consta
     const int ncol = W * W;
     const int nzb = (a.F[2] + a.bz - 1) / a.bz;
     const int nyb = (a.F[1] + BX - 1) / BX;
-    const int blk = blockIdx.x;
+    const int blk = blockIdx.x + a.blk0;
     const int bzi = blk % nzb;
     const int fy0 = ((blk / nzb) % nyb) * BX;
     const int fx0 = (blk / (nzb * nyb)) * BX;
@@ -585,13 +587,14 @@ __global__ void __launch_bounds__(128, 6) k_pair(PairArgs a, const __grid_consta
 // All-pairs fallback when some nc_d < 3 (ewald.hpp:457-470): min image by
 // rounding, thread per target atom.
 template <int ND>
-__global__ void __launch_bounds__(128) k_pair_allpairs(long N, const double4* __restrict__ xyzq,
+__global__ void __launch_bounds__(128) k_pair_allpairs(long N, long i0, long i1,
+                                                       const double4* __restrict__ xyzq,
                                                        double4* __restrict__ loc, double bx,
                                                        double by, double bz,
                                                        unsigned long long* npairs,
                                                        const __grid_constant__ PairConsts k) {
-    long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
-    if (i >= N) return;
+    const long i = i0 + blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+    if (i >= i1) return;
     const double4 pi = xyzq[i];
     double u = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
     int npair = 0;
@@ -637,7 +640,7 @@ __global__ void __launch_bounds__(512) k_spread(GridArgs g, const double4* __res
     double* tile = reinterpret_cast<double*>(smem) + kSpreadChunk * 3 * MP + kSpreadChunk * 2;
     const int W = g.W, RS = g.RS, PS = g.PS;
     const int nt = blockDim.x;
-    const int bin = blockIdx.x;
+    const int bin = blockIdx.x + g.bin0;
     const int bz = bin % g.nb[2], by = (bin / g.nb[2]) % g.nb[1], bx = bin / (g.nb[1] * g.nb[2]);
     const int ib = start[bin], ie = start[bin + 1];
     if (ib == ie) return;
@@ -748,6 +751,8 @@ struct InterpArgs {
     double* u;             // original order
     double* F;             // original order, N x 3
     double* epart;         // per-block energy partial sums
+    const int* startB;     // if set: only atoms of spread bins [bin_lo, bin_hi)
+    int bin_lo, bin_hi;
 };
 
 // Thread per atom (spread-bin order, so neighbouring threads share grid
@@ -765,9 +770,14 @@ __global__ void __launch_bounds__(128) k_interp(GridArgs g, InterpArgs a) {
     for (int t = threadIdx.x; t < ntab; t += blockDim.x) tab[t] = g.win[t];
     __syncthreads();
 
-    const long k = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+    long k = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+    long kend = a.N;
+    if (a.startB) {
+        k += a.startB[a.bin_lo];
+        kend = a.startB[a.bin_hi];
+    }
     double e = 0.0;
-    if (k < a.N) {
+    if (k < kend) {
         const double4 v = a.xyzq[k];
         const int o = a.orig[k];
         const Foot f[3] = {footprint(P, v.x, g.h[0], g.half[0]),
@@ -883,6 +893,8 @@ __global__ void __launch_bounds__(128) k_interp(GridArgs g, InterpArgs a) {
                 Fy += l.z;
                 Fz += l.w;
                 e = qi * us;
+            } else {
+                us -= qi * a.self_coef;  // self term (0 for the spectral_sum API)
             }
             a.u[o] = us;
             a.F[3 * o + 0] = Fx;
@@ -916,7 +928,7 @@ __global__ void __launch_bounds__(256) k_combine(long N, const double4* __restri
     if (i < N) {
         const double4 l = loc[i];
         const double qi = xyzq_orig[i].w;
-        const double ui = (l.x + u[i]) - qi * self_coef;
+        const double ui = l.x + u[i];  // u holds u_s - q s0 (self folded in K3)
         u[i] = ui;
         F[3 * i + 0] += l.y;
         F[3 * i + 1] += l.z;
@@ -1298,16 +1310,19 @@ void Engine::prepare(long N, const double* pos, const double* q, double* qsum_de
     }
 }
 
-void Engine::run_pair(long N, cudaStream_t s) {
+void Engine::run_pair(long N, cudaStream_t s, int rank, int nranks) {
     if (N == 0) return;
     const Plan& p = plan_;
     int nd = 20;
     PairConsts k = make_pair_consts(p, nd);
     if (!cells_ok_) {
-        // all-pairs path works on the folded, original-order copy
+        // all-pairs path works on the folded, original-order copy; a slab is a
+        // contiguous range of targets
+        const long i0 = N * rank / nranks, i1 = N * (rank + 1) / nranks;
+        if (i1 <= i0) return;
         auto go = [&](auto kern) {
-            kern<<<grid1(N, 128), 128, 0, s>>>(N, d_tmp_, d_loc_, p.box[0], p.box[1], p.box[2],
-                                               d_npairs_, k);
+            kern<<<grid1(i1 - i0, 128), 128, 0, s>>>(N, i0, i1, d_tmp_, d_loc_, p.box[0],
+                                                     p.box[1], p.box[2], d_npairs_, k);
         };
         if (nd == 20) go(k_pair_allpairs<20>);
         else if (nd == 28) go(k_pair_allpairs<28>);
@@ -1354,8 +1369,14 @@ void Engine::run_pair(long N, cudaStream_t s) {
         a.bx = best_bx;
         a.bz = best_bz;
     }
-    const int nblocks = ((F_[0] + a.bx - 1) / a.bx) * ((F_[1] + a.bx - 1) / a.bx) *
-                        ((F_[2] + a.bz - 1) / a.bz);
+    // slab decomposition: rank owns x-column blocks [lo, hi) (x-major block order)
+    const int nbx = (F_[0] + a.bx - 1) / a.bx;
+    const int per_x = ((F_[1] + a.bx - 1) / a.bx) * ((F_[2] + a.bz - 1) / a.bz);
+    const int xlo = static_cast<int>(static_cast<long>(nbx) * rank / nranks);
+    const int xhi = static_cast<int>(static_cast<long>(nbx) * (rank + 1) / nranks);
+    a.blk0 = xlo * per_x;
+    const int nblocks = (xhi - xlo) * per_x;
+    if (nblocks <= 0) return;
     if (N >= (1L << 27)) throw InvalidArgument("pair kernel: N must be < 2^27");
     size_t sm = (a.cap + 1) * sizeof(float4) + 4 * (64 + kMaxCol) * sizeof(int) +
                 4 * a.lcap * sizeof(unsigned short);
@@ -1378,17 +1399,87 @@ void Engine::run_pair(long N, cudaStream_t s) {
     ++launches_;
 }
 
-void Engine::run_spread(long N, cudaStream_t s) {
+void Engine::run_spread(long N, cudaStream_t s, int rank, int nranks, double* grid) {
     const Plan& p = plan_;
-    CK(cudaMemsetAsync(d_grid_, 0, sizeof(double) * M_, s));
+    if (!grid) grid = d_grid_;
+    CK(cudaMemsetAsync(grid, 0, sizeof(double) * M_, s));
     if (N == 0) return;
-    const GridArgs g = grid_args();
-    dispatch_P<SpreadLaunch>(p.P, g, nbin_, d_xyzqB_, d_startB_, d_grid_, s);
+    GridArgs g = grid_args();
+    int b0, b1;
+    slab_bins(rank, nranks, &b0, &b1);
+    if (b1 <= b0) return;
+    g.bin0 = b0;
+    dispatch_P<SpreadLaunch>(p.P, g, b1 - b0, d_xyzqB_, d_startB_, grid, s);
     ++launches_;
 }
 
+void Engine::slab_bins(int rank, int nranks, int* b0, int* b1) const {
+    // spread bins are x-major: rank owns bx in [lo, hi)
+    const int per_x = nb_[1] * nb_[2];
+    *b0 = static_cast<int>(static_cast<long>(nb_[0]) * rank / nranks) * per_x;
+    *b1 = static_cast<int>(static_cast<long>(nb_[0]) * (rank + 1) / nranks) * per_x;
+}
+
+void Engine::phase_a(long N, const double* pos, const double* q, int rank, int nranks,
+                     double* grid_out, cudaStream_t s) {
+    CK(cudaSetDevice(device_));
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw InvalidArgument("bad rank / nranks");
+    launches_ = 0;
+    ensure_capacity(N);
+    prepare(N, pos, q, nullptr, s);
+    if (N > 0) CK(cudaMemsetAsync(d_loc_, 0, sizeof(double4) * N, s));
+    run_pair(N, s, rank, nranks);
+    run_spread(N, s, rank, nranks, grid_out);
+    phase_n_ = N;
+}
+
+void Engine::phase_b(int rank, int nranks, const double* grid_in, double* u, double* F,
+                     double* energy_dev, cudaStream_t s) {
+    CK(cudaSetDevice(device_));
+    const long N = phase_n_;
+    if (N > 0) {
+        CK(cudaMemsetAsync(u, 0, sizeof(double) * N, s));
+        CK(cudaMemsetAsync(F, 0, sizeof(double) * 3 * N, s));
+    }
+    CF(cufftSetStream(fwd_, s));
+    CF(cufftExecD2Z(fwd_, const_cast<double*>(grid_in), d_spec_));
+    k_scale<<<grid1(Mh_, 256), 256, 0, s>>>(Mh_, plan_.nf[1], plan_.nf[2] / 2 + 1, d_influence_,
+                                            d_xi_, plan_.nf[0], plan_.nf[2], d_spec_, d_spec4_,
+                                            nfields_);
+    CK(cudaGetLastError());
+    ++launches_;
+    CF(cufftSetStream(inv_, s));
+    CF(cufftExecZ2D(inv_, d_spec4_, d_fields_));
+    InterpArgs a{};
+    a.N = N;
+    a.xyzq = d_xyzqB_;
+    a.orig = d_origB_;
+    a.fields = d_fields_;
+    a.M = M_;
+    a.u = u;
+    a.F = F;
+    a.self_coef = plan_.self_coef;
+    a.startB = d_startB_;
+    slab_bins(rank, nranks, &a.bin_lo, &a.bin_hi);
+    const GridArgs g = grid_args();
+    if (N > 0 && a.bin_hi > a.bin_lo) {
+        dispatch_P<InterpLaunch>(plan_.P, static_cast<int>(kSpectral), nfields_ == 4, g, a, s);
+        ++launches_;
+    }
+    const int nblk = static_cast<int>(grid1(std::max<long>(N, 1), 256));
+    if (N > 0) {
+        k_combine<<<nblk, 256, 0, s>>>(N, d_loc_, d_tmp_, plan_.self_coef, u, F, d_epart_);
+        CK(cudaGetLastError());
+        k_energy<<<1, 256, 0, s>>>(d_epart_, nblk, energy_dev);
+        CK(cudaGetLastError());
+        launches_ += 2;
+    } else {
+        CK(cudaMemsetAsync(energy_dev, 0, sizeof(double), s));
+    }
+}
+
 void Engine::run_grid(long N, cudaStream_t s, StageTimes* t) {
-    run_spread(N, s);
+    run_spread(N, s, 0, 1, nullptr);
     if (t) CK(cudaEventRecord(ev_t_[3], s));
     CF(cufftSetStream(fwd_, s));
     CF(cufftExecD2Z(fwd_, d_grid_, d_spec_));
@@ -1478,15 +1569,16 @@ void Engine::enqueue(long N, const double* pos, const double* q, double* u, doub
     a.orig = d_origB_;
     a.fields = d_fields_;
     a.M = M_;
-    a.u = u;  // spectral part lands in the caller's arrays, combined below
+    a.u = u;  // spectral part (minus self) lands in the caller's arrays, combined below
     a.F = F;
+    a.self_coef = plan_.self_coef;
     const GridArgs g = grid_args();
     if (t) {
         // serialised on the caller's stream so that each stage is timed alone
         CK(cudaEventRecord(ev_t_[0], s));
         prepare(N, pos, q, qsum_dev, s);
         CK(cudaEventRecord(ev_t_[1], s));
-        run_pair(N, s);
+        run_pair(N, s, 0, 1);
         CK(cudaEventRecord(ev_t_[2], s));
         run_grid(N, s, t);
         if (N > 0) {
@@ -1506,7 +1598,7 @@ void Engine::enqueue(long N, const double* pos, const double* q, double* u, doub
             ++launches_;
         }
         CK(cudaEventRecord(ev_join_, aux_));
-        run_pair(N, s);
+        run_pair(N, s, 0, 1);
         CK(cudaStreamWaitEvent(s, ev_join_, 0));
     }
     const int nblk = static_cast<int>(grid1(std::max<long>(N, 1), 256));
@@ -1543,7 +1635,7 @@ void Engine::local_sum(long N, const double* pos, const double* q, double* u, do
     CK(cudaSetDevice(device_));
     ensure_capacity(N);
     prepare(N, pos, q, nullptr, s);
-    run_pair(N, s);
+    run_pair(N, s, 0, 1);
     if (N > 0) {
         k_unpack<<<grid1(N, 256), 256, 0, s>>>(N, d_loc_, u, F);
         CK(cudaGetLastError());
@@ -1577,7 +1669,7 @@ void Engine::spread(long N, const double* pos, const double* q, double* grid, cu
     CK(cudaSetDevice(device_));
     ensure_capacity(N);
     prepare(N, pos, q, nullptr, s);
-    run_spread(N, s);
+    run_spread(N, s, 0, 1, nullptr);
     CK(cudaMemcpyAsync(grid, d_grid_, sizeof(double) * M_, cudaMemcpyDeviceToDevice, s));
 }
 

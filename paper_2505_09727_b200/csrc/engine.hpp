@@ -59,6 +59,18 @@ public:
     void interpolate_gradient(long N, const double* pos, const double* grid, double* out,
                               cudaStream_t s);
 
+    // Slab-decomposed evaluation over `nranks` GPUs (or emulated ranks).
+    // Phase A (rank-local): bin/sort all atoms, real-space sum for the targets
+    // in this rank's x-slab, spread this slab's atoms into grid_out (M reals).
+    // The caller sums grid_out over ranks (NCCL all-reduce), then phase B: the
+    // FFT pipeline on the summed grid, interpolation for this slab's atoms and
+    // the combine; u/F/energy are this rank's partial sums (zero elsewhere) to
+    // be summed over ranks.
+    void phase_a(long N, const double* pos, const double* q, int rank, int nranks,
+                 double* grid_out, cudaStream_t s);
+    void phase_b(int rank, int nranks, const double* grid_in, double* u, double* F,
+                 double* energy_dev, cudaStream_t s);
+
     // Launch count of the last evaluate() (our kernels only, excluding cuFFT).
     int last_launches() const { return launches_; }
     // Ordered in-range pairs (0 < r < r_c) evaluated by the last pair-kernel
@@ -70,9 +82,11 @@ private:
                  double* energy_dev, double* qsum_dev, cudaStream_t s, StageTimes* t);
     void ensure_capacity(long N);
     void prepare(long N, const double* pos, const double* q, double* qsum_dev, cudaStream_t s);
-    void run_pair(long N, cudaStream_t s);
+    void run_pair(long N, cudaStream_t s, int rank, int nranks);
     void run_grid(long N, cudaStream_t s, StageTimes* t);
-    void run_spread(long N, cudaStream_t s);
+    void run_spread(long N, cudaStream_t s, int rank, int nranks, double* grid);
+    void slab_bins(int rank, int nranks, int* b0, int* b1) const;
+    long phase_n_ = 0;
     GridArgs grid_args() const;
 
     const Plan& plan_;

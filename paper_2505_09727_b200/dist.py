@@ -38,3 +38,40 @@ def max_over_ranks(values, device=None):
 def weak_scaling_value(atoms_per_rank: int, world: int, ms_per_step: float) -> float:
     """Whole-job atoms*evals/s for `world` replicas timed at the max step time."""
     return atoms_per_rank * world / (ms_per_step * 1e-3)
+
+
+class _Lib:
+    """The real engine: the C-ABI phase entry points (device pointers)."""
+
+    @staticmethod
+    def phase_a(plan, box, N, pos, q, rank, nranks, grid, stream):
+        from . import eval_phase_a
+        eval_phase_a(plan, box, N, pos.data_ptr(), q.data_ptr(), rank, nranks, grid.data_ptr(),
+                     stream)
+
+    @staticmethod
+    def phase_b(plan, rank, nranks, grid, u, F, e, stream):
+        from . import eval_phase_b
+        eval_phase_b(plan, rank, nranks, grid.data_ptr(), u.data_ptr(), F.data_ptr(),
+                     e.data_ptr(), stream)
+
+
+def evaluate_slab(plan, box, N, pos, q, out, grid, rank, nranks, stream=0, group=None,
+                  engine=_Lib):
+    """One rank's share of a slab-decomposed ESP evaluation (strong scaling).
+
+    pos (3N), q (N): the full system on every rank (torch tensors); out: 4N+1
+    doubles receiving [u | F | energy] summed over ranks; grid: nx*ny*nz
+    doubles of scratch.  Two sums cross the ranks: the partial charge grids
+    (after spreading) and the partial outputs -- both NCCL all-reduces over
+    NVLink on the GPU box (gloo in the CPU tests).  engine is the per-rank
+    compute (the C-ABI phases by default)."""
+    import torch.distributed as dist
+    use = dist.is_available() and dist.is_initialized() and nranks > 1
+    engine.phase_a(plan, box, N, pos, q, rank, nranks, grid, stream)
+    if use:
+        dist.all_reduce(grid, group=group)
+    engine.phase_b(plan, rank, nranks, grid, out[:N], out[N:4 * N], out[4 * N:], stream)
+    if use:
+        dist.all_reduce(out, group=group)
+    return out
