@@ -170,6 +170,10 @@ int esp_last_pair_count(esp_plan* plan, unsigned long long* ordered_pairs);
  * microbenchmark; the fp64 roofline denominator). */
 int esp_fp64_peak(int device, double* tflops);
 
+/* Ordered pairs per second of the pair evaluation alone (operands in
+ * registers, no neighbour search): the ceiling of K4's inner work. */
+int esp_pair_eval_rate(esp_plan* plan, double* pairs_per_s);
+
 #ifdef __cplusplus
 }
 #endif

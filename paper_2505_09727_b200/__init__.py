@@ -114,6 +114,7 @@ _sig("esp_eval_phase_b", [_vp, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp])
 _sig("esp_grid_size", [_vp], C.c_long)
 _sig("esp_last_pair_count", [_vp, C.POINTER(C.c_ulonglong)])
 _sig("esp_fp64_peak", [C.c_int, C.POINTER(C.c_double)])
+_sig("esp_pair_eval_rate", [_vp, C.POINTER(C.c_double)])
 
 
 def _check(rc: int):
@@ -246,6 +247,13 @@ class EwaldPlan:
         v = C.c_ulonglong()
         _check(_lib.esp_last_pair_count(self._h, C.byref(v)))
         return int(v.value)
+
+
+def pair_eval_rate(plan) -> float:
+    """Ordered pairs/s of the K4 evaluation alone (no neighbour search)."""
+    v = C.c_double()
+    _check(_lib.esp_pair_eval_rate(plan._h, C.byref(v)))
+    return float(v.value)
 
 
 def fp64_peak_tflops(device: int = 0) -> float:

@@ -450,6 +450,13 @@ int esp_last_pair_count(esp_plan* p, unsigned long long* ordered_pairs) {
     });
 }
 
+int esp_pair_eval_rate(esp_plan* p, double* pairs_per_s) {
+    return guarded([&] {
+        engine(p);
+        *pairs_per_s = espb::pair_eval_rate(p->plan, p->device);
+    });
+}
+
 int esp_fp64_peak(int device, double* tflops) {
     return guarded([&] { *tflops = espb::fp64_peak_tflops(device); });
 }

@@ -987,6 +987,24 @@ __global__ void __launch_bounds__(256) k_dfma_peak(double* out, int iters, doubl
     if (s == 12345.678) out[0] = s;  // keep the chains alive
 }
 
+// Microbenchmark of the K4 pair evaluation alone (operands in registers):
+// the ceiling of K4's inner work, for the roofline discussion.
+template <int ND>
+__global__ void __launch_bounds__(128) k_pair_eval_bench(const __grid_constant__ PairConsts k,
+                                                         int iters, double* out) {
+    const int lane = threadIdx.x & 31;
+    double u = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
+    int npair = 0;
+    const double xi = 0.1 * lane, yi = 0.2, zi = 0.3;
+    double4 pj = make_double4(1.0 + 0.01 * lane, 0.9, 0.7, 1.0);
+    for (int it = 0; it < iters; ++it) {
+        pair_eval<ND>(k, pj, 0.0, 0.0, 0.0, xi, yi, zi, u, fx, fy, fz, npair);
+        pj.x += 1e-9;
+    }
+    if (u + fx + fy + fz == 1.2345) out[0] = u;
+    if (npair == -1) out[1] = 0.0;
+}
+
 // Unpack (u_l, F_l) to the caller's layout (local_sum only).
 __global__ void k_unpack(long N, const double4* __restrict__ loc, double* u, double* F) {
     long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
@@ -1353,10 +1371,10 @@ void Engine::run_pair(long N, cudaStream_t s, int rank, int nranks) {
     // fits one staging chunk
     {
         const double per_cell = static_cast<double>(N) / ncellF_;
-        int best_bx = 1, best_bz = 4;
+        int best_bx = 1, best_bz = 2;
         double best_t = -1.0;
         for (int bx : {1, 2})
-            for (int bz : {4, 8}) {
+            for (int bz : {2, 4, 8}) {
                 if (F_[0] < bx + 2 * pM_ || F_[1] < bx + 2 * pM_ || F_[2] < bz + 2 * pMz_) continue;
                 const double nbr = per_cell * (bx + 2 * pM_) * (bx + 2 * pM_) * (bz + 2 * pMz_);
                 const double tgt = per_cell * bx * bx * bz;
@@ -1715,6 +1733,41 @@ unsigned long long Engine::last_pair_count() const {
     unsigned long long v = 0;
     CK(cudaMemcpy(&v, d_npairs_, sizeof(v), cudaMemcpyDeviceToHost));
     return v;
+}
+
+double pair_eval_rate(const Plan& p, int device) {
+    CK(cudaSetDevice(device));
+    int nd = 20;
+    PairConsts k = make_pair_consts(p, nd);
+    k.rc2 = 1e30;  // every pair "in range"
+    double* out = nullptr;
+    CK(cudaMalloc(&out, 2 * sizeof(double)));
+    cudaDeviceProp prop{};
+    CK(cudaGetDeviceProperties(&prop, device));
+    const int blocks = prop.multiProcessorCount * 16, threads = 128, iters = 2000;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    auto go = [&](auto kern) {
+        kern<<<blocks, threads>>>(k, 100, out);
+        CK(cudaEventRecord(e0));
+        kern<<<blocks, threads>>>(k, iters, out);
+        CK(cudaEventRecord(e1));
+    };
+    switch (nd) {
+        case 15: go(k_pair_eval_bench<15>); break;
+        case 16: go(k_pair_eval_bench<16>); break;
+        case 17: go(k_pair_eval_bench<17>); break;
+        case 18: go(k_pair_eval_bench<18>); break;
+        default: go(k_pair_eval_bench<20>); break;
+    }
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    return static_cast<double>(blocks) * threads * iters / (ms * 1e-3);  // pairs / s
 }
 
 double fp64_peak_tflops(int device) {

@@ -32,6 +32,8 @@ struct StageTimes {
 
 // Measured fp64 FMA throughput of the device (TFLOP/s), for the roofline.
 double fp64_peak_tflops(int device);
+// Ordered pairs per second of the K4 evaluation alone (operands in registers).
+double pair_eval_rate(const Plan& p, int device);
 
 class Engine {
 public:
