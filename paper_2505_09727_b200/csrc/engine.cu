@@ -244,6 +244,7 @@ struct PairArgs {
     int bz;                      // target slices per CTA
     int bx;                      // target columns per CTA edge (1 or 2)
     int blk0;                    // first target block of this launch (slab decomposition)
+    int noeval;                  // diagnostics: skip the fp64 evaluation (search cost alone)
     int F[3];                    // fine cells per dim (columns x, y; slices z)
     double fw[3];                // fine cell edges
     double box[3];
@@ -302,6 +303,11 @@ constexpr int kMaxBZ = 8;     // target slices per CTA (runtime a.bz <= kMaxBZ)
 constexpr int kMaxCol = 36;   // (BX+2M)^2 with BX <= 2, M <= 2
 constexpr int kMaxSl = kMaxBZ + 8;  // bz + 2 Mz with Mz <= 4
 constexpr int kMaxEnt = kMaxCol * kMaxSl;
+#ifndef ESP_PAIR_WARPS
+#define ESP_PAIR_WARPS 8
+#endif
+constexpr int kPairWarps = ESP_PAIR_WARPS;        // warps per K4 CTA
+constexpr int kPairThreads = 32 * kPairWarps;
 
 // One CTA per (column, slice block), one warp per target atom i.  The CTA
 // stages its neighbourhood in shared memory, ordered by (column, slice), as
@@ -315,12 +321,12 @@ constexpr int kMaxEnt = kMaxCol * kMaxSl;
 // warp-reduced once.  Neighbourhoods larger than the staging capacity are
 // processed in chunks.
 template <int ND>
-__global__ void __launch_bounds__(128, 6) k_pair(PairArgs a, const __grid_constant__ PairConsts k) {
+__global__ void __launch_bounds__(kPairThreads, kPairWarps >= 8 ? 3 : 6) k_pair(PairArgs a, const __grid_constant__ PairConsts k) {
     extern __shared__ __align__(16) unsigned char smem[];
     float4* cand = reinterpret_cast<float4*>(smem);       // a.cap + 1 (sentinel)
     int* qall = reinterpret_cast<int*>(cand + a.cap + 1);  // 64 per warp
-    int* cball = qall + 4 * 64;                            // column begin, kMaxCol per warp
-    unsigned short* lall = reinterpret_cast<unsigned short*>(cball + 4 * kMaxCol);  // a.lcap per warp
+    int* cball = qall + kPairWarps * 64;                   // column begin, kMaxCol per warp
+    unsigned short* lall = reinterpret_cast<unsigned short*>(cball + kPairWarps * kMaxCol);  // a.lcap per warp
     __shared__ int ent_src[kMaxEnt], ent_off[kMaxEnt + 1];
     __shared__ unsigned char ent_slot[kMaxEnt];
     __shared__ double shiftv[27][3];
@@ -537,7 +543,7 @@ __global__ void __launch_bounds__(128, 6) k_pair(PairArgs a, const __grid_consta
                         __syncwarp();
                         qw[lane] = extra;
                         qn -= 32;
-                        if (have_pf)
+                        if (have_pf && !a.noeval)
                             pair_eval<ND>(k, pf, shiftv[tf][0], shiftv[tf][1], shiftv[tf][2],
                                           pi.x, pi.y, pi.z, u, fx, fy, fz, npair);
                         pf = a.xyzq[cd & 0x7ffffff];
@@ -1360,12 +1366,13 @@ void Engine::run_pair(long N, cudaStream_t s, int rank, int nranks) {
         a.fw[d] = p.box[d] / F_[d];
         a.box[d] = p.box[d];
     }
-    const int nw = 4;
+    const int nw = kPairWarps;
     pair_warps_ = nw;
     a.cap = pair_cap_;
     a.lcap = std::min(pair_cap_, 1024) + 32;
     a.M = pM_;
     a.Mz = pMz_;
+    a.noeval = std::getenv("ESP_PAIR_NOEVAL") ? 1 : 0;
     // target block (bx x bx columns, bz slices): the most targets per CTA
     // (amortises the neighbourhood staging) whose expected neighbourhood still
     // fits one staging chunk
@@ -1396,8 +1403,8 @@ void Engine::run_pair(long N, cudaStream_t s, int rank, int nranks) {
     const int nblocks = (xhi - xlo) * per_x;
     if (nblocks <= 0) return;
     if (N >= (1L << 27)) throw InvalidArgument("pair kernel: N must be < 2^27");
-    size_t sm = (a.cap + 1) * sizeof(float4) + 4 * (64 + kMaxCol) * sizeof(int) +
-                4 * a.lcap * sizeof(unsigned short);
+    size_t sm = (a.cap + 1) * sizeof(float4) + nw * (64 + kMaxCol) * sizeof(int) +
+                nw * a.lcap * sizeof(unsigned short);
     auto go = [&](auto kern) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(sm)));
