@@ -678,17 +678,35 @@ __global__ void __launch_bounds__(512) k_spread(GridArgs g, const double4* __res
             fch[ai * 3 + d] = clampi(f.first - lo[d], 0, W - P);
         }
         __syncthreads();
-        for (int ai = 0; ai < nc; ++ai) {
-            const int* fo = fch + ai * 3;
-            const double* w = wch + ai * 3 * MP;
-            const int base = fo[0] * PS + fo[1] * RS + fo[2];
-            for (int p = threadIdx.x; p < P3; p += nt) {
-                const int jx = p / P2, r = p - jx * P2;
-                const int jy = r / P, jz = r - jy * P;
-                const int off = base + jx * PS + jy * RS + jz;
-                tile[off] += w[jx] * w[MP + jy] * w[2 * MP + jz];
+        if (P3 <= nt) {
+            // one footprint node per thread: its decode is atom-invariant
+            const int p = threadIdx.x;
+            const bool act = p < P3;
+            const int jx = p / P2, r = p - jx * P2;
+            const int jy = r / P, jz = r - jy * P;
+            const int myoff = jx * PS + jy * RS + jz;
+            for (int ai = 0; ai < nc; ++ai) {
+                const int* fo = fch + ai * 3;
+                const double* w = wch + ai * 3 * MP;
+                if (act) {
+                    const int off = fo[0] * PS + fo[1] * RS + fo[2] + myoff;
+                    tile[off] += w[jx] * w[MP + jy] * w[2 * MP + jz];
+                }
+                __syncthreads();
             }
-            __syncthreads();
+        } else {
+            for (int ai = 0; ai < nc; ++ai) {
+                const int* fo = fch + ai * 3;
+                const double* w = wch + ai * 3 * MP;
+                const int base = fo[0] * PS + fo[1] * RS + fo[2];
+                for (int p = threadIdx.x; p < P3; p += nt) {
+                    const int jx = p / P2, r = p - jx * P2;
+                    const int jy = r / P, jz = r - jy * P;
+                    const int off = base + jx * PS + jy * RS + jz;
+                    tile[off] += w[jx] * w[MP + jy] * w[2 * MP + jz];
+                }
+                __syncthreads();
+            }
         }
     }
     for (int t = threadIdx.x; t < tsize; t += nt) {
