@@ -245,6 +245,7 @@ struct PairArgs {
     int bx;                      // target columns per CTA edge (1 or 2)
     int blk0;                    // first target block of this launch (slab decomposition)
     int noeval;                  // diagnostics: skip the fp64 evaluation (search cost alone)
+    int noscreen;                // evaluate every listed candidate (no fp32 screening)
     int F[3];                    // fine cells per dim (columns x, y; slices z)
     double fw[3];                // fine cell edges
     double box[3];
@@ -528,6 +529,19 @@ __global__ void __launch_bounds__(kPairThreads, kPairWarps >= 8 ? 3 : 6) k_pair(
                 const int n32 = (n + 31) & ~31;
                 if (n + lane < n32) lw[n + lane] = static_cast<unsigned short>(a.cap);
                 __syncwarp();
+                if (a.noscreen) {
+                    // no fp32 screening: every listed candidate goes straight to
+                    // the fp64 evaluation (its exact r^2 test masks the rest)
+                    for (int kb = lane; kb < n32; kb += 32) {
+                        const int cd = __float_as_int(cand[lw[kb]].w);
+                        const double4 pj = a.xyzq[cd & 0x7ffffff];
+                        const int t = static_cast<unsigned>(cd) >> 27;
+                        pair_eval<ND>(k, pj, shiftv[t][0], shiftv[t][1], shiftv[t][2], pi.x,
+                                      pi.y, pi.z, u, fx, fy, fz, npair);
+                    }
+                    __syncwarp();
+                    continue;
+                }
                 for (int kb = lane; kb < n32; kb += 32) {
                     const float4 c4 = cand[lw[kb]];
                     const float dx = c4.x - xf, dy = c4.y - yf, dz = c4.z - zf;
@@ -1391,6 +1405,7 @@ void Engine::run_pair(long N, cudaStream_t s, int rank, int nranks) {
     a.M = pM_;
     a.Mz = pMz_;
     a.noeval = std::getenv("ESP_PAIR_NOEVAL") ? 1 : 0;
+    a.noscreen = std::getenv("ESP_PAIR_NOSCREEN") ? 1 : 0;
     // target block (bx x bx columns, bz slices): the most targets per CTA
     // (amortises the neighbourhood staging) whose expected neighbourhood still
     // fits one staging chunk
