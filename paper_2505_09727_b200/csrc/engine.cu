@@ -326,8 +326,7 @@ __global__ void __launch_bounds__(kPairThreads, kPairWarps >= 8 ? 3 : 6) k_pair(
     extern __shared__ __align__(16) unsigned char smem[];
     float4* cand = reinterpret_cast<float4*>(smem);       // a.cap + 1 (sentinel)
     int* qall = reinterpret_cast<int*>(cand + a.cap + 1);  // 64 per warp
-    int* cball = qall + kPairWarps * 64;                   // column begin, kMaxCol per warp
-    unsigned short* lall = reinterpret_cast<unsigned short*>(cball + kPairWarps * kMaxCol);  // a.lcap per warp
+    unsigned short* lall = reinterpret_cast<unsigned short*>(qall + kPairWarps * 64);  // a.lcap per warp
     __shared__ int ent_src[kMaxEnt], ent_off[kMaxEnt + 1];
     __shared__ unsigned char ent_slot[kMaxEnt];
     __shared__ double shiftv[27][3];
@@ -336,7 +335,6 @@ __global__ void __launch_bounds__(kPairThreads, kPairWarps >= 8 ? 3 : 6) k_pair(
     const int nw = blockDim.x >> 5;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int* qw = qall + warp * 64;
-    int* cb = cball + warp * kMaxCol;
     unsigned short* lw = lall + warp * a.lcap;
     const unsigned lt_mask = (1u << lane) - 1u;
 
@@ -604,7 +602,8 @@ __global__ void __launch_bounds__(kPairThreads, kPairWarps >= 8 ? 3 : 6) k_pair(
     }
 }
 
-// All-pairs fallback when some nc_d < 3 (ewald.hpp:457-470): min image by
+// All-pairs fallback for boxes too small for the fine stencil (the reference
+// falls back when some nc_d < 3, ewald.hpp:457-470): min image by
 // rounding, thread per target atom.
 template <int ND>
 __global__ void __launch_bounds__(128) k_pair_allpairs(long N, long i0, long i1,
@@ -772,8 +771,8 @@ __global__ void __launch_bounds__(256) k_scale(long Mh, int ny, int nzh, const d
 // ----------------------------------------------------------------------------
 
 enum InterpMode : int {
-    kCombine = 0,     // u = u_l + u_s - self, F = F_l + F_s, energy partials
-    kSpectral = 1,    // u = u_s, F = F_s
+    kSpectral = 1,    // u = u_s - q self_coef, F = F_s (evaluate passes self_coef = s0,
+                      // spectral_sum passes 0); k_combine adds the real-space part
     kValue = 2,       // out = interpolate(grid) (plain adjoint)
     kGradient = 3,    // out = interpolate_gradient(grid)
 };
@@ -803,7 +802,7 @@ __global__ void __launch_bounds__(128) k_interp(GridArgs g, InterpArgs a) {
     double* tab = reinterpret_cast<double*>(smem);  // phi (3 x 4P x 13) [+ dphi]
     constexpr int MP = PT > 0 ? PT : 16;
     const int P = PT > 0 ? PT : g.P;
-    constexpr bool need_d = (MODE == kGradient) || (!IK && (MODE == kCombine || MODE == kSpectral));
+    constexpr bool need_d = (MODE == kGradient) || (!IK && MODE == kSpectral);
     const int ntab = (need_d ? 6 : 3) * 4 * P * kNc;
     for (int t = threadIdx.x; t < ntab; t += blockDim.x) tab[t] = g.win[t];
     __syncthreads();
@@ -814,7 +813,6 @@ __global__ void __launch_bounds__(128) k_interp(GridArgs g, InterpArgs a) {
         k += a.startB[a.bin_lo];
         kend = a.startB[a.bin_hi];
     }
-    double e = 0.0;
     if (k < kend) {
         const double4 v = a.xyzq[k];
         const int o = a.orig[k];
@@ -923,33 +921,12 @@ __global__ void __launch_bounds__(128) k_interp(GridArgs g, InterpArgs a) {
                 Fz = -qi * gz;
             }
         }
-        if (MODE == kCombine || MODE == kSpectral) {
-            if (MODE == kCombine) {
-                const double4 l = a.loc[o];
-                us = (l.x + us) - qi * a.self_coef;
-                Fx += l.y;
-                Fy += l.z;
-                Fz += l.w;
-                e = qi * us;
-            } else {
-                us -= qi * a.self_coef;  // self term (0 for the spectral_sum API)
-            }
+        if (MODE == kSpectral) {
+            us -= qi * a.self_coef;  // self term (0 for the spectral_sum API)
             a.u[o] = us;
             a.F[3 * o + 0] = Fx;
             a.F[3 * o + 1] = Fy;
             a.F[3 * o + 2] = Fz;
-        }
-    }
-    if (MODE == kCombine) {
-        __shared__ double red[4];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = e;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double s = 0.0;
-            for (int w = 0; w < (blockDim.x >> 5); ++w) s += red[w];
-            a.epart[blockIdx.x] = s;
         }
     }
 }
@@ -1115,7 +1092,6 @@ struct InterpLaunch {
             CK(cudaGetLastError());
         };
         switch (mode) {
-            case kCombine: ik ? go(k_interp<P, kCombine, true>) : go(k_interp<P, kCombine, false>); break;
             case kSpectral: ik ? go(k_interp<P, kSpectral, true>) : go(k_interp<P, kSpectral, false>); break;
             case kValue: go(k_interp<P, kValue, true>); break;
             default: go(k_interp<P, kGradient, false>); break;
@@ -1149,7 +1125,6 @@ PairConsts make_pair_consts(const Plan& p, int& nd) {
 Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
     CK(cudaSetDevice(device_));
     const Plan& p = plan_;
-    for (int d = 0; d < 3; ++d) nc_[d] = std::max(1, static_cast<int>(std::floor(p.box[d] / p.r_c)));
     // fine pair cells: columns >= r_c/2 in x, y; slices >= r_c/4 in z
     F_[0] = std::max(1, static_cast<int>(std::floor(p.box[0] / (0.5 * p.r_c))));
     F_[1] = std::max(1, static_cast<int>(std::floor(p.box[1] / (0.5 * p.r_c))));
@@ -1160,8 +1135,6 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
     // the fine stencil must not alias across the period; otherwise all pairs
     cells_ok_ = pM_ <= 2 && pMz_ <= 4 && F_[0] >= 2 * pM_ + 1 && F_[1] >= 2 * pM_ + 1 &&
                 F_[2] >= 4 + 2 * pMz_;
-    pbz_ = 4;
-    ncell_ = F_[0] * F_[1] * ((F_[2] + pbz_ - 1) / pbz_);
     ncellF_ = static_cast<long>(F_[0]) * F_[1] * F_[2];
     if (ncellF_ >= (1L << 30)) throw InvalidArgument("cell list too fine for this box / r_c");
     // spread bins: the largest S in {8, 6, 4} that still gives >= 4 CTAs per SM
@@ -1436,7 +1409,7 @@ void Engine::run_pair(long N, cudaStream_t s, int rank, int nranks) {
     const int nblocks = (xhi - xlo) * per_x;
     if (nblocks <= 0) return;
     if (N >= (1L << 27)) throw InvalidArgument("pair kernel: N must be < 2^27");
-    size_t sm = (a.cap + 1) * sizeof(float4) + nw * (64 + kMaxCol) * sizeof(int) +
+    size_t sm = (a.cap + 1) * sizeof(float4) + nw * 64 * sizeof(int) +
                 nw * a.lcap * sizeof(unsigned short);
     auto go = [&](auto kern) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

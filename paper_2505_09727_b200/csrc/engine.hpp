@@ -96,9 +96,7 @@ private:
     int launches_ = 0;
 
     // geometry
-    std::array<int, 3> nc_{};   // pair cells per dim
-    bool cells_ok_ = false;     // nc >= 3 in every dim (ewald.hpp:431-434)
-    int ncell_ = 0;             // coarse cells (CTAs of the pair kernel)
+    bool cells_ok_ = false;     // fine stencil fits the period (else all pairs)
     std::array<int, 3> F_{};    // fine cells per dim (sort key of the pair path)
     long ncellF_ = 0;
     int S_ = 8;                 // spread bin edge in grid cells
@@ -111,7 +109,6 @@ private:
     int pair_warps_ = 4;
     int pair_cap_ = 2048;
     int pM_ = 2, pMz_ = 4;      // fine stencil reach (columns, slices)
-    int pbz_ = 4;
 
     // tables on device
     double* d_win_ = nullptr;        // 3 x 4P x 13 phi, then 3 x 4P x 13 dphi

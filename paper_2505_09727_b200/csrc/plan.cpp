@@ -316,32 +316,6 @@ double bspline(int P, double v) {
 }
 
 
-// Fit f on z in [-1,1] by interpolation at deg+1 Chebyshev points, return the
-// monomial coefficients in z (extended-precision conversion).
-std::vector<double> fit_z_poly(const std::function<double(double)>& f, int deg) {
-    const int n = deg + 1;
-    std::vector<double> fv(n), cheb(n);
-    for (int k = 0; k < n; ++k) fv[k] = f(std::cos(kPi * (k + 0.5) / n));
-    for (int j = 0; j < n; ++j) {
-        double s = 0.0;
-        for (int k = 0; k < n; ++k) s += fv[k] * std::cos(kPi * j * (k + 0.5) / n);
-        cheb[j] = 2.0 * s / n;
-    }
-    cheb[0] *= 0.5;
-    std::vector<std::vector<long double>> T(n, std::vector<long double>(n, 0.0L));
-    T[0][0] = 1.0L;
-    if (n > 1) T[1][1] = 1.0L;
-    for (int j = 2; j < n; ++j)
-        for (int p = 0; p < n; ++p) T[j][p] = (p > 0 ? 2.0L * T[j - 1][p - 1] : 0.0L) - T[j - 2][p];
-    std::vector<double> mono(n);
-    for (int p = 0; p < n; ++p) {
-        long double s = 0.0L;
-        for (int j = 0; j < n; ++j) s += static_cast<long double>(cheb[j]) * T[j][p];
-        mono[p] = static_cast<double>(s);
-    }
-    return mono;
-}
-
 // Same fit with the samples, transform and basis change in long double.
 std::vector<double> fit_z_poly_ld(const std::function<long double(long double)>& f, int deg) {
     const int n = deg + 1;
@@ -745,8 +719,6 @@ Plan build_plan(const std::array<double, 3>& box, Family family, double eps, dou
                 return even_legendre_integral(sp.a, y) / (sp.C0 * y);
             };
         }
-        auto Gz = [&G](double z) { return G(std::sqrt(std::max(0.0, 0.5 * (z + 1.0)))); };
-        auto Hz = [&H](double z) { return H(std::sqrt(std::max(0.0, 0.5 * (z + 1.0)))); };
         std::function<long double(long double)> Hld;  // Psi(y)/y in long double
         if (gauss) {
             const long double alpha = p.shape, sa = std::sqrt(alpha);
