@@ -46,10 +46,15 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
                     help="budget of the cpu_baseline sample (rank 0, N=1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--strong", action="store_true",
-                    help="N>1: decompose ONE system over the ranks (x-slabs, NCCL all-reduce of "
-                         "the charge grid and of the outputs) instead of one replica per rank")
+    ap.add_argument("--decomp", choices=["replicas", "slab", "pencil"], default="replicas",
+                    help="N>1: replicas = one independent system per rank (weak scaling); "
+                         "slab = ONE system, x-slabs, NCCL all-reduce of the charge grid and "
+                         "outputs; pencil = ONE system with the grid/spectrum/fields split too "
+                         "(halo exchanges + all-to-all transposes)")
+    ap.add_argument("--strong", action="store_true", help="alias of --decomp slab")
     args = ap.parse_args()
+    if args.strong:
+        args.decomp = "slab"
     args.warmup = max(args.warmup, 3)
     return args
 
@@ -202,7 +207,8 @@ def run_ours(args):
 
     from paper_2505_09727_b200.dist import max_over_ranks, replica_seed, weak_scaling_value
     base = S.config(args.workload)
-    strong = args.strong
+    decomp = args.decomp if world > 1 else "replicas"
+    strong = decomp != "replicas"
     c = S.Config(base.name, base.kind, base.N, base.L, base.r_c, base.eps,
                  seed=base.seed if strong else replica_seed(base.seed, rank))
     pos, q, box = c.system()
@@ -218,7 +224,7 @@ def run_ours(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
 
-    if strong:
+    if decomp == "slab":
         from paper_2505_09727_b200.dist import evaluate_slab
         out_d = torch.empty(4 * N + 1, dtype=torch.float64, device=dev)
         grid_d = torch.empty(E.grid_size(plan), dtype=torch.float64, device=dev)
@@ -226,6 +232,14 @@ def run_ours(args):
         def step():
             evaluate_slab(plan, box, N, pos_d, q_d, out_d, grid_d, rank, world,
                           stream.cuda_stream)
+    elif decomp == "pencil":
+        from paper_2505_09727_b200.dist import PencilBuffers, PencilLayout, evaluate_pencil
+        layout = PencilLayout.of(plan, world)
+        pbufs = PencilBuffers(layout, rank, N, dev)
+        out_d = pbufs.out
+
+        def step():
+            evaluate_pencil(plan, box, N, pos_d, q_d, pbufs, layout, rank, stream.cuda_stream)
     else:
         def step():
             E.evaluate_device(plan, box, N, pos_d.data_ptr(), q_d.data_ptr(), u_d.data_ptr(),
@@ -344,8 +358,10 @@ def run_ours(args):
             "config": {"workload": c.name, "N": N, "box_L": box[0], "r_c": c.r_c, "eps": c.eps,
                        "nf": list(plan.nf), "P": plan.P, "force_method": plan.force_method,
                        "parallelism": (f"x-slabs x{world} (NCCL all-reduce of grid + outputs)"
-                                       if strong else f"replicas x{world}" if world > 1
-                                       else "single GPU"),
+                                       if decomp == "slab" else
+                                       f"distributed FFT x{world} (NCCL halo send/recv + "
+                                       "all-to-all transposes)" if decomp == "pencil" else
+                                       f"replicas x{world}" if world > 1 else "single GPU"),
                        "l2": "256 MiB flush write before every timed step (outside the events)"},
             "impl": "ours",
             "energy": energy,

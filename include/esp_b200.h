@@ -137,6 +137,58 @@ int esp_eval_phase_a(esp_plan* plan, const double box[3], long N, const double* 
                      const double* q_dev, int rank, int nranks, double* grid_dev, void* stream);
 int esp_eval_phase_b(esp_plan* plan, int rank, int nranks, const double* grid_dev, double* u_dev,
                      double* F_dev, double* energy_dev, void* stream);
+/* Distributed-FFT evaluation: the charge grid and the
+ * fields are distributed too -- rank r holds the x-planes [x0, x1) plus
+ * `halo` planes on each side, and the spectrum's y-rows [y0, y1) between the
+ * two transposes.  The caller moves data between the steps (NCCL over
+ * NVLink on the GPU box); every pointer is a device pointer, complex buffers
+ * are interleaved (re, im) doubles, all calls asynchronous on `stream`.
+ *   esp_pencil_phase_a   bin/sort, real-space part of the rank's targets,
+ *                        spread of its atoms into slab (slab_reals doubles,
+ *                        planes x0-halo .. x1+halo-1)
+ *   caller: send slab planes [0, halo) to rank r-1 and add them into its
+ *           planes [x1-x0, x1-x0+halo); send planes [x1-x0+halo, x1-x0+2halo)
+ *           to rank r+1 and add them into its planes [halo, 2halo) (periodic)
+ *   esp_pencil_forward   2-D FFTs of the owned planes -> send (spec_local
+ *                        complex; block for rank s = rows [y0(s), y1(s)))
+ *   caller: all-to-all send -> recv (recv: spec_pencil complex; block from
+ *           rank s = its planes [x0(s), x1(s)), in rank order)
+ *   esp_pencil_solve     x-FFT, influence multiply, inverse x-FFT: recv
+ *                        (clobbered) -> A, B (spec_pencil complex each; B
+ *                        only for the ik force method, else may be NULL)
+ *   caller: all-to-all A and B back (block for rank s = planes [x0(s), x1(s)))
+ *   esp_pencil_backward  derivative spectra + inverse 2-D FFTs -> the owned
+ *                        planes of fslab (nfields * slab_reals doubles, fields
+ *                        interleaved per node)
+ *   caller: fill fslab's halo planes from the neighbours' owned planes (the
+ *           mirror of the first exchange, copying instead of adding)
+ *   esp_pencil_phase_b   interpolation + combine for the rank's atoms:
+ *                        partial u, F, energy (caller sums over ranks)
+ * nranks >= 2; esp_pencil_geometry fails with INVALID_ARGUMENT when a rank
+ * would own fewer x-planes than the halo. */
+typedef struct esp_pencil_info {
+    int nranks, rank;
+    int halo;          /* planes exchanged with each x-neighbour */
+    int x0, x1;        /* owned real-space x-planes */
+    int y0, y1;        /* owned spectral y-rows */
+    int nfields;       /* 4 (ik) or 1 (ad) */
+    int nf[3];         /* grid size */
+    long slab_reals;   /* (x1-x0+2 halo)*ny*nz */
+    long spec_local;   /* (x1-x0)*ny*(nz/2+1) complex */
+    long spec_pencil;  /* nx*(y1-y0)*(nz/2+1) complex */
+} esp_pencil_info;
+int esp_pencil_geometry(const esp_plan* plan, int rank, int nranks, esp_pencil_info* out);
+int esp_pencil_phase_a(esp_plan* plan, const double box[3], long N, const double* pos_dev,
+                       const double* q_dev, int rank, int nranks, double* slab_dev, void* stream);
+int esp_pencil_forward(esp_plan* plan, int rank, int nranks, const double* slab_dev,
+                       double* send_dev, void* stream);
+int esp_pencil_solve(esp_plan* plan, int rank, int nranks, double* recv_dev, double* A_dev,
+                     double* B_dev, void* stream);
+int esp_pencil_backward(esp_plan* plan, int rank, int nranks, const double* A_dev,
+                        const double* B_dev, double* fslab_dev, void* stream);
+int esp_pencil_phase_b(esp_plan* plan, int rank, int nranks, const double* fslab_dev,
+                       double* u_dev, double* F_dev, double* energy_dev, void* stream);
+
 /* Number of reals in the charge grid (nx*ny*nz) for sizing grid_dev. */
 long esp_grid_size(const esp_plan* plan);
 

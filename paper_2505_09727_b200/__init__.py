@@ -74,6 +74,15 @@ class _Info(C.Structure):
     ]
 
 
+class _PencilInfo(C.Structure):
+    _fields_ = [
+        ("nranks", C.c_int), ("rank", C.c_int), ("halo", C.c_int), ("x0", C.c_int),
+        ("x1", C.c_int), ("y0", C.c_int), ("y1", C.c_int), ("nfields", C.c_int),
+        ("nf", C.c_int * 3),
+        ("slab_reals", C.c_long), ("spec_local", C.c_long), ("spec_pencil", C.c_long),
+    ]
+
+
 class _Timings(C.Structure):
     _fields_ = [(k, C.c_double) for k in
                 ("local", "spread", "fft", "scale", "ifft", "interpolate", "bin")]
@@ -112,6 +121,12 @@ _sig("esp_last_launch_count", [_vp])
 _sig("esp_eval_phase_a", [_vp, _dp, C.c_long, _vp, _vp, C.c_int, C.c_int, _vp, _vp])
 _sig("esp_eval_phase_b", [_vp, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp])
 _sig("esp_grid_size", [_vp], C.c_long)
+_sig("esp_pencil_geometry", [_vp, C.c_int, C.c_int, C.POINTER(_PencilInfo)])
+_sig("esp_pencil_phase_a", [_vp, _dp, C.c_long, _vp, _vp, C.c_int, C.c_int, _vp, _vp])
+_sig("esp_pencil_forward", [_vp, C.c_int, C.c_int, _vp, _vp, _vp])
+_sig("esp_pencil_solve", [_vp, C.c_int, C.c_int, _vp, _vp, _vp, _vp])
+_sig("esp_pencil_backward", [_vp, C.c_int, C.c_int, _vp, _vp, _vp, _vp])
+_sig("esp_pencil_phase_b", [_vp, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp])
 _sig("esp_last_pair_count", [_vp, C.POINTER(C.c_ulonglong)])
 _sig("esp_fp64_peak", [C.c_int, C.POINTER(C.c_double)])
 _sig("esp_pair_eval_rate", [_vp, C.POINTER(C.c_double)])
@@ -381,6 +396,51 @@ def eval_phase_b(plan: EwaldPlan, rank: int, nranks: int, grid_ptr: int, u_ptr: 
     _check(_lib.esp_eval_phase_b(plan._h, int(rank), int(nranks), C.c_void_p(grid_ptr),
                                  C.c_void_p(u_ptr), C.c_void_p(F_ptr), C.c_void_p(energy_ptr),
                                  C.c_void_p(stream)))
+
+
+def pencil_geometry(plan: EwaldPlan, rank: int, nranks: int) -> dict:
+    """Distributed-FFT geometry of one rank (include/esp_b200.h esp_pencil_info):
+    owned x-planes [x0, x1) with `halo` planes each side, spectral rows
+    [y0, y1), buffer sizes.  Host-only plans work too."""
+    g = _PencilInfo()
+    _check(_lib.esp_pencil_geometry(plan._h, int(rank), int(nranks), C.byref(g)))
+    d = {k: getattr(g, k) for k, _ in _PencilInfo._fields_}
+    d["nf"] = tuple(g.nf)
+    return d
+
+
+def pencil_phase_a(plan: EwaldPlan, box, N: int, pos_ptr: int, q_ptr: int, rank: int,
+                   nranks: int, slab_ptr: int, stream: int = 0) -> None:
+    _check(_lib.esp_pencil_phase_a(plan._h, _f64(box, (3,)), int(N), C.c_void_p(pos_ptr),
+                                   C.c_void_p(q_ptr), int(rank), int(nranks),
+                                   C.c_void_p(slab_ptr), C.c_void_p(stream)))
+
+
+def pencil_forward(plan: EwaldPlan, rank: int, nranks: int, slab_ptr: int, send_ptr: int,
+                   stream: int = 0) -> None:
+    _check(_lib.esp_pencil_forward(plan._h, int(rank), int(nranks), C.c_void_p(slab_ptr),
+                                   C.c_void_p(send_ptr), C.c_void_p(stream)))
+
+
+def pencil_solve(plan: EwaldPlan, rank: int, nranks: int, recv_ptr: int, A_ptr: int,
+                 B_ptr: int, stream: int = 0) -> None:
+    _check(_lib.esp_pencil_solve(plan._h, int(rank), int(nranks), C.c_void_p(recv_ptr),
+                                 C.c_void_p(A_ptr), C.c_void_p(B_ptr or None),
+                                 C.c_void_p(stream)))
+
+
+def pencil_backward(plan: EwaldPlan, rank: int, nranks: int, A_ptr: int, B_ptr: int,
+                    fslab_ptr: int, stream: int = 0) -> None:
+    _check(_lib.esp_pencil_backward(plan._h, int(rank), int(nranks), C.c_void_p(A_ptr),
+                                    C.c_void_p(B_ptr or None), C.c_void_p(fslab_ptr),
+                                    C.c_void_p(stream)))
+
+
+def pencil_phase_b(plan: EwaldPlan, rank: int, nranks: int, fslab_ptr: int, u_ptr: int,
+                   F_ptr: int, energy_ptr: int, stream: int = 0) -> None:
+    _check(_lib.esp_pencil_phase_b(plan._h, int(rank), int(nranks), C.c_void_p(fslab_ptr),
+                                   C.c_void_p(u_ptr), C.c_void_p(F_ptr), C.c_void_p(energy_ptr),
+                                   C.c_void_p(stream)))
 
 
 def grid_size(plan: EwaldPlan) -> int:

@@ -342,6 +342,72 @@ int esp_eval_phase_b(esp_plan* p, int rank, int nranks, const double* grid_dev, 
     });
 }
 
+int esp_pencil_geometry(const esp_plan* p, int rank, int nranks, esp_pencil_info* out) {
+    return guarded([&] {
+        if (!p || !out) throw espb::InvalidArgument("null argument");
+        const espb::PencilGeom G = espb::pencil_geometry(p->plan, rank, nranks);
+        out->nranks = G.nranks;
+        out->rank = G.rank;
+        out->halo = G.halo;
+        out->x0 = G.x0;
+        out->x1 = G.x1;
+        out->y0 = G.y0;
+        out->y1 = G.y1;
+        out->nfields = G.nfields;
+        for (int d = 0; d < 3; ++d) out->nf[d] = p->plan.nf[d];
+        out->slab_reals = G.slab_reals;
+        out->spec_local = G.spec_local;
+        out->spec_pencil = G.spec_pencil;
+    });
+}
+
+int esp_pencil_phase_a(esp_plan* p, const double box[3], long N, const double* pos_dev,
+                       const double* q_dev, int rank, int nranks, double* slab_dev, void* stream) {
+    return guarded([&] {
+        espb::Engine& e = engine(p);
+        check_box(p, box, "evaluate");
+        check_n(N);
+        e.pencil_phase_a(N, pos_dev, q_dev, rank, nranks, slab_dev,
+                         static_cast<cudaStream_t>(stream));
+    });
+}
+
+int esp_pencil_forward(esp_plan* p, int rank, int nranks, const double* slab_dev,
+                       double* send_dev, void* stream) {
+    return guarded([&] {
+        engine(p).pencil_forward(rank, nranks, slab_dev,
+                                 reinterpret_cast<cufftDoubleComplex*>(send_dev),
+                                 static_cast<cudaStream_t>(stream));
+    });
+}
+
+int esp_pencil_solve(esp_plan* p, int rank, int nranks, double* recv_dev, double* A_dev,
+                     double* B_dev, void* stream) {
+    return guarded([&] {
+        engine(p).pencil_solve(rank, nranks, reinterpret_cast<cufftDoubleComplex*>(recv_dev),
+                               reinterpret_cast<cufftDoubleComplex*>(A_dev),
+                               reinterpret_cast<cufftDoubleComplex*>(B_dev),
+                               static_cast<cudaStream_t>(stream));
+    });
+}
+
+int esp_pencil_backward(esp_plan* p, int rank, int nranks, const double* A_dev,
+                        const double* B_dev, double* fslab_dev, void* stream) {
+    return guarded([&] {
+        engine(p).pencil_backward(rank, nranks, reinterpret_cast<const cufftDoubleComplex*>(A_dev),
+                                  reinterpret_cast<const cufftDoubleComplex*>(B_dev), fslab_dev,
+                                  static_cast<cudaStream_t>(stream));
+    });
+}
+
+int esp_pencil_phase_b(esp_plan* p, int rank, int nranks, const double* fslab_dev, double* u_dev,
+                       double* F_dev, double* energy_dev, void* stream) {
+    return guarded([&] {
+        engine(p).pencil_phase_b(rank, nranks, fslab_dev, u_dev, F_dev, energy_dev,
+                                 static_cast<cudaStream_t>(stream));
+    });
+}
+
 long esp_grid_size(const esp_plan* p) {
     return p ? static_cast<long>(p->plan.nf[0]) * p->plan.nf[1] * p->plan.nf[2] : 0;
 }

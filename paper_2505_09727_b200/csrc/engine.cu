@@ -37,6 +37,8 @@ struct GridArgs {
     int RS, PS;         // padded row / plane strides of the spread tile (doubles)
     int P;
     int bin0;           // first spread bin of this launch (slab decomposition)
+    int xslab;          // 1: x indexes a rank's plane slab starting at plane x_lo
+    int x_lo;           //    (unwrapped; the slab's halos hold the periodic images)
     const double* win;  // 3 x 4P x 13 (phi) then 3 x 4P x 13 (dphi)
 };
 
@@ -728,7 +730,7 @@ __global__ void __launch_bounds__(512) k_spread(GridArgs g, const double4* __res
             const int ix = t / PS, rem = t - ix * PS;
             const int iy = rem / RS, iz = rem - iy * RS;
             if (iy >= W || iz >= W) continue;  // padding
-            const int gx = wrapi(lo[0] + ix, g.nf[0]);
+            const int gx = g.xslab ? lo[0] + ix - g.x_lo : wrapi(lo[0] + ix, g.nf[0]);
             const int gy = wrapi(lo[1] + iy, g.nf[1]);
             const int gz = wrapi(lo[2] + iz, g.nf[2]);
             atomicAdd(&grid[(static_cast<long>(gx) * g.nf[1] + gy) * g.nf[2] + gz], val);
@@ -826,7 +828,9 @@ __global__ void __launch_bounds__(128) k_interp(GridArgs g, InterpArgs a) {
             weights<MP>(P, tab + d * 4 * P * kNc, f[d], w[d]);
 #pragma unroll
             for (int j = 0; j < MP; ++j)
-                if (j < P) idx[d][j] = wrapi(f[d].first + j, g.nf[d]);
+                if (j < P)
+                    idx[d][j] = (d == 0 && g.xslab) ? f[d].first + j - g.x_lo
+                                                    : wrapi(f[d].first + j, g.nf[d]);
         }
         const long ny = g.nf[1], nz = g.nf[2];
         double qi = v.w;
@@ -1099,6 +1103,110 @@ struct InterpLaunch {
     }
 };
 
+
+// ----------------------------------------------------------------------------
+// distributed FFT: transposes and the pencil multiply
+// ----------------------------------------------------------------------------
+
+__host__ __device__ __forceinline__ int split_lo(int n, int s, int G) {
+    return static_cast<int>(static_cast<long>(n) * s / G);
+}
+
+// rank owning row y of an n-row block split evenly over G ranks
+__device__ __forceinline__ int split_owner(int y, int n, int G) {
+    int s = static_cast<int>(static_cast<long>(y) * G / n);
+    while (s + 1 < G && split_lo(n, s + 1, G) <= y) ++s;
+    while (s > 0 && split_lo(n, s, G) > y) --s;
+    return s;
+}
+
+// Forward transpose pack: the rank's 2-D spectra [nxl][ny][nzh] -> one block
+// [nxl][rows of s][nzh] per destination rank s, concatenated in rank order
+// (offset of block s = nxl * nzh * y0(s)).
+__global__ void __launch_bounds__(256) k_pencil_pack(long n, int ny, int nzh, int G,
+                                                     const double2* __restrict__ in,
+                                                     double2* __restrict__ out) {
+    const long m = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+    if (m >= n) return;
+    const int z = static_cast<int>(m % nzh);
+    const long r = m / nzh;
+    const int y = static_cast<int>(r % ny);
+    const long x = r / ny;
+    const long nxl = n / (static_cast<long>(ny) * nzh);
+    const int s = split_owner(y, ny, G);
+    const int ylo = split_lo(ny, s, G), nyl = split_lo(ny, s + 1, G) - ylo;
+    out[nxl * nzh * ylo + (x * nyl + (y - ylo)) * nzh + z] = in[m];
+}
+
+// Pencil multiply (ewald.hpp:545-548, 567-595 restricted to the rank's rows):
+// T [nx][nyl][nzh] (x transformed) -> A = p T, B = i xi_x p T (ik only).
+__global__ void __launch_bounds__(256) k_pencil_scale(long n, int ny, int nyl, int nzh, int y0,
+                                                      const double* __restrict__ p,
+                                                      const double* __restrict__ xi,
+                                                      const double2* __restrict__ T,
+                                                      double2* __restrict__ A,
+                                                      double2* __restrict__ B) {
+    const long m = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+    if (m >= n) return;
+    const int z = static_cast<int>(m % nzh);
+    const long r = m / nzh;
+    const int yl = static_cast<int>(r % nyl);
+    const int x = static_cast<int>(r / nyl);
+    const double pk = p[(static_cast<long>(x) * ny + y0 + yl) * nzh + z];
+    const double2 t = T[m];
+    const double ar = t.x * pk, ai = t.y * pk;
+    A[m] = make_double2(ar, ai);
+    if (B) {
+        const double fx = xi[x];
+        B[m] = make_double2(-ai * fx, ar * fx);
+    }
+}
+
+// Backward transpose unpack + the y/z derivative spectra: blocks from every
+// source rank s ([nxl][rows of s][nzh], offset nxl * nzh * y0(s)) -> the
+// spectra [nfields][nxl][ny][nzh] of the inverse 2-D FFTs.
+__global__ void __launch_bounds__(256) k_pencil_unpack(long n, int nx, int ny, int nzh, int G,
+                                                       const double* __restrict__ xi,
+                                                       const double2* __restrict__ A,
+                                                       const double2* __restrict__ B,
+                                                       double2* __restrict__ out, int nfields) {
+    const long m = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+    if (m >= n) return;
+    const int z = static_cast<int>(m % nzh);
+    const long r = m / nzh;
+    const int y = static_cast<int>(r % ny);
+    const long x = r / ny;
+    const long nxl = n / (static_cast<long>(ny) * nzh);
+    const int s = split_owner(y, ny, G);
+    const int ylo = split_lo(ny, s, G), nyl = split_lo(ny, s + 1, G) - ylo;
+    const long src = nxl * nzh * ylo + (x * nyl + (y - ylo)) * nzh + z;
+    const double2 a = A[src];
+    if (nfields == 4) {
+        // field-planar [f][nxl][ny][nzh]: each inverse 2-D FFT only touches its own field
+        const double2 b = B[src];
+        const double fy = xi[nx + y], fz = xi[nx + ny + z];
+        out[m] = a;
+        out[n + m] = b;
+        out[2 * n + m] = make_double2(-a.y * fy, a.x * fy);
+        out[3 * n + m] = make_double2(-a.y * fz, a.x * fz);
+    } else {
+        out[m] = a;
+    }
+}
+
+// planar fields [f][node] -> interleaved [node][f] (the field slab's owned planes)
+__global__ void __launch_bounds__(256) k_pencil_interleave(long n, int nf,
+                                                           const double* __restrict__ in,
+                                                           double* __restrict__ out) {
+    const long m = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+    if (m >= n) return;
+    if (nf == 4)
+        reinterpret_cast<double4*>(out)[m] = make_double4(in[m], in[n + m], in[2 * n + m],
+                                                          in[3 * n + m]);
+    else
+        out[m] = in[m];
+}
+
 PairConsts make_pair_consts(const Plan& p, int& nd) {
     PairConsts k{};
     k.rc2 = p.r_c * p.r_c;
@@ -1117,6 +1225,49 @@ PairConsts make_pair_consts(const Plan& p, int& nd) {
 }
 
 }  // namespace
+
+int spread_bin_edge(const Plan& p) {
+    // the largest S in {8, 6, 4} that still gives >= 4 CTAs per SM
+    for (int cand : {8, 6}) {
+        long nb = 1;
+        for (int d = 0; d < 3; ++d) nb *= (p.nf[d] + cand - 1) / cand;
+        if (nb >= 4 * 148) return cand;
+    }
+    return 4;
+}
+
+PencilGeom pencil_geometry(const Plan& p, int rank, int nranks) {
+    if (nranks < 2 || rank < 0 || rank >= nranks)
+        throw InvalidArgument("distributed FFT: need 0 <= rank < nranks and nranks >= 2");
+    const int S = spread_bin_edge(p);
+    const int nbx = (p.nf[0] + S - 1) / S;
+    const int nx = p.nf[0], ny = p.nf[1], nz = p.nf[2], nzh = nz / 2 + 1;
+    PencilGeom G;
+    G.nranks = nranks;
+    G.rank = rank;
+    // footprints of a bin's atoms reach P/2 planes below and P/2 + 1 above
+    // its planes (spread tile: S + P + 2 planes from bx S - P/2)
+    G.halo = p.P / 2 + 2;
+    for (int r = 0; r < nranks; ++r) {
+        const int x0 = std::min(nx, split_lo(nbx, r, nranks) * S);
+        const int x1 = std::min(nx, split_lo(nbx, r + 1, nranks) * S);
+        if (x1 - x0 < G.halo)
+            throw InvalidArgument("distributed FFT: rank " + std::to_string(r) + " would own " +
+                                  std::to_string(x1 - x0) + " x-planes, fewer than the halo (" +
+                                  std::to_string(G.halo) + "); use fewer ranks");
+        if (r == rank) {
+            G.x0 = x0;
+            G.x1 = x1;
+        }
+    }
+    G.y0 = split_lo(ny, rank, nranks);
+    G.y1 = split_lo(ny, rank + 1, nranks);
+    G.nfields = p.force_method == ForceMethod::ik ? 4 : 1;
+    G.slab_reals = static_cast<long>(G.x1 - G.x0 + 2 * G.halo) * ny * nz;
+    G.spec_local = static_cast<long>(G.x1 - G.x0) * ny * nzh;
+    G.spec_pencil = static_cast<long>(nx) * (G.y1 - G.y0) * nzh;
+    return G;
+}
 
 // ----------------------------------------------------------------------------
 // Engine
@@ -1137,16 +1288,7 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
                 F_[2] >= 4 + 2 * pMz_;
     ncellF_ = static_cast<long>(F_[0]) * F_[1] * F_[2];
     if (ncellF_ >= (1L << 30)) throw InvalidArgument("cell list too fine for this box / r_c");
-    // spread bins: the largest S in {8, 6, 4} that still gives >= 4 CTAs per SM
-    S_ = 4;
-    for (int cand : {8, 6}) {
-        long nb = 1;
-        for (int d = 0; d < 3; ++d) nb *= (p.nf[d] + cand - 1) / cand;
-        if (nb >= 4 * 148) {
-            S_ = cand;
-            break;
-        }
-    }
+    S_ = spread_bin_edge(p);
     for (int d = 0; d < 3; ++d) nb_[d] = (p.nf[d] + S_ - 1) / S_;
     nbin_ = nb_[0] * nb_[1] * nb_[2];
     W_ = S_ + p.P + 2;
@@ -1233,6 +1375,9 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
 Engine::~Engine() {
     cudaSetDevice(device_);
     if (fwd_) cufftDestroy(fwd_);
+    if (pen_f2d_) cufftDestroy(pen_f2d_);
+    if (pen_x_) cufftDestroy(pen_x_);
+    if (pen_i2d_) cufftDestroy(pen_i2d_);
     if (inv_) cufftDestroy(inv_);
     if (d_cufft_work_) cudaFree(d_cufft_work_);
     if (d_scan_tmp_) cudaFree(d_scan_tmp_);
@@ -1430,12 +1575,13 @@ void Engine::run_pair(long N, cudaStream_t s, int rank, int nranks) {
     ++launches_;
 }
 
-void Engine::run_spread(long N, cudaStream_t s, int rank, int nranks, double* grid) {
+void Engine::run_spread(long N, cudaStream_t s, int rank, int nranks, double* grid,
+                        const GridArgs* gslab, long nreals) {
     const Plan& p = plan_;
     if (!grid) grid = d_grid_;
-    CK(cudaMemsetAsync(grid, 0, sizeof(double) * M_, s));
+    CK(cudaMemsetAsync(grid, 0, sizeof(double) * (nreals >= 0 ? nreals : M_), s));
     if (N == 0) return;
-    GridArgs g = grid_args();
+    GridArgs g = gslab ? *gslab : grid_args();
     int b0, b1;
     slab_bins(rank, nranks, &b0, &b1);
     if (b1 <= b0) return;
@@ -1481,18 +1627,23 @@ void Engine::phase_b(int rank, int nranks, const double* grid_in, double* u, dou
     ++launches_;
     CF(cufftSetStream(inv_, s));
     CF(cufftExecZ2D(inv_, d_spec4_, d_fields_));
+    finish(N, rank, nranks, d_fields_, grid_args(), u, F, energy_dev, s);
+}
+
+// Interpolation of this rank's atoms + combine + energy partial (phase B).
+void Engine::finish(long N, int rank, int nranks, const double* fields, const GridArgs& g,
+                    double* u, double* F, double* energy_dev, cudaStream_t s) {
     InterpArgs a{};
     a.N = N;
     a.xyzq = d_xyzqB_;
     a.orig = d_origB_;
-    a.fields = d_fields_;
+    a.fields = fields;
     a.M = M_;
     a.u = u;
     a.F = F;
     a.self_coef = plan_.self_coef;
     a.startB = d_startB_;
     slab_bins(rank, nranks, &a.bin_lo, &a.bin_hi);
-    const GridArgs g = grid_args();
     if (N > 0 && a.bin_hi > a.bin_lo) {
         dispatch_P<InterpLaunch>(plan_.P, static_cast<int>(kSpectral), nfields_ == 4, g, a, s);
         ++launches_;
@@ -1524,6 +1675,127 @@ void Engine::run_grid(long N, cudaStream_t s, StageTimes* t) {
     CF(cufftSetStream(inv_, s));
     CF(cufftExecZ2D(inv_, d_spec4_, d_fields_));
     if (t) CK(cudaEventRecord(ev_t_[6], s));
+}
+
+// ---- distributed FFT (pencil_geometry) ------------------------------------
+
+void Engine::pencil_plans(const PencilGeom& G) {
+    if (pen_rank_ == G.rank && pen_nranks_ == G.nranks) return;
+    for (cufftHandle* h : {&pen_f2d_, &pen_x_, &pen_i2d_})
+        if (*h) {
+            cufftDestroy(*h);
+            *h = 0;
+        }
+    const int nx = plan_.nf[0], ny = plan_.nf[1], nz = plan_.nf[2], nzh = nz / 2 + 1;
+    const int nxl = G.x1 - G.x0, nyl = G.y1 - G.y0, nf = G.nfields;
+    size_t w = 0;
+    int n2[2] = {ny, nz};
+    int rin[2] = {ny, nz}, cin[2] = {ny, nzh};
+    // forward 2-D D2Z of the owned planes
+    CF(cufftCreate(&pen_f2d_));
+    CF(cufftMakePlanMany(pen_f2d_, 2, n2, rin, 1, ny * nz, cin, 1, ny * nzh, CUFFT_D2Z, nxl, &w));
+    // 1-D Z2Z along x of the rank's rows (x stride = nyl * nzh), in place
+    if (nyl > 0) {
+        int n1[1] = {nx};
+        CF(cufftCreate(&pen_x_));
+        CF(cufftMakePlanMany(pen_x_, 1, n1, n1, nyl * nzh, 1, n1, nyl * nzh, 1, CUFFT_Z2Z,
+                             nyl * nzh, &w));
+    }
+    // inverse 2-D Z2D of all fields and planes: planar spectra [f][x] in,
+    // planar fields out (interleaved afterwards for K3's 256-bit loads)
+    CF(cufftCreate(&pen_i2d_));
+    CF(cufftMakePlanMany(pen_i2d_, 2, n2, cin, 1, ny * nzh, rin, 1, ny * nz, CUFFT_Z2D,
+                         nxl * nf, &w));
+    pen_rank_ = G.rank;
+    pen_nranks_ = G.nranks;
+}
+
+void Engine::pencil_phase_a(long N, const double* pos, const double* q, int rank, int nranks,
+                            double* slab, cudaStream_t s) {
+    CK(cudaSetDevice(device_));
+    const PencilGeom G = pencil_geometry(plan_, rank, nranks);
+    pencil_plans(G);
+    launches_ = 0;
+    ensure_capacity(N);
+    prepare(N, pos, q, nullptr, s);
+    if (N > 0) CK(cudaMemsetAsync(d_loc_, 0, sizeof(double4) * N, s));
+    run_pair(N, s, rank, nranks);
+    GridArgs g = grid_args();
+    g.xslab = 1;
+    g.x_lo = G.x0 - G.halo;
+    run_spread(N, s, rank, nranks, slab, &g, G.slab_reals);
+    phase_n_ = N;
+}
+
+void Engine::pencil_forward(int rank, int nranks, const double* slab, cufftDoubleComplex* send,
+                            cudaStream_t s) {
+    CK(cudaSetDevice(device_));
+    const PencilGeom G = pencil_geometry(plan_, rank, nranks);
+    pencil_plans(G);
+    const long plane = static_cast<long>(plan_.nf[1]) * plan_.nf[2];
+    CF(cufftSetStream(pen_f2d_, s));
+    CF(cufftExecD2Z(pen_f2d_, const_cast<double*>(slab) + G.halo * plane, d_spec_));
+    k_pencil_pack<<<grid1(G.spec_local, 256), 256, 0, s>>>(
+        G.spec_local, plan_.nf[1], plan_.nf[2] / 2 + 1, nranks,
+        reinterpret_cast<const double2*>(d_spec_), reinterpret_cast<double2*>(send));
+    CK(cudaGetLastError());
+    ++launches_;
+}
+
+void Engine::pencil_solve(int rank, int nranks, cufftDoubleComplex* recv, cufftDoubleComplex* A,
+                          cufftDoubleComplex* B, cudaStream_t s) {
+    CK(cudaSetDevice(device_));
+    const PencilGeom G = pencil_geometry(plan_, rank, nranks);
+    pencil_plans(G);
+    if (G.spec_pencil == 0) return;
+    if (G.nfields == 4 && !B) throw InvalidArgument("pencil_solve: ik needs the B buffer");
+    CF(cufftSetStream(pen_x_, s));
+    CF(cufftExecZ2Z(pen_x_, recv, recv, CUFFT_FORWARD));
+    k_pencil_scale<<<grid1(G.spec_pencil, 256), 256, 0, s>>>(
+        G.spec_pencil, plan_.nf[1], G.y1 - G.y0, plan_.nf[2] / 2 + 1, G.y0, d_influence_, d_xi_,
+        reinterpret_cast<const double2*>(recv), reinterpret_cast<double2*>(A),
+        G.nfields == 4 ? reinterpret_cast<double2*>(B) : nullptr);
+    CK(cudaGetLastError());
+    ++launches_;
+    CF(cufftExecZ2Z(pen_x_, A, A, CUFFT_INVERSE));
+    if (G.nfields == 4) CF(cufftExecZ2Z(pen_x_, B, B, CUFFT_INVERSE));
+}
+
+void Engine::pencil_backward(int rank, int nranks, const cufftDoubleComplex* A,
+                             const cufftDoubleComplex* B, double* fslab, cudaStream_t s) {
+    CK(cudaSetDevice(device_));
+    const PencilGeom G = pencil_geometry(plan_, rank, nranks);
+    pencil_plans(G);
+    const int nf = G.nfields;
+    k_pencil_unpack<<<grid1(G.spec_local, 256), 256, 0, s>>>(
+        G.spec_local, plan_.nf[0], plan_.nf[1], plan_.nf[2] / 2 + 1, nranks, d_xi_,
+        reinterpret_cast<const double2*>(A), reinterpret_cast<const double2*>(B),
+        reinterpret_cast<double2*>(d_spec4_), nf);
+    CK(cudaGetLastError());
+    ++launches_;
+    const long plane = static_cast<long>(plan_.nf[1]) * plan_.nf[2];
+    CF(cufftSetStream(pen_i2d_, s));
+    CF(cufftExecZ2D(pen_i2d_, d_spec4_, d_fields_));
+    const long n = static_cast<long>(G.x1 - G.x0) * plane;
+    k_pencil_interleave<<<grid1(n, 256), 256, 0, s>>>(n, nf, d_fields_,
+                                                      fslab + nf * G.halo * plane);
+    CK(cudaGetLastError());
+    ++launches_;
+}
+
+void Engine::pencil_phase_b(int rank, int nranks, const double* fslab, double* u, double* F,
+                            double* energy_dev, cudaStream_t s) {
+    CK(cudaSetDevice(device_));
+    const PencilGeom G = pencil_geometry(plan_, rank, nranks);
+    const long N = phase_n_;
+    if (N > 0) {
+        CK(cudaMemsetAsync(u, 0, sizeof(double) * N, s));
+        CK(cudaMemsetAsync(F, 0, sizeof(double) * 3 * N, s));
+    }
+    GridArgs g = grid_args();
+    g.xslab = 1;
+    g.x_lo = G.x0 - G.halo;
+    finish(N, rank, nranks, fslab, g, u, F, energy_dev, s);
 }
 
 GridArgs Engine::grid_args() const {

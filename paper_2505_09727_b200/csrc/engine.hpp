@@ -35,6 +35,26 @@ double fp64_peak_tflops(int device);
 // Ordered pairs per second of the K4 evaluation alone (operands in registers).
 double pair_eval_rate(const Plan& p, int device);
 
+// Distributed-FFT decomposition over `nranks` GPUs:
+// rank r owns the real-space x-planes [x0, x1) (whole spread-bin slabs, so
+// its atoms' footprints stay within `halo` planes of them) and, after the
+// forward transpose, the spectral y-rows [y0, y1).  Host-only (no device).
+struct PencilGeom {
+    int nranks = 1, rank = 0;
+    int halo = 0;           // planes exchanged with each x-neighbour
+    int x0 = 0, x1 = 0;     // owned real-space planes
+    int y0 = 0, y1 = 0;     // owned spectral rows after the transpose
+    long slab_reals = 0;    // (x1 - x0 + 2 halo) * ny * nz: spread slab / one field slab
+    long spec_local = 0;    // (x1 - x0) * ny * (nz/2+1): forward send size (complex)
+    long spec_pencil = 0;   // nx * (y1 - y0) * (nz/2+1): forward receive size (complex)
+    int nfields = 4;        // interleaved fields per node of the field slab
+};
+// Spread bin edge S (grid cells) the engine uses for a plan.
+int spread_bin_edge(const Plan& p);
+// Throws InvalidArgument when the decomposition is not possible (a rank
+// with fewer planes than the halo, or nranks < 2).
+PencilGeom pencil_geometry(const Plan& p, int rank, int nranks);
+
 class Engine {
 public:
     Engine(const Plan& plan, int device);
@@ -73,6 +93,33 @@ public:
     void phase_b(int rank, int nranks, const double* grid_in, double* u, double* F,
                  double* energy_dev, cudaStream_t s);
 
+    // Distributed-FFT evaluation (pencil_geometry above).  Per rank, with the
+    // caller moving data between the phases (NCCL send/recv, all-to-all):
+    //   pencil_phase_a  bin/sort, real-space part of this rank's targets,
+    //                   spread of its atoms into slab (slab_reals, with halos)
+    //   [caller: add each halo into the neighbour's owned planes]
+    //   pencil_forward  2-D FFT of the owned planes, packed per destination
+    //                   rank into send (spec_local complex)
+    //   [caller: all-to-all send -> recv (spec_pencil complex)]
+    //   pencil_solve    x-FFT, influence (and x-derivative) multiply, inverse
+    //                   x-FFT of the rank's y-rows -> A (and B for ik)
+    //   [caller: all-to-all A, B back (same split sizes, reversed)]
+    //   pencil_backward y/z-derivative spectra, inverse 2-D FFT into the
+    //                   owned planes of fslab (nfields x slab_reals, interleaved)
+    //   [caller: fill each halo of fslab from the neighbour's owned planes]
+    //   pencil_phase_b  interpolation of the rank's atoms + combine: partial
+    //                   u, F, energy (sum over ranks)
+    void pencil_phase_a(long N, const double* pos, const double* q, int rank, int nranks,
+                        double* slab, cudaStream_t s);
+    void pencil_forward(int rank, int nranks, const double* slab, cufftDoubleComplex* send,
+                        cudaStream_t s);
+    void pencil_solve(int rank, int nranks, cufftDoubleComplex* recv, cufftDoubleComplex* A,
+                      cufftDoubleComplex* B, cudaStream_t s);
+    void pencil_backward(int rank, int nranks, const cufftDoubleComplex* A,
+                         const cufftDoubleComplex* B, double* fslab, cudaStream_t s);
+    void pencil_phase_b(int rank, int nranks, const double* fslab, double* u, double* F,
+                        double* energy_dev, cudaStream_t s);
+
     // Launch count of the last evaluate() (our kernels only, excluding cuFFT).
     int last_launches() const { return launches_; }
     // Ordered in-range pairs (0 < r < r_c) evaluated by the last pair-kernel
@@ -86,7 +133,11 @@ private:
     void prepare(long N, const double* pos, const double* q, double* qsum_dev, cudaStream_t s);
     void run_pair(long N, cudaStream_t s, int rank, int nranks);
     void run_grid(long N, cudaStream_t s, StageTimes* t);
-    void run_spread(long N, cudaStream_t s, int rank, int nranks, double* grid);
+    void run_spread(long N, cudaStream_t s, int rank, int nranks, double* grid,
+                    const GridArgs* gslab = nullptr, long nreals = -1);
+    void finish(long N, int rank, int nranks, const double* fields, const GridArgs& g,
+                double* u, double* F, double* energy_dev, cudaStream_t s);
+    void pencil_plans(const PencilGeom& G);
     void slab_bins(int rank, int nranks, int* b0, int* b1) const;
     long phase_n_ = 0;
     GridArgs grid_args() const;
@@ -142,6 +193,9 @@ private:
     unsigned long long* d_npairs_ = nullptr;
 
     cufftHandle fwd_ = 0, inv_ = 0;
+    // distributed-FFT plans, built for one (rank, nranks) at a time
+    int pen_rank_ = -1, pen_nranks_ = 0;
+    cufftHandle pen_f2d_ = 0, pen_x_ = 0, pen_i2d_ = 0;
     void* d_cufft_work_ = nullptr;
     cudaStream_t aux_ = nullptr;
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;

@@ -1,9 +1,13 @@
-"""Multi-process plumbing for the benchmark's multi-GPU mode (torch.distributed).
+"""Multi-process plumbing (torch.distributed; "nccl" on the GPU box, "gloo" in
+the CPU tests).
 
-Round 1 runs one independent replica of the workload per rank (weak
-scaling, no data-path collective): each rank evaluates its own seeded system
-on its own GPU; the only collective is the max-over-ranks reduction of the
-measured step times.  Backend "nccl" on the GPU box, "gloo" in the CPU tests.
+Three multi-GPU modes:
+  * replicas (bench default): one independent seeded system per rank, weak
+    scaling, no data-path collective;
+  * evaluate_slab: one system, real-space targets and spread/interp atoms
+    split into x-slabs, the charge grid all-reduced and the FFT replicated;
+  * evaluate_pencil: one system with the grid, spectrum and fields split
+    too (halo exchanges + two all-to-all transposes).
 """
 from __future__ import annotations
 
@@ -44,6 +48,38 @@ class _Lib:
     """The real engine: the C-ABI phase entry points (device pointers)."""
 
     @staticmethod
+    def geometry(plan, rank, nranks):
+        from . import pencil_geometry
+        return pencil_geometry(plan, rank, nranks)
+
+    @staticmethod
+    def pencil_phase_a(plan, box, N, pos, q, rank, nranks, slab, stream):
+        from . import pencil_phase_a
+        pencil_phase_a(plan, box, N, pos.data_ptr(), q.data_ptr(), rank, nranks,
+                       slab.data_ptr(), stream)
+
+    @staticmethod
+    def pencil_forward(plan, rank, nranks, slab, send, stream):
+        from . import pencil_forward
+        pencil_forward(plan, rank, nranks, slab.data_ptr(), send.data_ptr(), stream)
+
+    @staticmethod
+    def pencil_solve(plan, rank, nranks, recv, A, B, stream):
+        from . import pencil_solve
+        pencil_solve(plan, rank, nranks, recv.data_ptr(), A.data_ptr(), _ptr(B), stream)
+
+    @staticmethod
+    def pencil_backward(plan, rank, nranks, A, B, fslab, stream):
+        from . import pencil_backward
+        pencil_backward(plan, rank, nranks, A.data_ptr(), _ptr(B), fslab.data_ptr(), stream)
+
+    @staticmethod
+    def pencil_phase_b(plan, rank, nranks, fslab, u, F, e, stream):
+        from . import pencil_phase_b
+        pencil_phase_b(plan, rank, nranks, fslab.data_ptr(), u.data_ptr(), F.data_ptr(),
+                       e.data_ptr(), stream)
+
+    @staticmethod
     def phase_a(plan, box, N, pos, q, rank, nranks, grid, stream):
         from . import eval_phase_a
         eval_phase_a(plan, box, N, pos.data_ptr(), q.data_ptr(), rank, nranks, grid.data_ptr(),
@@ -75,3 +111,240 @@ def evaluate_slab(plan, box, N, pos, q, out, grid, rank, nranks, stream=0, group
     if use:
         dist.all_reduce(out, group=group)
     return out
+
+
+# ----------------------------------------------------------------------------
+# Distributed-FFT evaluation (include/esp_b200.h
+# esp_pencil_*): the charge grid, the spectrum and the fields are split over
+# the ranks -- x-planes in real space, y-rows between the two transposes --
+# so no rank holds the whole grid.  Data crossing ranks per evaluation:
+# two halo exchanges (P/2+2 planes each side), two all-to-all transposes of
+# the half spectrum (the backward one carries A and B for ik), one all-reduce
+# of [u | F | E].
+# ----------------------------------------------------------------------------
+
+
+class PencilLayout:
+    """Geometry of every rank of a decomposition (esp_pencil_geometry); the
+    split sizes and halo offsets below are in doubles (complex = 2)."""
+
+    def __init__(self, geoms):
+        self.g = list(geoms)
+        self.G = len(self.g)
+        g0 = self.g[0]
+        self.nx, self.ny, self.nz = g0["nf"]
+        self.nzh = self.nz // 2 + 1
+        self.halo = g0["halo"]
+        self.nfields = g0["nfields"]
+
+    @classmethod
+    def of(cls, plan, nranks, engine=None):
+        engine = engine or _Lib
+        return cls([engine.geometry(plan, r, nranks) for r in range(nranks)])
+
+    def nxl(self, r):
+        return self.g[r]["x1"] - self.g[r]["x0"]
+
+    def nyl(self, r):
+        return self.g[r]["y1"] - self.g[r]["y0"]
+
+    def plane(self, nfields=1):
+        return self.ny * self.nz * nfields
+
+    # forward transpose (rank r's send to s / receive from s)
+    def fwd_send_splits(self, r):
+        return [2 * self.nxl(r) * self.nyl(s) * self.nzh for s in range(self.G)]
+
+    def fwd_recv_splits(self, r):
+        return [2 * self.nxl(s) * self.nyl(r) * self.nzh for s in range(self.G)]
+
+    # backward transpose: the reverse
+    def bwd_send_splits(self, r):
+        return self.fwd_recv_splits(r)
+
+    def bwd_recv_splits(self, r):
+        return self.fwd_send_splits(r)
+
+    def neighbours(self, r):
+        return (r - 1) % self.G, (r + 1) % self.G
+
+    def halo_out(self, r, nfields=1):
+        """(to left, to right) plane ranges of rank r's spread slab that carry
+        the neighbours' charge (its halos), in doubles."""
+        pl, h, n = self.plane(nfields), self.halo, self.nxl(r)
+        return (0, h * pl), ((n + h) * pl, (n + 2 * h) * pl)
+
+    def halo_in(self, r, nfields=1):
+        """(from right, from left) owned-plane ranges of rank r that receive
+        the right neighbour's low halo and the left neighbour's high halo."""
+        pl, h, n = self.plane(nfields), self.halo, self.nxl(r)
+        return (n * pl, (n + h) * pl), (h * pl, 2 * h * pl)
+
+    def fill_out(self, r, nfields):
+        """(to left, to right) owned planes of rank r's field slab that fill
+        the neighbours' halos."""
+        pl, h, n = self.plane(nfields), self.halo, self.nxl(r)
+        return (h * pl, 2 * h * pl), (n * pl, (n + h) * pl)
+
+    def fill_in(self, r, nfields):
+        """(from right, from left) halo ranges of rank r's field slab."""
+        pl, h, n = self.plane(nfields), self.halo, self.nxl(r)
+        return ((n + h) * pl, (n + 2 * h) * pl), (0, h * pl)
+
+
+class PencilBuffers:
+    """One rank's device buffers for the distributed-FFT evaluation."""
+
+    def __init__(self, layout, rank, N, device):
+        import torch
+        g = layout.g[rank]
+        f64 = dict(dtype=torch.float64, device=device)
+        self.slab = torch.empty(g["slab_reals"], **f64)
+        self.send = torch.empty(2 * g["spec_local"], **f64)
+        self.recv = torch.empty(max(2 * g["spec_pencil"], 1), **f64)
+        self.A = torch.empty(max(2 * g["spec_pencil"], 1), **f64)
+        self.B = torch.empty(max(2 * g["spec_pencil"], 1), **f64) if g["nfields"] == 4 else None
+        self.A2 = torch.empty(2 * g["spec_local"], **f64)
+        self.B2 = torch.empty(2 * g["spec_local"], **f64) if g["nfields"] == 4 else None
+        self.fslab = torch.empty(g["nfields"] * g["slab_reals"], **f64)
+        self.out = torch.empty(4 * N + 1, **f64)
+
+
+def _ptr(t):
+    return t.data_ptr() if t is not None else 0
+
+
+def _neighbour_exchange(t, outs, ins, left, right, add, group):
+    """Send t[outs[0]] to `left` and t[outs[1]] to `right`; receive the right
+    neighbour's piece into t[ins[0]] and the left's into t[ins[1]] (added or
+    copied).  One message per peer (with two ranks both pieces go to the same
+    peer, concatenated in a fixed order)."""
+    import torch
+    import torch.distributed as dist
+    send = {}
+    for peer, (a, b) in ((left, outs[0]), (right, outs[1])):
+        send.setdefault(peer, []).append(t[a:b])
+    recv_order = {}
+    for peer, (a, b) in ((right, ins[0]), (left, ins[1])):
+        recv_order.setdefault(peer, []).append((a, b))
+    ops, bufs = [], {}
+    for peer, parts in send.items():
+        ops.append(dist.P2POp(dist.isend, torch.cat(parts) if len(parts) > 1 else parts[0].contiguous(),
+                              peer, group))
+    for peer, rngs in recv_order.items():
+        bufs[peer] = torch.empty(sum(b - a for a, b in rngs), dtype=t.dtype, device=t.device)
+        ops.append(dist.P2POp(dist.irecv, bufs[peer], peer, group))
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+    for peer, rngs in recv_order.items():
+        off = 0
+        for a, b in rngs:
+            piece = bufs[peer][off:off + (b - a)]
+            if add:
+                t[a:b] += piece
+            else:
+                t[a:b] = piece
+            off += b - a
+
+
+def evaluate_pencil(plan, box, N, pos, q, bufs, layout, rank, stream=0, group=None, engine=None):
+    """One rank's share of a distributed-FFT ESP evaluation (strong scaling;
+    every rank calls this collectively).  pos (3N), q (N): the full system on
+    every rank; returns bufs.out = [u | F | E] summed over ranks."""
+    import torch.distributed as dist
+    engine = engine or _Lib
+    G = layout.G
+    left, right = layout.neighbours(rank)
+    engine.pencil_phase_a(plan, box, N, pos, q, rank, G, bufs.slab, stream)
+    _neighbour_exchange(bufs.slab, layout.halo_out(rank), layout.halo_in(rank), left, right,
+                        True, group)
+    engine.pencil_forward(plan, rank, G, bufs.slab, bufs.send, stream)
+    dist.all_to_all_single(bufs.recv, bufs.send, layout.fwd_recv_splits(rank),
+                           layout.fwd_send_splits(rank), group=group)
+    engine.pencil_solve(plan, rank, G, bufs.recv, bufs.A, bufs.B, stream)
+    dist.all_to_all_single(bufs.A2, bufs.A, layout.bwd_recv_splits(rank),
+                           layout.bwd_send_splits(rank), group=group)
+    if bufs.B is not None:
+        dist.all_to_all_single(bufs.B2, bufs.B, layout.bwd_recv_splits(rank),
+                               layout.bwd_send_splits(rank), group=group)
+    engine.pencil_backward(plan, rank, G, bufs.A2, bufs.B2, bufs.fslab, stream)
+    nf = layout.nfields
+    _neighbour_exchange(bufs.fslab, layout.fill_out(rank, nf), layout.fill_in(rank, nf), left,
+                        right, False, group)
+    N_ = N
+    engine.pencil_phase_b(plan, rank, G, bufs.fslab, bufs.out[:N_], bufs.out[N_:4 * N_],
+                          bufs.out[4 * N_:], stream)
+    dist.all_reduce(bufs.out, group=group)
+    return bufs.out
+
+
+def evaluate_pencil_emulated(plans, box, N, pos, q, bufs, layout, stream=0, engine=None):
+    """The same algorithm with all ranks in one process (lockstep; the
+    exchanges become device copies): one plan and one PencilBuffers per
+    emulated rank.  Used by the single-GPU tests and the bench's --pencil
+    mode; the result must equal evaluate() on the whole system."""
+    engine = engine or _Lib
+    G = layout.G
+    for r in range(G):
+        engine.pencil_phase_a(plans[r], box, N, pos, q, r, G, bufs[r].slab, stream)
+    _emulated_exchange([b.slab for b in bufs], layout, 1, add=True)
+    for r in range(G):
+        engine.pencil_forward(plans[r], r, G, bufs[r].slab, bufs[r].send, stream)
+    _emulated_alltoall([b.send for b in bufs], [b.recv for b in bufs],
+                       [layout.fwd_send_splits(r) for r in range(G)])
+    for r in range(G):
+        engine.pencil_solve(plans[r], r, G, bufs[r].recv, bufs[r].A, bufs[r].B, stream)
+    _emulated_alltoall([b.A for b in bufs], [b.A2 for b in bufs],
+                       [layout.bwd_send_splits(r) for r in range(G)])
+    if layout.nfields == 4:
+        _emulated_alltoall([b.B for b in bufs], [b.B2 for b in bufs],
+                           [layout.bwd_send_splits(r) for r in range(G)])
+    for r in range(G):
+        engine.pencil_backward(plans[r], r, G, bufs[r].A2, bufs[r].B2, bufs[r].fslab, stream)
+    _emulated_exchange([b.fslab for b in bufs], layout, layout.nfields, add=False)
+    for r in range(G):
+        o = bufs[r].out
+        engine.pencil_phase_b(plans[r], r, G, bufs[r].fslab, o[:N], o[N:4 * N], o[4 * N:],
+                              stream)
+    return sum(b.out for b in bufs)
+
+
+def _emulated_exchange(ts, layout, nfields, add):
+    G = layout.G
+    if add:
+        outs = [layout.halo_out(r, nfields) for r in range(G)]
+        ins = [layout.halo_in(r, nfields) for r in range(G)]
+    else:
+        outs = [layout.fill_out(r, nfields) for r in range(G)]
+        ins = [layout.fill_in(r, nfields) for r in range(G)]
+    # snapshot the outgoing pieces first (a copy may overwrite a halo another
+    # rank still has to send from -- never for adds, but keep it uniform)
+    pieces = [(ts[r][slice(*outs[r][0])].clone(), ts[r][slice(*outs[r][1])].clone())
+              for r in range(G)]
+    for r in range(G):
+        left, right = layout.neighbours(r)
+        to_left, to_right = pieces[r]
+        # left neighbour receives it "from right"; right neighbour "from left"
+        for peer, piece, which in ((left, to_left, 0), (right, to_right, 1)):
+            a, b = ins[peer][which]
+            if add:
+                ts[peer][a:b] += piece
+            else:
+                ts[peer][a:b] = piece
+
+
+def _emulated_alltoall(sends, recvs, send_splits):
+    G = len(sends)
+    offs = []
+    for r in range(G):
+        o, acc = [], 0
+        for n in send_splits[r]:
+            o.append(acc)
+            acc += n
+        offs.append(o)
+    for r in range(G):
+        pos = 0
+        for s in range(G):
+            n = send_splits[s][r]
+            recvs[r][pos:pos + n] = sends[s][offs[s][r]:offs[s][r] + n]
+            pos += n

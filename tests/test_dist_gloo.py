@@ -123,3 +123,199 @@ def test_slab_decomposition_plumbing_gloo():
         assert np.allclose(res[:N], u, rtol=0, atol=1e-12 * np.abs(u).max())
         assert np.allclose(res[N:4 * N].reshape(N, 3), F, rtol=0, atol=1e-12 * np.abs(F).max())
         assert abs(res[4 * N] - E) <= 1e-12 * abs(E)
+
+
+# ---- distributed FFT (dist.evaluate_pencil) ---------------------------------
+
+
+class _OraclePencilEngine:
+    """CPU stand-in for the esp_pencil_* phases (test infrastructure): same
+    buffer layouts and sizes as the C ABI (include/esp_b200.h), physics from
+    the numpy oracle.  A rank spreads/interpolates the atoms whose grid cell
+    floor(x/h) lies in its planes [x0, x1) and sums the real-space part of an
+    index range of targets."""
+
+    def __init__(self, oplan, pos, q, host_plan):
+        from oracle import esp_oracle as O
+        self.O, self.p, self.q = O, oplan, q
+        self.pos = O.fold(pos, oplan.box)
+        self.host_plan = host_plan
+        self.state = {}
+
+    def geometry(self, plan, rank, nranks):
+        import paper_2505_09727_b200 as esp
+        return esp.pencil_geometry(self.host_plan, rank, nranks)
+
+    def _atoms(self, g):
+        l = np.minimum(np.floor(self.pos[:, 0] / self.p.h[0]).astype(int), self.p.nf[0] - 1)
+        return (l >= g["x0"]) & (l < g["x1"])
+
+    def _planes(self, g):
+        return np.arange(g["x0"] - g["halo"], g["x1"] + g["halo"]) % self.p.nf[0]
+
+    def pencil_phase_a(self, plan, box, N, pos, q, rank, nranks, slab, stream):
+        g = self.geometry(plan, rank, nranks)
+        own = self._atoms(g)
+        full = self.O.spread(self.p, self.pos[own], self.q[own])
+        # own atoms touch only [x0-halo, x1+halo): the slab is exact
+        slab.copy_(torch.from_numpy(np.ascontiguousarray(full[self._planes(g)]).ravel()))
+        ul, Fl = self.O.local_sum(self.p, self.pos, self.q)
+        tgt = slice(N * rank // nranks, N * (rank + 1) // nranks)
+        u0, F0 = np.zeros_like(ul), np.zeros_like(Fl)
+        u0[tgt], F0[tgt] = ul[tgt], Fl[tgt]
+        self.state[rank] = (u0, F0)
+
+    def pencil_forward(self, plan, rank, nranks, slab, send, stream):
+        g = self.geometry(plan, rank, nranks)
+        nx, ny, nz = g["nf"]
+        h, nxl = g["halo"], g["x1"] - g["x0"]
+        own = slab.numpy().reshape(nxl + 2 * h, ny, nz)[h:h + nxl]
+        spec = np.fft.rfft2(own, axes=(1, 2))                       # [nxl][ny][nzh]
+        parts = []
+        for s in range(nranks):
+            gs = self.geometry(plan, s, nranks)
+            parts.append(spec[:, gs["y0"]:gs["y1"], :].ravel())
+        send.copy_(torch.from_numpy(np.concatenate(parts).view(np.float64)))
+
+    def pencil_solve(self, plan, rank, nranks, recv, A, B, stream):
+        g = self.geometry(plan, rank, nranks)
+        nx, ny, nz = g["nf"]
+        nyl, nzh = g["y1"] - g["y0"], nz // 2 + 1
+        T = recv.numpy()[:2 * nx * nyl * nzh].view(np.complex128).reshape(nx, nyl, nzh)
+        T = np.fft.fft(T, axis=0)
+        c = T * self.p.influence[:, g["y0"]:g["y1"], :nzh]
+        xi = np.where(2 * np.arange(nx) == nx, 0.0,
+                      2 * np.pi * self.O.signed_mode(nx) / self.p.box[0])
+        a = np.fft.ifft(c, axis=0) * nx
+        A[:a.size * 2].copy_(torch.from_numpy(a.ravel().view(np.float64)))
+        if B is not None:
+            b = np.fft.ifft(c * (1j * xi)[:, None, None], axis=0) * nx
+            B[:b.size * 2].copy_(torch.from_numpy(b.ravel().view(np.float64)))
+
+    def pencil_backward(self, plan, rank, nranks, A, B, fslab, stream):
+        g = self.geometry(plan, rank, nranks)
+        nx, ny, nz = g["nf"]
+        h, nxl, nzh, nf = g["halo"], g["x1"] - g["x0"], nz // 2 + 1, g["nfields"]
+        def unpack(t):
+            out = np.empty((nxl, ny, nzh), complex)
+            flat = t.numpy().view(np.complex128)
+            off = 0
+            for s in range(nranks):
+                gs = self.geometry(plan, s, nranks)
+                n = nxl * (gs["y1"] - gs["y0"]) * nzh
+                out[:, gs["y0"]:gs["y1"], :] = flat[off:off + n].reshape(nxl, -1, nzh)
+                off += n
+            return out
+        a = unpack(A)
+        specs = [a]
+        if nf == 4:
+            xiy = np.where(2 * np.arange(ny) == ny, 0.0,
+                           2 * np.pi * self.O.signed_mode(ny) / self.p.box[1])
+            xiz = np.where(2 * np.arange(nzh) == nz, 0.0,
+                           2 * np.pi * np.arange(nzh) / self.p.box[2])
+            specs += [unpack(B), a * (1j * xiy)[None, :, None], a * (1j * xiz)[None, None, :]]
+        fs = fslab.numpy().reshape(nxl + 2 * h, ny, nz, nf)
+        fs[:] = 0.0
+        for f, sp in enumerate(specs):
+            fs[h:h + nxl, :, :, f] = np.fft.irfft2(sp, s=(ny, nz), axes=(1, 2)) * (ny * nz)
+
+    def pencil_phase_b(self, plan, rank, nranks, fslab, u, F, e, stream):
+        g = self.geometry(plan, rank, nranks)
+        nx, ny, nz = g["nf"]
+        h, nxl, nf = g["halo"], g["x1"] - g["x0"], g["nfields"]
+        fs = fslab.numpy().reshape(nxl + 2 * h, ny, nz, nf)
+        own = self._atoms(g)
+        P = self.pos[own]
+        uu, FF = self.state[rank]
+        uu, FF = uu.copy(), FF.copy()
+        full = np.zeros((nx, ny, nz))
+        def interp(f, deriv=-1):
+            full[:] = 0.0
+            full[self._planes(g)] = fs[:, :, :, f]   # halo copies agree with their owners
+            return self.O.interpolate(self.p, full, P, deriv)
+        qo = self.q[own]
+        uu[own] += interp(0) - self.O.self_correction(self.p, qo)
+        if nf == 4:
+            for d in range(3):
+                FF[own, d] += -qo * interp(1 + d)
+        else:
+            for d in range(3):
+                FF[own, d] += -qo * interp(0, d)
+        u.copy_(torch.from_numpy(uu))
+        F.copy_(torch.from_numpy(FF.ravel()))
+        e.fill_(0.5 * float(np.dot(self.q, uu)))
+
+
+def _pencil_case(fm="ik"):
+    from oracle import esp_oracle as O
+    import paper_2505_09727_b200 as esp
+    box = (12.0, 10.0, 11.0)
+    pos, q = O.random_system(240, box, 5)
+    p = O.build_plan(box, "pswf", 1e-3, 1.0, force_method=fm)
+    hp = esp.build_plan(box, "pswf", 1e-3, 1.0, esp.Overrides(force_method=fm), device=-1)
+    return box, pos, q, p, hp
+
+
+def _pencil_worker(rank, world, port, fm, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2505_09727_b200.dist import PencilBuffers, PencilLayout, evaluate_pencil
+    box, pos, q, p, hp = _pencil_case(fm)
+    eng = _OraclePencilEngine(p, pos, q, hp)
+    layout = PencilLayout.of(hp, world, engine=eng)
+    bufs = PencilBuffers(layout, rank, q.size, "cpu")
+    res = evaluate_pencil(hp, box, q.size, None, None, bufs, layout, rank, engine=eng)
+    out[rank] = res.numpy().copy()
+    dist.destroy_process_group()
+
+
+def _check_against_oracle(res, p, pos, q):
+    from oracle import esp_oracle as O
+    E, u, F = O.evaluate(p, pos, q)
+    N = q.size
+    assert np.allclose(res[:N], u, rtol=0, atol=1e-11 * np.abs(u).max())
+    assert np.allclose(res[N:4 * N].reshape(N, 3), F, rtol=0, atol=1e-11 * np.abs(F).max())
+    assert abs(res[4 * N] - E) <= 1e-11 * abs(E)
+
+
+@pytest.mark.parametrize("world,fm", [(2, "ik"), (3, "ik"), (2, "ad")])
+def test_pencil_decomposition_gloo(world, fm):
+    """Halo exchanges + both all-to-all transposes over gloo reproduce the
+    single-process oracle evaluation."""
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_pencil_worker, args=(world, _free_port(), fm, out), nprocs=world, join=True)
+    box, pos, q, p, hp = _pencil_case(fm)
+    for r in range(world):
+        _check_against_oracle(out[r], p, pos, q)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_pencil_emulated_matches_oracle(world):
+    """The lockstep emulation (the single-GPU test driver) on the same engine."""
+    from paper_2505_09727_b200.dist import PencilBuffers, PencilLayout, evaluate_pencil_emulated
+    box, pos, q, p, hp = _pencil_case()
+    eng = _OraclePencilEngine(p, pos, q, hp)
+    layout = PencilLayout.of(hp, world, engine=eng)
+    bufs = [PencilBuffers(layout, r, q.size, "cpu") for r in range(world)]
+    res = evaluate_pencil_emulated([hp] * world, box, q.size, None, None, bufs, layout, engine=eng)
+    _check_against_oracle(res.numpy(), p, pos, q)
+
+
+def test_pencil_geometry_host():
+    """Geometry from a host-only plan: planes and rows tile the grid; a rank
+    with fewer planes than the halo is refused."""
+    import paper_2505_09727_b200 as esp
+    hp = esp.build_plan((12.0, 10.0, 11.0), "pswf", 1e-3, 1.0, device=-1)
+    for G in (2, 3):
+        gs = [esp.pencil_geometry(hp, r, G) for r in range(G)]
+        assert gs[0]["x0"] == 0 and gs[-1]["x1"] == gs[0]["nf"][0]
+        assert gs[0]["y0"] == 0 and gs[-1]["y1"] == gs[0]["nf"][1]
+        for a, b in zip(gs, gs[1:]):
+            assert a["x1"] == b["x0"] and a["y1"] == b["y0"]
+        for g in gs:
+            assert g["x1"] - g["x0"] >= g["halo"]
+    with pytest.raises(esp.InvalidArgument):
+        esp.pencil_geometry(hp, 0, 64)
+    with pytest.raises(esp.InvalidArgument):
+        esp.pencil_geometry(hp, 0, 1)
