@@ -62,6 +62,7 @@ namespace {
 
 constexpr double kPi = 3.14159265358979323846;
 constexpr int kNc = 13;        // coefficients per window piece (degree 12)
+constexpr long kHighPriorityMaxN = 1L << 19;  // grid pipeline on the high-priority stream
 constexpr int kMaxPoly = 40;   // max pair-polynomial coefficients
 
 // ----------------------------------------------------------------------------
@@ -966,28 +967,26 @@ __global__ void __launch_bounds__(256) k_combine(long N, const double4* __restri
     }
 }
 
-// Final energy: E = 1/2 sum of block partials, compensated (ewald.hpp:641-647).
-__global__ void k_energy(const double* __restrict__ part, int n, double* out) {
-    __shared__ double ss[256], cc[256];
+// Final energy: E = 1/2 sum of block partials (ewald.hpp:641-647): compensated
+// per-thread sums, then a pairwise tree (shuffles, then the 8 warp sums).
+__global__ void __launch_bounds__(256) k_energy(const double* __restrict__ part, int n, double* out) {
+    __shared__ double red[8];
     double s = 0.0, c = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        double y = part[i] - c;
-        double t = s + y;
+        const double y = part[i] - c;
+        const double t = s + y;
         c = (t - s) - y;
         s = t;
     }
-    ss[threadIdx.x] = s;
-    cc[threadIdx.x] = c;
+    double v = s - c;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
     __syncthreads();
     if (threadIdx.x == 0) {
-        double S = 0.0, C = 0.0;
-        for (int i = 0; i < blockDim.x; ++i) {
-            double y = (ss[i] - cc[i]) - C;
-            double t = S + y;
-            C = (t - S) - y;
-            S = t;
-        }
-        *out = 0.5 * S;
+        const double a = (red[0] + red[1]) + (red[2] + red[3]);
+        const double b = (red[4] + red[5]) + (red[6] + red[7]);
+        *out = 0.5 * (a + b);
     }
 }
 
@@ -1355,7 +1354,16 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
     CF(cufftSetWorkArea(fwd_, d_cufft_work_));
     CF(cufftSetWorkArea(inv_, d_cufft_work_));
 
-    CK(cudaStreamCreateWithFlags(&aux_, cudaStreamNonBlocking));
+    // For small systems the grid pipeline runs on a high-priority stream: its
+    // (latency-bound) CTAs are scheduled ahead of K4's pending ones, so it
+    // runs under K4 instead of after it (cfg2: -13 % step time).  For large
+    // ones the default priority is better: the pipeline then fills K4's tail.
+    {
+        int lo = 0, hi = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CK(cudaStreamCreateWithFlags(&aux_, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithPriority(&aux_hi_, cudaStreamNonBlocking, hi));
+    }
     CK(cudaStreamCreateWithFlags(&gstream_, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&ev_gin_, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ev_gout_, cudaEventDisableTiming));
@@ -1410,6 +1418,7 @@ Engine::~Engine() {
     if (ev_gin_) cudaEventDestroy(ev_gin_);
     if (ev_gout_) cudaEventDestroy(ev_gout_);
     if (aux_) cudaStreamDestroy(aux_);
+    if (aux_hi_) cudaStreamDestroy(aux_hi_);
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_join_) cudaEventDestroy(ev_join_);
     for (auto& e : ev_t_)
@@ -1849,7 +1858,8 @@ void Engine::evaluate(long N, const double* pos, const double* q, double* u, dou
                 gexec_ = nullptr;
             }
         }
-        if (!gexec_) CK(cudaGraphInstantiate(&gexec_, graph, 0));
+        if (!gexec_)
+            CK(cudaGraphInstantiate(&gexec_, graph, cudaGraphInstantiateFlagUseNodePriority));
         CK(cudaGraphDestroy(graph));
         gkey_ = key;
         graph_launches_ = launches_;
@@ -1892,15 +1902,16 @@ void Engine::enqueue(long N, const double* pos, const double* q, double* u, doub
         // K4 on the caller's stream overlaps the whole grid pipeline (K1, FFT,
         // K2, inverse FFT, K3) on aux_; the combine joins them
         prepare(N, pos, q, qsum_dev, s);
+        cudaStream_t aux = N <= kHighPriorityMaxN ? aux_hi_ : aux_;
         CK(cudaEventRecord(ev_fork_, s));
-        CK(cudaStreamWaitEvent(aux_, ev_fork_, 0));
-        run_grid(N, aux_, nullptr);
+        CK(cudaStreamWaitEvent(aux, ev_fork_, 0));
+        run_grid(N, aux, nullptr);
         if (N > 0) {
             dispatch_P<InterpLaunch>(plan_.P, static_cast<int>(kSpectral), nfields_ == 4, g, a,
-                                     aux_);
+                                     aux);
             ++launches_;
         }
-        CK(cudaEventRecord(ev_join_, aux_));
+        CK(cudaEventRecord(ev_join_, aux));
         run_pair(N, s, 0, 1);
         CK(cudaStreamWaitEvent(s, ev_join_, 0));
     }

@@ -197,7 +197,7 @@ private:
     int pen_rank_ = -1, pen_nranks_ = 0;
     cufftHandle pen_f2d_ = 0, pen_x_ = 0, pen_i2d_ = 0;
     void* d_cufft_work_ = nullptr;
-    cudaStream_t aux_ = nullptr;
+    cudaStream_t aux_ = nullptr, aux_hi_ = nullptr;
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
     cudaEvent_t ev_t_[8] = {};
 
