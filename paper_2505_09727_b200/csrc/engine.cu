@@ -201,6 +201,72 @@ __global__ void __launch_bounds__(256) k_fold_bin(BinArgs a) {
     }
 }
 
+// Both counting-sort scans for small cell counts in one CTA (replaces two CUB
+// scans + their init kernels + two memsets): start = exclusive scan of count,
+// then count is zeroed for the next evaluation (counts are zero at rest on
+// this path), and the pair counter is reset.
+constexpr int kSmallScanMax = 32768;  // ncell + nbin for the single-CTA path
+
+// In-place exclusive scan of sm[0, n) by one CTA (per-thread chunks + a
+// block scan of the chunk sums).
+__device__ void block_exclusive_scan_smem(int* sm, int n, int* wsum) {
+    const int nt = blockDim.x, t = threadIdx.x;
+    const int per = (n + nt - 1) / nt;
+    const int b = min(n, t * per), e = min(n, b + per);
+    int sum = 0;
+    for (int i = b; i < e; ++i) sum += sm[i];
+    const int lane = t & 31, w = t >> 5;
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        const int v = lane < (nt >> 5) ? wsum[lane] : 0;
+        int iv = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, iv, o);
+            if (lane >= o) iv += u;
+        }
+        if (lane < (nt >> 5)) wsum[lane] = iv - v;
+    }
+    __syncthreads();
+    int run = wsum[w] + incl - sum;
+    for (int i = b; i < e; ++i) {
+        const int c = sm[i];
+        sm[i] = run;
+        run += c;
+    }
+    __syncthreads();
+}
+
+// counts staged in shared memory with coalesced loads (and zeroed in HBM),
+// scanned there, written back coalesced
+__global__ void __launch_bounds__(1024) k_scan_small(int* countA, int* startA, int nA, int* countB,
+                                                     int* startB, int nB,
+                                                     unsigned long long* npairs) {
+    extern __shared__ int sm[];
+    __shared__ int wsum[32];
+    for (int i = threadIdx.x; i < nA; i += blockDim.x) {
+        sm[i] = countA[i];
+        countA[i] = 0;
+    }
+    for (int i = threadIdx.x; i < nB; i += blockDim.x) {
+        sm[nA + i] = countB[i];
+        countB[i] = 0;
+    }
+    __syncthreads();
+    block_exclusive_scan_smem(sm, nA, wsum);
+    block_exclusive_scan_smem(sm + nA, nB, wsum);
+    for (int i = threadIdx.x; i < nA; i += blockDim.x) startA[i] = sm[i];
+    for (int i = threadIdx.x; i < nB; i += blockDim.x) startB[i] = sm[nA + i];
+    if (threadIdx.x == 0) *npairs = 0ull;
+}
+
 __global__ void __launch_bounds__(256) k_scatter(long N, const double4* __restrict__ tmp,
                                                  const int* __restrict__ cellA,
                                                  const int* __restrict__ rankA,
@@ -1320,6 +1386,9 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
     dalloc(d_startA_, ncellF_ + 1);
     dalloc(d_countB_, nbin_ + 1);
     dalloc(d_startB_, nbin_ + 1);
+    // counts are zero at rest on the single-CTA scan path (prepare)
+    CK(cudaMemset(d_countA_, 0, sizeof(int) * (ncellF_ + 1)));
+    CK(cudaMemset(d_countB_, 0, sizeof(int) * (nbin_ + 1)));
     size_t t1 = 0, t2 = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, t1, d_countA_, d_startA_,
                                      static_cast<int>(ncellF_ + 1)));
@@ -1449,9 +1518,12 @@ void Engine::ensure_capacity(long N) {
 void Engine::prepare(long N, const double* pos, const double* q, double* qsum_dev,
                      cudaStream_t s) {
     const Plan& p = plan_;
-    CK(cudaMemsetAsync(d_countA_, 0, sizeof(int) * (ncellF_ + 1), s));
-    CK(cudaMemsetAsync(d_npairs_, 0, sizeof(unsigned long long), s));
-    CK(cudaMemsetAsync(d_countB_, 0, sizeof(int) * (nbin_ + 1), s));
+    const bool small = ncellF_ + nbin_ + 2 <= kSmallScanMax;
+    if (!small) {
+        CK(cudaMemsetAsync(d_countA_, 0, sizeof(int) * (ncellF_ + 1), s));
+        CK(cudaMemsetAsync(d_npairs_, 0, sizeof(unsigned long long), s));
+        CK(cudaMemsetAsync(d_countB_, 0, sizeof(int) * (nbin_ + 1), s));
+    }
     if (qsum_dev) CK(cudaMemsetAsync(qsum_dev, 0, sizeof(double) * 2, s));
     BinArgs a{};
     a.N = N;
@@ -1478,12 +1550,23 @@ void Engine::prepare(long N, const double* pos, const double* q, double* qsum_de
         CK(cudaGetLastError());
         ++launches_;
     }
-    size_t tb = scan_tmp_bytes_;
-    CK(cub::DeviceScan::ExclusiveSum(d_scan_tmp_, tb, d_countA_, d_startA_,
-                                     static_cast<int>(ncellF_ + 1), s));
-    tb = scan_tmp_bytes_;
-    CK(cub::DeviceScan::ExclusiveSum(d_scan_tmp_, tb, d_countB_, d_startB_, nbin_ + 1, s));
-    launches_ += 2;
+    if (small) {
+        const size_t sm = sizeof(int) * (ncellF_ + nbin_ + 2);
+        if (sm > 48 * 1024)
+            CK(cudaFuncSetAttribute(k_scan_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(sm)));
+        k_scan_small<<<1, 1024, sm, s>>>(d_countA_, d_startA_, static_cast<int>(ncellF_ + 1),
+                                         d_countB_, d_startB_, nbin_ + 1, d_npairs_);
+        CK(cudaGetLastError());
+        ++launches_;
+    } else {
+        size_t tb = scan_tmp_bytes_;
+        CK(cub::DeviceScan::ExclusiveSum(d_scan_tmp_, tb, d_countA_, d_startA_,
+                                         static_cast<int>(ncellF_ + 1), s));
+        tb = scan_tmp_bytes_;
+        CK(cub::DeviceScan::ExclusiveSum(d_scan_tmp_, tb, d_countB_, d_startB_, nbin_ + 1, s));
+        launches_ += 2;
+    }
     if (N > 0) {
         k_scatter<<<grid1(N, 256), 256, 0, s>>>(N, d_tmp_, d_cellA_, d_rankA_, d_startA_, d_xyzqA_,
                                                  d_origA_, d_cellB_, d_rankB_, d_startB_, d_xyzqB_,
