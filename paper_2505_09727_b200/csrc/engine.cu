@@ -493,25 +493,36 @@ __global__ void __launch_bounds__(kPairThreads, kPairWarps >= 8 ? 3 : 6) k_pair(
     const float R2 = k.rc2_test;
     const float fwx = static_cast<float>(a.fw[0]), fwy = static_cast<float>(a.fw[1]);
     const float fwz = static_cast<float>(a.fw[2]);
+    const float ifwz = 1.0f / fwz;
 
     for (int base = 0; base < total; base += a.cap) {
         const int nk = min(a.cap, total - base);
         if (base > 0) __syncthreads();
-        for (int c = threadIdx.x; c < nk; c += blockDim.x) {
-            const int g = base + c;
-            int lo = 0, hi = nent - 1;  // last entry with ent_off[e] <= g
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (ent_off[mid] <= g) lo = mid;
-                else hi = mid - 1;
+        // stage: each column's slices are at most three contiguous runs of the
+        // sorted atoms (below, inside, above the z period), one warp per run
+        for (int task = warp; task < ncol * 3; task += nw) {
+            const int col = task / 3, part = task - 3 * (task / 3);
+            const int lo_in = max(0, min(nsl, Mz - z0));            // first slice with fz >= 0
+            const int hi_in = max(0, min(nsl, a.F[2] - z0 + Mz));   // first slice with fz >= F
+            const int sa = part == 0 ? 0 : (part == 1 ? lo_in : hi_in);
+            const int sb = part == 0 ? lo_in : (part == 1 ? hi_in : nsl);
+            if (sb <= sa) continue;
+            const int e0 = col * nsl + sa;
+            int g0 = ent_off[e0], g1 = ent_off[col * nsl + sb];
+            const int src0 = ent_src[e0] - g0;
+            const int sl = ent_slot[e0];
+            const double shx = shiftv[sl][0] - ox, shy = shiftv[sl][1] - oy,
+                         shz = shiftv[sl][2] - oz;
+            g0 = max(g0, base);
+            g1 = min(g1, base + nk);
+            for (int g = g0 + lane; g < g1; g += 32) {
+                const int src = g + src0;
+                const double4 v = a.xyzq[src];
+                cand[g - base] = make_float4(static_cast<float>(v.x + shx),
+                                             static_cast<float>(v.y + shy),
+                                             static_cast<float>(v.z + shz),
+                                             __int_as_float(src | (sl << 27)));
             }
-            const int src = ent_src[lo] + (g - ent_off[lo]);
-            const int sl = ent_slot[lo];
-            const double4 v = a.xyzq[src];
-            cand[c] = make_float4(static_cast<float>(v.x + shiftv[sl][0] - ox),
-                                  static_cast<float>(v.y + shiftv[sl][1] - oy),
-                                  static_cast<float>(v.z + shiftv[sl][2] - oz),
-                                  __int_as_float(src | (sl << 27)));
         }
         if (threadIdx.x == 0) cand[a.cap] = make_float4(1e30f, 1e30f, 1e30f, __int_as_float(0));
         __syncthreads();
@@ -526,6 +537,7 @@ __global__ void __launch_bounds__(kPairThreads, kPairWarps >= 8 ? 3 : 6) k_pair(
             int beg0 = 0, cnt0 = 0, beg1 = 0, cnt1 = 0;
 #pragma unroll
             for (int pass = 0; pass < 2; ++pass) {
+                if (pass == 1 && ncol <= 32) break;
                 const int col = lane + 32 * pass;
                 int beg = 0, cnt = 0;
                 if (col < ncol) {
@@ -536,8 +548,10 @@ __global__ void __launch_bounds__(kPairThreads, kPairWarps >= 8 ? 3 : 6) k_pair(
                     const float g2 = fmaf(gx, gx, gy * gy);
                     if (g2 < R2) {
                         const float zm = sqrtf(R2 - g2);
-                        int klo = static_cast<int>(floorf((zf - zm) / fwz)) + Mz;
-                        int khi = static_cast<int>(floorf((zf + zm) / fwz)) + Mz;
+                        // reciprocal: the <= 1e-6-slice rounding is far inside the
+                        // 1e-4 r_c margin of R2
+                        int klo = static_cast<int>(floorf((zf - zm) * ifwz)) + Mz;
+                        int khi = static_cast<int>(floorf((zf + zm) * ifwz)) + Mz;
                         klo = max(0, min(nsl - 1, klo));
                         khi = max(0, min(nsl - 1, khi));
                         int lo = ent_off[col * nsl + klo], hi = ent_off[col * nsl + khi + 1];
