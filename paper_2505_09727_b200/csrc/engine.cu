@@ -660,26 +660,28 @@ __global__ void __launch_bounds__(kPairThreads, kPairWarps >= 8 ? 3 : 6) k_pair(
             }
             __syncwarp();
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                u += __shfl_xor_sync(0xffffffffu, u, o);
-                fx += __shfl_xor_sync(0xffffffffu, fx, o);
-                fy += __shfl_xor_sync(0xffffffffu, fy, o);
-                fz += __shfl_xor_sync(0xffffffffu, fz, o);
-            }
-            npair = __reduce_add_sync(0xffffffffu, npair);
-            if (lane == 0) {
-                const double qi = pi.w;
-                const int o = a.orig[i];
-                double4 r = make_double4(u, -qi * fx, -qi * fy, -qi * fz);
-                if (base > 0) {
-                    const double4 p = a.loc[o];
-                    r.x += p.x;
-                    r.y += p.y;
-                    r.z += p.z;
-                    r.w += p.w;
+            // transpose-reduce of (u, fx, fy, fz) over the warp: 6 double
+            // shuffles instead of 20; lane 8c ends with component c
+            {
+                const bool h16 = lane & 16, h8 = lane & 8;
+                const double s0 = h16 ? u : fy, s1 = h16 ? fx : fz;
+                const double k0 = h16 ? fy : u, k1 = h16 ? fz : fx;
+                const double v0 = k0 + __shfl_xor_sync(0xffffffffu, s0, 16);
+                const double v1 = k1 + __shfl_xor_sync(0xffffffffu, s1, 16);
+                double w = (h8 ? v1 : v0) + __shfl_xor_sync(0xffffffffu, h8 ? v0 : v1, 8);
+                w += __shfl_xor_sync(0xffffffffu, w, 4);
+                w += __shfl_xor_sync(0xffffffffu, w, 2);
+                w += __shfl_xor_sync(0xffffffffu, w, 1);
+                npair = __reduce_add_sync(0xffffffffu, npair);
+                if ((lane & 7) == 0) {
+                    const int comp = lane >> 3;  // 0 u, 1 Fx, 2 Fy, 3 Fz
+                    double* dst = reinterpret_cast<double*>(a.loc + a.orig[i]) + comp;
+                    double r = comp == 0 ? w : -pi.w * w;
+                    if (base > 0) r += *dst;
+                    *dst = r;
                 }
-                a.loc[o] = r;
-                if (a.npairs) atomicAdd(a.npairs, static_cast<unsigned long long>(npair));
+                if (lane == 0 && a.npairs)
+                    atomicAdd(a.npairs, static_cast<unsigned long long>(npair));
             }
         }
     }
