@@ -24,6 +24,7 @@ struct esp_plan {
     double* d_u = nullptr;
     double* d_F = nullptr;
     double* d_e = nullptr;  // energy + qsum[2]
+    double* h_e = nullptr;  // pinned host copy of d_e
     long cap = 0;
     cudaStream_t stream = nullptr;
 
@@ -35,6 +36,7 @@ struct esp_plan {
             cudaFree(d_u);
             cudaFree(d_F);
             cudaFree(d_e);
+            if (h_e) cudaFreeHost(h_e);
             if (stream) cudaStreamDestroy(stream);
         }
     }
@@ -101,6 +103,7 @@ void stage(esp_plan* p, long N) {
     cuda_ok(cudaSetDevice(p->device), "cudaSetDevice");
     if (!p->stream) cuda_ok(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking), "stream");
     if (!p->d_e) cuda_ok(cudaMalloc(&p->d_e, 4 * sizeof(double)), "cudaMalloc");
+    if (!p->h_e) cuda_ok(cudaMallocHost(&p->h_e, 4 * sizeof(double)), "cudaMallocHost");
     if (N <= p->cap) return;
     cudaFree(p->d_pos);
     cudaFree(p->d_q);
@@ -290,7 +293,7 @@ int esp_evaluate(esp_plan* p, const double box[3], long N, const double* pos, co
                    timings ? &st : nullptr);
         d2h(p, u, p->d_u, N);
         d2h(p, F, p->d_F, 3 * N);
-        double hv[3];
+        double* hv = p->h_e;  // pinned: the small read stays on the async path
         cuda_ok(cudaMemcpyAsync(hv, p->d_e, 3 * sizeof(double), cudaMemcpyDeviceToHost, p->stream),
                 "D2H");
         sync(p);

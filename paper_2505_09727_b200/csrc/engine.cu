@@ -63,6 +63,9 @@ namespace {
 constexpr double kPi = 3.14159265358979323846;
 constexpr int kNc = 13;        // coefficients per window piece (degree 12)
 constexpr long kHighPriorityMaxN = 1L << 19;  // grid pipeline on the high-priority stream
+constexpr int kColDivDefault = 2;
+constexpr long kColDiv3MinN = 100000;      // r_c/3 columns: enough CTAs to fill the GPU
+constexpr double kColDiv3MinPairs = 300.0;  // ... and enough pairs per target
 constexpr int kMaxPoly = 40;   // max pair-polynomial coefficients
 
 // ----------------------------------------------------------------------------
@@ -370,7 +373,9 @@ __device__ __forceinline__ void pair_eval(const PairConsts& k, double4 pj, doubl
 // period (otherwise the all-pairs path runs, as in the reference for
 // nc < 3, ewald.hpp:457-470).
 constexpr int kMaxBZ = 8;     // target slices per CTA (runtime a.bz <= kMaxBZ)
-constexpr int kMaxCol = 36;   // (BX+2M)^2 with BX <= 2, M <= 2
+constexpr int kMaxColDiv = 3;  // columns of edge >= r_c / col_div, col_div in {2, 3}
+constexpr int kMaxCol = (2 + 2 * kMaxColDiv) * (2 + 2 * kMaxColDiv);  // (BX+2M)^2, BX <= 2
+static_assert(kMaxCol <= 64, "two column passes per target");
 constexpr int kMaxSl = kMaxBZ + 8;  // bz + 2 Mz with Mz <= 4
 constexpr int kMaxEnt = kMaxCol * kMaxSl;
 #ifndef ESP_PAIR_WARPS
@@ -462,28 +467,27 @@ __global__ void __launch_bounds__(kPairThreads, kPairWarps >= 8 ? 3 : 6) k_pair(
     __syncthreads();
     if (warp == 0) {
         // exclusive scan of the entry counts
-        constexpr int per = (kMaxEnt + 31) / 32;
-        int loc[per];
+        const int per = (nent + 31) / 32;
+        const int e0 = min(nent, lane * per), e1 = min(nent, e0 + per);
         int sum = 0;
-#pragma unroll
-        for (int j = 0; j < per; ++j) {
-            const int e = lane * per + j;
-            loc[j] = e < nent ? ent_off[e + 1] : 0;
-            sum += loc[j];
-        }
+        for (int e = e0; e < e1; ++e) sum += ent_off[e + 1];
         int incl = sum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int v = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += v;
         }
+        // in place (slot e+1 holds entry e's count): every lane keeps its last
+        // count in a register before the writes reach the next lane's slot
+        const int last = e1 > e0 ? ent_off[e1] : 0;
+        __syncwarp();
         int run = incl - sum;
-#pragma unroll
-        for (int j = 0; j < per; ++j) {
-            const int e = lane * per + j;
-            if (e < nent) ent_off[e] = run;
-            run += loc[j];
+        for (int e = e0; e < e1; ++e) {
+            const int c = e == e1 - 1 ? last : ent_off[e + 1];
+            ent_off[e] = run;
+            run += c;
         }
+        __syncwarp();
         if (lane == 31) ent_off[nent] = incl;
     }
     __syncthreads();
@@ -1357,18 +1361,7 @@ PencilGeom pencil_geometry(const Plan& p, int rank, int nranks) {
 Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
     CK(cudaSetDevice(device_));
     const Plan& p = plan_;
-    // fine pair cells: columns >= r_c/2 in x, y; slices >= r_c/4 in z
-    F_[0] = std::max(1, static_cast<int>(std::floor(p.box[0] / (0.5 * p.r_c))));
-    F_[1] = std::max(1, static_cast<int>(std::floor(p.box[1] / (0.5 * p.r_c))));
-    F_[2] = std::max(1, static_cast<int>(std::floor(p.box[2] / (0.25 * p.r_c))));
-    pM_ = std::max(static_cast<int>(std::ceil(p.r_c / (p.box[0] / F_[0]) - 1e-12)),
-                   static_cast<int>(std::ceil(p.r_c / (p.box[1] / F_[1]) - 1e-12)));
-    pMz_ = static_cast<int>(std::ceil(p.r_c / (p.box[2] / F_[2]) - 1e-12));
-    // the fine stencil must not alias across the period; otherwise all pairs
-    cells_ok_ = pM_ <= 2 && pMz_ <= 4 && F_[0] >= 2 * pM_ + 1 && F_[1] >= 2 * pM_ + 1 &&
-                F_[2] >= 4 + 2 * pMz_;
-    ncellF_ = static_cast<long>(F_[0]) * F_[1] * F_[2];
-    if (ncellF_ >= (1L << 30)) throw InvalidArgument("cell list too fine for this box / r_c");
+    set_cells(kColDivDefault);
     S_ = spread_bin_edge(p);
     for (int d = 0; d < 3; ++d) nb_[d] = (p.nf[d] + S_ - 1) / S_;
     nbin_ = nb_[0] * nb_[1] * nb_[2];
@@ -1398,19 +1391,11 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
     dalloc(d_xi_, xi.size());
     CK(cudaMemcpy(d_xi_, xi.data(), sizeof(double) * xi.size(), cudaMemcpyHostToDevice));
 
-    dalloc(d_countA_, ncellF_ + 1);
-    dalloc(d_startA_, ncellF_ + 1);
     dalloc(d_countB_, nbin_ + 1);
     dalloc(d_startB_, nbin_ + 1);
     // counts are zero at rest on the single-CTA scan path (prepare)
-    CK(cudaMemset(d_countA_, 0, sizeof(int) * (ncellF_ + 1)));
     CK(cudaMemset(d_countB_, 0, sizeof(int) * (nbin_ + 1)));
-    size_t t1 = 0, t2 = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, t1, d_countA_, d_startA_,
-                                     static_cast<int>(ncellF_ + 1)));
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, t2, d_countB_, d_startB_, nbin_ + 1));
-    scan_tmp_bytes_ = std::max(t1, t2);
-    CK(cudaMalloc(&d_scan_tmp_, std::max<size_t>(scan_tmp_bytes_, 16)));
+    alloc_cells();
     dalloc(d_grid_, M_);
     dalloc(d_spec_, Mh_);
     dalloc(d_spec4_, nfields_ * Mh_);
@@ -1508,6 +1493,62 @@ Engine::~Engine() {
     if (ev_join_) cudaEventDestroy(ev_join_);
     for (auto& e : ev_t_)
         if (e) cudaEventDestroy(e);
+}
+
+// Fine pair cells: columns of edge >= r_c / col_div in x and y, slices of
+// edge >= r_c/4 in z.  col_div 3 tightens the per-column sphere bounds (1.8
+// instead of 2.2 candidates per in-range pair) at the price of 49-64 columns
+// per target: it pays for large systems with many pairs per atom
+// (reconfigure); ESP_COL_DIV forces either.
+void Engine::set_cells(int col_div) {
+    const Plan& p = plan_;
+    col_div_ = col_div;
+    F_[0] = std::max(1, static_cast<int>(std::floor(p.box[0] / (p.r_c / col_div_))));
+    F_[1] = std::max(1, static_cast<int>(std::floor(p.box[1] / (p.r_c / col_div_))));
+    F_[2] = std::max(1, static_cast<int>(std::floor(p.box[2] / (0.25 * p.r_c))));
+    pM_ = std::max(static_cast<int>(std::ceil(p.r_c / (p.box[0] / F_[0]) - 1e-12)),
+                   static_cast<int>(std::ceil(p.r_c / (p.box[1] / F_[1]) - 1e-12)));
+    pMz_ = static_cast<int>(std::ceil(p.r_c / (p.box[2] / F_[2]) - 1e-12));
+    // the fine stencil must not alias across the period; otherwise all pairs
+    cells_ok_ = pM_ <= col_div_ && pMz_ <= 4 && F_[0] >= 2 * pM_ + 1 && F_[1] >= 2 * pM_ + 1 &&
+                F_[2] >= 4 + 2 * pMz_;
+    ncellF_ = static_cast<long>(F_[0]) * F_[1] * F_[2];
+    if (ncellF_ >= (1L << 30)) throw InvalidArgument("cell list too fine for this box / r_c");
+}
+
+void Engine::alloc_cells() {
+    dalloc(d_countA_, ncellF_ + 1);
+    dalloc(d_startA_, ncellF_ + 1);
+    CK(cudaMemset(d_countA_, 0, sizeof(int) * (ncellF_ + 1)));
+    size_t t1 = 0, t2 = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, t1, d_countA_, d_startA_,
+                                     static_cast<int>(ncellF_ + 1)));
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, t2, d_countB_, d_startB_, nbin_ + 1));
+    scan_tmp_bytes_ = std::max(t1, t2);
+    if (d_scan_tmp_) cudaFree(d_scan_tmp_);
+    d_scan_tmp_ = nullptr;
+    CK(cudaMalloc(&d_scan_tmp_, std::max<size_t>(scan_tmp_bytes_, 16)));
+}
+
+// Size-dependent setup, outside any stream capture: buffers for N atoms and
+// the column width of the pair cells.
+void Engine::reconfigure(long N) {
+    ensure_capacity(N);
+    int want = kColDivDefault;
+    const Plan& p = plan_;
+    const double pairs_per_atom =
+        static_cast<double>(N) / (p.box[0] * p.box[1] * p.box[2]) * 4.0 / 3.0 * kPi * p.r_c *
+        p.r_c * p.r_c;
+    if (N >= kColDiv3MinN && pairs_per_atom >= kColDiv3MinPairs) want = 3;
+    if (const char* e = std::getenv("ESP_COL_DIV")) want = std::max(2, std::min(kMaxColDiv, std::atoi(e)));
+    if (want == col_div_) return;
+    CK(cudaDeviceSynchronize());
+    if (gexec_) {
+        cudaGraphExecDestroy(gexec_);
+        gexec_ = nullptr;
+    }
+    set_cells(want);
+    alloc_cells();
 }
 
 void Engine::ensure_capacity(long N) {
@@ -1710,7 +1751,7 @@ void Engine::phase_a(long N, const double* pos, const double* q, int rank, int n
     CK(cudaSetDevice(device_));
     if (nranks < 1 || rank < 0 || rank >= nranks) throw InvalidArgument("bad rank / nranks");
     launches_ = 0;
-    ensure_capacity(N);
+    reconfigure(N);
     prepare(N, pos, q, nullptr, s);
     if (N > 0) CK(cudaMemsetAsync(d_loc_, 0, sizeof(double4) * N, s));
     run_pair(N, s, rank, nranks);
@@ -1824,7 +1865,7 @@ void Engine::pencil_phase_a(long N, const double* pos, const double* q, int rank
     const PencilGeom G = pencil_geometry(plan_, rank, nranks);
     pencil_plans(G);
     launches_ = 0;
-    ensure_capacity(N);
+    reconfigure(N);
     prepare(N, pos, q, nullptr, s);
     if (N > 0) CK(cudaMemsetAsync(d_loc_, 0, sizeof(double4) * N, s));
     run_pair(N, s, rank, nranks);
@@ -1926,6 +1967,7 @@ GridArgs Engine::grid_args() const {
 void Engine::evaluate(long N, const double* pos, const double* q, double* u, double* F,
                       double* energy_dev, double* qsum_dev, cudaStream_t s, StageTimes* t) {
     CK(cudaSetDevice(device_));
+    reconfigure(N);
     if (t || !use_graph_) {
         enqueue(N, pos, q, u, F, energy_dev, qsum_dev, s, t);
         return;
@@ -2046,7 +2088,7 @@ void Engine::enqueue(long N, const double* pos, const double* q, double* u, doub
 void Engine::local_sum(long N, const double* pos, const double* q, double* u, double* F,
                        cudaStream_t s) {
     CK(cudaSetDevice(device_));
-    ensure_capacity(N);
+    reconfigure(N);
     prepare(N, pos, q, nullptr, s);
     run_pair(N, s, 0, 1);
     if (N > 0) {

@@ -130,6 +130,9 @@ private:
     void enqueue(long N, const double* pos, const double* q, double* u, double* F,
                  double* energy_dev, double* qsum_dev, cudaStream_t s, StageTimes* t);
     void ensure_capacity(long N);
+    void reconfigure(long N);
+    void set_cells(int col_div);
+    void alloc_cells();
     void prepare(long N, const double* pos, const double* q, double* qsum_dev, cudaStream_t s);
     void run_pair(long N, cudaStream_t s, int rank, int nranks);
     void run_grid(long N, cudaStream_t s, StageTimes* t);
@@ -160,6 +163,7 @@ private:
     int pair_warps_ = 4;
     int pair_cap_ = 2048;
     int pM_ = 2, pMz_ = 4;      // fine stencil reach (columns, slices)
+    int col_div_ = 2;           // column edge >= r_c / col_div_
 
     // tables on device
     double* d_win_ = nullptr;        // 3 x 4P x 13 phi, then 3 x 4P x 13 dphi

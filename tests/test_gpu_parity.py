@@ -149,3 +149,30 @@ def test_zero_and_empty(esp, gpu):
     assert np.all(sp.u == 0.0) and np.all(sp.F == 0.0)
     ef = esp.evaluate(plan, esp.ParticleSystem(box, np.zeros(0), np.zeros((0, 3))))
     assert ef.energy == 0.0 and ef.u.shape == (0,)
+
+
+@pytest.mark.parametrize("col_div", ["2", "3"])
+@pytest.mark.parametrize("name", ["cfg1", "small_n512", "small_n64_rc1"])
+def test_pair_cell_widths(esp, gpu, name, col_div, monkeypatch):
+    """Both pair-cell column widths (r_c/2, r_c/3; the engine picks one by
+    system size) give the reference's real-space sum."""
+    from paper_2505_09727_b200 import systems as S
+    monkeypatch.setenv("ESP_COL_DIV", col_div)
+    g = golden(name + ".npz")
+    if name == "cfg1":
+        c = S.config("cfg1")
+        pos, q, box = c.system()
+        eps, r_c = c.eps, c.r_c
+    else:
+        L = float(g["L"])
+        box = (L, L, L)
+        pos, q = S.generate_system("random", int(g["N"]), box, int(g["seed"]))
+        eps, r_c = float(g["eps"]), float(g["r_c"])
+    sysm = esp.ParticleSystem(box, q, pos)
+    plan = esp.build_plan(box, "pswf", eps, r_c, device=gpu)
+    loc = esp.local_sum(plan, sysm)
+    assert max_rel(loc.u, g["u_local"]) <= 1e-12
+    assert rel_rms(loc.F, g["F_local"]) <= 1e-12
+    ef = esp.evaluate(plan, sysm)
+    assert abs(ef.energy - g["energy"]) <= E_TOL * abs(g["energy"])
+    assert rel_rms(ef.F, g["F"]) <= F_TOL
