@@ -64,8 +64,7 @@ constexpr double kPi = 3.14159265358979323846;
 constexpr int kNc = 13;        // coefficients per window piece (degree 12)
 constexpr long kHighPriorityMaxN = 1L << 19;  // grid pipeline on the high-priority stream
 constexpr int kColDivDefault = 2;
-constexpr long kColDiv3MinN = 100000;      // r_c/3 columns: enough CTAs to fill the GPU
-constexpr double kColDiv3MinPairs = 300.0;  // ... and enough pairs per target
+constexpr double kColDiv3MinPairs = 300.0;  // r_c/3 columns: enough pairs per target
 constexpr int kMaxPoly = 40;   // max pair-polynomial coefficients
 
 // ----------------------------------------------------------------------------
@@ -1498,7 +1497,7 @@ Engine::~Engine() {
 // Fine pair cells: columns of edge >= r_c / col_div in x and y, slices of
 // edge >= r_c/4 in z.  col_div 3 tightens the per-column sphere bounds (1.8
 // instead of 2.2 candidates per in-range pair) at the price of 49-64 columns
-// per target: it pays for large systems with many pairs per atom
+// per target: it pays when there are many pairs per atom
 // (reconfigure); ESP_COL_DIV forces either.
 void Engine::set_cells(int col_div) {
     const Plan& p = plan_;
@@ -1539,7 +1538,7 @@ void Engine::reconfigure(long N) {
     const double pairs_per_atom =
         static_cast<double>(N) / (p.box[0] * p.box[1] * p.box[2]) * 4.0 / 3.0 * kPi * p.r_c *
         p.r_c * p.r_c;
-    if (N >= kColDiv3MinN && pairs_per_atom >= kColDiv3MinPairs) want = 3;
+    if (pairs_per_atom >= kColDiv3MinPairs) want = 3;
     if (const char* e = std::getenv("ESP_COL_DIV")) want = std::max(2, std::min(kMaxColDiv, std::atoi(e)));
     if (want == col_div_) return;
     CK(cudaDeviceSynchronize());
@@ -1685,12 +1684,21 @@ void Engine::run_pair(long N, cudaStream_t s, int rank, int nranks) {
                 if (F_[0] < bx + 2 * pM_ || F_[1] < bx + 2 * pM_ || F_[2] < bz + 2 * pMz_) continue;
                 const double nbr = per_cell * (bx + 2 * pM_) * (bx + 2 * pM_) * (bz + 2 * pMz_);
                 const double tgt = per_cell * bx * bx * bz;
-                if (nbr <= 0.9 * a.cap && tgt > best_t) {
+                if (nbr <= 1.0 * a.cap && tgt > best_t) {
                     best_t = tgt;
                     best_bx = bx;
                     best_bz = bz;
                 }
             }
+        if (const char* e = std::getenv("ESP_PAIR_BLOCK")) {  // "bx,bz" (experiments)
+            int bx = 0, bz = 0;
+            if (std::sscanf(e, "%d,%d", &bx, &bz) == 2 && bx >= 1 && bx <= 2 && bz >= 1 &&
+                bz <= kMaxBZ && F_[0] >= bx + 2 * pM_ && F_[1] >= bx + 2 * pM_ &&
+                F_[2] >= bz + 2 * pMz_) {
+                best_bx = bx;
+                best_bz = bz;
+            }
+        }
         a.bx = best_bx;
         a.bz = best_bz;
     }
