@@ -142,3 +142,21 @@ def test_cfg2_direct_ewald_target_subset(esp, gpu):
     _, ud, Fd = O.direct_ewald(pos, q, box, 1e-9, targets=tg)
     assert rel_rms(ef.F[tg], Fd) <= c.eps
     assert max_rel(ef.u[tg], ud) <= 10 * c.eps
+
+
+def test_plan_reuse_across_sizes(esp, gpu):
+    """One plan evaluating systems of different N in turn (the engine regrows
+    its buffers, switches the pair-cell width between r_c/2 and r_c/3 and
+    re-captures its CUDA graph) gives the same results as fresh plans."""
+    from oracle import esp_oracle as O
+    box = (40.0, 40.0, 40.0)
+    small = O.random_system(2000, box, 41)     # ~28 pairs per atom: r_c/2 columns
+    large = O.random_system(30000, box, 42)    # ~420 pairs per atom: r_c/3 columns
+    shared = esp.build_plan(box, "pswf", 1e-4, 6.0, device=gpu)
+    for pos, q in (small, large, small, large):
+        s = esp.ParticleSystem(box, q, pos)
+        a = esp.evaluate(shared, s)
+        b = esp.evaluate(esp.build_plan(box, "pswf", 1e-4, 6.0, device=gpu), s)
+        assert abs(a.energy - b.energy) <= 1e-12 * abs(b.energy)
+        assert rel_rms(a.F, b.F) <= 1e-12
+        assert max_rel(a.u, b.u) <= 1e-12
