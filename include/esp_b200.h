@@ -189,6 +189,26 @@ int esp_pencil_backward(esp_plan* plan, int rank, int nranks, const double* A_de
 int esp_pencil_phase_b(esp_plan* plan, int rank, int nranks, const double* fslab_dev,
                        double* u_dev, double* F_dev, double* energy_dev, void* stream);
 
+/* Direct (mesh-free) Ewald summation on the GPU: one pass of the reference's
+ * ground-truth solver (direct_ewald_pass, reference.hpp:42-206) at splitting
+ * width `lambda` (<= 0: min(L)/6, reference.hpp:222), same stopping rules
+ * (tol/10 per image shell and per reciprocal mode).  Host pointers.  targets:
+ * ntarget atom indices whose u and F are computed (every atom remains a
+ * source), or NULL for all N atoms -- the subset form lifts the reference's
+ * N <= 1e4 cap (reference.hpp:213) so the ESP path can be certified at the
+ * benchmark sizes.  u: ntarget (or N), F: ntarget*3 (or N*3); energy (may be
+ * NULL) = 1/2 sum q u when targets == NULL, NaN otherwise.  tol >= 1e-12,
+ * neutral systems only (NUMERICAL otherwise). */
+typedef struct esp_direct_info {
+    double lambda;
+    int real_shells;
+    int recip_kmax;
+    double tail_bound;
+} esp_direct_info;
+int esp_direct_ewald(const double box[3], long N, const double* pos, const double* q,
+                     long ntarget, const long* targets, double tol, double lambda, double* u,
+                     double* F, double* energy, esp_direct_info* info, int device);
+
 /* Number of reals in the charge grid (nx*ny*nz) for sizing grid_dev. */
 long esp_grid_size(const esp_plan* plan);
 

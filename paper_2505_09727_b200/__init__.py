@@ -28,6 +28,7 @@ __all__ = [
     "ParticleSystem", "EnergyForces", "PartialField", "build_plan", "evaluate",
     "evaluate_device", "local_sum", "spectral_sum", "self_correction", "spread",
     "interpolate", "interpolate_gradient", "require_neutral", "fold", "device_count",
+    "direct_ewald", "ReferenceResult",
     "LIB_PATH",
 ]
 
@@ -83,6 +84,11 @@ class _PencilInfo(C.Structure):
     ]
 
 
+class _DirectInfo(C.Structure):
+    _fields_ = [("lambda_", C.c_double), ("real_shells", C.c_int), ("recip_kmax", C.c_int),
+                ("tail_bound", C.c_double)]
+
+
 class _Timings(C.Structure):
     _fields_ = [(k, C.c_double) for k in
                 ("local", "spread", "fft", "scale", "ifft", "interpolate", "bin")]
@@ -121,6 +127,8 @@ _sig("esp_last_launch_count", [_vp])
 _sig("esp_eval_phase_a", [_vp, _dp, C.c_long, _vp, _vp, C.c_int, C.c_int, _vp, _vp])
 _sig("esp_eval_phase_b", [_vp, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp])
 _sig("esp_grid_size", [_vp], C.c_long)
+_sig("esp_direct_ewald", [_dp, C.c_long, _dp, _dp, C.c_long, _vp, C.c_double, C.c_double, _dp,
+                          _dp, C.POINTER(C.c_double), C.POINTER(_DirectInfo), C.c_int])
 _sig("esp_pencil_geometry", [_vp, C.c_int, C.c_int, C.POINTER(_PencilInfo)])
 _sig("esp_pencil_phase_a", [_vp, _dp, C.c_long, _vp, _vp, C.c_int, C.c_int, _vp, _vp])
 _sig("esp_pencil_forward", [_vp, C.c_int, C.c_int, _vp, _vp, _vp])
@@ -441,6 +449,55 @@ def pencil_phase_b(plan: EwaldPlan, rank: int, nranks: int, fslab_ptr: int, u_pt
     _check(_lib.esp_pencil_phase_b(plan._h, int(rank), int(nranks), C.c_void_p(fslab_ptr),
                                    C.c_void_p(u_ptr), C.c_void_p(F_ptr), C.c_void_p(energy_ptr),
                                    C.c_void_p(stream)))
+
+
+@dataclass
+class ReferenceResult:
+    """reference.hpp:21-29 (u, F for the targets; energy NaN for subsets)."""
+    u: np.ndarray
+    F: np.ndarray
+    energy: float
+    lambda_: float
+    real_shells: int
+    recip_kmax: int
+    residual: float
+
+
+def _direct_pass(system: ParticleSystem, tol, lam, targets, device):
+    N = system.size()
+    tg = None if targets is None else np.ascontiguousarray(targets, dtype=np.int64)
+    n = N if tg is None else tg.size
+    u = np.empty(n)
+    F = np.empty((n, 3))
+    e = C.c_double()
+    info = _DirectInfo()
+    _check(_lib.esp_direct_ewald(_f64(system.box, (3,)), N, system.pos, system.q,
+                                 0 if tg is None else tg.size,
+                                 None if tg is None else tg.ctypes.data_as(C.c_void_p),
+                                 float(tol), float(lam), u, F, C.byref(e), C.byref(info),
+                                 int(device)))
+    return u, F, e.value, info
+
+
+def direct_ewald(system: ParticleSystem, tol: float = 1e-9, targets=None,
+                 device: int = 0) -> ReferenceResult:
+    """esp::direct_ewald (reference.hpp:212-238) on the GPU: a pass at
+    lambda = min(L)/6 and a check pass at 1.3 lambda, whose gap (energy, or the
+    target potentials for a subset) must stay within tol.  targets: optional
+    atom indices (the subset form has no N cap; the reference's is 1e4)."""
+    lam = min(system.box) / 6.0
+    u1, F1, E1, i1 = _direct_pass(system, tol, lam, targets, device)
+    u2, F2, E2, _ = _direct_pass(system, tol, 1.3 * lam, targets, device)
+    if targets is None:
+        gap = abs(E1 - E2)
+        scale = max(1.0, abs(E1))
+    else:
+        gap = float(np.max(np.abs(u1 - u2))) if u1.size else 0.0
+        scale = max(1.0, float(np.max(np.abs(u1))) if u1.size else 1.0)
+    if gap > tol * scale:
+        raise NumericalError("direct_ewald: splitting-width invariance check failed")
+    return ReferenceResult(u1, F1, E1, i1.lambda_, i1.real_shells, i1.recip_kmax,
+                           max(gap, i1.tail_bound))
 
 
 def grid_size(plan: EwaldPlan) -> int:

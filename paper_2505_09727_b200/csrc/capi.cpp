@@ -2,6 +2,7 @@
 
 #include "../../include/esp_b200.h"
 
+#include "direct.hpp"
 #include "engine.hpp"
 #include "plan.hpp"
 
@@ -408,6 +409,44 @@ int esp_pencil_phase_b(esp_plan* p, int rank, int nranks, const double* fslab_de
     return guarded([&] {
         engine(p).pencil_phase_b(rank, nranks, fslab_dev, u_dev, F_dev, energy_dev,
                                  static_cast<cudaStream_t>(stream));
+    });
+}
+
+int esp_direct_ewald(const double box[3], long N, const double* pos, const double* q,
+                     long ntarget, const long* targets, double tol, double lambda, double* u,
+                     double* F, double* energy, esp_direct_info* info, int device) {
+    return guarded([&] {
+        if (!box || !pos || !q || !u || !F) throw espb::InvalidArgument("null argument");
+        if (N <= 0) throw espb::InvalidArgument("direct_ewald: empty system");
+        if (targets && ntarget < 0) throw espb::InvalidArgument("direct_ewald: bad target count");
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+            cudaGetLastError();
+            throw espb::CudaError("direct_ewald: no such CUDA device");
+        }
+        require_neutral(N, q);  // reference.hpp:218
+        const espb::DirectPassResult r = espb::direct_ewald_pass(
+            device, box, N, pos, q, targets ? ntarget : N, targets, tol, lambda, u, F);
+        if (energy) {
+            if (targets) {
+                *energy = std::nan("");
+            } else {
+                double s = 0.0, c = 0.0;  // Kahan, as the reference
+                for (long i = 0; i < N; ++i) {
+                    const double y = q[i] * u[i] - c;
+                    const double t = s + y;
+                    c = (t - s) - y;
+                    s = t;
+                }
+                *energy = 0.5 * s;
+            }
+        }
+        if (info) {
+            info->lambda = r.lambda;
+            info->real_shells = r.real_shells;
+            info->recip_kmax = r.recip_kmax;
+            info->tail_bound = r.tail_bound;
+        }
     });
 }
 
