@@ -310,7 +310,8 @@ struct PairArgs {
     double4* loc;         // original order: (u_l, F_l)
     unsigned long long* npairs;  // ordered in-range pairs evaluated (r < r_c, r > 0)
     int cap;                     // candidates staged per chunk
-    int lcap;                    // per-warp candidate-list capacity
+    int lcap;                    // per-warp candidate-list capacity (even)
+    int nent_max;                // cell entries per CTA neighbourhood
     int M, Mz;                   // neighbourhood reach in columns / slices
     int bz;                      // target slices per CTA
     int bx;                      // target columns per CTA edge (1 or 2)
@@ -400,8 +401,10 @@ __global__ void __launch_bounds__(kPairThreads, kPairWarps >= 8 ? 3 : 6) k_pair(
     float4* cand = reinterpret_cast<float4*>(smem);       // a.cap + 1 (sentinel)
     int* qall = reinterpret_cast<int*>(cand + a.cap + 1);  // 64 per warp
     unsigned short* lall = reinterpret_cast<unsigned short*>(qall + kPairWarps * 64);  // a.lcap per warp
-    __shared__ int ent_src[kMaxEnt], ent_off[kMaxEnt + 1];
-    __shared__ unsigned char ent_slot[kMaxEnt];
+    // cell-entry tables, sized for this launch's (bx+2M)^2 x (bz+2Mz) entries
+    int* ent_src = reinterpret_cast<int*>(lall + kPairWarps * a.lcap);
+    int* ent_off = ent_src + a.nent_max;                       // nent_max + 1
+    unsigned char* ent_slot = reinterpret_cast<unsigned char*>(ent_off + a.nent_max + 1);
     __shared__ double shiftv[27][3];
     __shared__ int isrc[4], ipre[5];
 
@@ -1540,6 +1543,14 @@ void Engine::reconfigure(long N) {
         p.r_c * p.r_c;
     if (pairs_per_atom >= kColDiv3MinPairs) want = 3;
     if (const char* e = std::getenv("ESP_COL_DIV")) want = std::max(2, std::min(kMaxColDiv, std::atoi(e)));
+    // per-warp list pieces: the expected candidates per target (~1.8 / 2.2 per
+    // in-range pair for r_c/3 / r_c/2 columns) plus 20 %, in [256, 1024]
+    {
+        const double cand = pairs_per_atom * (want == 3 ? 1.8 : 2.2) * 1.2;
+        pair_lcap_ = std::max(256, std::min(1024, (static_cast<int>(cand) + 127) / 128 * 128));
+        if (const char* e = std::getenv("ESP_PAIR_LCAP"))
+            pair_lcap_ = std::max(128, std::min(2048, std::atoi(e) / 2 * 2));
+    }
     if (want == col_div_) return;
     CK(cudaDeviceSynchronize());
     if (gexec_) {
@@ -1667,7 +1678,7 @@ void Engine::run_pair(long N, cudaStream_t s, int rank, int nranks) {
     const int nw = kPairWarps;
     pair_warps_ = nw;
     a.cap = pair_cap_;
-    a.lcap = std::min(pair_cap_, 1024) + 32;
+    a.lcap = std::min(pair_cap_, pair_lcap_) + 32;
     a.M = pM_;
     a.Mz = pMz_;
     a.noeval = std::getenv("ESP_PAIR_NOEVAL") ? 1 : 0;
@@ -1711,8 +1722,10 @@ void Engine::run_pair(long N, cudaStream_t s, int rank, int nranks) {
     const int nblocks = (xhi - xlo) * per_x;
     if (nblocks <= 0) return;
     if (N >= (1L << 27)) throw InvalidArgument("pair kernel: N must be < 2^27");
+    a.nent_max = (a.bx + 2 * pM_) * (a.bx + 2 * pM_) * (a.bz + 2 * pMz_);
     size_t sm = (a.cap + 1) * sizeof(float4) + nw * 64 * sizeof(int) +
-                nw * a.lcap * sizeof(unsigned short);
+                nw * a.lcap * sizeof(unsigned short) + (2 * a.nent_max + 1) * sizeof(int) +
+                a.nent_max;
     auto go = [&](auto kern) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(sm)));

@@ -162,6 +162,7 @@ private:
     int nfields_ = 4;           // 4 for ik, 1 for ad
     int pair_warps_ = 4;
     int pair_cap_ = 2048;
+    int pair_lcap_ = 1024;      // per-warp candidate-list pieces
     int pM_ = 2, pMz_ = 4;      // fine stencil reach (columns, slices)
     int col_div_ = 2;           // column edge >= r_c / col_div_
 
