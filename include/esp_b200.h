@@ -165,7 +165,11 @@ int esp_eval_phase_b(esp_plan* plan, int rank, int nranks, const double* grid_de
  *   esp_pencil_phase_b   interpolation + combine for the rank's atoms:
  *                        partial u, F, energy (caller sums over ranks)
  * nranks >= 2; esp_pencil_geometry fails with INVALID_ARGUMENT when a rank
- * would own fewer x-planes than the halo. */
+ * would own fewer x-planes than the halo.
+ * Inputs: every rank passes either the whole system or only its own atoms
+ * (ownership below) plus ghost atoms within r_c of its x-slab (the
+ * neighbours' atoms, any order); a rank computes u, F and the energy share of
+ * the atoms it owns, zero for the others. */
 typedef struct esp_pencil_info {
     int nranks, rank;
     int halo;          /* planes exchanged with each x-neighbour */
@@ -173,6 +177,12 @@ typedef struct esp_pencil_info {
     int y0, y1;        /* owned spectral y-rows */
     int nfields;       /* 4 (ik) or 1 (ad) */
     int nf[3];         /* grid size */
+    /* atom ownership: an atom belongs to the rank whose spread-bin range
+     * [bx0, bx1) holds clamp(floor(fold(x)/hx) / S, 0, nbx-1) (integer
+     * division; fold as system.hpp:29-36) -- the rank computes u and F of
+     * exactly those atoms */
+    double hx;
+    int S, nbx, bx0, bx1;
     long slab_reals;   /* (x1-x0+2 halo)*ny*nz */
     long spec_local;   /* (x1-x0)*ny*(nz/2+1) complex */
     long spec_pencil;  /* nx*(y1-y0)*(nz/2+1) complex */

@@ -64,7 +64,8 @@ class _Overrides(C.Structure):
 class _Info(C.Structure):
     _fields_ = [
         ("family", C.c_int), ("force_method", C.c_int), ("P", C.c_int),
-        ("nf", C.c_int * 3), ("base_nf", C.c_int * 3),
+        ("nf", C.c_int * 3), ("hx", C.c_double), ("S", C.c_int), ("nbx", C.c_int),
+        ("bx0", C.c_int), ("bx1", C.c_int), ("base_nf", C.c_int * 3),
         ("eps", C.c_double), ("r_c", C.c_double), ("shape", C.c_double), ("c1", C.c_double),
         ("chi0", C.c_double),
         ("box", C.c_double * 3), ("h", C.c_double * 3), ("demand", C.c_double * 3),
@@ -79,7 +80,8 @@ class _PencilInfo(C.Structure):
     _fields_ = [
         ("nranks", C.c_int), ("rank", C.c_int), ("halo", C.c_int), ("x0", C.c_int),
         ("x1", C.c_int), ("y0", C.c_int), ("y1", C.c_int), ("nfields", C.c_int),
-        ("nf", C.c_int * 3),
+        ("nf", C.c_int * 3), ("hx", C.c_double), ("S", C.c_int), ("nbx", C.c_int),
+        ("bx0", C.c_int), ("bx1", C.c_int),
         ("slab_reals", C.c_long), ("spec_local", C.c_long), ("spec_pencil", C.c_long),
     ]
 

@@ -359,6 +359,11 @@ int esp_pencil_geometry(const esp_plan* p, int rank, int nranks, esp_pencil_info
         out->y1 = G.y1;
         out->nfields = G.nfields;
         for (int d = 0; d < 3; ++d) out->nf[d] = p->plan.nf[d];
+        out->hx = G.hx;
+        out->S = G.S;
+        out->nbx = G.nbx;
+        out->bx0 = G.bx0;
+        out->bx1 = G.bx1;
         out->slab_reals = G.slab_reals;
         out->spec_local = G.spec_local;
         out->spec_pencil = G.spec_pencil;

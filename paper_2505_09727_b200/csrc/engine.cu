@@ -321,6 +321,11 @@ struct PairArgs {
     int F[3];                    // fine cells per dim (columns x, y; slices z)
     double fw[3];                // fine cell edges
     double box[3];
+    // distributed FFT: targets are the atoms whose spread bin x-index
+    // clamp(floor(x/own_h)/own_S) lies in [own_lo, own_hi) (k_fold_bin's
+    // formula); own_lo < 0: every atom of the launched blocks is a target
+    int own_lo, own_hi, own_S, own_nbx;
+    double own_h;
 };
 
 // d = (r_j - r_i) + image shift, in that order: the reference's min-image
@@ -536,6 +541,11 @@ __global__ void __launch_bounds__(kPairThreads, kPairWarps >= 8 ? 3 : 6) k_pair(
             const int ic = (ii >= ipre[1]) + (ii >= ipre[2]) + (ii >= ipre[3]);
             const int i = isrc[ic] + (ii - ipre[ic]);
             const double4 pi = a.xyzq[i];
+            if (a.own_lo >= 0) {
+                const int bxi = clampi(static_cast<int>(floor(pi.x / a.own_h)) / a.own_S, 0,
+                                       a.own_nbx - 1);
+                if (bxi < a.own_lo || bxi >= a.own_hi) continue;  // another rank's target
+            }
             const float xf = static_cast<float>(pi.x - ox);
             const float yf = static_cast<float>(pi.y - oy);
             const float zf = static_cast<float>(pi.z - oz);
@@ -1345,8 +1355,13 @@ PencilGeom pencil_geometry(const Plan& p, int rank, int nranks) {
         if (r == rank) {
             G.x0 = x0;
             G.x1 = x1;
+            G.bx0 = split_lo(nbx, r, nranks);
+            G.bx1 = split_lo(nbx, r + 1, nranks);
         }
     }
+    G.hx = p.h[0];
+    G.S = S;
+    G.nbx = nbx;
     G.y0 = split_lo(ny, rank, nranks);
     G.y1 = split_lo(ny, rank + 1, nranks);
     G.nfields = p.force_method == ForceMethod::ik ? 4 : 1;
@@ -1643,9 +1658,11 @@ void Engine::prepare(long N, const double* pos, const double* q, double* qsum_de
     }
 }
 
-void Engine::run_pair(long N, cudaStream_t s, int rank, int nranks) {
+void Engine::run_pair(long N, cudaStream_t s, int rank, int nranks, bool own_bins) {
     if (N == 0) return;
     const Plan& p = plan_;
+    if (own_bins && !cells_ok_)
+        throw InvalidArgument("distributed FFT: the box is too small for the cell-list pair path");
     int nd = 20;
     PairConsts k = make_pair_consts(p, nd);
     if (!cells_ok_) {
@@ -1716,8 +1733,27 @@ void Engine::run_pair(long N, cudaStream_t s, int rank, int nranks) {
     // slab decomposition: rank owns x-column blocks [lo, hi) (x-major block order)
     const int nbx = (F_[0] + a.bx - 1) / a.bx;
     const int per_x = ((F_[1] + a.bx - 1) / a.bx) * ((F_[2] + a.bz - 1) / a.bz);
-    const int xlo = static_cast<int>(static_cast<long>(nbx) * rank / nranks);
-    const int xhi = static_cast<int>(static_cast<long>(nbx) * (rank + 1) / nranks);
+    int xlo = static_cast<int>(static_cast<long>(nbx) * rank / nranks);
+    int xhi = static_cast<int>(static_cast<long>(nbx) * (rank + 1) / nranks);
+    a.own_lo = -1;
+    if (own_bins) {
+        // the blocks covering this rank's spread-bin slab (one column of
+        // margin each side); targets filtered by their bin in the kernel
+        int b0, b1;
+        slab_bins(rank, nranks, &b0, &b1);
+        const int per_b = nb_[1] * nb_[2];
+        a.own_lo = b0 / per_b;
+        a.own_hi = b1 / per_b;
+        a.own_S = S_;
+        a.own_nbx = nb_[0];
+        a.own_h = p.h[0];
+        const double X0 = a.own_lo * S_ * p.h[0], X1 = a.own_hi * S_ * p.h[0];
+        const int c0 = std::max(0, static_cast<int>(std::floor(X0 / a.fw[0])) - 1);
+        const int c1 = std::min(F_[0] - 1, static_cast<int>(std::floor(X1 / a.fw[0])) + 1);
+        xlo = c0 / a.bx;
+        xhi = (a.own_hi >= nb_[0]) ? nbx : std::min(nbx, c1 / a.bx + 1);
+        if (a.own_lo >= a.own_hi) return;
+    }
     a.blk0 = xlo * per_x;
     const int nblocks = (xhi - xlo) * per_x;
     if (nblocks <= 0) return;
@@ -1889,7 +1925,7 @@ void Engine::pencil_phase_a(long N, const double* pos, const double* q, int rank
     reconfigure(N);
     prepare(N, pos, q, nullptr, s);
     if (N > 0) CK(cudaMemsetAsync(d_loc_, 0, sizeof(double4) * N, s));
-    run_pair(N, s, rank, nranks);
+    run_pair(N, s, rank, nranks, true);
     GridArgs g = grid_args();
     g.xslab = 1;
     g.x_lo = G.x0 - G.halo;

@@ -48,6 +48,10 @@ struct PencilGeom {
     long spec_local = 0;    // (x1 - x0) * ny * (nz/2+1): forward send size (complex)
     long spec_pencil = 0;   // nx * (y1 - y0) * (nz/2+1): forward receive size (complex)
     int nfields = 4;        // interleaved fields per node of the field slab
+    // atom ownership: an atom belongs to the rank whose spread-bin x-range
+    // [bx0, bx1) holds clamp(floor(fold(x) / hx) / S, 0, nbx - 1)
+    double hx = 0.0;
+    int S = 0, nbx = 0, bx0 = 0, bx1 = 0;
 };
 // Spread bin edge S (grid cells) the engine uses for a plan.
 int spread_bin_edge(const Plan& p);
@@ -134,7 +138,7 @@ private:
     void set_cells(int col_div);
     void alloc_cells();
     void prepare(long N, const double* pos, const double* q, double* qsum_dev, cudaStream_t s);
-    void run_pair(long N, cudaStream_t s, int rank, int nranks);
+    void run_pair(long N, cudaStream_t s, int rank, int nranks, bool own_bins = false);
     void run_grid(long N, cudaStream_t s, StageTimes* t);
     void run_spread(long N, cudaStream_t s, int rank, int nranks, double* grid,
                     const GridArgs* gslab = nullptr, long nreals = -1);

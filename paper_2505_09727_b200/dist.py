@@ -247,10 +247,14 @@ def _neighbour_exchange(t, outs, ins, left, right, add, group):
             off += b - a
 
 
-def evaluate_pencil(plan, box, N, pos, q, bufs, layout, rank, stream=0, group=None, engine=None):
+def evaluate_pencil(plan, box, N, pos, q, bufs, layout, rank, stream=0, group=None, engine=None,
+                    reduce_outputs=True):
     """One rank's share of a distributed-FFT ESP evaluation (strong scaling;
     every rank calls this collectively).  pos (3N), q (N): the full system on
-    every rank; returns bufs.out = [u | F | E] summed over ranks."""
+    every rank, or this rank's own atoms plus its ghosts (see
+    evaluate_pencil_local); returns bufs.out = [u | F | E], summed over the
+    ranks when reduce_outputs (replicated inputs), else this rank's share
+    (its own atoms' u and F, zero elsewhere, and its energy part)."""
     import torch.distributed as dist
     engine = engine or _Lib
     G = layout.G
@@ -274,19 +278,25 @@ def evaluate_pencil(plan, box, N, pos, q, bufs, layout, rank, stream=0, group=No
     N_ = N
     engine.pencil_phase_b(plan, rank, G, bufs.fslab, bufs.out[:N_], bufs.out[N_:4 * N_],
                           bufs.out[4 * N_:], stream)
-    dist.all_reduce(bufs.out, group=group)
+    if reduce_outputs:
+        dist.all_reduce(bufs.out, group=group)
     return bufs.out
 
 
 def evaluate_pencil_emulated(plans, box, N, pos, q, bufs, layout, stream=0, engine=None):
     """The same algorithm with all ranks in one process (lockstep; the
     exchanges become device copies): one plan and one PencilBuffers per
-    emulated rank.  Used by the single-GPU tests and the bench's --pencil
-    mode; the result must equal evaluate() on the whole system."""
+    emulated rank.  N, pos, q: the whole system (replicated inputs), or lists
+    with one (local) system per rank.  Used by the single-GPU tests; the
+    rank sum must equal evaluate() on the whole system."""
     engine = engine or _Lib
     G = layout.G
+    per_rank = isinstance(N, (list, tuple))
+    Ns = list(N) if per_rank else [N] * G
+    poss = list(pos) if per_rank else [pos] * G
+    qs = list(q) if per_rank else [q] * G
     for r in range(G):
-        engine.pencil_phase_a(plans[r], box, N, pos, q, r, G, bufs[r].slab, stream)
+        engine.pencil_phase_a(plans[r], box, Ns[r], poss[r], qs[r], r, G, bufs[r].slab, stream)
     _emulated_exchange([b.slab for b in bufs], layout, 1, add=True)
     for r in range(G):
         engine.pencil_forward(plans[r], r, G, bufs[r].slab, bufs[r].send, stream)
@@ -303,10 +313,10 @@ def evaluate_pencil_emulated(plans, box, N, pos, q, bufs, layout, stream=0, engi
         engine.pencil_backward(plans[r], r, G, bufs[r].A2, bufs[r].B2, bufs[r].fslab, stream)
     _emulated_exchange([b.fslab for b in bufs], layout, layout.nfields, add=False)
     for r in range(G):
-        o = bufs[r].out
-        engine.pencil_phase_b(plans[r], r, G, bufs[r].fslab, o[:N], o[N:4 * N], o[4 * N:],
+        o, n = bufs[r].out, Ns[r]
+        engine.pencil_phase_b(plans[r], r, G, bufs[r].fslab, o[:n], o[n:4 * n], o[4 * n:],
                               stream)
-    return sum(b.out for b in bufs)
+    return [b.out for b in bufs] if per_rank else sum(b.out for b in bufs)
 
 
 def _emulated_exchange(ts, layout, nfields, add):
@@ -348,3 +358,127 @@ def _emulated_alltoall(sends, recvs, send_splits):
             n = send_splits[s][r]
             recvs[r][pos:pos + n] = sends[s][offs[s][r]:offs[s][r] + n]
             pos += n
+
+
+# ---- local inputs: own atoms + ghosts instead of the replicated system -----
+
+
+def fold_positions(pos, box):
+    """system.hpp:29-36 on an (N, 3) numpy array or torch tensor (the
+    engine's own fold; idempotent)."""
+    import numpy as np
+    if isinstance(pos, np.ndarray):
+        L = np.asarray(box, dtype=np.float64)
+        p = pos - L * np.floor(pos / L)
+        return np.where(p >= L, 0.0, p)
+    import torch
+    L = torch.tensor(box, dtype=pos.dtype, device=pos.device)
+    p = pos - L * torch.floor(pos / L)
+    return torch.where(p >= L, torch.zeros_like(p), p)
+
+
+def atom_owner(layout, x):
+    """Rank owning each atom, from its folded x (the engine's spread-bin
+    formula: clamp(floor(x/hx) // S, 0, nbx-1) in [bx0, bx1) of the rank)."""
+    import numpy as np
+    g0 = layout.g[0]
+    hx, S, nbx = g0["hx"], g0["S"], g0["nbx"]
+    ends = [g["bx1"] for g in layout.g]
+    if isinstance(x, np.ndarray):
+        bx = np.clip(np.floor(x / hx).astype(np.int64) // S, 0, nbx - 1)
+        return np.searchsorted(np.asarray(ends), bx, side="right")
+    import torch
+    bx = torch.clamp(torch.div(torch.floor(x / hx).to(torch.int64), S, rounding_mode="floor"),
+                     0, nbx - 1)
+    return torch.searchsorted(torch.tensor(ends, device=x.device), bx, right=True)
+
+
+def slab_bounds(layout, r, box_x):
+    """[X0, X1) of rank r's atoms in x."""
+    g, g0 = layout.g[r], layout.g[0]
+    X0 = g["bx0"] * g0["S"] * g0["hx"]
+    X1 = box_x if g["bx1"] >= g0["nbx"] else g["bx1"] * g0["S"] * g0["hx"]
+    return X0, X1
+
+
+def check_ghost_reach(layout, box_x, r_c):
+    """Ghosts come from the two x-neighbours only: every slab must be at
+    least r_c wide."""
+    for r in range(layout.G):
+        X0, X1 = slab_bounds(layout, r, box_x)
+        if X1 - X0 < r_c * (1.0 + 1e-9):
+            from . import InvalidArgument
+            raise InvalidArgument(f"distributed FFT: rank {r} slab ({X1 - X0:.3g}) is narrower "
+                                  f"than r_c ({r_c:g}); use fewer ranks")
+
+
+def ghost_masks(layout, r, x, box_x, r_c):
+    """Masks of rank r's own atoms (folded x) to send to its left and right
+    neighbours: those within r_c (plus a margin) of the shared slab faces."""
+    X0, X1 = slab_bounds(layout, r, box_x)
+    reach = r_c * (1.0 + 1e-9) + 1e-12 * box_x
+    return (x - X0) <= reach, (X1 - x) <= reach
+
+
+def exchange_ghosts(layout, rank, pos_own, q_own, box, r_c, group=None):
+    """Send this rank's atoms near its x-faces to the neighbours and receive
+    theirs (NCCL send/recv on the GPU box, gloo in the CPU tests): returns the
+    ghost positions (k, 3) and charges (k,).  pos_own must be folded."""
+    import torch
+    import torch.distributed as dist
+    left, right = layout.neighbours(rank)
+    to_l, to_r = ghost_masks(layout, rank, pos_own[:, 0], box[0], r_c)
+    packed = torch.cat([pos_own, q_own[:, None]], dim=1)
+    sends = {}
+    if left == right:
+        sends[left] = packed[to_l | to_r]
+    else:
+        sends[left] = packed[to_l]
+        sends[right] = packed[to_r]
+    peers = sorted(sends)
+    cnt_out = {p: torch.tensor([sends[p].shape[0]], dtype=torch.int64, device=pos_own.device)
+               for p in peers}
+    cnt_in = {p: torch.zeros(1, dtype=torch.int64, device=pos_own.device) for p in peers}
+    ops = [dist.P2POp(dist.isend, cnt_out[p], p, group) for p in peers]
+    ops += [dist.P2POp(dist.irecv, cnt_in[p], p, group) for p in peers]
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+    recv = {p: torch.empty((int(cnt_in[p].item()), 4), dtype=pos_own.dtype, device=pos_own.device)
+            for p in peers}
+    ops = [dist.P2POp(dist.isend, sends[p].contiguous(), p, group)
+           for p in peers if sends[p].shape[0] > 0]
+    ops += [dist.P2POp(dist.irecv, recv[p], p, group) for p in peers if recv[p].shape[0] > 0]
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    g = torch.cat([recv[p] for p in peers], dim=0)
+    return g[:, :3].contiguous(), g[:, 3].contiguous()
+
+
+def evaluate_pencil_local(plan, box, pos_own, q_own, layout, rank, r_c, stream=0, group=None,
+                          engine=None, cache=None):
+    """Distributed-FFT evaluation from LOCAL inputs: each rank holds only the
+    atoms it owns (atom_owner), receives its ghosts from the x-neighbours,
+    and returns (u, F) of its own atoms plus the total energy (one all-reduce
+    of a double) -- no rank ever holds the whole system.  pos_own: (n, 3)
+    torch tensor (folded or not), q_own: (n,).  cache: optional dict keeping
+    the rank's buffers between calls."""
+    import torch
+    import torch.distributed as dist
+    check_ghost_reach(layout, box[0], r_c)
+    pos_own = fold_positions(pos_own, box)
+    gpos, gq = exchange_ghosts(layout, rank, pos_own, q_own, box, r_c, group)
+    pos_l = torch.cat([pos_own, gpos], dim=0).contiguous()
+    q_l = torch.cat([q_own, gq]).contiguous()
+    n_own, n = q_own.numel(), q_l.numel()
+    bufs = cache.get("bufs") if cache is not None else None
+    if bufs is None or bufs.out.numel() != 4 * n + 1:
+        bufs = PencilBuffers(layout, rank, n, pos_l.device)
+        if cache is not None:
+            cache["bufs"] = bufs
+    out = evaluate_pencil(plan, box, n, pos_l.reshape(-1), q_l, bufs, layout, rank, stream,
+                          group, engine, reduce_outputs=False)
+    e = out[4 * n:].clone()
+    if dist.is_available() and dist.is_initialized():
+        dist.all_reduce(e, group=group)
+    return out[:n_own], out[n:4 * n].reshape(n, 3)[:n_own], e

@@ -130,15 +130,14 @@ def test_slab_decomposition_plumbing_gloo():
 
 class _OraclePencilEngine:
     """CPU stand-in for the esp_pencil_* phases (test infrastructure): same
-    buffer layouts and sizes as the C ABI (include/esp_b200.h), physics from
-    the numpy oracle.  A rank spreads/interpolates the atoms whose grid cell
-    floor(x/h) lies in its planes [x0, x1) and sums the real-space part of an
-    index range of targets."""
+    buffer layouts, sizes and atom ownership as the C ABI
+    (include/esp_b200.h), physics from the numpy oracle.  The inputs of
+    pencil_phase_a (whole system or own atoms + ghosts) are what the rank
+    computes with; it owns the atoms whose spread bin lies in its range."""
 
-    def __init__(self, oplan, pos, q, host_plan):
+    def __init__(self, oplan, host_plan):
         from oracle import esp_oracle as O
-        self.O, self.p, self.q = O, oplan, q
-        self.pos = O.fold(pos, oplan.box)
+        self.O, self.p = O, oplan
         self.host_plan = host_plan
         self.state = {}
 
@@ -146,24 +145,25 @@ class _OraclePencilEngine:
         import paper_2505_09727_b200 as esp
         return esp.pencil_geometry(self.host_plan, rank, nranks)
 
-    def _atoms(self, g):
-        l = np.minimum(np.floor(self.pos[:, 0] / self.p.h[0]).astype(int), self.p.nf[0] - 1)
-        return (l >= g["x0"]) & (l < g["x1"])
+    def _owned(self, g, pos):
+        bx = np.clip(np.floor(pos[:, 0] / g["hx"]).astype(np.int64) // g["S"], 0, g["nbx"] - 1)
+        return (bx >= g["bx0"]) & (bx < g["bx1"])
 
     def _planes(self, g):
         return np.arange(g["x0"] - g["halo"], g["x1"] + g["halo"]) % self.p.nf[0]
 
     def pencil_phase_a(self, plan, box, N, pos, q, rank, nranks, slab, stream):
         g = self.geometry(plan, rank, nranks)
-        own = self._atoms(g)
-        full = self.O.spread(self.p, self.pos[own], self.q[own])
+        pos = self.O.fold(np.asarray(pos).reshape(-1, 3), self.p.box)
+        q = np.asarray(q)
+        own = self._owned(g, pos)
+        full = self.O.spread(self.p, pos[own], q[own])
         # own atoms touch only [x0-halo, x1+halo): the slab is exact
         slab.copy_(torch.from_numpy(np.ascontiguousarray(full[self._planes(g)]).ravel()))
-        ul, Fl = self.O.local_sum(self.p, self.pos, self.q)
-        tgt = slice(N * rank // nranks, N * (rank + 1) // nranks)
+        ul, Fl = self.O.local_sum(self.p, pos, q)
         u0, F0 = np.zeros_like(ul), np.zeros_like(Fl)
-        u0[tgt], F0[tgt] = ul[tgt], Fl[tgt]
-        self.state[rank] = (u0, F0)
+        u0[own], F0[own] = ul[own], Fl[own]
+        self.state[rank] = (u0, F0, pos, q, own)
 
     def pencil_forward(self, plan, rank, nranks, slab, send, stream):
         g = self.geometry(plan, rank, nranks)
@@ -224,16 +224,15 @@ class _OraclePencilEngine:
         nx, ny, nz = g["nf"]
         h, nxl, nf = g["halo"], g["x1"] - g["x0"], g["nfields"]
         fs = fslab.numpy().reshape(nxl + 2 * h, ny, nz, nf)
-        own = self._atoms(g)
-        P = self.pos[own]
-        uu, FF = self.state[rank]
+        uu, FF, pos, q, own = self.state[rank]
+        P = pos[own]
         uu, FF = uu.copy(), FF.copy()
         full = np.zeros((nx, ny, nz))
         def interp(f, deriv=-1):
             full[:] = 0.0
             full[self._planes(g)] = fs[:, :, :, f]   # halo copies agree with their owners
             return self.O.interpolate(self.p, full, P, deriv)
-        qo = self.q[own]
+        qo = q[own]
         uu[own] += interp(0) - self.O.self_correction(self.p, qo)
         if nf == 4:
             for d in range(3):
@@ -243,7 +242,7 @@ class _OraclePencilEngine:
                 FF[own, d] += -qo * interp(0, d)
         u.copy_(torch.from_numpy(uu))
         F.copy_(torch.from_numpy(FF.ravel()))
-        e.fill_(0.5 * float(np.dot(self.q, uu)))
+        e.fill_(0.5 * float(np.dot(q, uu)))
 
 
 def _pencil_case(fm="ik"):
@@ -261,10 +260,11 @@ def _pencil_worker(rank, world, port, fm, out):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2505_09727_b200.dist import PencilBuffers, PencilLayout, evaluate_pencil
     box, pos, q, p, hp = _pencil_case(fm)
-    eng = _OraclePencilEngine(p, pos, q, hp)
+    eng = _OraclePencilEngine(p, hp)
     layout = PencilLayout.of(hp, world, engine=eng)
     bufs = PencilBuffers(layout, rank, q.size, "cpu")
-    res = evaluate_pencil(hp, box, q.size, None, None, bufs, layout, rank, engine=eng)
+    res = evaluate_pencil(hp, box, q.size, torch.from_numpy(pos.ravel().copy()),
+                          torch.from_numpy(q), bufs, layout, rank, engine=eng)
     out[rank] = res.numpy().copy()
     dist.destroy_process_group()
 
@@ -295,10 +295,11 @@ def test_pencil_emulated_matches_oracle(world):
     """The lockstep emulation (the single-GPU test driver) on the same engine."""
     from paper_2505_09727_b200.dist import PencilBuffers, PencilLayout, evaluate_pencil_emulated
     box, pos, q, p, hp = _pencil_case()
-    eng = _OraclePencilEngine(p, pos, q, hp)
+    eng = _OraclePencilEngine(p, hp)
     layout = PencilLayout.of(hp, world, engine=eng)
     bufs = [PencilBuffers(layout, r, q.size, "cpu") for r in range(world)]
-    res = evaluate_pencil_emulated([hp] * world, box, q.size, None, None, bufs, layout, engine=eng)
+    res = evaluate_pencil_emulated([hp] * world, box, q.size, pos.ravel(), q, bufs, layout,
+                                   engine=eng)
     _check_against_oracle(res.numpy(), p, pos, q)
 
 
@@ -319,3 +320,72 @@ def test_pencil_geometry_host():
         esp.pencil_geometry(hp, 0, 64)
     with pytest.raises(esp.InvalidArgument):
         esp.pencil_geometry(hp, 0, 1)
+
+
+def _pencil_local_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2505_09727_b200.dist import (PencilLayout, atom_owner, evaluate_pencil_local,
+                                            fold_positions)
+    box, pos, q, p, hp = _pencil_case()
+    eng = _OraclePencilEngine(p, hp)
+    layout = PencilLayout.of(hp, world, engine=eng)
+    posf = fold_positions(pos, box)
+    idx = np.nonzero(atom_owner(layout, posf[:, 0]) == rank)[0]
+    # this rank only ever sees its own atoms (unfolded, to exercise the fold)
+    mine = pos[idx] + np.array(box) * (rank + 1)
+    u, F, E = evaluate_pencil_local(hp, box, torch.from_numpy(mine), torch.from_numpy(q[idx]),
+                                    layout, rank, 1.0, engine=eng)
+    out[rank] = (idx, u.numpy().copy(), F.numpy().copy(), float(E))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_pencil_local_inputs_gloo(world):
+    """Each rank holds only its own atoms; ghosts travel between x-neighbours
+    (send/recv), only the energy is all-reduced; the union of the ranks'
+    outputs is the single-process oracle evaluation."""
+    from oracle import esp_oracle as O
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_pencil_local_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    box, pos, q, p, hp = _pencil_case()
+    E, u, F = O.evaluate(p, pos, q)
+    seen = np.zeros(q.size, dtype=int)
+    for r in range(world):
+        idx, ur, Fr, Er = out[r]
+        seen[idx] += 1
+        assert np.allclose(ur, u[idx], rtol=0, atol=1e-11 * np.abs(u).max())
+        assert np.allclose(Fr, F[idx], rtol=0, atol=1e-11 * np.abs(F).max())
+        assert abs(Er - E) <= 1e-11 * abs(E)
+    assert (seen == 1).all()
+
+
+def test_ghost_selection_host():
+    """Ghost masks: an atom within r_c of a slab face goes to that neighbour;
+    every atom within r_c (periodic, in x) of a rank's slab is either owned
+    by it or one of its ghosts."""
+    import paper_2505_09727_b200 as esp
+    from paper_2505_09727_b200.dist import (PencilLayout, atom_owner, fold_positions,
+                                            ghost_masks, slab_bounds)
+    box = (12.0, 10.0, 11.0)
+    hp = esp.build_plan(box, "pswf", 1e-3, 1.0, device=-1)
+    pos = np.random.default_rng(2).uniform(-3.0, 15.0, (4000, 3))
+    posf = fold_positions(pos, box)
+    for G in (2, 3, 4):
+        lay = PencilLayout.of(hp, G)
+        own = atom_owner(lay, posf[:, 0])
+        for r in range(G):
+            X0, X1 = slab_bounds(lay, r, box[0])
+            left, right = lay.neighbours(r)
+            have = own == r
+            for nb, side in ((left, 1), (right, 0)):
+                m = own == nb
+                tl, tr = ghost_masks(lay, nb, posf[:, 0], box[0], 1.0)
+                have |= m & (tr if side == 1 else tl)
+            d = np.minimum.reduce([np.abs(posf[:, 0] - X0), np.abs(posf[:, 0] - X1),
+                                   np.abs(posf[:, 0] - X0 + box[0]),
+                                   np.abs(posf[:, 0] - X1 - box[0])])
+            inside = (posf[:, 0] >= X0) & (posf[:, 0] < X1)
+            need = inside | (d < 1.0)
+            assert (have | ~need).all()

@@ -79,3 +79,56 @@ def test_pencil_refuses_thin_slabs(esp, gpu):
     plan = esp.build_plan((c.L,) * 3, "pswf", c.eps, c.r_c, device=gpu)
     with pytest.raises(esp.InvalidArgument):
         esp.pencil_geometry(plan, 0, 8)
+
+
+def _pencil_local(esp, box, pos, q, eps, r_c, nranks):
+    """Local inputs: each emulated rank gets only its own atoms plus the
+    ghosts its x-neighbours would send it (dist.ghost_masks)."""
+    from paper_2505_09727_b200.dist import (PencilBuffers, PencilLayout, atom_owner,
+                                            evaluate_pencil_emulated, fold_positions,
+                                            ghost_masks)
+    dev = torch.device("cuda", 0)
+    N = q.size
+    plans = [esp.build_plan(box, "pswf", eps, r_c, device=0) for _ in range(nranks)]
+    layout = PencilLayout.of(plans[0], nranks)
+    posf = fold_positions(pos, box)
+    own = atom_owner(layout, posf[:, 0])
+    masks = [ghost_masks(layout, r, posf[:, 0], box[0], r_c) for r in range(nranks)]
+    idx, Ns, poss, qs = [], [], [], []
+    for r in range(nranks):
+        left, right = layout.neighbours(r)
+        mine = np.nonzero(own == r)[0]
+        gh = (own == left) & masks[left][1] | (own == right) & masks[right][0]
+        loc = np.concatenate([mine, np.nonzero(gh & (own != r))[0]])
+        idx.append(mine)
+        Ns.append(loc.size)
+        poss.append(torch.from_numpy(np.ascontiguousarray(pos[loc]).ravel()).to(dev))
+        qs.append(torch.from_numpy(q[loc]).to(dev))
+        assert loc.size < N or nranks == 1
+    bufs = [PencilBuffers(layout, r, Ns[r], dev) for r in range(nranks)]
+    st = torch.cuda.current_stream().cuda_stream
+    outs = evaluate_pencil_emulated(plans, box, Ns, poss, qs, bufs, layout, st)
+    u, F, E = np.zeros(N), np.zeros((N, 3)), 0.0
+    for r in range(nranks):
+        o = outs[r].cpu().numpy()
+        n, m = Ns[r], idx[r].size
+        u[idx[r]] = o[:m]
+        F[idx[r]] = o[n:4 * n].reshape(n, 3)[:m]
+        E += float(o[4 * n])
+    return u, F, E
+
+
+@pytest.mark.parametrize("name,nranks", [("cfg2", 2), ("cfg2", 3), ("cfg4", 4), ("cfg4", 8),
+                                         ("cfg5", 8)])
+def test_pencil_local_inputs_equal_single_gpu(esp, gpu, name, nranks):
+    """No rank holds the whole system: own atoms + ghosts per rank; the
+    gathered own outputs equal the single-GPU evaluation."""
+    from paper_2505_09727_b200 import systems as S
+    c = S.config(name)
+    pos, q, box = c.system()
+    full = esp.evaluate(esp.build_plan(box, "pswf", c.eps, c.r_c, device=gpu),
+                        esp.ParticleSystem(box, q, pos))
+    u, F, E = _pencil_local(esp, box, pos, q, c.eps, c.r_c, nranks)
+    assert abs(E - full.energy) <= 1e-12 * abs(full.energy)
+    assert rel_rms(F, full.F) <= 1e-12
+    assert max_rel(u, full.u) <= 1e-12
