@@ -137,7 +137,7 @@ int esp_eval_phase_a(esp_plan* plan, const double box[3], long N, const double* 
                      const double* q_dev, int rank, int nranks, double* grid_dev, void* stream);
 int esp_eval_phase_b(esp_plan* plan, int rank, int nranks, const double* grid_dev, double* u_dev,
                      double* F_dev, double* energy_dev, void* stream);
-/* Distributed-FFT evaluation (DESIGN.md section 5b): the charge grid and the
+/* Distributed-FFT evaluation (DESIGN.md section 6): the charge grid and the
  * fields are distributed too -- rank r holds the x-planes [x0, x1) plus
  * `halo` planes on each side, and the spectrum's y-rows [y0, y1) between the
  * two transposes.  The caller moves data between the steps (NCCL over
@@ -177,10 +177,10 @@ typedef struct esp_pencil_info {
     int y0, y1;        /* owned spectral y-rows */
     int nfields;       /* 4 (ik) or 1 (ad) */
     int nf[3];         /* grid size */
-    /* atom ownership: an atom belongs to the rank whose spread-bin range
-     * [bx0, bx1) holds clamp(floor(fold(x)/hx) / S, 0, nbx-1) (integer
-     * division; fold as system.hpp:29-36) -- the rank computes u and F of
-     * exactly those atoms */
+    /* atom ownership: an atom belongs to the rank whose planes [x0, x1)
+     * hold clamp(floor(fold(x)/hx), 0, nf[0]-1) (fold as system.hpp:29-36)
+     * -- the rank computes u and F of exactly those atoms; it processes the
+     * spread bins [bx0, bx1) of edge S (of nbx) that intersect its planes */
     double hx;
     int S, nbx, bx0, bx1;
     long slab_reals;   /* (x1-x0+2 halo)*ny*nz */

@@ -39,6 +39,8 @@ struct GridArgs {
     int bin0;           // first spread bin of this launch (slab decomposition)
     int xslab;          // 1: x indexes a rank's plane slab starting at plane x_lo
     int x_lo;           //    (unwrapped; the slab's halos hold the periodic images)
+    int own_x0, own_x1; // xslab: only atoms with clamp(floor(x/h), 0, nx-1) in
+                        //    [own_x0, own_x1) are spread / interpolated
     const double* win;  // 3 x 4P x 13 (phi) then 3 x 4P x 13 (dphi)
 };
 
@@ -321,10 +323,10 @@ struct PairArgs {
     int F[3];                    // fine cells per dim (columns x, y; slices z)
     double fw[3];                // fine cell edges
     double box[3];
-    // distributed FFT: targets are the atoms whose spread bin x-index
-    // clamp(floor(x/own_h)/own_S) lies in [own_lo, own_hi) (k_fold_bin's
-    // formula); own_lo < 0: every atom of the launched blocks is a target
-    int own_lo, own_hi, own_S, own_nbx;
+    // distributed FFT: targets are the atoms whose grid plane
+    // clamp(floor(x/own_h), 0, own_nx-1) lies in [own_lo, own_hi);
+    // own_lo < 0: every atom of the launched blocks is a target
+    int own_lo, own_hi, own_nx;
     double own_h;
 };
 
@@ -542,9 +544,8 @@ __global__ void __launch_bounds__(kPairThreads, kPairWarps >= 8 ? 3 : 6) k_pair(
             const int i = isrc[ic] + (ii - ipre[ic]);
             const double4 pi = a.xyzq[i];
             if (a.own_lo >= 0) {
-                const int bxi = clampi(static_cast<int>(floor(pi.x / a.own_h)) / a.own_S, 0,
-                                       a.own_nbx - 1);
-                if (bxi < a.own_lo || bxi >= a.own_hi) continue;  // another rank's target
+                const int l = clampi(static_cast<int>(floor(pi.x / a.own_h)), 0, a.own_nx - 1);
+                if (l < a.own_lo || l >= a.own_hi) continue;  // another rank's target
             }
             const float xf = static_cast<float>(pi.x - ox);
             const float yf = static_cast<float>(pi.y - oy);
@@ -779,7 +780,11 @@ __global__ void __launch_bounds__(512) k_spread(GridArgs g, const double4* __res
             const Foot f = footprint(P, x, g.h[d], g.half[d]);
             const double* tab = g.win + static_cast<long>(d) * 4 * P * kNc;
             double* w = wch + (ai * 3 + d) * MP;
-            const double scale = d == 0 ? v.w : 1.0;
+            double scale = d == 0 ? v.w : 1.0;
+            if (d == 0 && g.xslab) {  // distributed FFT: another rank's atom in a shared bin
+                const int l = clampi(static_cast<int>(floor(v.x / g.h[0])), 0, g.nf[0] - 1);
+                if (l < g.own_x0 || l >= g.own_x1) scale = 0.0;
+            }
 #pragma unroll
             for (int j = 0; j < MP; ++j) {
                 if (j < P) {
@@ -914,7 +919,12 @@ __global__ void __launch_bounds__(128) k_interp(GridArgs g, InterpArgs a) {
         k += a.startB[a.bin_lo];
         kend = a.startB[a.bin_hi];
     }
-    if (k < kend) {
+    bool mine = k < kend;
+    if (mine && g.xslab) {  // distributed FFT: another rank's atom in a shared bin
+        const int l = clampi(static_cast<int>(floor(a.xyzq[k].x / g.h[0])), 0, g.nf[0] - 1);
+        mine = l >= g.own_x0 && l < g.own_x1;
+    }
+    if (mine) {
         const double4 v = a.xyzq[k];
         const int o = a.orig[k];
         const Foot f[3] = {footprint(P, v.x, g.h[0], g.half[0]),
@@ -1202,7 +1212,7 @@ struct InterpLaunch {
 
 
 // ----------------------------------------------------------------------------
-// distributed FFT: transposes and the pencil multiply (DESIGN.md section 5b)
+// distributed FFT: transposes and the pencil multiply (DESIGN.md section 6)
 // ----------------------------------------------------------------------------
 
 __host__ __device__ __forceinline__ int split_lo(int n, int s, int G) {
@@ -1342,12 +1352,13 @@ PencilGeom pencil_geometry(const Plan& p, int rank, int nranks) {
     PencilGeom G;
     G.nranks = nranks;
     G.rank = rank;
-    // footprints of a bin's atoms reach P/2 planes below and P/2 + 1 above
-    // its planes (spread tile: S + P + 2 planes from bx S - P/2)
+    // footprints of an atom in plane l reach planes [l - P/2, l + P/2 + 1]
     G.halo = p.P / 2 + 2;
+    // ownership by grid plane (balanced to one plane); the spread bins that
+    // intersect a rank's planes are processed by it, atoms filtered by plane
     for (int r = 0; r < nranks; ++r) {
-        const int x0 = std::min(nx, split_lo(nbx, r, nranks) * S);
-        const int x1 = std::min(nx, split_lo(nbx, r + 1, nranks) * S);
+        const int x0 = split_lo(nx, r, nranks);
+        const int x1 = split_lo(nx, r + 1, nranks);
         if (x1 - x0 < G.halo)
             throw InvalidArgument("distributed FFT: rank " + std::to_string(r) + " would own " +
                                   std::to_string(x1 - x0) + " x-planes, fewer than the halo (" +
@@ -1355,8 +1366,8 @@ PencilGeom pencil_geometry(const Plan& p, int rank, int nranks) {
         if (r == rank) {
             G.x0 = x0;
             G.x1 = x1;
-            G.bx0 = split_lo(nbx, r, nranks);
-            G.bx1 = split_lo(nbx, r + 1, nranks);
+            G.bx0 = x0 / S;
+            G.bx1 = std::min(nbx, (x1 + S - 1) / S);
         }
     }
     G.hx = p.h[0];
@@ -1737,21 +1748,18 @@ void Engine::run_pair(long N, cudaStream_t s, int rank, int nranks, bool own_bin
     int xhi = static_cast<int>(static_cast<long>(nbx) * (rank + 1) / nranks);
     a.own_lo = -1;
     if (own_bins) {
-        // the blocks covering this rank's spread-bin slab (one column of
-        // margin each side); targets filtered by their bin in the kernel
-        int b0, b1;
-        slab_bins(rank, nranks, &b0, &b1);
-        const int per_b = nb_[1] * nb_[2];
-        a.own_lo = b0 / per_b;
-        a.own_hi = b1 / per_b;
-        a.own_S = S_;
-        a.own_nbx = nb_[0];
+        // the blocks covering this rank's x-planes (one column of margin each
+        // side); targets filtered by their plane in the kernel
+        const PencilGeom G = pencil_geometry(p, rank, nranks);
+        a.own_lo = G.x0;
+        a.own_hi = G.x1;
+        a.own_nx = p.nf[0];
         a.own_h = p.h[0];
-        const double X0 = a.own_lo * S_ * p.h[0], X1 = a.own_hi * S_ * p.h[0];
+        const double X0 = G.x0 * p.h[0], X1 = G.x1 * p.h[0];
         const int c0 = std::max(0, static_cast<int>(std::floor(X0 / a.fw[0])) - 1);
         const int c1 = std::min(F_[0] - 1, static_cast<int>(std::floor(X1 / a.fw[0])) + 1);
         xlo = c0 / a.bx;
-        xhi = (a.own_hi >= nb_[0]) ? nbx : std::min(nbx, c1 / a.bx + 1);
+        xhi = (G.x1 >= p.nf[0]) ? nbx : std::min(nbx, c1 / a.bx + 1);
         if (a.own_lo >= a.own_hi) return;
     }
     a.blk0 = xlo * per_x;
@@ -1782,14 +1790,13 @@ void Engine::run_pair(long N, cudaStream_t s, int rank, int nranks, bool own_bin
 }
 
 void Engine::run_spread(long N, cudaStream_t s, int rank, int nranks, double* grid,
-                        const GridArgs* gslab, long nreals) {
+                        const GridArgs* gslab, long nreals, int b0, int b1) {
     const Plan& p = plan_;
     if (!grid) grid = d_grid_;
     CK(cudaMemsetAsync(grid, 0, sizeof(double) * (nreals >= 0 ? nreals : M_), s));
     if (N == 0) return;
     GridArgs g = gslab ? *gslab : grid_args();
-    int b0, b1;
-    slab_bins(rank, nranks, &b0, &b1);
+    if (b0 < 0) slab_bins(rank, nranks, &b0, &b1);
     if (b1 <= b0) return;
     g.bin0 = b0;
     dispatch_P<SpreadLaunch>(p.P, g, b1 - b0, d_xyzqB_, d_startB_, grid, s);
@@ -1838,7 +1845,7 @@ void Engine::phase_b(int rank, int nranks, const double* grid_in, double* u, dou
 
 // Interpolation of this rank's atoms + combine + energy partial (phase B).
 void Engine::finish(long N, int rank, int nranks, const double* fields, const GridArgs& g,
-                    double* u, double* F, double* energy_dev, cudaStream_t s) {
+                    double* u, double* F, double* energy_dev, cudaStream_t s, int b0, int b1) {
     InterpArgs a{};
     a.N = N;
     a.xyzq = d_xyzqB_;
@@ -1849,7 +1856,12 @@ void Engine::finish(long N, int rank, int nranks, const double* fields, const Gr
     a.F = F;
     a.self_coef = plan_.self_coef;
     a.startB = d_startB_;
-    slab_bins(rank, nranks, &a.bin_lo, &a.bin_hi);
+    if (b0 >= 0) {
+        a.bin_lo = b0;
+        a.bin_hi = b1;
+    } else {
+        slab_bins(rank, nranks, &a.bin_lo, &a.bin_hi);
+    }
     if (N > 0 && a.bin_hi > a.bin_lo) {
         dispatch_P<InterpLaunch>(plan_.P, static_cast<int>(kSpectral), nfields_ == 4, g, a, s);
         ++launches_;
@@ -1929,7 +1941,11 @@ void Engine::pencil_phase_a(long N, const double* pos, const double* q, int rank
     GridArgs g = grid_args();
     g.xslab = 1;
     g.x_lo = G.x0 - G.halo;
-    run_spread(N, s, rank, nranks, slab, &g, G.slab_reals);
+    g.own_x0 = G.x0;
+    g.own_x1 = G.x1;
+    const int per_b = nb_[1] * nb_[2];
+    if (G.S != S_) throw InvalidArgument("distributed FFT: spread-bin edge mismatch");
+    run_spread(N, s, rank, nranks, slab, &g, G.slab_reals, G.bx0 * per_b, G.bx1 * per_b);
     phase_n_ = N;
 }
 
@@ -2001,7 +2017,10 @@ void Engine::pencil_phase_b(int rank, int nranks, const double* fslab, double* u
     GridArgs g = grid_args();
     g.xslab = 1;
     g.x_lo = G.x0 - G.halo;
-    finish(N, rank, nranks, fslab, g, u, F, energy_dev, s);
+    g.own_x0 = G.x0;
+    g.own_x1 = G.x1;
+    const int per_b = nb_[1] * nb_[2];
+    finish(N, rank, nranks, fslab, g, u, F, energy_dev, s, G.bx0 * per_b, G.bx1 * per_b);
 }
 
 GridArgs Engine::grid_args() const {

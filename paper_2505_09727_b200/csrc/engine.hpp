@@ -35,10 +35,10 @@ double fp64_peak_tflops(int device);
 // Ordered pairs per second of the K4 evaluation alone (operands in registers).
 double pair_eval_rate(const Plan& p, int device);
 
-// Distributed-FFT decomposition over `nranks` GPUs (DESIGN.md section 5b):
-// rank r owns the real-space x-planes [x0, x1) (whole spread-bin slabs, so
-// its atoms' footprints stay within `halo` planes of them) and, after the
-// forward transpose, the spectral y-rows [y0, y1).  Host-only (no device).
+// Distributed-FFT decomposition over `nranks` GPUs (DESIGN.md section 6):
+// rank r owns the real-space x-planes [x0, x1) and the atoms in them (their
+// footprints stay within `halo` planes) and, after the forward transpose, the
+// spectral y-rows [y0, y1).  Host-only (no device).
 struct PencilGeom {
     int nranks = 1, rank = 0;
     int halo = 0;           // planes exchanged with each x-neighbour
@@ -48,8 +48,9 @@ struct PencilGeom {
     long spec_local = 0;    // (x1 - x0) * ny * (nz/2+1): forward send size (complex)
     long spec_pencil = 0;   // nx * (y1 - y0) * (nz/2+1): forward receive size (complex)
     int nfields = 4;        // interleaved fields per node of the field slab
-    // atom ownership: an atom belongs to the rank whose spread-bin x-range
-    // [bx0, bx1) holds clamp(floor(fold(x) / hx) / S, 0, nbx - 1)
+    // atom ownership: an atom belongs to the rank whose planes [x0, x1) hold
+    // clamp(floor(fold(x) / hx), 0, nx - 1); the rank processes the spread
+    // bins [bx0, bx1) (edge S) that intersect its planes
     double hx = 0.0;
     int S = 0, nbx = 0, bx0 = 0, bx1 = 0;
 };
@@ -141,9 +142,11 @@ private:
     void run_pair(long N, cudaStream_t s, int rank, int nranks, bool own_bins = false);
     void run_grid(long N, cudaStream_t s, StageTimes* t);
     void run_spread(long N, cudaStream_t s, int rank, int nranks, double* grid,
-                    const GridArgs* gslab = nullptr, long nreals = -1);
+                    const GridArgs* gslab = nullptr, long nreals = -1, int b0 = -1,
+                    int b1 = -1);
     void finish(long N, int rank, int nranks, const double* fields, const GridArgs& g,
-                double* u, double* F, double* energy_dev, cudaStream_t s);
+                double* u, double* F, double* energy_dev, cudaStream_t s, int b0 = -1,
+                int b1 = -1);
     void pencil_plans(const PencilGeom& G);
     void slab_bins(int rank, int nranks, int* b0, int* b1) const;
     long phase_n_ = 0;

@@ -378,26 +378,24 @@ def fold_positions(pos, box):
 
 
 def atom_owner(layout, x):
-    """Rank owning each atom, from its folded x (the engine's spread-bin
-    formula: clamp(floor(x/hx) // S, 0, nbx-1) in [bx0, bx1) of the rank)."""
+    """Rank owning each atom, from its folded x: the rank whose planes
+    [x0, x1) hold clamp(floor(x/hx), 0, nx-1) (the engine's formula)."""
     import numpy as np
-    g0 = layout.g[0]
-    hx, S, nbx = g0["hx"], g0["S"], g0["nbx"]
-    ends = [g["bx1"] for g in layout.g]
+    hx, nx = layout.g[0]["hx"], layout.nx
+    ends = [g["x1"] for g in layout.g]
     if isinstance(x, np.ndarray):
-        bx = np.clip(np.floor(x / hx).astype(np.int64) // S, 0, nbx - 1)
-        return np.searchsorted(np.asarray(ends), bx, side="right")
+        pl = np.clip(np.floor(x / hx).astype(np.int64), 0, nx - 1)
+        return np.searchsorted(np.asarray(ends), pl, side="right")
     import torch
-    bx = torch.clamp(torch.div(torch.floor(x / hx).to(torch.int64), S, rounding_mode="floor"),
-                     0, nbx - 1)
-    return torch.searchsorted(torch.tensor(ends, device=x.device), bx, right=True)
+    pl = torch.clamp(torch.floor(x / hx).to(torch.int64), 0, nx - 1)
+    return torch.searchsorted(torch.tensor(ends, device=x.device), pl, right=True)
 
 
 def slab_bounds(layout, r, box_x):
     """[X0, X1) of rank r's atoms in x."""
-    g, g0 = layout.g[r], layout.g[0]
-    X0 = g["bx0"] * g0["S"] * g0["hx"]
-    X1 = box_x if g["bx1"] >= g0["nbx"] else g["bx1"] * g0["S"] * g0["hx"]
+    g, hx = layout.g[r], layout.g[0]["hx"]
+    X0 = g["x0"] * hx
+    X1 = box_x if g["x1"] >= layout.nx else g["x1"] * hx
     return X0, X1
 
 

@@ -133,7 +133,7 @@ class _OraclePencilEngine:
     buffer layouts, sizes and atom ownership as the C ABI
     (include/esp_b200.h), physics from the numpy oracle.  The inputs of
     pencil_phase_a (whole system or own atoms + ghosts) are what the rank
-    computes with; it owns the atoms whose spread bin lies in its range."""
+    computes with; it owns the atoms in its grid planes."""
 
     def __init__(self, oplan, host_plan):
         from oracle import esp_oracle as O
@@ -146,8 +146,8 @@ class _OraclePencilEngine:
         return esp.pencil_geometry(self.host_plan, rank, nranks)
 
     def _owned(self, g, pos):
-        bx = np.clip(np.floor(pos[:, 0] / g["hx"]).astype(np.int64) // g["S"], 0, g["nbx"] - 1)
-        return (bx >= g["bx0"]) & (bx < g["bx1"])
+        pl = np.clip(np.floor(pos[:, 0] / g["hx"]).astype(np.int64), 0, g["nf"][0] - 1)
+        return (pl >= g["x0"]) & (pl < g["x1"])
 
     def _planes(self, g):
         return np.arange(g["x0"] - g["halo"], g["x1"] + g["halo"]) % self.p.nf[0]
