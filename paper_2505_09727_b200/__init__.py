@@ -64,8 +64,7 @@ class _Overrides(C.Structure):
 class _Info(C.Structure):
     _fields_ = [
         ("family", C.c_int), ("force_method", C.c_int), ("P", C.c_int),
-        ("nf", C.c_int * 3), ("hx", C.c_double), ("S", C.c_int), ("nbx", C.c_int),
-        ("bx0", C.c_int), ("bx1", C.c_int), ("base_nf", C.c_int * 3),
+        ("nf", C.c_int * 3), ("base_nf", C.c_int * 3),
         ("eps", C.c_double), ("r_c", C.c_double), ("shape", C.c_double), ("c1", C.c_double),
         ("chi0", C.c_double),
         ("box", C.c_double * 3), ("h", C.c_double * 3), ("demand", C.c_double * 3),

@@ -312,7 +312,7 @@ struct PairArgs {
     double4* loc;         // original order: (u_l, F_l)
     unsigned long long* npairs;  // ordered in-range pairs evaluated (r < r_c, r > 0)
     int cap;                     // candidates staged per chunk
-    int lcap;                    // per-warp candidate-list capacity (even)
+    int lcap;                    // per-warp list capacity (even): pieces of lcap - 32 + padding
     int nent_max;                // cell entries per CTA neighbourhood
     int M, Mz;                   // neighbourhood reach in columns / slices
     int bz;                      // target slices per CTA
@@ -607,8 +607,10 @@ __global__ void __launch_bounds__(kPairThreads, kPairWarps >= 8 ? 3 : 6) k_pair(
             double4 pf = make_double4(0.0, 0.0, 0.0, 0.0);
             int tf = 13;
             // the list holds at most a.lcap entries: walk it in pieces if needed
-            for (int lb = 0; lb < T; lb += a.lcap) {
-                const int le = min(T, lb + a.lcap);
+            // pieces of lcap - 32 entries: the 32 spare slots take the sentinel
+            // padding of the last step of a piece
+            for (int lb = 0; lb < T; lb += a.lcap - 32) {
+                const int le = min(T, lb + a.lcap - 32);
                 {
                     // this lane's columns cover stream positions [inc-cnt, inc)
                     int p0 = max(inc0 - cnt0, lb), p1 = min(inc0, le);

@@ -95,3 +95,19 @@ def test_particles_file_round_trip(tmp_path):
     p2, q2, box = S.read_particles(str(f))
     assert box == (3.0, 4.0, 5.0)
     assert np.array_equal(p2, pos) and np.array_equal(q2, q)
+
+
+def test_plan_info_layout_matches_the_header():
+    """The ctypes mirror of esp_plan_info / esp_pencil_info reads the values
+    the C side wrote (a field-order slip shows up as shuffled values)."""
+    import paper_2505_09727_b200 as esp
+    box = (50.0, 44.0, 47.0)
+    p = esp.build_plan(box, "pswf", 1e-4, 8.0, device=-1)
+    assert p.box == box
+    assert all(abs(p.h[d] - box[d] / p.nf[d]) < 1e-12 for d in range(3))
+    assert p.r_c == 8.0 and p.eps == 1e-4 and p.P >= 3
+    assert all(n >= d for n, d in zip(p.nf, p.base_nf))
+    g = esp.pencil_geometry(p, 1, 2)
+    assert g["nf"] == p.nf and g["rank"] == 1 and g["nranks"] == 2
+    assert abs(g["hx"] - p.h[0]) < 1e-15 and g["x1"] == p.nf[0]
+    assert g["slab_reals"] == (g["x1"] - g["x0"] + 2 * g["halo"]) * p.nf[1] * p.nf[2]
