@@ -1052,17 +1052,24 @@ __global__ void __launch_bounds__(128) k_interp(GridArgs g, InterpArgs a) {
 __global__ void __launch_bounds__(256) k_combine(long N, const double4* __restrict__ loc,
                                                  const double4* __restrict__ xyzq_orig,
                                                  double self_coef, double* __restrict__ u,
-                                                 double* __restrict__ F, double* __restrict__ epart) {
+                                                 double* __restrict__ F, double* __restrict__ epart,
+                                                 double* __restrict__ u_out,
+                                                 double* __restrict__ F_out) {
+    // u_out / F_out (optional, e.g. pinned host memory written over PCIe):
+    // the final values go there instead of back into u / F
     const long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
     double e = 0.0;
     if (i < N) {
         const double4 l = loc[i];
         const double qi = xyzq_orig[i].w;
         const double ui = l.x + u[i];  // u holds u_s - q s0 (self folded in K3)
-        u[i] = ui;
-        F[3 * i + 0] += l.y;
-        F[3 * i + 1] += l.z;
-        F[3 * i + 2] += l.w;
+        double* uo = u_out ? u_out : u;
+        double* Fo = F_out ? F_out : F;
+        uo[i] = ui;
+        const double fx = F[3 * i + 0] + l.y, fy = F[3 * i + 1] + l.z, fz = F[3 * i + 2] + l.w;
+        Fo[3 * i + 0] = fx;
+        Fo[3 * i + 1] = fy;
+        Fo[3 * i + 2] = fz;
         e = qi * ui;
     }
     __shared__ double red[8];
@@ -1870,7 +1877,8 @@ void Engine::finish(long N, int rank, int nranks, const double* fields, const Gr
     }
     const int nblk = static_cast<int>(grid1(std::max<long>(N, 1), 256));
     if (N > 0) {
-        k_combine<<<nblk, 256, 0, s>>>(N, d_loc_, d_tmp_, plan_.self_coef, u, F, d_epart_);
+        k_combine<<<nblk, 256, 0, s>>>(N, d_loc_, d_tmp_, plan_.self_coef, u, F, d_epart_,
+                                       nullptr, nullptr);
         CK(cudaGetLastError());
         k_energy<<<1, 256, 0, s>>>(d_epart_, nblk, energy_dev);
         CK(cudaGetLastError());
@@ -2043,22 +2051,23 @@ GridArgs Engine::grid_args() const {
 }
 
 void Engine::evaluate(long N, const double* pos, const double* q, double* u, double* F,
-                      double* energy_dev, double* qsum_dev, cudaStream_t s, StageTimes* t) {
+                      double* energy_dev, double* qsum_dev, cudaStream_t s, StageTimes* t,
+                      double* u_out, double* F_out) {
     CK(cudaSetDevice(device_));
     reconfigure(N);
     if (t || !use_graph_) {
-        enqueue(N, pos, q, u, F, energy_dev, qsum_dev, s, t);
+        enqueue(N, pos, q, u, F, energy_dev, qsum_dev, s, t, u_out, F_out);
         return;
     }
     // CUDA-graph path: the whole evaluation (2 sorts, K4 || grid pipeline,
     // combine, energy: ~14 kernels + cuFFT) is captured once per argument set
     // on the engine's own stream and replayed; the caller's stream is joined
     // with events, so any stream (including the legacy default) works.
-    const GraphKey key{N, pos, q, u, F, energy_dev, qsum_dev};
+    const GraphKey key{N, pos, q, u, F, energy_dev, qsum_dev, u_out, F_out};
     if (!gexec_ || !(key == gkey_)) {
         if (!warm_) {
             // first call: run eagerly (sets kernel attributes, sizes buffers)
-            enqueue(N, pos, q, u, F, energy_dev, qsum_dev, s, nullptr);
+            enqueue(N, pos, q, u, F, energy_dev, qsum_dev, s, nullptr, u_out, F_out);
             warm_ = true;
             return;
         }
@@ -2067,7 +2076,7 @@ void Engine::evaluate(long N, const double* pos, const double* q, double* u, dou
         CK(cudaStreamSynchronize(gstream_));
         cudaGraph_t graph = nullptr;
         CK(cudaStreamBeginCapture(gstream_, cudaStreamCaptureModeThreadLocal));
-        enqueue(N, pos, q, u, F, energy_dev, qsum_dev, gstream_, nullptr);
+        enqueue(N, pos, q, u, F, energy_dev, qsum_dev, gstream_, nullptr, u_out, F_out);
         CK(cudaStreamEndCapture(gstream_, &graph));
         if (gexec_) {
             cudaGraphExecUpdateResultInfo info{};
@@ -2092,7 +2101,8 @@ void Engine::evaluate(long N, const double* pos, const double* q, double* u, dou
 }
 
 void Engine::enqueue(long N, const double* pos, const double* q, double* u, double* F,
-                     double* energy_dev, double* qsum_dev, cudaStream_t s, StageTimes* t) {
+                     double* energy_dev, double* qsum_dev, cudaStream_t s, StageTimes* t,
+                     double* u_out, double* F_out) {
     launches_ = 0;
     ensure_capacity(N);
     InterpArgs a{};
@@ -2136,7 +2146,8 @@ void Engine::enqueue(long N, const double* pos, const double* q, double* u, doub
     }
     const int nblk = static_cast<int>(grid1(std::max<long>(N, 1), 256));
     if (N > 0) {
-        k_combine<<<nblk, 256, 0, s>>>(N, d_loc_, d_tmp_, plan_.self_coef, u, F, d_epart_);
+        k_combine<<<nblk, 256, 0, s>>>(N, d_loc_, d_tmp_, plan_.self_coef, u, F, d_epart_,
+                                       u_out, F_out);
         CK(cudaGetLastError());
         ++launches_;
         k_energy<<<1, 256, 0, s>>>(d_epart_, nblk, energy_dev);

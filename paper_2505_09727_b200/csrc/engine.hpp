@@ -72,8 +72,11 @@ public:
     // Full evaluation (ewald.hpp:619-649): u = u_l + u_s - self, F = F_l + F_s,
     // energy_dev[0] = 1/2 sum q u.  qsum_dev (optional, 2 doubles) receives
     // (sum q, sum |q|) for the neutrality check.
+    // u_out / F_out (optional): final u and F written there (e.g. pinned host
+    // memory, over PCIe) instead of into u / F, which are then device scratch.
     void evaluate(long N, const double* pos, const double* q, double* u, double* F,
-                  double* energy_dev, double* qsum_dev, cudaStream_t s, StageTimes* t = nullptr);
+                  double* energy_dev, double* qsum_dev, cudaStream_t s, StageTimes* t = nullptr,
+                  double* u_out = nullptr, double* F_out = nullptr);
     // Parts (ewald.hpp:419 local_sum, :524 spectral_sum).
     void local_sum(long N, const double* pos, const double* q, double* u, double* F,
                    cudaStream_t s);
@@ -133,7 +136,8 @@ public:
 
 private:
     void enqueue(long N, const double* pos, const double* q, double* u, double* F,
-                 double* energy_dev, double* qsum_dev, cudaStream_t s, StageTimes* t);
+                 double* energy_dev, double* qsum_dev, cudaStream_t s, StageTimes* t,
+                 double* u_out, double* F_out);
     void ensure_capacity(long N);
     void reconfigure(long N);
     void set_cells(int col_div);
@@ -216,10 +220,10 @@ private:
     // CUDA graph of a full evaluation, keyed by its arguments
     struct GraphKey {
         long N;
-        const void *pos, *q, *u, *F, *e, *qs;
+        const void *pos, *q, *u, *F, *e, *qs, *uo, *Fo;
         bool operator==(const GraphKey& o) const {
             return N == o.N && pos == o.pos && q == o.q && u == o.u && F == o.F && e == o.e &&
-                   qs == o.qs;
+                   qs == o.qs && uo == o.uo && Fo == o.Fo;
         }
     };
     bool use_graph_ = true;

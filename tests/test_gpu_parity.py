@@ -176,3 +176,27 @@ def test_pair_cell_widths(esp, gpu, name, col_div, monkeypatch):
     ef = esp.evaluate(plan, sysm)
     assert abs(ef.energy - g["energy"]) <= E_TOL * abs(g["energy"])
     assert rel_rms(ef.F, g["F"]) <= F_TOL
+
+
+def test_pinned_host_buffers(esp, gpu):
+    """Page-locked host arrays take the zero-copy path (positions read and
+    u/F written over PCIe by the kernels); results equal the pageable path."""
+    import torch
+    from paper_2505_09727_b200 import systems as S
+    c = S.config("cfg2")
+    pos, q, box = c.system()
+    plan = esp.build_plan(box, "pswf", c.eps, c.r_c, device=gpu)
+    ref = esp.evaluate(plan, esp.ParticleSystem(box, q, pos))
+    pin = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
+    sp = esp.ParticleSystem(box, pin(q), pin(pos))
+    u, F = pin(np.empty(q.size)), pin(np.empty((q.size, 3)))
+    for _ in range(3):  # eager, captured, replayed
+        u[:] = np.nan
+        F[:] = np.nan
+        ef = esp.evaluate(plan, sp, out=(u, F))
+        assert abs(ef.energy - ref.energy) <= 1e-13 * abs(ref.energy)
+        assert max_rel(u, ref.u) <= 1e-13 and rel_rms(F, ref.F) <= 1e-13
+    q2 = pin(q.copy())
+    q2[0] += 1.0
+    with pytest.raises(esp.NumericalError):
+        esp.evaluate(plan, esp.ParticleSystem(box, q2, pin(pos)))
