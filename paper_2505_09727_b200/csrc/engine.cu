@@ -64,6 +64,7 @@ namespace {
 
 constexpr double kPi = 3.14159265358979323846;
 constexpr int kNc = 13;        // coefficients per window piece (degree 12)
+constexpr int kSubPerBin = 8;  // sort keys per spread bin (2x2x2 sub-bins)
 constexpr long kHighPriorityMaxN = 1L << 19;  // grid pipeline on the high-priority stream
 constexpr int kColDivDefault = 2;
 constexpr double kColDiv3MinPairs = 300.0;  // r_c/3 columns: enough pairs per target
@@ -184,11 +185,20 @@ __global__ void __launch_bounds__(256) k_fold_bin(BinArgs a) {
         int c = (cx * a.nc[1] + cy) * a.nc[2] + cz;
         a.cellA[i] = c;
         a.rankA[i] = atomicAdd(&a.countA[c], 1);
-        // spread bin: S grid cells per side, by floor(x/h)
-        int bx = clampi(static_cast<int>(floor(x / a.h[0])) / a.S, 0, a.nb[0] - 1);
-        int by = clampi(static_cast<int>(floor(y / a.h[1])) / a.S, 0, a.nb[1] - 1);
-        int bz = clampi(static_cast<int>(floor(z / a.h[2])) / a.S, 0, a.nb[2] - 1);
-        int b = (bx * a.nb[1] + by) * a.nb[2] + bz;
+        // spread bin: S grid cells per side, by floor(x/h); atoms are ordered
+        // by bin and, inside a bin, by its 2x2x2 sub-bins (neighbouring K3
+        // threads then gather overlapping footprints)
+        const int lx = static_cast<int>(floor(x / a.h[0]));
+        const int ly = static_cast<int>(floor(y / a.h[1]));
+        const int lz = static_cast<int>(floor(z / a.h[2]));
+        const int bx = clampi(lx / a.S, 0, a.nb[0] - 1);
+        const int by = clampi(ly / a.S, 0, a.nb[1] - 1);
+        const int bz = clampi(lz / a.S, 0, a.nb[2] - 1);
+        const int hs = a.S / 2;
+        const int sx = clampi((lx - bx * a.S) / hs, 0, 1);
+        const int sy = clampi((ly - by * a.S) / hs, 0, 1);
+        const int sz = clampi((lz - bz * a.S) / hs, 0, 1);
+        const int b = ((bx * a.nb[1] + by) * a.nb[2] + bz) * kSubPerBin + (sx * 2 + sy) * 2 + sz;
         a.cellB[i] = b;
         a.rankB[i] = atomicAdd(&a.countB[b], 1);
     }
@@ -765,7 +775,7 @@ __global__ void __launch_bounds__(512) k_spread(GridArgs g, const double4* __res
     const int nt = blockDim.x;
     const int bin = blockIdx.x + g.bin0;
     const int bz = bin % g.nb[2], by = (bin / g.nb[2]) % g.nb[1], bx = bin / (g.nb[1] * g.nb[2]);
-    const int ib = start[bin], ie = start[bin + 1];
+    const int ib = start[bin * kSubPerBin], ie = start[(bin + 1) * kSubPerBin];
     if (ib == ie) return;
     const int lo[3] = {bx * g.S - P / 2, by * g.S - P / 2, bz * g.S - P / 2};
     const int tsize = PS * W;
@@ -918,8 +928,8 @@ __global__ void __launch_bounds__(128) k_interp(GridArgs g, InterpArgs a) {
     long k = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
     long kend = a.N;
     if (a.startB) {
-        k += a.startB[a.bin_lo];
-        kend = a.startB[a.bin_hi];
+        k += a.startB[a.bin_lo * kSubPerBin];
+        kend = a.startB[a.bin_hi * kSubPerBin];
     }
     bool mine = k < kend;
     if (mine && g.xslab) {  // distributed FFT: another rank's atom in a shared bin
@@ -1343,6 +1353,10 @@ PairConsts make_pair_consts(const Plan& p, int& nd) {
 }  // namespace
 
 int spread_bin_edge(const Plan& p) {
+    if (const char* e = std::getenv("ESP_SPREAD_S")) {  // experiments
+        const int v = std::atoi(e);
+        if (v == 4 || v == 6 || v == 8) return v;
+    }
     // the largest S in {8, 6, 4} that still gives >= 4 CTAs per SM
     for (int cand : {8, 6}) {
         long nb = 1;
@@ -1428,10 +1442,10 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
     dalloc(d_xi_, xi.size());
     CK(cudaMemcpy(d_xi_, xi.data(), sizeof(double) * xi.size(), cudaMemcpyHostToDevice));
 
-    dalloc(d_countB_, nbin_ + 1);
-    dalloc(d_startB_, nbin_ + 1);
+    dalloc(d_countB_, static_cast<long>(nbin_) * kSubPerBin + 1);
+    dalloc(d_startB_, static_cast<long>(nbin_) * kSubPerBin + 1);
     // counts are zero at rest on the single-CTA scan path (prepare)
-    CK(cudaMemset(d_countB_, 0, sizeof(int) * (nbin_ + 1)));
+    CK(cudaMemset(d_countB_, 0, sizeof(int) * (nbin_ * kSubPerBin + 1)));
     alloc_cells();
     dalloc(d_grid_, M_);
     dalloc(d_spec_, Mh_);
@@ -1560,7 +1574,7 @@ void Engine::alloc_cells() {
     size_t t1 = 0, t2 = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, t1, d_countA_, d_startA_,
                                      static_cast<int>(ncellF_ + 1)));
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, t2, d_countB_, d_startB_, nbin_ + 1));
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, t2, d_countB_, d_startB_, nbin_ * kSubPerBin + 1));
     scan_tmp_bytes_ = std::max(t1, t2);
     if (d_scan_tmp_) cudaFree(d_scan_tmp_);
     d_scan_tmp_ = nullptr;
@@ -1620,11 +1634,12 @@ void Engine::ensure_capacity(long N) {
 void Engine::prepare(long N, const double* pos, const double* q, double* qsum_dev,
                      cudaStream_t s) {
     const Plan& p = plan_;
-    const bool small = ncellF_ + nbin_ + 2 <= kSmallScanMax;
+    const int nkeyB = nbin_ * kSubPerBin;
+    const bool small = ncellF_ + nkeyB + 2 <= kSmallScanMax;
     if (!small) {
         CK(cudaMemsetAsync(d_countA_, 0, sizeof(int) * (ncellF_ + 1), s));
         CK(cudaMemsetAsync(d_npairs_, 0, sizeof(unsigned long long), s));
-        CK(cudaMemsetAsync(d_countB_, 0, sizeof(int) * (nbin_ + 1), s));
+        CK(cudaMemsetAsync(d_countB_, 0, sizeof(int) * (nkeyB + 1), s));
     }
     if (qsum_dev) CK(cudaMemsetAsync(qsum_dev, 0, sizeof(double) * 2, s));
     BinArgs a{};
@@ -1653,12 +1668,12 @@ void Engine::prepare(long N, const double* pos, const double* q, double* qsum_de
         ++launches_;
     }
     if (small) {
-        const size_t sm = sizeof(int) * (ncellF_ + nbin_ + 2);
+        const size_t sm = sizeof(int) * (ncellF_ + nkeyB + 2);
         if (sm > 48 * 1024)
             CK(cudaFuncSetAttribute(k_scan_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(sm)));
         k_scan_small<<<1, 1024, sm, s>>>(d_countA_, d_startA_, static_cast<int>(ncellF_ + 1),
-                                         d_countB_, d_startB_, nbin_ + 1, d_npairs_);
+                                         d_countB_, d_startB_, nkeyB + 1, d_npairs_);
         CK(cudaGetLastError());
         ++launches_;
     } else {
@@ -1666,7 +1681,7 @@ void Engine::prepare(long N, const double* pos, const double* q, double* qsum_de
         CK(cub::DeviceScan::ExclusiveSum(d_scan_tmp_, tb, d_countA_, d_startA_,
                                          static_cast<int>(ncellF_ + 1), s));
         tb = scan_tmp_bytes_;
-        CK(cub::DeviceScan::ExclusiveSum(d_scan_tmp_, tb, d_countB_, d_startB_, nbin_ + 1, s));
+        CK(cub::DeviceScan::ExclusiveSum(d_scan_tmp_, tb, d_countB_, d_startB_, nkeyB + 1, s));
         launches_ += 2;
     }
     if (N > 0) {
