@@ -37,6 +37,7 @@ struct GridArgs {
     int RS, PS;         // padded row / plane strides of the spread tile (doubles)
     int P;
     int bin0;           // first spread bin of this launch (slab decomposition)
+    int kpb;            // sort keys per spread bin (start[] has kpb entries per bin)
     int xslab;          // 1: x indexes a rank's plane slab starting at plane x_lo
     int x_lo;           //    (unwrapped; the slab's halos hold the periodic images)
     int own_x0, own_x1; // xslab: only atoms with clamp(floor(x/h), 0, nx-1) in
@@ -64,7 +65,7 @@ namespace {
 
 constexpr double kPi = 3.14159265358979323846;
 constexpr int kNc = 13;        // coefficients per window piece (degree 12)
-constexpr int kSubPerBin = 8;  // sort keys per spread bin (2x2x2 sub-bins)
+constexpr long kSubDiv4MinN = 1L << 17;  // 4^3 sort sub-bins per spread bin from here, else 2^3
 constexpr long kHighPriorityMaxN = 1L << 19;  // grid pipeline on the high-priority stream
 constexpr int kColDivDefault = 2;
 constexpr double kColDiv3MinPairs = 300.0;  // r_c/3 columns: enough pairs per target
@@ -165,6 +166,7 @@ struct BinArgs {
     int* cellB;
     int* rankB;
     int* countB;
+    int sub;             // sort sub-bins per spread-bin edge (keys per bin: sub^3)
     double* qsum;  // [2]
 };
 
@@ -194,11 +196,11 @@ __global__ void __launch_bounds__(256) k_fold_bin(BinArgs a) {
         const int bx = clampi(lx / a.S, 0, a.nb[0] - 1);
         const int by = clampi(ly / a.S, 0, a.nb[1] - 1);
         const int bz = clampi(lz / a.S, 0, a.nb[2] - 1);
-        const int hs = a.S / 2;
-        const int sx = clampi((lx - bx * a.S) / hs, 0, 1);
-        const int sy = clampi((ly - by * a.S) / hs, 0, 1);
-        const int sz = clampi((lz - bz * a.S) / hs, 0, 1);
-        const int b = ((bx * a.nb[1] + by) * a.nb[2] + bz) * kSubPerBin + (sx * 2 + sy) * 2 + sz;
+        const int D = a.sub;
+        const int sx = clampi((lx - bx * a.S) * D / a.S, 0, D - 1);
+        const int sy = clampi((ly - by * a.S) * D / a.S, 0, D - 1);
+        const int sz = clampi((lz - bz * a.S) * D / a.S, 0, D - 1);
+        const int b = ((bx * a.nb[1] + by) * a.nb[2] + bz) * (D * D * D) + (sx * D + sy) * D + sz;
         a.cellB[i] = b;
         a.rankB[i] = atomicAdd(&a.countB[b], 1);
     }
@@ -219,7 +221,7 @@ __global__ void __launch_bounds__(256) k_fold_bin(BinArgs a) {
 // scans + their init kernels + two memsets): start = exclusive scan of count,
 // then count is zeroed for the next evaluation (counts are zero at rest on
 // this path), and the pair counter is reset.
-constexpr int kSmallScanMax = 32768;  // ncell + nbin for the single-CTA path
+constexpr int kSmallScanMax = 32768;  // ncell + nkeyB for the single-CTA path
 
 // In-place exclusive scan of sm[0, n) by one CTA (per-thread chunks + a
 // block scan of the chunk sums).
@@ -775,7 +777,7 @@ __global__ void __launch_bounds__(512) k_spread(GridArgs g, const double4* __res
     const int nt = blockDim.x;
     const int bin = blockIdx.x + g.bin0;
     const int bz = bin % g.nb[2], by = (bin / g.nb[2]) % g.nb[1], bx = bin / (g.nb[1] * g.nb[2]);
-    const int ib = start[bin * kSubPerBin], ie = start[(bin + 1) * kSubPerBin];
+    const int ib = start[bin * g.kpb], ie = start[(bin + 1) * g.kpb];
     if (ib == ie) return;
     const int lo[3] = {bx * g.S - P / 2, by * g.S - P / 2, bz * g.S - P / 2};
     const int tsize = PS * W;
@@ -928,8 +930,8 @@ __global__ void __launch_bounds__(128) k_interp(GridArgs g, InterpArgs a) {
     long k = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
     long kend = a.N;
     if (a.startB) {
-        k += a.startB[a.bin_lo * kSubPerBin];
-        kend = a.startB[a.bin_hi * kSubPerBin];
+        k += a.startB[a.bin_lo * g.kpb];
+        kend = a.startB[a.bin_hi * g.kpb];
     }
     bool mine = k < kend;
     if (mine && g.xslab) {  // distributed FFT: another rank's atom in a shared bin
@@ -1442,10 +1444,7 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
     dalloc(d_xi_, xi.size());
     CK(cudaMemcpy(d_xi_, xi.data(), sizeof(double) * xi.size(), cudaMemcpyHostToDevice));
 
-    dalloc(d_countB_, static_cast<long>(nbin_) * kSubPerBin + 1);
-    dalloc(d_startB_, static_cast<long>(nbin_) * kSubPerBin + 1);
-    // counts are zero at rest on the single-CTA scan path (prepare)
-    CK(cudaMemset(d_countB_, 0, sizeof(int) * (nbin_ * kSubPerBin + 1)));
+    alloc_bins(2);
     alloc_cells();
     dalloc(d_grid_, M_);
     dalloc(d_spec_, Mh_);
@@ -1567,6 +1566,15 @@ void Engine::set_cells(int col_div) {
     if (ncellF_ >= (1L << 30)) throw InvalidArgument("cell list too fine for this box / r_c");
 }
 
+// Spread-bin sort keys: `sub`^3 sub-bins per bin (counts zero at rest).
+void Engine::alloc_bins(int sub) {
+    sub_ = sub;
+    nkeyB_ = nbin_ * sub * sub * sub;
+    dalloc(d_countB_, static_cast<long>(nkeyB_) + 1);
+    dalloc(d_startB_, static_cast<long>(nkeyB_) + 1);
+    CK(cudaMemset(d_countB_, 0, sizeof(int) * (nkeyB_ + 1)));
+}
+
 void Engine::alloc_cells() {
     dalloc(d_countA_, ncellF_ + 1);
     dalloc(d_startA_, ncellF_ + 1);
@@ -1574,7 +1582,7 @@ void Engine::alloc_cells() {
     size_t t1 = 0, t2 = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, t1, d_countA_, d_startA_,
                                      static_cast<int>(ncellF_ + 1)));
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, t2, d_countB_, d_startB_, nbin_ * kSubPerBin + 1));
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, t2, d_countB_, d_startB_, nkeyB_ + 1));
     scan_tmp_bytes_ = std::max(t1, t2);
     if (d_scan_tmp_) cudaFree(d_scan_tmp_);
     d_scan_tmp_ = nullptr;
@@ -1600,12 +1608,15 @@ void Engine::reconfigure(long N) {
         if (const char* e = std::getenv("ESP_PAIR_LCAP"))
             pair_lcap_ = std::max(128, std::min(2048, std::atoi(e) / 2 * 2));
     }
-    if (want == col_div_) return;
+    // finer sort sub-bins for large systems: better K3 locality, more keys
+    const int want_sub = N >= kSubDiv4MinN ? 4 : 2;
+    if (want == col_div_ && want_sub == sub_) return;
     CK(cudaDeviceSynchronize());
     if (gexec_) {
         cudaGraphExecDestroy(gexec_);
         gexec_ = nullptr;
     }
+    if (want_sub != sub_) alloc_bins(want_sub);
     set_cells(want);
     alloc_cells();
 }
@@ -1634,7 +1645,7 @@ void Engine::ensure_capacity(long N) {
 void Engine::prepare(long N, const double* pos, const double* q, double* qsum_dev,
                      cudaStream_t s) {
     const Plan& p = plan_;
-    const int nkeyB = nbin_ * kSubPerBin;
+    const int nkeyB = nkeyB_;
     const bool small = ncellF_ + nkeyB + 2 <= kSmallScanMax;
     if (!small) {
         CK(cudaMemsetAsync(d_countA_, 0, sizeof(int) * (ncellF_ + 1), s));
@@ -1654,6 +1665,7 @@ void Engine::prepare(long N, const double* pos, const double* q, double* qsum_de
         a.h[d] = p.h[d];
     }
     a.S = S_;
+    a.sub = sub_;
     a.tmp = d_tmp_;
     a.cellA = d_cellA_;
     a.rankA = d_rankA_;
@@ -2057,6 +2069,7 @@ GridArgs Engine::grid_args() const {
         g.nb[d] = nb_[d];
     }
     g.S = S_;
+    g.kpb = sub_ * sub_ * sub_;
     g.W = W_;
     g.RS = RS_;
     g.PS = PS_;

@@ -142,6 +142,7 @@ private:
     void reconfigure(long N);
     void set_cells(int col_div);
     void alloc_cells();
+    void alloc_bins(int sub);
     void prepare(long N, const double* pos, const double* q, double* qsum_dev, cudaStream_t s);
     void run_pair(long N, cudaStream_t s, int rank, int nranks, bool own_bins = false);
     void run_grid(long N, cudaStream_t s, StageTimes* t);
@@ -167,6 +168,8 @@ private:
     int S_ = 8;                 // spread bin edge in grid cells
     std::array<int, 3> nb_{};   // spread bins per dim
     int nbin_ = 0;
+    int sub_ = 2;               // sort sub-bins per spread-bin edge
+    int nkeyB_ = 0;             // spread sort keys: nbin_ * sub_^3
     int W_ = 0;                 // spread tile edge (nodes)
     int RS_ = 0, PS_ = 0;       // padded tile strides
     long M_ = 0, Mh_ = 0;       // real grid size, half spectrum size
