@@ -654,8 +654,9 @@ __global__ void __launch_bounds__(kPairThreads, kPairWarps >= 8 ? 3 : 6) k_pair(
                     __syncwarp();
                     continue;
                 }
-                for (int kb = lane; kb < n32; kb += 32) {
-                    const float4 c4 = cand[lw[kb]];
+                const unsigned short* lend = lw + n32;
+                for (const unsigned short* lp = lw + lane; lp < lend; lp += 32) {
+                    const float4 c4 = cand[*lp];
                     const float dx = c4.x - xf, dy = c4.y - yf, dz = c4.z - zf;
                     const bool in = fmaf(dz, dz, fmaf(dy, dy, dx * dx)) < R2;
                     const int code = __float_as_int(c4.w);
