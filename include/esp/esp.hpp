@@ -14,18 +14,25 @@
 //                          systems, window underflow;
 //   esp::CudaError         (new) CUDA/cuFFT failure or no GPU -- there is no
 //                          CPU fallback.
+// Also mirrored: SplitKernel / WindowKernel (plan.split, plan.win with
+// their evaluators), GridArray, spread / interpolate / interpolate_gradient,
+// influence_coefficients, fft_forward / fft_inverse, select_parameters /
+// SelectResult, direct_ewald / ReferenceResult -- all executed on the GPU.
 // Differences (documented in INTEGRATION.md): results are not bitwise
 // reproducible run to run (GPU atomics); EwaldPlan::influence is a method
 // returning the full n_f^3 array on demand; thread_count() is accepted and
-// ignored; set_device() picks the CUDA device for subsequent plans.
+// ignored; set_device() picks the CUDA device for subsequent plans;
+// direct_ewald has no N <= 1e4 cap.
 //
 // Link: -L<repo>/paper_2505_09727_b200 -lesp_b200 -Wl,-rpath,<that dir>
 #pragma once
 
 #include "../esp_b200.h"
 
+#include <algorithm>
 #include <array>
 #include <cmath>
+#include <complex>
 #include <limits>
 #include <map>
 #include <memory>
@@ -124,6 +131,59 @@ inline int& thread_count() {
     return n;
 }
 
+// Split and window kernels of a plan (kernels.hpp:63-229): the parameters of
+// the reference's structs plus evaluators backed by the plan's tables.
+struct SplitKernel {  // kernels.hpp:63-101
+    SplitFamily family = SplitFamily::pswf;
+    double eps = 0.0, shape = 0.0, r_c = 0.0, chi0 = 0.0;
+    double Psi(double y) const { return eval(0, y); }
+    double chi(double y) const { return eval(1, y); }
+    double chihat_n(double k) const { return eval(2, k); }
+    std::shared_ptr<detail::Handle> plan;
+
+private:
+    double eval(int what, double x) const {
+        double y = 0.0;
+        detail::check(esp_plan_eval_kernel(plan->p, what, 1, &x, &y));
+        return y;
+    }
+};
+
+struct WindowKernel {  // kernels.hpp:178-229
+    WindowFamily family = WindowFamily::pswf;
+    int P = 0;
+    double h = 0.0;
+    double c1 = std::numeric_limits<double>::quiet_NaN();
+    double half = 0.0;  // P h / 2
+    int dim = 0;        // which grid dimension of the plan
+    double phi(double x) const { return eval(8 + dim, x); }
+    double dphi(double x) const { return eval(11 + dim, x); }
+    double phi_hat(double xi) const { return eval(14 + dim, xi); }
+    std::shared_ptr<detail::Handle> plan;
+
+private:
+    double eval(int what, double x) const {
+        double y = 0.0;
+        detail::check(esp_plan_eval_kernel(plan->p, what, 1, &x, &y));
+        return y;
+    }
+};
+
+// gridder.hpp:59-72: complex128 row-major grid, z fastest
+struct GridArray {
+    std::array<int, 3> nf{0, 0, 0};
+    std::vector<std::complex<double>> v;
+    static GridArray zeros(std::array<int, 3> nf) {
+        GridArray g;
+        g.nf = nf;
+        g.v.assign(static_cast<std::size_t>(nf[0]) * nf[1] * nf[2], {0.0, 0.0});
+        return g;
+    }
+    std::size_t idx(int ix, int iy, int iz) const {
+        return (static_cast<std::size_t>(ix) * nf[1] + iy) * nf[2] + iz;
+    }
+};
+
 class EwaldPlan {  // ewald.hpp:67-94
 public:
     SplitFamily family = SplitFamily::pswf;
@@ -138,6 +198,8 @@ public:
     double shape = 0.0;
     double c1 = std::numeric_limits<double>::quiet_NaN();
     ForceMethod force_method = ForceMethod::ik;
+    SplitKernel split;
+    std::array<WindowKernel, 3> win;
     PlanStats stats;
 
     std::size_t total_modes() const { return static_cast<std::size_t>(nf[0]) * nf[1] * nf[2]; }
@@ -190,7 +252,63 @@ inline EwaldPlan build_plan(const Vec3& box, SplitFamily family, double eps, dou
     plan.c1 = info.c1;
     plan.force_method = ov.force_method;
     plan.stats = {info.E_A, info.E_T, info.E_SI};
+    plan.split.family = family;
+    plan.split.eps = info.eps;
+    plan.split.shape = info.shape;
+    plan.split.r_c = info.r_c;
+    plan.split.chi0 = info.chi0;
+    plan.split.plan = h;
+    for (int d = 0; d < 3; ++d) {
+        WindowKernel& w = plan.win[d];
+        w.family = plan.window_family;
+        w.P = info.P;
+        w.h = info.h[d];
+        w.c1 = info.c1;
+        w.half = 0.5 * info.P * info.h[d];
+        w.dim = d;
+        w.plan = h;
+    }
     return plan;
+}
+
+// ewald.hpp:49-59, 338-350: the parameter selection alone (a host-only plan)
+struct SelectResult {
+    SplitFamily family = SplitFamily::pswf;
+    double shape = 0.0;
+    int P = 0;
+    double c1 = std::numeric_limits<double>::quiet_NaN();
+    std::array<double, 3> demand{};
+    std::array<int, 3> base_nf{};
+    std::array<int, 3> nf{};
+    double E_A = 0.0;
+    double E_SI = 0.0;
+};
+
+inline SelectResult select_parameters(SplitFamily family, double eps, const Vec3& box,
+                                      double r_c, const Overrides& ov = {}) {
+    esp_overrides o{ov.nf, ov.P, ov.c1, ov.force_method == ForceMethod::ad ? ESP_FORCE_AD
+                                                                           : ESP_FORCE_IK,
+                    ov.allow_degraded ? 1 : 0};
+    detail::Handle h;
+    detail::check(esp_plan_create(box.data(),
+                                  family == SplitFamily::gaussian ? ESP_FAMILY_GAUSSIAN
+                                                                  : ESP_FAMILY_PSWF,
+                                  eps, r_c, &o, -1, &h.p));
+    esp_plan_info info{};
+    detail::check(esp_plan_get_info(h.p, &info));
+    SelectResult r;
+    r.family = family;
+    r.shape = info.shape;
+    r.P = info.P;
+    r.c1 = info.c1;
+    for (int d = 0; d < 3; ++d) {
+        r.demand[d] = info.demand[d];
+        r.base_nf[d] = info.base_nf[d];
+        r.nf[d] = info.nf[d];
+    }
+    r.E_A = info.E_A;
+    r.E_SI = info.E_SI;
+    return r;
 }
 
 // system.hpp:29-36
@@ -260,6 +378,131 @@ inline std::vector<double> self_correction(const EwaldPlan& plan, const std::vec
     detail::check(esp_self_correction(plan.handle(), static_cast<long>(q.size()), q.data(),
                                       out.data()));
     return out;
+}
+
+namespace detail {
+inline esp_plan* window_plan(const std::array<WindowKernel, 3>& win,
+                             const std::array<int, 3>& nf) {
+    if (!win[0].plan) throw std::invalid_argument("window kernels do not belong to a plan");
+    esp_plan_info info{};
+    check(esp_plan_get_info(win[0].plan->p, &info));
+    for (int d = 0; d < 3; ++d)
+        if (info.nf[d] != nf[d])  // gridder.hpp:141-148
+            throw std::invalid_argument("grid size does not match the window kernels' plan");
+    return win[0].plan->p;
+}
+inline std::vector<double> positions(const ParticleSystem& s) {
+    std::vector<double> p(3 * s.size());
+    for (std::size_t i = 0; i < s.size(); ++i)
+        for (int d = 0; d < 3; ++d) p[3 * i + d] = s.pos[i][d];
+    return p;
+}
+}  // namespace detail
+
+// gridder.hpp:215-241 (GPU; the imaginary part is zero)
+inline GridArray spread(const ParticleSystem& s, const std::array<WindowKernel, 3>& win,
+                        const std::array<int, 3>& nf) {
+    esp_plan* p = detail::window_plan(win, nf);
+    std::vector<double> re(static_cast<std::size_t>(nf[0]) * nf[1] * nf[2]);
+    const std::vector<double> pos = detail::positions(s);
+    std::lock_guard<std::mutex> lk(win[0].plan->m);
+    detail::check(esp_spread(p, static_cast<long>(s.size()), pos.data(), s.q.data(), re.data()));
+    GridArray g = GridArray::zeros(nf);
+    for (std::size_t i = 0; i < re.size(); ++i) g.v[i] = {re[i], 0.0};
+    return g;
+}
+
+// gridder.hpp:244-277 (the real part of the grid)
+inline std::vector<double> interpolate(const GridArray& g, const std::array<WindowKernel, 3>& win,
+                                       const ParticleSystem& s) {
+    esp_plan* p = detail::window_plan(win, g.nf);
+    std::vector<double> re(g.v.size()), out(s.size());
+    for (std::size_t i = 0; i < re.size(); ++i) re[i] = g.v[i].real();
+    const std::vector<double> pos = detail::positions(s);
+    std::lock_guard<std::mutex> lk(win[0].plan->m);
+    detail::check(esp_interpolate(p, static_cast<long>(s.size()), pos.data(), re.data(),
+                                  out.data()));
+    return out;
+}
+
+// gridder.hpp:280-314
+inline std::vector<Vec3> interpolate_gradient(const GridArray& g,
+                                              const std::array<WindowKernel, 3>& win,
+                                              const ParticleSystem& s) {
+    esp_plan* p = detail::window_plan(win, g.nf);
+    std::vector<double> re(g.v.size());
+    std::vector<Vec3> out(s.size());
+    for (std::size_t i = 0; i < re.size(); ++i) re[i] = g.v[i].real();
+    const std::vector<double> pos = detail::positions(s);
+    std::lock_guard<std::mutex> lk(win[0].plan->m);
+    detail::check(esp_interpolate_gradient(p, static_cast<long>(s.size()), pos.data(), re.data(),
+                                           detail::flat(out)));
+    return out;
+}
+
+// gridder.hpp:162-210 (the plan's coefficients; full nf^3 layout)
+inline std::vector<double> influence_coefficients(const SplitKernel& split,
+                                                  const std::array<WindowKernel, 3>& win,
+                                                  const std::array<int, 3>& nf, const Vec3& box) {
+    esp_plan* p = detail::window_plan(win, nf);
+    if (split.plan.get() != win[0].plan.get())
+        throw std::invalid_argument("split and window kernels come from different plans");
+    esp_plan_info info{};
+    detail::check(esp_plan_get_info(p, &info));
+    for (int d = 0; d < 3; ++d)
+        if (info.box[d] != box[d]) throw std::invalid_argument("box does not match the plan");
+    std::vector<double> out(static_cast<std::size_t>(nf[0]) * nf[1] * nf[2]);
+    detail::check(esp_plan_get_influence(p, out.data()));
+    return out;
+}
+
+// gridder.hpp:153-154: unnormalised forward (e^{-i}) / inverse (e^{+i}) on the GPU
+inline void fft_forward(GridArray& g) {
+    detail::check(esp_fft3(g.nf.data(), reinterpret_cast<double*>(g.v.data()), -1,
+                           detail::device_slot()));
+}
+inline void fft_inverse(GridArray& g) {
+    detail::check(esp_fft3(g.nf.data(), reinterpret_cast<double*>(g.v.data()), 1,
+                           detail::device_slot()));
+}
+
+// reference.hpp:21-29
+struct ReferenceResult {
+    std::vector<double> u;
+    std::vector<Vec3> F;
+    double energy = 0.0;
+    double lambda = 0.0;
+    int real_shells = 0;
+    int recip_kmax = 0;
+    double residual = 0.0;
+};
+
+// reference.hpp:212-238 on the GPU: a pass at lambda = min(L)/6 plus the
+// 1.3 lambda invariance pass.  Difference: no N <= 1e4 cap.
+inline ReferenceResult direct_ewald(const ParticleSystem& system, double tol) {
+    const long N = static_cast<long>(system.size());
+    const std::vector<double> pos = detail::positions(system);
+    ReferenceResult r;
+    r.u.resize(N);
+    r.F.resize(N);
+    esp_direct_info i1{}, i2{};
+    double e2 = 0.0;
+    const double lam = std::min({system.box[0], system.box[1], system.box[2]}) / 6.0;
+    detail::check(esp_direct_ewald(system.box.data(), N, pos.data(), system.q.data(), 0, nullptr,
+                                   tol, lam, r.u.data(), detail::flat(r.F), &r.energy, &i1,
+                                   detail::device_slot()));
+    std::vector<double> u2(N), F2(3 * N);
+    detail::check(esp_direct_ewald(system.box.data(), N, pos.data(), system.q.data(), 0, nullptr,
+                                   tol, 1.3 * lam, u2.data(), F2.data(), &e2, &i2,
+                                   detail::device_slot()));
+    const double gap = std::fabs(r.energy - e2);
+    if (gap > tol * std::max(1.0, std::fabs(r.energy)))
+        throw NumericalError("direct_ewald: splitting-width invariance check failed");
+    r.lambda = i1.lambda;
+    r.real_shells = i1.real_shells;
+    r.recip_kmax = i1.recip_kmax;
+    r.residual = std::max(gap, i1.tail_bound);
+    return r;
 }
 
 // reference.hpp:241-255

@@ -102,9 +102,15 @@ int esp_plan_get_influence(const esp_plan* plan, double* out);
 int esp_plan_get_table(const esp_plan* plan, int which, int dim, double* out, int* nseg);
 int esp_plan_get_prolate(const esp_plan* plan, int which, double* out, int* n);
 /* Host evaluators of the plan kernels: what 0 Psi, 1 chi, 2 chihat_n,
- * 3 phi(dim 0), 4 dphi, 5 phi_hat, 6 local potential, 7 local radial force
- * (kernels.hpp:63-229). */
+ * 3 phi(dim 0), 4 dphi, 5 phi_hat, 6 local potential, 7 local radial force,
+ * 8+d phi(dim d), 11+d dphi(dim d), 14+d phi_hat(dim d) (kernels.hpp:63-229). */
 int esp_plan_eval_kernel(const esp_plan* plan, int what, long n, const double* x, double* y);
+
+/* Unnormalised in-place 3-D DFT of nf[0]*nf[1]*nf[2] complex doubles
+ * (interleaved re, im; row-major, z fastest) on the GPU: direction -1 forward
+ * e^{-i}, +1 inverse e^{+i}; inverse(forward(g)) = N g (fft_forward /
+ * fft_inverse, gridder.hpp:85-100, 153-154).  Host buffer, synchronous. */
+int esp_fft3(const int nf[3], double* data, int direction, int device);
 
 /* evaluate (ewald.hpp:619-649) on HOST buffers: copies in, evaluates on the
  * GPU, copies out, synchronises, checks charge neutrality.  Raises the

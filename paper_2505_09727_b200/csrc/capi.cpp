@@ -7,6 +7,7 @@
 #include "plan.hpp"
 
 #include <cuda_runtime.h>
+#include <cufft.h>
 
 #include <algorithm>
 #include <cmath>
@@ -278,9 +279,39 @@ int esp_plan_eval_kernel(const esp_plan* p, int what, long n, const double* x, d
                 case 5: y[i] = P.phi_hat(0, x[i]); break;
                 case 6: y[i] = P.local_kernel(x[i]).first; break;
                 case 7: y[i] = P.local_kernel(x[i]).second; break;
+                case 8: case 9: case 10: y[i] = P.phi_at(what - 8, x[i]); break;
+                case 11: case 12: case 13: y[i] = P.dphi_at(what - 11, x[i]); break;
+                case 14: case 15: case 16: y[i] = P.phi_hat(what - 14, x[i]); break;
                 default: throw espb::InvalidArgument("kernel selector out of range");
             }
         }
+    });
+}
+
+int esp_fft3(const int nf[3], double* data, int direction, int device) {
+    return guarded([&] {
+        if (!nf || !data) throw espb::InvalidArgument("null argument");
+        if (nf[0] < 1 || nf[1] < 1 || nf[2] < 1) throw espb::InvalidArgument("fft: bad grid");
+        if (direction != -1 && direction != 1)
+            throw espb::InvalidArgument("fft: direction must be -1 (forward) or +1 (inverse)");
+        cuda_ok(cudaSetDevice(device), "cudaSetDevice");
+        const size_t n = static_cast<size_t>(nf[0]) * nf[1] * nf[2];
+        void* d = nullptr;
+        cuda_ok(cudaMalloc(&d, n * 2 * sizeof(double)), "cudaMalloc");
+        struct Free {
+            void* p;
+            ~Free() { cudaFree(p); }
+        } guard{d};
+        cuda_ok(cudaMemcpy(d, data, n * 2 * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+        cufftHandle h = 0;
+        if (cufftPlan3d(&h, nf[0], nf[1], nf[2], CUFFT_Z2Z) != CUFFT_SUCCESS)
+            throw espb::CudaError("fft: cufftPlan3d failed");
+        const cufftResult r = cufftExecZ2Z(h, static_cast<cufftDoubleComplex*>(d),
+                                           static_cast<cufftDoubleComplex*>(d),
+                                           direction < 0 ? CUFFT_FORWARD : CUFFT_INVERSE);
+        cufftDestroy(h);
+        if (r != CUFFT_SUCCESS) throw espb::CudaError("fft: cufftExecZ2Z failed");
+        cuda_ok(cudaMemcpy(data, d, n * 2 * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
     });
 }
 

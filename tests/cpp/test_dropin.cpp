@@ -6,6 +6,7 @@
 #include "esp/esp.hpp"
 
 #include <cmath>
+#include <complex>
 #include <cstdint>
 #include <cstdio>
 #include <stdexcept>
@@ -190,6 +191,80 @@ int main() {
         CHECK(plan.total_modes() == 40ull * 40ull * 40ull);
         CHECK(std::fabs(plan.avg_neighbors(512) - 4.0 * M_PI / 3.0 * 512.0 / 1000.0) <= 1e-12);
         CHECK(plan.influence()[0] == 0.0);
+    }
+    // kernel objects, parameter selection, influence (kernels.hpp, ewald.hpp:338)
+    {
+        esp::EwaldPlan plan = esp::build_plan(box, esp::SplitFamily::pswf, 1e-4, 1.0);
+        CHECK(std::fabs(plan.split.Psi(0.0)) <= 1e-14);
+        CHECK(std::fabs(plan.split.Psi(1.0) - 1.0) <= 1e-12);
+        CHECK(std::fabs(plan.split.chi(0.0) - plan.split.chi0) <= 1e-12 * plan.split.chi0);
+        CHECK(plan.win[1].P == plan.P && plan.win[2].dim == 2);
+        CHECK(plan.win[0].phi(0.0) > 0.0 && plan.win[0].phi(plan.win[0].half) == 0.0);
+        esp::SelectResult sel = esp::select_parameters(esp::SplitFamily::pswf, 1e-4, box, 1.0);
+        CHECK(sel.nf == plan.nf && sel.P == plan.P && sel.c1 == plan.c1);
+        std::vector<double> a = plan.influence();
+        std::vector<double> b = esp::influence_coefficients(plan.split, plan.win, plan.nf, box);
+        CHECK(a == b);
+        CHECK(throws<std::invalid_argument>(
+            [&] { esp::influence_coefficients(plan.split, plan.win, {32, 32, 32}, box); }));
+    }
+    // spread / interpolate adjointness and the gradient (gridder.hpp:215-314,
+    // test_gridder.cpp)
+    {
+        esp::EwaldPlan plan = esp::build_plan(box, esp::SplitFamily::pswf, 1e-4, 1.0);
+        esp::ParticleSystem s = random_system(64, box, 5);
+        esp::GridArray g = esp::spread(s, plan.win, plan.nf);
+        esp::GridArray f = esp::GridArray::zeros(plan.nf);
+        std::uint64_t st = 99;
+        for (auto& c : f.v) {
+            st = st * 6364136223846793005ull + 1442695040888963407ull;
+            c = {static_cast<double>(st >> 11) * 0x1.0p-53 - 0.5, 0.0};
+        }
+        double lhs = 0.0, rhs = 0.0;
+        for (std::size_t i = 0; i < g.v.size(); ++i) lhs += g.v[i].real() * f.v[i].real();
+        std::vector<double> u = esp::interpolate(f, plan.win, s);
+        for (std::size_t i = 0; i < u.size(); ++i) rhs += s.q[i] * u[i];
+        CHECK(std::fabs(lhs - rhs) <= 1e-12 * std::fabs(lhs));
+        std::vector<esp::Vec3> gr = esp::interpolate_gradient(f, plan.win, s);
+        // central difference of interpolate along x for atom 0
+        esp::ParticleSystem sp = s, sm = s;
+        const double dx = 1e-5;
+        sp.pos[0][0] += dx;
+        sm.pos[0][0] -= dx;
+        const double fd = (esp::interpolate(f, plan.win, sp)[0] - esp::interpolate(f, plan.win, sm)[0]) / (2 * dx);
+        CHECK(std::fabs(fd - gr[0][0]) <= 1e-5 * (1.0 + std::fabs(gr[0][0])));
+    }
+    // FFT conventions (gridder.hpp:6-13, 85-100): inverse(forward(g)) = N g
+    {
+        esp::GridArray g = esp::GridArray::zeros({6, 10, 15});
+        std::uint64_t st = 7;
+        for (auto& c : g.v) {
+            st = st * 6364136223846793005ull + 1442695040888963407ull;
+            c = {static_cast<double>(st >> 11) * 0x1.0p-53, static_cast<double>(st >> 40) * 0x1.0p-24};
+        }
+        esp::GridArray h = g;
+        esp::fft_forward(h);
+        // mode (1, 0, 0) against a direct sum with e^{-i}
+        std::complex<double> m{0.0, 0.0};
+        for (int ix = 0; ix < 6; ++ix)
+            for (int iy = 0; iy < 10; ++iy)
+                for (int iz = 0; iz < 15; ++iz)
+                    m += g.v[g.idx(ix, iy, iz)] * std::polar(1.0, -2.0 * M_PI * ix / 6.0);
+        CHECK(std::abs(h.v[h.idx(1, 0, 0)] - m) <= 1e-12 * std::abs(m));
+        esp::fft_inverse(h);
+        double err = 0.0;
+        for (std::size_t i = 0; i < g.v.size(); ++i)
+            err = std::max(err, std::abs(h.v[i] / 900.0 - g.v[i]));
+        CHECK(err <= 1e-13);
+    }
+    // direct Ewald (reference.hpp:212-238) against the ESP evaluation: Delta <= eps
+    {
+        esp::ParticleSystem s = random_system(200, box, 77);
+        esp::ReferenceResult d = esp::direct_ewald(s, 1e-9);
+        esp::EnergyForces ef = esp::evaluate(esp::build_plan(box, esp::SplitFamily::pswf, 1e-4, 1.0), s);
+        CHECK(esp::relative_force_error(ef.F, d.F) <= 1e-4);
+        CHECK(std::fabs(ef.energy - d.energy) <= 1e-4 * std::fabs(d.energy));
+        CHECK(d.real_shells >= 1 && d.recip_kmax >= 1 && d.lambda > 0.0);
     }
     std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "PASSED", failures);
     return failures ? 1 : 0;
