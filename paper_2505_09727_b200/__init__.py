@@ -28,7 +28,7 @@ __all__ = [
     "ParticleSystem", "EnergyForces", "PartialField", "build_plan", "evaluate",
     "evaluate_device", "local_sum", "spectral_sum", "self_correction", "spread",
     "interpolate", "interpolate_gradient", "require_neutral", "fold", "device_count",
-    "direct_ewald", "ReferenceResult",
+    "direct_ewald", "ReferenceResult", "fft_forward", "fft_inverse", "select_parameters",
     "LIB_PATH",
 ]
 
@@ -128,6 +128,7 @@ _sig("esp_last_launch_count", [_vp])
 _sig("esp_eval_phase_a", [_vp, _dp, C.c_long, _vp, _vp, C.c_int, C.c_int, _vp, _vp])
 _sig("esp_eval_phase_b", [_vp, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp])
 _sig("esp_grid_size", [_vp], C.c_long)
+_sig("esp_fft3", [C.POINTER(C.c_int), _vp, C.c_int, C.c_int])
 _sig("esp_direct_ewald", [_dp, C.c_long, _dp, _dp, C.c_long, _vp, C.c_double, C.c_double, _dp,
                           _dp, C.POINTER(C.c_double), C.POINTER(_DirectInfo), C.c_int])
 _sig("esp_pencil_geometry", [_vp, C.c_int, C.c_int, C.POINTER(_PencilInfo)])
@@ -499,6 +500,34 @@ def direct_ewald(system: ParticleSystem, tol: float = 1e-9, targets=None,
         raise NumericalError("direct_ewald: splitting-width invariance check failed")
     return ReferenceResult(u1, F1, E1, i1.lambda_, i1.real_shells, i1.recip_kmax,
                            max(gap, i1.tail_bound))
+
+
+def fft_forward(grid: np.ndarray, device: int = 0) -> np.ndarray:
+    """gridder.hpp:153: unnormalised forward 3-D DFT (e^{-i}) on the GPU;
+    returns a new complex128 array of the same shape."""
+    return _fft3(grid, -1, device)
+
+
+def fft_inverse(grid: np.ndarray, device: int = 0) -> np.ndarray:
+    """gridder.hpp:154: unnormalised inverse 3-D DFT (e^{+i}) on the GPU."""
+    return _fft3(grid, 1, device)
+
+
+def _fft3(grid, direction, device):
+    g = np.ascontiguousarray(grid, dtype=np.complex128).copy()
+    if g.ndim != 3:
+        raise InvalidArgument("fft: need a 3-D grid")
+    nf = (C.c_int * 3)(*g.shape)
+    _check(_lib.esp_fft3(nf, g.ctypes.data_as(C.c_void_p), int(direction), int(device)))
+    return g
+
+
+def select_parameters(family: str, eps: float, box, r_c: float,
+                      overrides: Overrides | None = None) -> dict:
+    """ewald.hpp:338-350 (SelectResult): the parameter choice alone."""
+    p = build_plan(box, family, eps, r_c, overrides, device=-1)
+    return {"family": p.family, "shape": p.shape, "P": p.P, "c1": p.c1, "demand": p.demand,
+            "base_nf": p.base_nf, "nf": p.nf, "E_A": p.stats.E_A, "E_SI": p.stats.E_SI}
 
 
 def grid_size(plan: EwaldPlan) -> int:

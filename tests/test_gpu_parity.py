@@ -200,3 +200,13 @@ def test_pinned_host_buffers(esp, gpu):
     q2[0] += 1.0
     with pytest.raises(esp.NumericalError):
         esp.evaluate(plan, esp.ParticleSystem(box, q2, pin(pos)))
+
+
+def test_fft_conventions(esp, gpu):
+    """gridder.hpp:6-13: forward e^{-i} unnormalised (numpy's fftn), inverse
+    e^{+i} unnormalised; inverse(forward(g)) = N g (test_gridder.cpp:44-76)."""
+    g = np.random.default_rng(4).normal(size=(6, 10, 15)) + 1j * np.random.default_rng(5).normal(size=(6, 10, 15))
+    f = esp.fft_forward(g, device=gpu)
+    assert np.abs(f - np.fft.fftn(g)).max() <= 1e-12 * np.abs(f).max()
+    back = esp.fft_inverse(f, device=gpu)
+    assert np.abs(back / g.size - g).max() <= 1e-13 * np.abs(g).max()

@@ -110,3 +110,20 @@ def test_pair_polynomials_are_exact_change_of_basis(esp):
         p = esp.build_plan((10.0, 10.0, 10.0), "pswf", eps, 1.0, device=-1)
         assert p.pair_fit_err <= 2e-14
         assert p.pair_poly_degree <= len(p.prolate_coef(-1)) - 1
+
+
+def test_select_parameters_matches_golden_plans():
+    """ewald.hpp:338-350: select_parameters alone gives the compiled
+    reference's (nf, P, c1) for the benchmark configs."""
+    import json
+    import os
+    import paper_2505_09727_b200 as esp
+    from paper_2505_09727_b200 import systems as S
+    from conftest import GOLDEN
+    plans = json.load(open(os.path.join(GOLDEN, "plans.json")))
+    for name in ("cfg1", "cfg2", "cfg4"):
+        c = S.config(name)
+        ref = plans[name]
+        sel = esp.select_parameters("pswf", c.eps, (c.L,) * 3, c.r_c)
+        assert list(sel["nf"]) == list(ref["nf"]) and sel["P"] == ref["P"]
+        assert abs(sel["c1"] - ref["c1"]) <= 1e-12 * abs(ref["c1"])
