@@ -813,18 +813,24 @@ __global__ void __launch_bounds__(512) k_spread(GridArgs g, const double4* __res
         }
         __syncthreads();
         if (P3 <= nt) {
+            // the atom's tile base offset, once per atom
+            int* fbase = fch + 3 * kSpreadChunk;
+            if (threadIdx.x < nc)
+                fbase[threadIdx.x] = fch[3 * threadIdx.x] * PS + fch[3 * threadIdx.x + 1] * RS +
+                                     fch[3 * threadIdx.x + 2];
+            __syncthreads();
             // one footprint node per thread: its decode is atom-invariant
             const int p = threadIdx.x;
             const bool act = p < P3;
             const int jx = p / P2, r = p - jx * P2;
             const int jy = r / P, jz = r - jy * P;
-            const int myoff = jx * PS + jy * RS + jz;
+            double* tl = tile + jx * PS + jy * RS + jz;
+            const double* wl = wch + jx;
+            const int oy = MP + jy, oz = 2 * MP + jz;
             for (int ai = 0; ai < nc; ++ai) {
-                const int* fo = fch + ai * 3;
-                const double* w = wch + ai * 3 * MP;
                 if (act) {
-                    const int off = fo[0] * PS + fo[1] * RS + fo[2] + myoff;
-                    tile[off] += w[jx] * w[MP + jy] * w[2 * MP + jz];
+                    const double* w = wl + ai * 3 * MP;
+                    tl[fbase[ai]] += w[0] * w[oy - jx] * w[oz - jx];
                 }
                 __syncthreads();
             }
