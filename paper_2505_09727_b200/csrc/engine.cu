@@ -70,6 +70,7 @@ constexpr long kHighPriorityMaxN = 1L << 19;  // grid pipeline on the high-prior
 constexpr int kColDivDefault = 2;
 constexpr double kColDiv3MinPairs = 300.0;  // r_c/3 columns: enough pairs per target
 constexpr int kMaxPoly = 40;   // max pair-polynomial coefficients
+constexpr long kHalfMinN = 4096;  // half-shell K4 from this many atoms
 
 // ----------------------------------------------------------------------------
 // small device helpers
@@ -745,6 +746,504 @@ __global__ void __launch_bounds__(128) k_pair_allpairs(long N, long i0, long i1,
     }
     loc[i] = make_double4(u, -pi.w * fx, -pi.w * fy, -pi.w * fz);
     if (npairs) atomicAdd(npairs, static_cast<unsigned long long>(npair));
+}
+
+// ----------------------------------------------------------------------------
+// K4, half-shell form: every unordered pair evaluated once
+// ----------------------------------------------------------------------------
+//
+// The reference evaluates both orders of every pair (ewald.hpp:473-509, full
+// neighbour list per target).  Here the target i takes only its FORWARD
+// neighbours: fine-cell offsets (dx, dy, dz) with dx > 0, or dx = 0 and dy > 0,
+// or dx = dy = 0 (own column) and the atom after i in the column's sorted
+// order (dz > 0, or the same cell and j > i).  With >= 2M+1 columns and
+// >= 2Mz+1 slices per period every (i, j, image) pair is reached from exactly
+// one side.  The j-side terms are bitwise the terms j's own evaluation would
+// produce (the displacement (r_i - r_j) - s is -((r_j - r_i) + s) exactly), so
+// only the summation order differs from the full-list kernel.
+//
+// A CTA owns the targets of a block of bx x bx columns x bz slices and stages
+// their forward neighbourhood -- columns [0, bx + M) x [-M, bx + M), slices
+// [-Mz, bz + Mz) around the block -- in shared memory as fp32 coordinates
+// relative to the block origin + the source code (as k_pair).  Warp per
+// target: forward columns (M(2M+1) + M + 1 <= 25, one per lane, rotated per
+// target), list, fp32 screen + ballot compaction, fp64 rounds that keep the
+// i-side terms in registers and send the j-side terms to global planar
+// accumulators in pair-sorted order (u | Fx | Fy | Fz) with fire-and-forget
+// fp64 REDs: a round's partners are mostly consecutive sorted atoms, so a RED
+// instruction touches a few 32-byte sectors per component (the L2 atomic
+// units, not the issuing warp, absorb the adds).  Measured against the
+// alternatives: REDs into the original-order (u, F) buffer (one sector per
+// lane) were 1.4x slower at cfg5, and staged fp64 shared accumulators (CAS
+// loops, 3x the shared memory, a flush per block) were no faster than the
+// full-list kernel.  k_acc_to_loc then scatters the sums to the caller's order
+// and re-zeroes the accumulators.  A block whose neighbourhood exceeds the
+// staging capacity is queued for k_pair_half_ovf.
+
+struct HalfArgs {
+    const double4* xyzq;  // sorted by pair cell
+    const int* orig;
+    const int* start;     // ncell + 1
+    double* acc;          // pair-sorted order, planar: u | Fx | Fy | Fz (stride nacc), zero at rest
+    long nacc;
+    unsigned long long* npairs;  // ordered in-range pairs (2 per evaluated unordered pair)
+    int* ovf;                    // [0] overflowed blocks, [1..] their ids
+    int cap;                     // staged atoms per CTA
+    int lcap;                    // per-warp list capacity (even): pieces of lcap - 32 + padding
+    int nent_max;                // cell entries per CTA neighbourhood
+    int M, Mz;                   // reach in columns / slices
+    int bx, bz;                  // target block: bx x bx columns, bz slices
+    int F[3];                    // fine cells per dim
+    double fw[3];
+    double box[3];
+};
+
+constexpr int kHalfMaxBX = 4;
+constexpr int kHalfWarps = 8;
+constexpr int kHalfThreads = 32 * kHalfWarps;
+
+// (u, F) terms of one pair from both sides; returns false out of range.
+template <int ND>
+__device__ __forceinline__ bool pair_eval2(const PairConsts& k, double4 pj, double sx, double sy,
+                                           double sz, double xi, double yi, double zi, double qi,
+                                           double& u, double& fx, double& fy, double& fz,
+                                           double4& gj) {
+    const double dx = (pj.x - xi) + sx, dy = (pj.y - yi) + sy, dz = (pj.z - zi) + sz;
+    const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+    if (!(r2 < k.rc2 && r2 > 0.0)) return false;
+    double rinv;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rinv) : "d"(r2));
+    {
+        const double hr = 0.5 * r2;
+        double e = fma(-hr * rinv, rinv, 0.5);
+        rinv = fma(rinv, e, rinv);
+        e = fma(-hr * rinv, rinv, 0.5);
+        rinv = fma(rinv, e, rinv);
+    }
+    const double z = fma(r2, k.two_irc2, -1.0);
+    double H = k.H[ND - 1], dH = 0.0;
+#pragma unroll
+    for (int m = ND - 2; m >= 0; --m) {
+        dH = fma(dH, z, H);
+        H = fma(H, z, k.H[m]);
+    }
+    const double G = fma(2.0 * (z + 1.0), dH, H);
+    const double y = r2 * rinv * k.irc;
+    const double w = k.inv4pi * rinv;
+    const double pot = (1.0 - y * H) * w;
+    const double fr = fma(G * w, k.irc, pot * rinv);
+    u = fma(pj.w, pot, u);
+    const double c = pj.w * fr * rinv;
+    fx = fma(c, dx, fx);
+    fy = fma(c, dy, fy);
+    fz = fma(c, dz, fz);
+    // F_j = -q_j sum_i q_i (fr/r) (r_i - r_j) = q_i c d
+    const double b = qi * c;
+    gj = make_double4(qi * pot, b * dx, b * dy, b * dz);
+    return true;
+}
+
+// (u, F) terms of sorted atom j into the planar accumulators (global REDs;
+// the 32 lanes of a round mostly hold consecutive sorted atoms, so one RED
+// instruction touches a few 32-byte sectors per component)
+__device__ __forceinline__ void red_acc(double* acc, long n, int j, double a, double b, double c,
+                                        double d) {
+    atomicAdd(acc + j, a);
+    atomicAdd(acc + n + j, b);
+    atomicAdd(acc + 2 * n + j, c);
+    atomicAdd(acc + 3 * n + j, d);
+}
+
+// forward column l of a target (lane l < M(2M+1) + M + 1): offsets (dx, dy)
+__device__ __forceinline__ void fwd_col(int l, int M, int& dx, int& dy) {
+    const int n1 = M * (2 * M + 1);
+    if (l < n1) {
+        dx = 1 + l / (2 * M + 1);
+        dy = l % (2 * M + 1) - M;
+    } else if (l < n1 + M) {
+        dx = 0;
+        dy = 1 + (l - n1);
+    } else {
+        dx = 0;
+        dy = 0;
+    }
+}
+
+template <int ND>
+__global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const __grid_constant__ PairConsts k) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    float4* cand = reinterpret_cast<float4*>(smem);                 // a.cap + 1 (sentinel)
+    int* qall = reinterpret_cast<int*>(cand + a.cap + 1);           // 64 per warp
+    unsigned short* lall = reinterpret_cast<unsigned short*>(qall + kHalfWarps * 64);
+    int* ent_src = reinterpret_cast<int*>(lall + kHalfWarps * a.lcap);
+    int* ent_off = ent_src + a.nent_max;                            // nent_max + 1
+    unsigned char* ent_slot = reinterpret_cast<unsigned char*>(ent_off + a.nent_max + 1);
+    __shared__ double shiftv[27][3];
+    __shared__ int tbeg[kHalfMaxBX * kHalfMaxBX], tpre[kHalfMaxBX * kHalfMaxBX + 1];
+    __shared__ int tnext;  // next unassigned target
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int* qw = qall + warp * 64;
+    unsigned short* lw = lall + warp * a.lcap;
+    const unsigned lt_mask = (1u << lane) - 1u;
+
+    const int M = a.M, Mz = a.Mz, BX = a.bx;
+    const int nzb = (a.F[2] + a.bz - 1) / a.bz;
+    const int nyb = (a.F[1] + BX - 1) / BX;
+    const int blk = blockIdx.x;
+    const int bzi = blk % nzb;
+    const int fy0 = ((blk / nzb) % nyb) * BX;
+    const int fx0 = (blk / (nzb * nyb)) * BX;
+    const int bxe = min(BX, a.F[0] - fx0), bye = min(BX, a.F[1] - fy0);
+    const int z0 = bzi * a.bz, z1 = min(a.F[2], z0 + a.bz), bze = z1 - z0;
+    const int Wx = bxe + M, Wy = bye + 2 * M;
+    const int ncol = Wx * Wy;
+    const int nsl = bze + 2 * Mz;
+    const int nent = ncol * nsl;
+    const double ox = fx0 * a.fw[0], oy = fy0 * a.fw[1], oz = z0 * a.fw[2];
+
+    if (threadIdx.x < 27) {
+        const int t = threadIdx.x;
+        shiftv[t][0] = (t / 9 - 1) * a.box[0];
+        shiftv[t][1] = ((t / 3) % 3 - 1) * a.box[1];
+        shiftv[t][2] = (t % 3 - 1) * a.box[2];
+    }
+    for (int e = threadIdx.x; e < nent; e += blockDim.x) {
+        const int col = e / nsl, sl = e - col * nsl;
+        const int cx = col / Wy, cy = col - cx * Wy;
+        int fx = fx0 + cx, fy = fy0 - M + cy, fz = z0 - Mz + sl;
+        const int ix = fx < 0 ? 0 : (fx >= a.F[0] ? 2 : 1);
+        const int iy = fy < 0 ? 0 : (fy >= a.F[1] ? 2 : 1);
+        const int iz = fz < 0 ? 0 : (fz >= a.F[2] ? 2 : 1);
+        fx += (1 - ix) * a.F[0];
+        fy += (1 - iy) * a.F[1];
+        fz += (1 - iz) * a.F[2];
+        const int f = (fx * a.F[1] + fy) * a.F[2] + fz;
+        const int s0 = a.start[f];
+        ent_src[e] = s0;
+        ent_off[e + 1] = a.start[f + 1] - s0;
+        ent_slot[e] = static_cast<unsigned char>((ix * 3 + iy) * 3 + iz);
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const int per = (nent + 31) / 32;
+        const int e0 = min(nent, lane * per), e1 = min(nent, e0 + per);
+        int sum = 0;
+        for (int e = e0; e < e1; ++e) sum += ent_off[e + 1];
+        int incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const int last = e1 > e0 ? ent_off[e1] : 0;
+        __syncwarp();
+        int run = incl - sum;
+        for (int e = e0; e < e1; ++e) {
+            const int c = e == e1 - 1 ? last : ent_off[e + 1];
+            ent_off[e] = run;
+            run += c;
+        }
+        __syncwarp();
+        if (lane == 31) ent_off[nent] = incl;
+    }
+    __syncthreads();
+    const int total = ent_off[nent];
+    if (total > a.cap) {
+        // too many atoms for the staging area: the overflow kernel takes the block
+        if (threadIdx.x == 0) {
+            const int q = atomicAdd(a.ovf, 1);
+            a.ovf[1 + q] = blk;
+        }
+        return;
+    }
+    if (threadIdx.x == 32) {
+        // target columns (cx < bxe, cy in [M, M + bye)), slices [Mz, Mz + bze)
+        int accn = 0;
+        const int ntc = bxe * bye;
+        for (int c = 0; c < ntc; ++c) {
+            const int col = (c / bye) * Wy + M + c % bye;
+            const int b = ent_off[col * nsl + Mz], e = ent_off[col * nsl + Mz + bze];
+            tbeg[c] = b;
+            tpre[c] = accn;
+            accn += e - b;
+        }
+        tpre[ntc] = accn;
+        tnext = kHalfWarps;
+    }
+    // stage: each column's slices are at most three contiguous runs (below,
+    // inside, above the z period), one warp per run
+    {
+        const int lo_in = max(0, min(nsl, Mz - z0));
+        const int hi_in = max(0, min(nsl, a.F[2] - z0 + Mz));
+        for (int task = warp; task < ncol * 3; task += kHalfWarps) {
+            const int col = task / 3, part = task - 3 * (task / 3);
+            const int sa = part == 0 ? 0 : (part == 1 ? lo_in : hi_in);
+            const int sb = part == 0 ? lo_in : (part == 1 ? hi_in : nsl);
+            if (sb <= sa) continue;
+            const int e0 = col * nsl + sa;
+            const int g0 = ent_off[e0], g1 = ent_off[col * nsl + sb];
+            const int src0 = ent_src[e0] - g0;
+            const int sl = ent_slot[e0];
+            const double shx = shiftv[sl][0] - ox, shy = shiftv[sl][1] - oy,
+                         shz = shiftv[sl][2] - oz;
+            for (int g = g0 + lane; g < g1; g += 32) {
+                const int src = g + src0;
+                const double4 v = a.xyzq[src];
+                cand[g] = make_float4(static_cast<float>(v.x + shx), static_cast<float>(v.y + shy),
+                                      static_cast<float>(v.z + shz),
+                                      __int_as_float(src | (sl << 27)));
+            }
+        }
+        if (threadIdx.x == 0) cand[a.cap] = make_float4(1e30f, 1e30f, 1e30f, __int_as_float(0));
+    }
+    __syncthreads();
+    const int ntc = bxe * bye;
+    const int ni = tpre[ntc];
+    const float R2 = k.rc2_test;
+    const float fwx = static_cast<float>(a.fw[0]), fwy = static_cast<float>(a.fw[1]);
+    const float ifwz = 1.0f / static_cast<float>(a.fw[2]);
+    const int nfc = M * (2 * M + 1) + M + 1;  // forward columns (own column last)
+    int npair = 0;
+
+    for (int ii = warp;;) {
+        if (ii >= ni) break;
+        int tc = 0;
+        while (tc + 1 < ntc && ii >= tpre[tc + 1]) ++tc;
+        const int si = tbeg[tc] + (ii - tpre[tc]);
+        const float4 ci = cand[si];
+        const int gi = __float_as_int(ci.w) & 0x7ffffff;
+        const double4 pi = a.xyzq[gi];
+        const float xf = ci.x, yf = ci.y, zf = ci.z;
+        const int tx = tc / bye, ty = M + tc % bye;
+        int beg = 0, cnt = 0;
+        if (lane < nfc) {
+            // rotated column order per target: warps working on neighbouring
+            // targets then walk their (shared) neighbours in different orders,
+            // which keeps their CAS adds on the accumulators apart
+            int lc = lane + 5 * ii;
+            lc -= nfc * (lc / nfc);
+            int dx, dy;
+            fwd_col(lc, M, dx, dy);
+            const int ca = tx + dx, cb = ty + dy;
+            const int col = ca * Wy + cb;
+            const float x0 = ca * fwx, y0 = (cb - M) * fwy;
+            const float gx = fmaxf(0.f, fmaxf(x0 - xf, xf - (x0 + fwx)));
+            const float gy = fmaxf(0.f, fmaxf(y0 - yf, yf - (y0 + fwy)));
+            const float g2 = fmaf(gx, gx, gy * gy);
+            if (g2 < R2) {
+                const float zm = sqrtf(R2 - g2);
+                int klo = static_cast<int>(floorf((zf - zm) * ifwz)) + Mz;
+                int khi = static_cast<int>(floorf((zf + zm) * ifwz)) + Mz;
+                klo = max(0, min(nsl - 1, klo));
+                khi = max(0, min(nsl - 1, khi));
+                int lo = ent_off[col * nsl + klo];
+                const int hi = ent_off[col * nsl + khi + 1];
+                if (lc == nfc - 1) lo = si + 1;  // own column: after i
+                if (hi > lo) {
+                    beg = lo;
+                    cnt = hi - lo;
+                }
+            }
+        }
+        int inc = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
+        }
+        const int T = __shfl_sync(0xffffffffu, inc, 31);
+        double u = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
+        int qn = 0;
+        bool have_pf = false;
+        double4 pf = make_double4(0.0, 0.0, 0.0, 0.0);
+        int tf = 13, sf = 0;
+        for (int lb = 0; lb < T; lb += a.lcap - 32) {
+            const int le = min(T, lb + a.lcap - 32);
+            {
+                const int p0 = max(inc - cnt, lb), p1 = min(inc, le);
+                const int off = beg - (inc - cnt);
+#pragma unroll 4
+                for (int p = p0; p < p1; ++p) lw[p - lb] = static_cast<unsigned short>(off + p);
+            }
+            const int n = le - lb;
+            const int n32 = (n + 31) & ~31;
+            if (n + lane < n32) lw[n + lane] = static_cast<unsigned short>(a.cap);
+            __syncwarp();
+            const unsigned short* lend = lw + n32;
+            for (const unsigned short* lp = lw + lane; lp < lend; lp += 32) {
+                const int s = *lp;
+                const float4 c4 = cand[s];
+                const float dx = c4.x - xf, dy = c4.y - yf, dz = c4.z - zf;
+                const bool in = fmaf(dz, dz, fmaf(dy, dy, dx * dx)) < R2;
+                const unsigned m = __ballot_sync(0xffffffffu, in);
+                if (in) qw[qn + __popc(m & lt_mask)] = s;
+                qn += __popc(m);
+                if (qn >= 32) {
+                    __syncwarp();
+                    const int sq = qw[lane];
+                    const int extra = qw[32 + lane];
+                    __syncwarp();
+                    qw[lane] = extra;
+                    qn -= 32;
+                    if (have_pf) {
+                        double4 g;
+                        if (pair_eval2<ND>(k, pf, shiftv[tf][0], shiftv[tf][1], shiftv[tf][2],
+                                           pi.x, pi.y, pi.z, pi.w, u, fx, fy, fz, g)) {
+                            ++npair;
+                            red_acc(a.acc, a.nacc, sf, g.x, g.y, g.z, g.w);
+                        }
+                    }
+                    const int cd = __float_as_int(cand[sq].w);
+                    pf = a.xyzq[cd & 0x7ffffff];
+                    tf = static_cast<unsigned>(cd) >> 27;
+                    sf = cd & 0x7ffffff;
+                    have_pf = true;
+                }
+            }
+            __syncwarp();
+        }
+        if (have_pf) {
+            double4 g;
+            if (pair_eval2<ND>(k, pf, shiftv[tf][0], shiftv[tf][1], shiftv[tf][2], pi.x, pi.y,
+                               pi.z, pi.w, u, fx, fy, fz, g)) {
+                ++npair;
+                red_acc(a.acc, a.nacc, sf, g.x, g.y, g.z, g.w);
+            }
+        }
+        if (lane < qn) {
+            const int sq = qw[lane];
+            const int cd = __float_as_int(cand[sq].w);
+            const double4 pj = a.xyzq[cd & 0x7ffffff];
+            const int t = static_cast<unsigned>(cd) >> 27;
+            double4 g;
+            if (pair_eval2<ND>(k, pj, shiftv[t][0], shiftv[t][1], shiftv[t][2], pi.x, pi.y, pi.z,
+                               pi.w, u, fx, fy, fz, g)) {
+                ++npair;
+                red_acc(a.acc, a.nacc, cd & 0x7ffffff, g.x, g.y, g.z, g.w);
+            }
+        }
+        __syncwarp();
+        {
+            const bool h16 = lane & 16, h8 = lane & 8;
+            const double s0 = h16 ? u : fy, s1 = h16 ? fx : fz;
+            const double k0 = h16 ? fy : u, k1 = h16 ? fz : fx;
+            const double v0 = k0 + __shfl_xor_sync(0xffffffffu, s0, 16);
+            const double v1 = k1 + __shfl_xor_sync(0xffffffffu, s1, 16);
+            double w = (h8 ? v1 : v0) + __shfl_xor_sync(0xffffffffu, h8 ? v0 : v1, 8);
+            w += __shfl_xor_sync(0xffffffffu, w, 4);
+            w += __shfl_xor_sync(0xffffffffu, w, 2);
+            w += __shfl_xor_sync(0xffffffffu, w, 1);
+            if ((lane & 7) == 0) {
+                const int comp = lane >> 3;  // 0 u, 1 Fx, 2 Fy, 3 Fz
+                atomicAdd(a.acc + comp * a.nacc + gi, comp == 0 ? w : -pi.w * w);
+            }
+        }
+        // next target: dynamic assignment balances the warps of the CTA
+        int nx = 0;
+        if (lane == 0) nx = atomicAdd(&tnext, 1);
+        ii = __shfl_sync(0xffffffffu, nx, 0);
+    }
+    npair = __reduce_add_sync(0xffffffffu, npair);
+    if (lane == 0 && a.npairs && npair)
+        atomicAdd(a.npairs, 2ull * static_cast<unsigned long long>(npair));
+}
+
+// Blocks whose forward neighbourhood did not fit the staging area: warp per
+// target, lane per forward column, exact tests only, both sides with global
+// REDs.  Rare (strongly non-uniform systems); correctness path.
+template <int ND>
+__global__ void __launch_bounds__(256) k_pair_half_ovf(HalfArgs a, const __grid_constant__ PairConsts k) {
+    __shared__ double shiftv[27][3];
+    if (threadIdx.x < 27) {
+        const int t = threadIdx.x;
+        shiftv[t][0] = (t / 9 - 1) * a.box[0];
+        shiftv[t][1] = ((t / 3) % 3 - 1) * a.box[1];
+        shiftv[t][2] = (t % 3 - 1) * a.box[2];
+    }
+    __syncthreads();
+    const int nov = *a.ovf;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int M = a.M, Mz = a.Mz, BX = a.bx;
+    const int nzb = (a.F[2] + a.bz - 1) / a.bz;
+    const int nyb = (a.F[1] + BX - 1) / BX;
+    const int nfc = M * (2 * M + 1) + M + 1;
+    int npair = 0;
+    for (int b = blockIdx.x; b < nov; b += gridDim.x) {
+        const int blk = a.ovf[1 + b];
+        const int bzi = blk % nzb;
+        const int fy0 = ((blk / nzb) % nyb) * BX;
+        const int fx0 = (blk / (nzb * nyb)) * BX;
+        const int bxe = min(BX, a.F[0] - fx0), bye = min(BX, a.F[1] - fy0);
+        const int z0 = bzi * a.bz, z1 = min(a.F[2], z0 + a.bz);
+        for (int tc = 0; tc < bxe * bye; ++tc) {
+            const int cx = fx0 + tc / bye, cy = fy0 + tc % bye;
+            const int fc = (cx * a.F[1] + cy) * a.F[2];
+            const int i0 = a.start[fc + z0], i1 = a.start[fc + z1];
+            for (int i = i0 + warp; i < i1; i += nw) {
+                const double4 pi = a.xyzq[i];
+                // own slice of i: the cell whose range holds i
+                int cz = z0;
+                while (cz + 1 < z1 && a.start[fc + cz + 1] <= i) ++cz;
+                double u = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
+                if (lane < nfc) {
+                    int dx, dy;
+                    fwd_col(lane, M, dx, dy);
+                    const bool own = lane == nfc - 1;
+                    int gx = cx + dx, gy = cy + dy;
+                    const int ix = gx < 0 ? 0 : (gx >= a.F[0] ? 2 : 1);
+                    const int iy = gy < 0 ? 0 : (gy >= a.F[1] ? 2 : 1);
+                    gx += (1 - ix) * a.F[0];
+                    gy += (1 - iy) * a.F[1];
+                    for (int dz = own ? 0 : -Mz; dz <= Mz; ++dz) {
+                        int gz = cz + dz;
+                        const int iz = gz < 0 ? 0 : (gz >= a.F[2] ? 2 : 1);
+                        gz += (1 - iz) * a.F[2];
+                        const int t = (ix * 3 + iy) * 3 + iz;
+                        const int f = (gx * a.F[1] + gy) * a.F[2] + gz;
+                        int j0 = a.start[f];
+                        const int j1 = a.start[f + 1];
+                        if (own && dz == 0) j0 = i + 1;
+                        for (int j = j0; j < j1; ++j) {
+                            double4 g;
+                            if (pair_eval2<ND>(k, a.xyzq[j], shiftv[t][0], shiftv[t][1],
+                                               shiftv[t][2], pi.x, pi.y, pi.z, pi.w, u, fx, fy,
+                                               fz, g)) {
+                                ++npair;
+                                red_acc(a.acc, a.nacc, j, g.x, g.y, g.z, g.w);
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    u += __shfl_xor_sync(0xffffffffu, u, o);
+                    fx += __shfl_xor_sync(0xffffffffu, fx, o);
+                    fy += __shfl_xor_sync(0xffffffffu, fy, o);
+                    fz += __shfl_xor_sync(0xffffffffu, fz, o);
+                }
+                if (lane == 0) red_acc(a.acc, a.nacc, i, u, -pi.w * fx, -pi.w * fy, -pi.w * fz);
+            }
+        }
+    }
+    npair = __reduce_add_sync(0xffffffffu, npair);
+    if (lane == 0 && a.npairs && npair)
+        atomicAdd(a.npairs, 2ull * static_cast<unsigned long long>(npair));
+}
+
+// Planar pair-sorted accumulators -> (u_l, F_l) in the caller's order; the
+// accumulators are left zeroed for the next evaluation.
+__global__ void __launch_bounds__(256) k_acc_to_loc(long N, double* __restrict__ acc,
+                                                   const int* __restrict__ orig,
+                                                   double4* __restrict__ loc) {
+    const long j = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+    if (j >= N) return;
+    const double4 v = make_double4(acc[j], acc[N + j], acc[2 * N + j], acc[3 * N + j]);
+    acc[j] = 0.0;
+    acc[N + j] = 0.0;
+    acc[2 * N + j] = 0.0;
+    acc[3 * N + j] = 0.0;
+    loc[orig[j]] = v;
 }
 
 // ----------------------------------------------------------------------------
@@ -1505,6 +2004,7 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
     pair_warps_ = 4;
     pair_cap_ = 2048;
     if (const char* e = std::getenv("ESP_PAIR_CAP")) pair_cap_ = std::max(256, std::min(4096, std::atoi(e)));
+    if (const char* e = std::getenv("ESP_PAIR_HALF")) half_mode_ = std::atoi(e);
 }
 
 Engine::~Engine() {
@@ -1540,6 +2040,8 @@ Engine::~Engine() {
     dfree(d_fields_);
     dfree(d_qsum_);
     dfree(d_npairs_);
+    dfree(d_ovf_);
+    dfree(d_acc_);
     if (gexec_) cudaGraphExecDestroy(gexec_);
     if (gstream_) cudaStreamDestroy(gstream_);
     if (ev_gin_) cudaEventDestroy(ev_gin_);
@@ -1583,6 +2085,8 @@ void Engine::alloc_bins(int sub) {
 }
 
 void Engine::alloc_cells() {
+    dalloc(d_ovf_, ncellF_ + 1);  // half-shell K4 overflow list: at most one entry per block
+    ovf_cap_ = ncellF_ + 1;
     dalloc(d_countA_, ncellF_ + 1);
     dalloc(d_startA_, ncellF_ + 1);
     CK(cudaMemset(d_countA_, 0, sizeof(int) * (ncellF_ + 1)));
@@ -1645,6 +2149,8 @@ void Engine::ensure_capacity(long N) {
     dalloc(d_xyzqB_, c);
     dalloc(d_origB_, c);
     dalloc(d_loc_, c);
+    dalloc(d_acc_, 4 * c);  // half-shell K4 accumulators: zero at rest
+    CK(cudaMemset(d_acc_, 0, sizeof(double) * 4 * c));
     dalloc(d_epart_, grid1(c, 128) + 1);
     cap_ = c;
 }
@@ -1735,6 +2241,10 @@ void Engine::run_pair(long N, cudaStream_t s, int rank, int nranks, bool own_bin
         ++launches_;
         return;
     }
+    // half-shell K4 on the single-GPU path (tiny systems: the full-list kernel's
+    // single launch is faster); ESP_PAIR_HALF=0 never, 2 always
+    const bool half = half_mode_ == 2 || (half_mode_ == 1 && N >= kHalfMinN);
+    if (half && nranks == 1 && !own_bins && run_pair_half(N, s)) return;
     PairArgs a{};
     a.xyzq = d_xyzqA_;
     a.orig = d_origA_;
@@ -1830,6 +2340,113 @@ void Engine::run_pair(long N, cudaStream_t s, int rank, int nranks, bool own_bin
     }
     CK(cudaGetLastError());
     ++launches_;
+}
+
+// Half-shell K4 (k_pair_half) for the single-GPU evaluation.  Target block:
+// the most targets per CTA whose expected forward neighbourhood fits the
+// staging capacity while keeping >= 3 CTAs per SM in flight.  Returns false
+// (full-list kernel instead) when no block shape fits the period.
+bool Engine::run_pair_half(long N, cudaStream_t s) {
+    const Plan& p = plan_;
+    int nd = 20;
+    const PairConsts k = make_pair_consts(p, nd);
+    const double per_cell = static_cast<double>(N) / ncellF_;
+    const int M = pM_, Mz = pMz_;
+    int sms = 148;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
+    int best_bx = 0, best_bz = 0, best_cap = 0;
+    double best_t = -1.0;
+    const long want_blocks = 3L * 2 * sms;  // 2 CTAs per SM, 3 waves
+    int cap_max = 4096;
+    if (const char* e = std::getenv("ESP_HALF_CAP")) cap_max = std::max(256, std::min(8192, std::atoi(e)));
+    for (int bx = 1; bx <= kHalfMaxBX; ++bx)
+        for (int bz : {2, 3, 4, 6, 8}) {
+            if (F_[0] < bx + 2 * M || F_[1] < bx + 2 * M || F_[2] < bz + 2 * Mz) continue;
+            const double staged = per_cell * (bx + M) * (bx + 2 * M) * (bz + 2 * Mz);
+            const int cap = (static_cast<int>(staged * 1.15 + 6.0 * std::sqrt(staged) + 64.0) + 31) / 32 * 32;
+            if (cap > cap_max) continue;
+            const long nblocks = static_cast<long>((F_[0] + bx - 1) / bx) * ((F_[1] + bx - 1) / bx) *
+                                 ((F_[2] + bz - 1) / bz);
+            const double tgt = per_cell * bx * bx * bz;
+            // prefer enough blocks to fill the GPU, then the most targets per block
+            const double score = (nblocks >= want_blocks ? 1e9 : 0.0) + tgt;
+            if (score > best_t) {
+                best_t = score;
+                best_bx = bx;
+                best_bz = bz;
+                best_cap = cap;
+            }
+        }
+    if (const char* e = std::getenv("ESP_HALF_BLOCK")) {  // "bx,bz" (experiments)
+        int bx = 0, bz = 0;
+        if (std::sscanf(e, "%d,%d", &bx, &bz) == 2 && bx >= 1 && bx <= kHalfMaxBX && bz >= 1 &&
+            F_[0] >= bx + 2 * M && F_[1] >= bx + 2 * M && F_[2] >= bz + 2 * Mz) {
+            const double staged = per_cell * (bx + M) * (bx + 2 * M) * (bz + 2 * Mz);
+            best_cap = std::min(cap_max, (static_cast<int>(staged * 1.15 + 6.0 * std::sqrt(staged) + 64.0) + 31) / 32 * 32);
+            best_bx = bx;
+            best_bz = bz;
+        }
+    }
+    if (best_bx == 0) return false;
+    HalfArgs a{};
+    a.xyzq = d_xyzqA_;
+    a.orig = d_origA_;
+    a.start = d_startA_;
+    a.acc = d_acc_;
+    a.nacc = N;
+    a.npairs = d_npairs_;
+    for (int d = 0; d < 3; ++d) {
+        a.F[d] = F_[d];
+        a.fw[d] = p.box[d] / F_[d];
+        a.box[d] = p.box[d];
+    }
+    a.M = M;
+    a.Mz = Mz;
+    a.bx = best_bx;
+    a.bz = best_bz;
+    a.cap = best_cap;
+    {
+        // forward list per target: about half the full-list estimate
+        const double ppa = static_cast<double>(N) / (p.box[0] * p.box[1] * p.box[2]) * 4.0 / 3.0 *
+                           kPi * p.r_c * p.r_c * p.r_c;
+        const double cand = ppa * (col_div_ == 3 ? 1.8 : 2.2) * 0.6;
+        int l = std::max(128, std::min(1024, (static_cast<int>(cand) + 63) / 64 * 64));
+        if (const char* e = std::getenv("ESP_PAIR_LCAP")) l = std::max(128, std::min(2048, std::atoi(e) / 2 * 2));
+        a.lcap = std::min(l, a.cap) + 32;
+    }
+    a.nent_max = (a.bx + M) * (a.bx + 2 * M) * (a.bz + 2 * Mz);
+    const long nblocks = static_cast<long>((F_[0] + a.bx - 1) / a.bx) *
+                         ((F_[1] + a.bx - 1) / a.bx) * ((F_[2] + a.bz - 1) / a.bz);
+    if (N >= (1L << 27)) throw InvalidArgument("pair kernel: N must be < 2^27");
+    if (nblocks + 1 > ovf_cap_) return false;  // sized in alloc_cells (no allocation under capture)
+    a.ovf = d_ovf_;
+    CK(cudaMemsetAsync(d_ovf_, 0, sizeof(int), s));
+    size_t sm = (a.cap + 1) * sizeof(float4) +
+                kHalfWarps * 64 * sizeof(int) + kHalfWarps * a.lcap * sizeof(unsigned short);
+    sm = (sm + 3) / 4 * 4 + (2 * a.nent_max + 1) * sizeof(int) + a.nent_max;
+    const int ovf_grid = 2 * sms;
+    auto go = [&](auto kern, auto ovfk) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(sm)));
+        kern<<<static_cast<unsigned>(nblocks), kHalfThreads, sm, s>>>(a, k);
+        CK(cudaGetLastError());
+        ovfk<<<ovf_grid, 256, 0, s>>>(a, k);
+        CK(cudaGetLastError());
+        k_acc_to_loc<<<grid1(N, 256), 256, 0, s>>>(N, d_acc_, d_origA_, d_loc_);
+        CK(cudaGetLastError());
+    };
+    switch (nd) {
+        case 14: go(k_pair_half<14>, k_pair_half_ovf<14>); break;
+        case 15: go(k_pair_half<15>, k_pair_half_ovf<15>); break;
+        case 16: go(k_pair_half<16>, k_pair_half_ovf<16>); break;
+        case 17: go(k_pair_half<17>, k_pair_half_ovf<17>); break;
+        case 18: go(k_pair_half<18>, k_pair_half_ovf<18>); break;
+        case 20: go(k_pair_half<20>, k_pair_half_ovf<20>); break;
+        case 28: go(k_pair_half<28>, k_pair_half_ovf<28>); break;
+        default: go(k_pair_half<kMaxPoly>, k_pair_half_ovf<kMaxPoly>); break;
+    }
+    launches_ += 3;
+    return true;
 }
 
 void Engine::run_spread(long N, cudaStream_t s, int rank, int nranks, double* grid,

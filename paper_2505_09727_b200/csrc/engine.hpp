@@ -145,6 +145,7 @@ private:
     void alloc_bins(int sub);
     void prepare(long N, const double* pos, const double* q, double* qsum_dev, cudaStream_t s);
     void run_pair(long N, cudaStream_t s, int rank, int nranks, bool own_bins = false);
+    bool run_pair_half(long N, cudaStream_t s);
     void run_grid(long N, cudaStream_t s, StageTimes* t);
     void run_spread(long N, cudaStream_t s, int rank, int nranks, double* grid,
                     const GridArgs* gslab = nullptr, long nreals = -1, int b0 = -1,
@@ -210,6 +211,10 @@ private:
     double* d_fields_ = nullptr;        // nfields * M
     double* d_qsum_ = nullptr;          // scratch for neutrality sums
     unsigned long long* d_npairs_ = nullptr;
+    int* d_ovf_ = nullptr;
+    double* d_acc_ = nullptr;           // half-shell K4: planar pair-sorted (u, F) sums, 4 x cap_              // half-shell K4: overflowed blocks (count, ids)
+    long ovf_cap_ = 0;
+    int half_mode_ = 1;                 // half-shell K4: 0 never, 1 from kHalfMinN atoms, 2 always (ESP_PAIR_HALF)
 
     cufftHandle fwd_ = 0, inv_ = 0;
     // distributed-FFT plans, built for one (rank, nranks) at a time
