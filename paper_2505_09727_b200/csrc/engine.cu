@@ -316,6 +316,7 @@ struct PairConsts {
     float rc2_test;    // fp32 screening radius^2 (superset of the exact test)
     int pad;
     double H[kMaxPoly];  // Psi(y)/y = sum H_k z^k, z = 2y^2 - 1 (chi from dH/dz)
+    double Hs[kMaxPoly];  // H_k / r_c (half-shell kernel, 4 pi-scaled form)
 };
 
 struct PairArgs {
@@ -802,7 +803,12 @@ constexpr int kHalfMaxBX = 4;
 constexpr int kHalfWarps = 8;
 constexpr int kHalfThreads = 32 * kHalfWarps;
 
-// (u, F) terms of one pair from both sides; returns false out of range.
+// (u, F) terms of one pair from both sides, scaled by 4 pi (the caller applies
+// 1/(4 pi) once per atom); returns false out of range.  With Hs = H / r_c and
+// Gs = chi / r_c (coefficients pre-scaled, PairConsts::Hs):
+//   4 pi S(r)      = (1 - y H) / r       = 1/r - Hs
+//   4 pi (-dS/dr)  = chi/(r_c r) + 4 pi S / r = (Gs + 4 pi S) / r
+// which drops y = r / r_c, w = 1/(4 pi r) and two products from every pair.
 template <int ND>
 __device__ __forceinline__ bool pair_eval2(const PairConsts& k, double4 pj, double sx, double sy,
                                            double sz, double xi, double yi, double zi, double qi,
@@ -821,19 +827,17 @@ __device__ __forceinline__ bool pair_eval2(const PairConsts& k, double4 pj, doub
         rinv = fma(rinv, e, rinv);
     }
     const double z = fma(r2, k.two_irc2, -1.0);
-    double H = k.H[ND - 1], dH = 0.0;
+    double H = k.Hs[ND - 1], dH = 0.0;
 #pragma unroll
     for (int m = ND - 2; m >= 0; --m) {
         dH = fma(dH, z, H);
-        H = fma(H, z, k.H[m]);
+        H = fma(H, z, k.Hs[m]);
     }
-    const double G = fma(2.0 * (z + 1.0), dH, H);
-    const double y = r2 * rinv * k.irc;
-    const double w = k.inv4pi * rinv;
-    const double pot = (1.0 - y * H) * w;
-    const double fr = fma(G * w, k.irc, pot * rinv);
+    const double G = fma(fma(2.0, z, 2.0), dH, H);  // chi / r_c
+    const double pot = rinv - H;                     // 4 pi S
+    const double c0 = (G + pot) * (rinv * rinv);     // 4 pi (-dS/dr) / r
     u = fma(pj.w, pot, u);
-    const double c = pj.w * fr * rinv;
+    const double c = pj.w * c0;
     fx = fma(c, dx, fx);
     fy = fma(c, dy, fy);
     fz = fma(c, dz, fz);
@@ -881,6 +885,8 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
     __shared__ double shiftv[27][3];
     __shared__ int tbeg[kHalfMaxBX * kHalfMaxBX], tpre[kHalfMaxBX * kHalfMaxBX + 1];
     __shared__ int tnext;  // next unassigned target
+    __shared__ int tcxy[kHalfMaxBX * kHalfMaxBX];  // target column -> tx | ty << 8
+    __shared__ int fwdc[64];  // l -> forward column (l mod nfc): dx | (dy + M) << 4 | own << 8
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int* qw = qall + warp * 64;
@@ -907,6 +913,13 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
         shiftv[t][0] = (t / 9 - 1) * a.box[0];
         shiftv[t][1] = ((t / 3) % 3 - 1) * a.box[1];
         shiftv[t][2] = (t % 3 - 1) * a.box[2];
+    }
+    if (threadIdx.x >= 64 && threadIdx.x < 128) {
+        const int nfc = M * (2 * M + 1) + M + 1;
+        const int l = (threadIdx.x - 64) % nfc;
+        int dx, dy;
+        fwd_col(l, M, dx, dy);
+        fwdc[threadIdx.x - 64] = dx | ((dy + M) << 4) | ((l == nfc - 1) << 8);
     }
     for (int e = threadIdx.x; e < nent; e += blockDim.x) {
         const int col = e / nsl, sl = e - col * nsl;
@@ -962,10 +975,12 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
         int accn = 0;
         const int ntc = bxe * bye;
         for (int c = 0; c < ntc; ++c) {
-            const int col = (c / bye) * Wy + M + c % bye;
+            const int tx = c / bye, ty = M + c % bye;
+            const int col = tx * Wy + ty;
             const int b = ent_off[col * nsl + Mz], e = ent_off[col * nsl + Mz + bze];
             tbeg[c] = b;
             tpre[c] = accn;
+            tcxy[c] = tx | (ty << 8);
             accn += e - b;
         }
         tpre[ntc] = accn;
@@ -1008,23 +1023,23 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
 
     for (int ii = warp;;) {
         if (ii >= ni) break;
-        int tc = 0;
-        while (tc + 1 < ntc && ii >= tpre[tc + 1]) ++tc;
+        // target column: the last column starting at or before ii (empty
+        // columns repeat the next one's start and are skipped by the count)
+        const int tc = __popc(__ballot_sync(0xffffffffu, lane >= 1 && lane < ntc && tpre[lane] <= ii));
         const int si = tbeg[tc] + (ii - tpre[tc]);
         const float4 ci = cand[si];
         const int gi = __float_as_int(ci.w) & 0x7ffffff;
         const double4 pi = a.xyzq[gi];
         const float xf = ci.x, yf = ci.y, zf = ci.z;
-        const int tx = tc / bye, ty = M + tc % bye;
+        const int txy = tcxy[tc];
+        const int tx = txy & 0xff, ty = txy >> 8;
         int beg = 0, cnt = 0;
         if (lane < nfc) {
             // rotated column order per target: warps working on neighbouring
-            // targets then walk their (shared) neighbours in different orders,
-            // which keeps their CAS adds on the accumulators apart
-            int lc = lane + 5 * ii;
-            lc -= nfc * (lc / nfc);
-            int dx, dy;
-            fwd_col(lc, M, dx, dy);
+            // targets walk their (shared) neighbours in different orders, which
+            // spreads their REDs over the accumulators
+            const int fc = fwdc[lane + ((5 * ii) & 31)];
+            const int dx = fc & 15, dy = ((fc >> 4) & 15) - M;
             const int ca = tx + dx, cb = ty + dy;
             const int col = ca * Wy + cb;
             const float x0 = ca * fwx, y0 = (cb - M) * fwy;
@@ -1039,7 +1054,7 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
                 khi = max(0, min(nsl - 1, khi));
                 int lo = ent_off[col * nsl + klo];
                 const int hi = ent_off[col * nsl + khi + 1];
-                if (lc == nfc - 1) lo = si + 1;  // own column: after i
+                if (fc >> 8) lo = si + 1;  // own column: after i
                 if (hi > lo) {
                     beg = lo;
                     cnt = hi - lo;
@@ -1135,7 +1150,7 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
             w += __shfl_xor_sync(0xffffffffu, w, 2);
             w += __shfl_xor_sync(0xffffffffu, w, 1);
             if ((lane & 7) == 0) {
-                const int comp = lane >> 3;  // 0 u, 1 Fx, 2 Fy, 3 Fz
+                const int comp = lane >> 3;  // 0 u, 1 Fx, 2 Fy, 3 Fz (4 pi-scaled, as acc)
                 atomicAdd(a.acc + comp * a.nacc + gi, comp == 0 ? w : -pi.w * w);
             }
         }
@@ -1231,14 +1246,15 @@ __global__ void __launch_bounds__(256) k_pair_half_ovf(HalfArgs a, const __grid_
         atomicAdd(a.npairs, 2ull * static_cast<unsigned long long>(npair));
 }
 
-// Planar pair-sorted accumulators -> (u_l, F_l) in the caller's order; the
-// accumulators are left zeroed for the next evaluation.
+// Planar pair-sorted accumulators (4 pi-scaled) -> (u_l, F_l) in the caller's
+// order; the accumulators are left zeroed for the next evaluation.
 __global__ void __launch_bounds__(256) k_acc_to_loc(long N, double* __restrict__ acc,
                                                    const int* __restrict__ orig,
                                                    double4* __restrict__ loc) {
     const long j = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
     if (j >= N) return;
-    const double4 v = make_double4(acc[j], acc[N + j], acc[2 * N + j], acc[3 * N + j]);
+    constexpr double s = 1.0 / (4.0 * kPi);
+    const double4 v = make_double4(s * acc[j], s * acc[N + j], s * acc[2 * N + j], s * acc[3 * N + j]);
     acc[j] = 0.0;
     acc[N + j] = 0.0;
     acc[2 * N + j] = 0.0;
@@ -1853,8 +1869,10 @@ PairConsts make_pair_consts(const Plan& p, int& nd) {
     nd = n <= 14 ? 14 : n <= 15 ? 15 : n <= 16 ? 16 : n <= 17 ? 17 : n <= 18 ? 18 : n <= 20 ? 20
                                                                                    : n <= 28 ? 28
                                                                                              : kMaxPoly;
-    for (int i = 0; i < kMaxPoly; ++i)
+    for (int i = 0; i < kMaxPoly; ++i) {
         k.H[i] = i < n ? p.pair_H[i] : 0.0;
+        k.Hs[i] = k.H[i] / p.r_c;
+    }
     return k;
 }
 

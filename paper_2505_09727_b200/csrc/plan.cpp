@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <functional>
 #include <limits>
 #include <thread>
@@ -741,6 +742,14 @@ Plan build_plan(const std::array<double, 3>& box, Family family, double eps, dou
         // Smallest degree meeting 2e-15 on Psi and 2e-14 * max|chi| on chi.
         double gmax = 0.0;
         for (int i = 0; i <= 400; ++i) gmax = std::max(gmax, std::fabs(G(i / 400.0)));
+        double fit_psi = 2e-15, fit_chi = 2e-14;
+        if (const char* e = std::getenv("ESP_PAIR_FIT")) {  // experiments: scale both targets
+            const double f = std::atof(e);
+            if (f > 0.0) {
+                fit_psi *= f;
+                fit_chi *= f;
+            }
+        }
         for (int deg = 6;; ++deg) {
             p.pair_H = fit_z_poly_ld(Hzl, deg);
             double epsi = 0.0, echi = 0.0;
@@ -755,7 +764,7 @@ Plan build_plan(const std::array<double, 3>& box, Family family, double eps, dou
                 echi = std::max(echi, std::fabs(hv + 2.0 * (z + 1.0) * dh - G(y)));
             }
             p.pair_fit_err = std::max(epsi, echi / std::max(1.0, gmax));
-            if ((epsi <= 2e-15 && echi <= 2e-14 * std::max(1.0, gmax)) || deg >= 39) break;
+            if ((epsi <= fit_psi && echi <= fit_chi * std::max(1.0, gmax)) || deg >= 39) break;
         }
         p.pair_G.clear();
     }
