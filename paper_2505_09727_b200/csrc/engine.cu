@@ -2374,7 +2374,7 @@ bool Engine::run_pair_half(long N, cudaStream_t s) {
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
     int best_bx = 0, best_bz = 0, best_cap = 0;
     double best_t = -1.0;
-    const long want_blocks = 3L * 2 * sms;  // 2 CTAs per SM, 3 waves
+    const long want_blocks = 2L * 3 * sms;  // 3 CTAs per SM, 2 waves
     int cap_max = 4096;
     if (const char* e = std::getenv("ESP_HALF_CAP")) cap_max = std::max(256, std::min(8192, std::atoi(e)));
     for (int bx = 1; bx <= kHalfMaxBX; ++bx)
@@ -2386,8 +2386,11 @@ bool Engine::run_pair_half(long N, cudaStream_t s) {
             const long nblocks = static_cast<long>((F_[0] + bx - 1) / bx) * ((F_[1] + bx - 1) / bx) *
                                  ((F_[2] + bz - 1) / bz);
             const double tgt = per_cell * bx * bx * bz;
-            // prefer enough blocks to fill the GPU, then the most targets per block
-            const double score = (nblocks >= want_blocks ? 1e9 : 0.0) + tgt;
+            // prefer enough blocks to fill the GPU (>= 2 waves of 3 CTAs per
+            // SM), then ~140 targets per block (measured optimum across cfg2-5:
+            // staging amortised, dynamic target assignment still balanced)
+            const double score = (nblocks >= want_blocks ? 1e9 : 0.0) +
+                                 (nblocks >= want_blocks ? -std::fabs(std::log(tgt / 140.0)) : tgt);
             if (score > best_t) {
                 best_t = score;
                 best_bx = bx;
