@@ -313,7 +313,9 @@ def run_ours(args):
             traffic = tr.get(args.workload)
         except Exception:
             traffic = None
-    roofline = {"bound": "fp64", "kernel": "k_pair (K4 real-space pair sum)",
+    kname = ("k_pair_half (K4 real-space pair sum, half-shell: each unordered pair once)"
+             if N >= 4096 else "k_pair (K4 real-space pair sum, full lists)")
+    roofline = {"bound": "fp64", "kernel": kname,
                 "achieved": achieved, "peak": peak64, "unit": "TFLOP/s",
                 "frac": achieved / peak64 if peak64 > 0 else None, "traffic": traffic,
                 "peak_source": "fp64 DFMA microbenchmark measured in this run "
@@ -321,11 +323,12 @@ def run_ours(args):
                 "work": f"{FLOPS_PER_UNORDERED_PAIR} flops x {ordered_pairs // 2} unordered "
                         "in-range pairs (counted on device)",
                 "kernel_ms": stages_ms["local"],
-                "limiter": "instruction issue (~60 % of issue slots active, profiles/r01_full_cfg2.md): "
-                           "the neighbour search (per-target column ranges, fp32 screening, ballot "
-                           "compaction) is ~50 % of K4's instructions; the fp64 evaluation alone "
-                           "reaches 38 % of the fp64 peak (esp_pair_eval_rate), and each unordered "
-                           "pair is evaluated from both sides, as in the reference"}
+                "limiter": "instruction issue and fp64 dependency latency (profiles/r01_full_cfg*.md): "
+                           "the fp64 rounds (~68 fp64 ops per pair, both sides' terms) run at "
+                           "~2x the issue rate they need, while the neighbour search (forward "
+                           "columns, list, fp32 screen, ballot compaction) and the last partial "
+                           "round per target take ~40 % of the instructions; the partner terms go "
+                           "to L2 as fire-and-forget fp64 REDs"}
 
     # ---- e2e through the public API on pinned host buffers
     pos_h = torch.from_numpy(pos).pin_memory().numpy()

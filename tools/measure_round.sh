@@ -16,7 +16,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --no-cpu-baseline > gpurun_out/${R}_ncu_launch.log 2>&1
 for w in cfg2 cfg4 cfg5; do
   ESP_GRAPH=0 timeout 900 ncu --set full --import-source on --clock-control none \
-    -k regex:"k_pair|k_spread|k_interp" -s 3 -c 3 -o gpurun_out/${R}_full_$w \
+    -k regex:"^k_pair_half$|k_spread|k_interp" -s 3 -c 3 -o gpurun_out/${R}_full_$w \
     python tools/run_eval.py --workload $w --reps 2 > gpurun_out/${R}_ncu_full_$w.log 2>&1
 done
 echo done
