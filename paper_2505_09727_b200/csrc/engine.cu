@@ -65,7 +65,7 @@ namespace {
 
 constexpr double kPi = 3.14159265358979323846;
 constexpr int kNc = 13;        // coefficients per window piece (degree 12)
-constexpr long kSubDiv4MinN = 1L << 17;  // 4^3 sort sub-bins per spread bin from here, else 2^3
+constexpr long kSubDivCellMinN = 1L << 17;  // sort by grid cell inside a spread bin from here, else 2^3 sub-bins
 constexpr long kHighPriorityMaxN = 1L << 19;  // grid pipeline on the high-priority stream
 constexpr int kColDivDefault = 2;
 constexpr double kColDiv3MinPairs = 300.0;  // r_c/3 columns: enough pairs per target
@@ -189,8 +189,9 @@ __global__ void __launch_bounds__(256) k_fold_bin(BinArgs a) {
         a.cellA[i] = c;
         a.rankA[i] = atomicAdd(&a.countA[c], 1);
         // spread bin: S grid cells per side, by floor(x/h); atoms are ordered
-        // by bin and, inside a bin, by its 2x2x2 sub-bins (neighbouring K3
-        // threads then gather overlapping footprints)
+        // by bin and, inside a bin, by its sub-bins (large systems: single grid
+        // cells), z fastest: neighbouring K3 threads then gather overlapping
+        // footprint rows (a Morton order of the sub-bins was measured slower)
         const int lx = static_cast<int>(floor(x / a.h[0]));
         const int ly = static_cast<int>(floor(y / a.h[1]));
         const int lz = static_cast<int>(floor(z / a.h[2]));
@@ -2138,7 +2139,10 @@ void Engine::reconfigure(long N) {
             pair_lcap_ = std::max(128, std::min(2048, std::atoi(e) / 2 * 2));
     }
     // finer sort sub-bins for large systems: better K3 locality, more keys
-    const int want_sub = N >= kSubDiv4MinN ? 4 : 2;
+    // sort sub-bins: single grid cells for large systems (K3 cfg5 4.66 -> 3.50
+    // ms, cfg3 0.41 -> 0.32 ms; the finer counting sort costs ~0.35 ms at cfg5)
+    int want_sub = N >= kSubDivCellMinN ? S_ : 2;
+    if (const char* e = std::getenv("ESP_SORT_SUB")) want_sub = std::max(1, std::min(S_, std::atoi(e)));
     if (want == col_div_ && want_sub == sub_) return;
     CK(cudaDeviceSynchronize());
     if (gexec_) {
