@@ -71,6 +71,10 @@ constexpr int kColDivDefault = 2;
 constexpr double kColDiv3MinPairs = 300.0;  // r_c/3 columns: enough pairs per target
 constexpr int kMaxPoly = 40;   // max pair-polynomial coefficients
 constexpr long kHalfMinN = 4096;  // half-shell K4 from this many atoms
+#ifndef ESP_PAIR_SPLIT
+#define ESP_PAIR_SPLIT 1
+#endif
+constexpr bool kPairSplit = ESP_PAIR_SPLIT;  // even/odd Horner chains in the half-shell kernel
 
 // ----------------------------------------------------------------------------
 // small device helpers
@@ -318,6 +322,10 @@ struct PairConsts {
     int pad;
     double H[kMaxPoly];  // Psi(y)/y = sum H_k z^k, z = 2y^2 - 1 (chi from dH/dz)
     double Hs[kMaxPoly];  // H_k / r_c (half-shell kernel, 4 pi-scaled form)
+    // even/odd split of Hs and dHs/dz in w = z^2 (four independent Horner
+    // chains of ~ND/2 instead of two of ND): Hs = He(w) + z Ho(w),
+    // dHs/dz = De(w) + z Do(w)
+    double He[kMaxPoly / 2 + 1], Ho[kMaxPoly / 2 + 1], De[kMaxPoly / 2 + 1], Do[kMaxPoly / 2 + 1];
 };
 
 struct PairArgs {
@@ -828,11 +836,30 @@ __device__ __forceinline__ bool pair_eval2(const PairConsts& k, double4 pj, doub
         rinv = fma(rinv, e, rinv);
     }
     const double z = fma(r2, k.two_irc2, -1.0);
-    double H = k.Hs[ND - 1], dH = 0.0;
+    double H, dH;
+    if (kPairSplit) {
+        // Hs has ND coefficients (degree ND-1): He ceil(ND/2), Ho floor(ND/2),
+        // De floor(ND/2) (odd k >= 1), Do ceil(ND/2)-1 (even k >= 2)
+        constexpr int NE = (ND + 1) / 2, NO = ND / 2, NDE = ND / 2, NDO = (ND + 1) / 2 - 1;
+        const double w = z * z;
+        double he = k.He[NE - 1], ho = k.Ho[NO - 1], de = k.De[NDE - 1], dO = k.Do[NDO - 1];
 #pragma unroll
-    for (int m = ND - 2; m >= 0; --m) {
-        dH = fma(dH, z, H);
-        H = fma(H, z, k.Hs[m]);
+        for (int m = NE - 2; m >= 0; --m) {
+            he = fma(he, w, k.He[m]);
+            if (m < NO - 1) ho = fma(ho, w, k.Ho[m]);
+            if (m < NDE - 1) de = fma(de, w, k.De[m]);
+            if (m < NDO - 1) dO = fma(dO, w, k.Do[m]);
+        }
+        H = fma(z, ho, he);
+        dH = fma(z, dO, de);
+    } else {
+        H = k.Hs[ND - 1];
+        dH = 0.0;
+#pragma unroll
+        for (int m = ND - 2; m >= 0; --m) {
+            dH = fma(dH, z, H);
+            H = fma(H, z, k.Hs[m]);
+        }
     }
     const double G = fma(fma(2.0, z, 2.0), dH, H);  // chi / r_c
     const double pot = rinv - H;                     // 4 pi S
@@ -1873,6 +1900,13 @@ PairConsts make_pair_consts(const Plan& p, int& nd) {
     for (int i = 0; i < kMaxPoly; ++i) {
         k.H[i] = i < n ? p.pair_H[i] : 0.0;
         k.Hs[i] = k.H[i] / p.r_c;
+    }
+    for (int j = 0; j <= kMaxPoly / 2; ++j) {
+        const int e = 2 * j, o = 2 * j + 1;
+        k.He[j] = e < kMaxPoly ? k.Hs[e] : 0.0;
+        k.Ho[j] = o < kMaxPoly ? k.Hs[o] : 0.0;
+        k.De[j] = o < kMaxPoly ? o * k.Hs[o] : 0.0;       // z^(o-1) = w^j
+        k.Do[j] = e + 2 < kMaxPoly ? (e + 2) * k.Hs[e + 2] : 0.0;  // z^(e+1) = z w^j
     }
     return k;
 }
