@@ -28,7 +28,7 @@ NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-pthread",
           "-I" + os.path.join(ROOT, "include")]
-SOURCES = ["plan.cpp", "engine.cu", "direct.cu", "capi.cpp"]
+SOURCES = ["plan.cpp", "plan_device.cu", "engine.cu", "direct.cu", "capi.cpp"]
 HEADERS = ["plan.hpp", "engine.hpp", "direct.hpp", os.path.join("..", "..", "include", "esp_b200.h")]
 
 

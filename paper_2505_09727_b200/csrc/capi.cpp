@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -182,10 +183,6 @@ int esp_plan_create(const double box[3], int family, double eps, double r_c,
             o.allow_degraded = ov->allow_degraded != 0;
         }
         auto h = std::make_unique<esp_plan>();
-        h->plan = espb::build_plan({box[0], box[1], box[2]},
-                                   family == ESP_FAMILY_GAUSSIAN ? espb::Family::gaussian
-                                                                 : espb::Family::pswf,
-                                   eps, r_c, o);
         if (device >= 0) {
             int n = 0;
             if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
@@ -193,6 +190,17 @@ int esp_plan_create(const double box[3], int family, double eps, double r_c,
                 throw espb::CudaError("no CUDA device available");
             }
             if (device >= n) throw espb::InvalidArgument("device index out of range");
+        }
+        // the O(n_f^3) plan tables on the plan's device;
+        // ESP_PLAN_DEVICE=0 keeps them on the host
+        std::unique_ptr<espb::PlanDevice> pdev;
+        const char* pd = std::getenv("ESP_PLAN_DEVICE");
+        if (device >= 0 && !(pd && std::atoi(pd) == 0)) pdev = espb::make_plan_device(device);
+        h->plan = espb::build_plan({box[0], box[1], box[2]},
+                                   family == ESP_FAMILY_GAUSSIAN ? espb::Family::gaussian
+                                                                 : espb::Family::pswf,
+                                   eps, r_c, o, pdev.get());
+        if (device >= 0) {
             h->device = device;
             h->eng = std::make_unique<espb::Engine>(h->plan, device);
         }

@@ -11,7 +11,9 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <functional>
 #include <limits>
@@ -614,21 +616,40 @@ Slabs alias_slabs(const Octant& o, const std::array<int, 3>& nf) {
         if (nf[d] % 2 == 0) mult[d][nf[d] / 2] = 1.0;
         if (nf[d] == 1) mult[d][0] = 1.0;
     }
-    // per-|k| marginals
+    // per-|k| marginals, long double; the ax range is split into fixed
+    // chunks whose partial sums are combined in chunk order (deterministic)
     std::array<std::vector<long double>, 3> marg;
     for (int d = 0; d < 3; ++d) marg[d].assign(o.half[d], 0.0L);
     long double den = 0.0L;
-    for (int ax = 0; ax < o.half[0]; ++ax)
-        for (int ay = 0; ay < o.half[1]; ++ay)
-            for (int az = 0; az < o.half[2]; ++az) {
-                double xi2 = (o.f2[0][ax] + o.f2[1][ay]) + o.f2[2][az];
-                if (xi2 == 0.0) continue;
-                long double g = std::fabs(o.at(ax, ay, az)) / xi2;
-                den += g * mult[0][ax] * mult[1][ay] * mult[2][az];
-                marg[0][ax] += g * mult[1][ay] * mult[2][az];
-                marg[1][ay] += g * mult[0][ax] * mult[2][az];
-                marg[2][az] += g * mult[0][ax] * mult[1][ay];
-            }
+    const int nchunk = std::min(o.half[0], 32);
+    std::vector<std::array<std::vector<long double>, 3>> pm(nchunk);
+    std::vector<long double> pden(nchunk, 0.0L);
+    par_for(nchunk, [&](int cb, int ce) {
+        for (int c = cb; c < ce; ++c) {
+            auto& m = pm[c];
+            for (int d = 0; d < 3; ++d) m[d].assign(o.half[d], 0.0L);
+            const int ax0 = static_cast<int>(static_cast<long>(o.half[0]) * c / nchunk);
+            const int ax1 = static_cast<int>(static_cast<long>(o.half[0]) * (c + 1) / nchunk);
+            long double dsum = 0.0L;
+            for (int ax = ax0; ax < ax1; ++ax)
+                for (int ay = 0; ay < o.half[1]; ++ay)
+                    for (int az = 0; az < o.half[2]; ++az) {
+                        double xi2 = (o.f2[0][ax] + o.f2[1][ay]) + o.f2[2][az];
+                        if (xi2 == 0.0) continue;
+                        long double g = std::fabs(o.at(ax, ay, az)) / xi2;
+                        dsum += g * mult[0][ax] * mult[1][ay] * mult[2][az];
+                        m[0][ax] += g * mult[1][ay] * mult[2][az];
+                        m[1][ay] += g * mult[0][ax] * mult[2][az];
+                        m[2][az] += g * mult[0][ax] * mult[1][ay];
+                    }
+            pden[c] = dsum;
+        }
+    });
+    for (int c = 0; c < nchunk; ++c) {
+        den += pden[c];
+        for (int d = 0; d < 3; ++d)
+            for (int i = 0; i < o.half[d]; ++i) marg[d][i] += pm[c][d][i];
+    }
     Slabs s;
     s.den = static_cast<double>(den);
     for (int d = 0; d < 3; ++d) {
@@ -651,8 +672,22 @@ double aliasing(const Slabs& s, const std::array<int, 3>& nf,
 
 }  // namespace
 
+namespace {
+// ESP_PLAN_TIMING=1: stage times of build_plan on stderr (diagnostics)
+std::chrono::steady_clock::time_point g_plan_t0;
+void plan_stage(const char* name) {
+    static const bool on = std::getenv("ESP_PLAN_TIMING") != nullptr;
+    if (!on) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "plan %-14s %8.3f ms\n", name,
+                 std::chrono::duration<double, std::milli>(t - g_plan_t0).count());
+    g_plan_t0 = t;
+}
+}  // namespace
+
 Plan build_plan(const std::array<double, 3>& box, Family family, double eps, double r_c,
-                const Overrides& ov) {
+                const Overrides& ov, PlanDevice* dev) {
+    g_plan_t0 = std::chrono::steady_clock::now();
     if (!(eps >= 1e-5 && eps <= 1e-3))
         throw InvalidArgument("build_plan: eps out of supported range [1e-5, 1e-3]");
     const double Lmin = std::min({box[0], box[1], box[2]});
@@ -695,6 +730,7 @@ Plan build_plan(const std::array<double, 3>& box, Family family, double eps, dou
     }
     p.self_coef = p.chi0 / (4.0 * kPi * r_c);
 
+    plan_stage("split");
     // --- pair-kernel polynomials in z = 2y^2 - 1 (device K4)
     {
         std::function<double(double)> G, H;  // exact chi(y) and Psi(y)/y
@@ -769,6 +805,7 @@ Plan build_plan(const std::array<double, 3>& box, Family family, double eps, dou
         p.pair_G.clear();
     }
 
+    plan_stage("pairpoly");
     // --- parameter selection (ewald.hpp:236-330)
     p.P = ov.P > 0 ? ov.P : (gauss ? 5 : default_order(eps));
     if (p.P < 3 || p.P > 16) throw InvalidArgument("select_parameters: P out of range [3,16]");
@@ -805,10 +842,28 @@ Plan build_plan(const std::array<double, 3>& box, Family family, double eps, dou
         });
     }
 
+    plan_stage("prolate-cands");
     Octant oct;
     for (int step = 0;; ++step) {
-        oct = build_octant(p, nf);
+        if (dev) {
+            // the octant on the device: same |k| tables, chihat per point there
+            oct.val.clear();
+            for (int d = 0; d < 3; ++d) {
+                oct.half[d] = nf[d] / 2 + 1;
+                oct.f2[d].resize(oct.half[d]);
+                for (int k = 0; k < oct.half[d]; ++k) {
+                    const double xi = 2.0 * kPi * k / p.box[d];
+                    oct.f2[d][k] = xi * xi;
+                }
+            }
+            p.nf = nf;
+            dev->octant(p, oct.f2, oct.val);
+        } else {
+            oct = build_octant(p, nf);
+        }
+        plan_stage("  octant");
         Slabs sl = alias_slabs(oct, nf);
+        plan_stage("  slabs");
         double ea = std::numeric_limits<double>::infinity(), esi = 0.0;
         double c1best = std::numeric_limits<double>::quiet_NaN();
         if (gauss) {
@@ -855,6 +910,7 @@ Plan build_plan(const std::array<double, 3>& box, Family family, double eps, dou
             if (box[d] / nf[d] >= hmax * (1.0 - 1e-12)) nf[d] = next_even_5smooth(nf[d] + 1.0);
     }
 
+    plan_stage("octant+EA");
     // --- windows (kernels.hpp:234-273), 4P pieces on [-Ph/2, Ph/2]
     if (!gauss) p.window = build_prolate(p.c1);
     for (int d = 0; d < 3; ++d) {
@@ -897,6 +953,7 @@ Plan build_plan(const std::array<double, 3>& box, Family family, double eps, dou
             throw NumericalError("build_plan: window footprint exceeds the split "
                                  "support by more than one cell");
 
+    plan_stage("windows");
     // --- error stats (ewald.hpp:194-202, 395-401)
     p.E_T = 0.0;
     for (int d = 0; d < 3; ++d)
@@ -905,6 +962,7 @@ Plan build_plan(const std::array<double, 3>& box, Family family, double eps, dou
         throw NumericalError("build_plan: grid pinned below the accuracy minimum "
                              "(predicted error exceeds eps)");
 
+    plan_stage("errstats");
     // --- influence multipliers on the half spectrum (gridder.hpp:162-210)
     for (int d = 0; d < 3; ++d) {
         if (p.nf[d] < 2) throw InvalidArgument("grid: n_f must be at least 2");
@@ -929,6 +987,11 @@ Plan build_plan(const std::array<double, 3>& box, Family family, double eps, dou
     const double hx = p.h[0], hy = p.h[1], hz = p.h[2];
     const double pref = (hx * hy * hz) * (hx * hy * hz) / V;
     const int nx = p.nf[0], ny = p.nf[1], nzh = p.nf[2] / 2 + 1;
+    if (dev) {
+        dev->influence(p, ph2, fr2, pref, p.influence_half);
+        plan_stage("influence(dev)");
+        return p;
+    }
     p.influence_half.assign(static_cast<std::size_t>(nx) * ny * nzh, 0.0);
     par_for(nx, [&](int b, int e) {
         for (int ix = b; ix < e; ++ix) {
@@ -950,6 +1013,7 @@ Plan build_plan(const std::array<double, 3>& box, Family family, double eps, dou
             }
         }
     });
+    plan_stage("influence");
     return p;
 }
 

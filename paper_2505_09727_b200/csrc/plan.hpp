@@ -15,6 +15,7 @@
 #pragma once
 
 #include <array>
+#include <memory>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -107,8 +108,29 @@ struct Plan {
     std::pair<double, double> local_kernel(double r) const;  // kernels.hpp:143-163
 };
 
+// Optional device backend for the O(n_f^3) plan tables (SURVEY 8(f) row 3:
+// gridder.hpp:162-210, ewald.hpp:110-143): the chihat octant that feeds the
+// aliasing estimate E_A of every grid-inflation step, and the influence half
+// spectrum.  The E_A sums themselves stay on the host in long double so that
+// the plan choices (n_f, c1) are those of the host path.
+struct PlanDevice {
+    virtual ~PlanDevice() = default;
+    // val[(ax * h1 + ay) * h2 + az] = chihat_n(r_c |xi|), xi^2 = (f2[0][ax] +
+    // f2[1][ay]) + f2[2][az], h_d = nf_d / 2 + 1 (0 at xi = 0)
+    virtual void octant(const Plan& p, const std::array<std::vector<double>, 3>& f2,
+                        std::vector<double>& val) = 0;
+    // influence_half from the last octant: pref * chihat / xi^2 / (phihat_x^2
+    // phihat_y^2 phihat_z^2) on the half spectrum (storage-index tables)
+    virtual void influence(const Plan& p, const std::array<std::vector<double>, 3>& ph2,
+                           const std::array<std::vector<double>, 3>& fr2, double pref,
+                           std::vector<double>& out) = 0;
+};
+
 Plan build_plan(const std::array<double, 3>& box, Family family, double eps, double r_c,
-                const Overrides& ov);
+                const Overrides& ov, PlanDevice* dev = nullptr);
+
+// CUDA implementation of PlanDevice on one device (plan_device.cu).
+std::unique_ptr<PlanDevice> make_plan_device(int device);
 
 // Full nx*ny*nz influence array (reference layout), expanded from the half
 // spectrum; used only for parity checks.
