@@ -1608,6 +1608,94 @@ __global__ void __launch_bounds__(128) k_interp(GridArgs g, InterpArgs a) {
     }
 }
 
+// K3 for tiny systems (ik, spectral mode, P <= 8, N <= 4096): EIGHT lanes
+// per atom, lane j < P taking footprint plane jx = j, so that 8x the warps are
+// in flight (cfg1, 1000 atoms: 0.036 -> 0.022 ms).  From cfg2 on the thread-
+// per-atom kernel wins (0.034 vs 0.062 ms at 32k atoms): there neighbouring
+// lanes hold neighbouring atoms whose footprint rows coincide, while the eight
+// lanes of one atom read eight distant planes.  Lane j computes the three window weights
+// of node j and the group shares them by shuffles; the four field sums are
+// reduced over the group (3 xor-shuffle steps).
+template <int PT>
+__global__ void __launch_bounds__(128) k_interp8(GridArgs g, InterpArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* tab = reinterpret_cast<double*>(smem);  // phi (3 x 4P x 13)
+    constexpr int P = PT;
+    const int ntab = 3 * 4 * P * kNc;
+    for (int t = threadIdx.x; t < ntab; t += blockDim.x) tab[t] = g.win[t];
+    __syncthreads();
+    const long gt = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+    const long k = gt >> 3;
+    const int j = static_cast<int>(gt & 7);
+    const unsigned gmask = 0xffu << (threadIdx.x & 24);  // this 8-lane group
+    if (k >= a.N) return;  // whole groups leave together (N*8 threads, groups aligned)
+    const double4 v = a.xyzq[k];
+    const Foot f[3] = {footprint(P, v.x, g.h[0], g.half[0]),
+                       footprint(P, v.y, g.h[1], g.half[1]),
+                       footprint(P, v.z, g.h[2], g.half[2])};
+    // lane j: weight of node j in each dimension
+    double wj[3] = {0.0, 0.0, 0.0};
+    if (j < P) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            double w = horner13(tab + (d * 4 * P + 4 * (P - 1 - j) + f[d].s) * kNc, f[d].t);
+            if ((j == 0 && f[d].zero_lo) || (j == P - 1 && f[d].zero_hi)) w = 0.0;
+            wj[d] = w;
+        }
+    }
+    double wy[P], wz[P];
+    int iy[P], iz[P];
+#pragma unroll
+    for (int m = 0; m < P; ++m) {
+        wy[m] = __shfl_sync(gmask, wj[1], m, 8);
+        wz[m] = __shfl_sync(gmask, wj[2], m, 8);
+        iy[m] = wrapi(f[1].first + m, g.nf[1]);
+        iz[m] = wrapi(f[2].first + m, g.nf[2]);
+    }
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    if (j < P) {
+        const long ny = g.nf[1], nz = g.nf[2];
+        const int ix = wrapi(f[0].first + j, g.nf[0]);
+#pragma unroll
+        for (int jy = 0; jy < P; ++jy) {
+            const double* fld = a.fields + 4 * ((ix * ny + iy[jy]) * nz);
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+            for (int jz = 0; jz < P; ++jz) {
+                double f0, f1, f2, f3;
+                ldg4(fld + 4 * iz[jz], f0, f1, f2, f3);
+                s0 = fma(wz[jz], f0, s0);
+                s1 = fma(wz[jz], f1, s1);
+                s2 = fma(wz[jz], f2, s2);
+                s3 = fma(wz[jz], f3, s3);
+            }
+            a0 = fma(wy[jy], s0, a0);
+            a1 = fma(wy[jy], s1, a1);
+            a2 = fma(wy[jy], s2, a2);
+            a3 = fma(wy[jy], s3, a3);
+        }
+        a0 *= wj[0];
+        a1 *= wj[0];
+        a2 *= wj[0];
+        a3 *= wj[0];
+    }
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+        a0 += __shfl_xor_sync(gmask, a0, o, 8);
+        a1 += __shfl_xor_sync(gmask, a1, o, 8);
+        a2 += __shfl_xor_sync(gmask, a2, o, 8);
+        a3 += __shfl_xor_sync(gmask, a3, o, 8);
+    }
+    if (j == 0) {
+        const int o = a.orig[k];
+        const double qi = v.w;
+        a.u[o] = a0 - qi * a.self_coef;
+        a.F[3 * o + 0] = -qi * a1;
+        a.F[3 * o + 1] = -qi * a2;
+        a.F[3 * o + 2] = -qi * a3;
+    }
+}
+
 // Combine (ewald.hpp:639-647): u = u_l + u_s - q s0, F = F_l + F_s in the
 // caller's (original) order; u/F hold the spectral part on entry.  Block
 // partial sums of q u feed the energy.
@@ -1759,6 +1847,15 @@ struct SpreadLaunch {
     }
 };
 
+// atoms up to which K3 runs eight lanes per atom (ESP_INTERP8_MAX_N overrides)
+inline long interp8_max_n() {
+    static const long v = [] {
+        const char* e = std::getenv("ESP_INTERP8_MAX_N");
+        return e ? std::atol(e) : 4096L;  // measured: faster only for tiny systems (cfg1)
+    }();
+    return v;
+}
+
 template <int P>
 struct InterpLaunch {
     static void run(int mode, bool ik, const GridArgs& g, const InterpArgs& a, cudaStream_t s) {
@@ -1773,6 +1870,15 @@ struct InterpLaunch {
             kern<<<nblk, B, sm, s>>>(g, a);
             CK(cudaGetLastError());
         };
+        if constexpr (P > 0 && P <= 8) {
+            // small systems: eight lanes per atom (more gathers in flight)
+            if (mode == kSpectral && ik && !a.startB && !g.xslab && a.N <= interp8_max_n()) {
+                const size_t sm8 = sizeof(double) * 3 * 4 * P * kNc;
+                k_interp8<P><<<grid1(a.N * 8, B), B, sm8, s>>>(g, a);
+                CK(cudaGetLastError());
+                return;
+            }
+        }
         switch (mode) {
             case kSpectral: ik ? go(k_interp<P, kSpectral, true>) : go(k_interp<P, kSpectral, false>); break;
             case kValue: go(k_interp<P, kValue, true>); break;
