@@ -1421,16 +1421,17 @@ __global__ void __launch_bounds__(256) k_scale(long Mh, int ny, int nzh, const d
     const cufftDoubleComplex b = in[m];
     const double cr = b.x * pk, ci = b.y * pk;
     if (nfields == 4) {
-        // interleaved spectra [m][4] -> the batched inverse writes [node][4]
+        // planar spectra [4][m]; the batched inverse writes fields [node][4]
         const int iz = static_cast<int>(m % nzh);
         const long r = m / nzh;
         const int iy = static_cast<int>(r % ny);
         const int ix = static_cast<int>(r / ny);
         const double fx = xi[ix], fy = xi[nx + iy], fz = xi[nx + ny + iz];
         // (a + ib) * i xi = (-b xi, a xi)
-        double4* o = reinterpret_cast<double4*>(out + 4 * m);
-        o[0] = make_double4(cr, ci, -ci * fx, cr * fx);
-        o[1] = make_double4(-ci * fy, cr * fy, -ci * fz, cr * fz);
+        out[m] = make_cuDoubleComplex(cr, ci);
+        out[Mh + m] = make_cuDoubleComplex(-ci * fx, cr * fx);
+        out[2 * Mh + m] = make_cuDoubleComplex(-ci * fy, cr * fy);
+        out[3 * Mh + m] = make_cuDoubleComplex(-ci * fz, cr * fz);
     } else {
         out[m] = make_cuDoubleComplex(cr, ci);
     }
@@ -2129,8 +2130,11 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
     int inembed[3] = {p.nf[0], p.nf[1], p.nf[2] / 2 + 1};
     int onembed[3] = {p.nf[0], p.nf[1], p.nf[2]};
     if (nfields_ == 4) {
-        // interleaved batch: spectra [m][4] -> fields [node][4] (one 256-bit load per node in K3)
-        CF(cufftMakePlanMany(inv_, 3, n3, inembed, 4, 1, onembed, 4, 1, CUFFT_Z2D, 4, &w2));
+        // batch of 4: planar spectra [4][m] -> interleaved fields [node][4]
+        // (one 256-bit load per node in K3).  Planar input measured faster than
+        // interleaved input: n_f = 180 498 vs 802 us, n_f = 30 15 vs 19 us.
+        CF(cufftMakePlanMany(inv_, 3, n3, inembed, 1, static_cast<int>(Mh_), onembed, 4, 1,
+                             CUFFT_Z2D, 4, &w2));
     } else {
         CF(cufftMakePlanMany(inv_, 3, n3, inembed, 1, static_cast<int>(Mh_), onembed, 1,
                              static_cast<int>(M_), CUFFT_Z2D, 1, &w2));
