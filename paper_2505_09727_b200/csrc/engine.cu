@@ -175,43 +175,73 @@ struct BinArgs {
     double* qsum;  // [2]
 };
 
+// Fold, keys and ranks.  A rank is the return value of an atomic on the
+// key's counter; these round trips dominate when they are exposed (host-API
+// evaluation at cfg5: 1.2 ms with one atom per thread vs 0.14 ms without the
+// atomics; the device-resident graph replay did not show the stall), so each
+// thread takes kFoldILP atoms (stride blockDim) and issues all their atomics
+// before using any result (cfg5: 0.25 ms).
+// (kFoldILP = 1 for small systems, where 4 atoms per thread leave too few threads).
+constexpr long kFoldILPMinN = 1L << 18;
+
+template <int kFoldILP>
 __global__ void __launch_bounds__(256) k_fold_bin(BinArgs a) {
-    long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
-    double qi = 0.0;
-    if (i < a.N) {
-        double x = fold1(a.pos[3 * i + 0], a.box[0]);
-        double y = fold1(a.pos[3 * i + 1], a.box[1]);
-        double z = fold1(a.pos[3 * i + 2], a.box[2]);
-        qi = a.q[i];
-        a.tmp[i] = make_double4(x, y, z, qi);
-        // fine pair cell (the reference's coarse cell ewald.hpp:479-482 split
-        // kFS x kFS x kFZ); nc = fine cells per dim here
-        int cx = clampi(static_cast<int>(x / a.cw[0]), 0, a.nc[0] - 1);
-        int cy = clampi(static_cast<int>(y / a.cw[1]), 0, a.nc[1] - 1);
-        int cz = clampi(static_cast<int>(z / a.cw[2]), 0, a.nc[2] - 1);
-        int c = (cx * a.nc[1] + cy) * a.nc[2] + cz;
-        a.cellA[i] = c;
-        a.rankA[i] = atomicAdd(&a.countA[c], 1);
-        // spread bin: S grid cells per side, by floor(x/h); atoms are ordered
-        // by bin and, inside a bin, by its sub-bins (large systems: single grid
-        // cells), z fastest: neighbouring K3 threads then gather overlapping
-        // footprint rows (a Morton order of the sub-bins was measured slower)
-        const int lx = static_cast<int>(floor(x / a.h[0]));
-        const int ly = static_cast<int>(floor(y / a.h[1]));
-        const int lz = static_cast<int>(floor(z / a.h[2]));
-        const int bx = clampi(lx / a.S, 0, a.nb[0] - 1);
-        const int by = clampi(ly / a.S, 0, a.nb[1] - 1);
-        const int bz = clampi(lz / a.S, 0, a.nb[2] - 1);
-        const int D = a.sub;
-        const int sx = clampi((lx - bx * a.S) * D / a.S, 0, D - 1);
-        const int sy = clampi((ly - by * a.S) * D / a.S, 0, D - 1);
-        const int sz = clampi((lz - bz * a.S) * D / a.S, 0, D - 1);
-        const int b = ((bx * a.nb[1] + by) * a.nb[2] + bz) * (D * D * D) + (sx * D + sy) * D + sz;
-        a.cellB[i] = b;
-        a.rankB[i] = atomicAdd(&a.countB[b], 1);
+    const long i0 = blockIdx.x * static_cast<long>(blockDim.x) * kFoldILP + threadIdx.x;
+    double s1 = 0.0, s2 = 0.0;
+    int ca[kFoldILP], cb[kFoldILP];
+#pragma unroll
+    for (int u = 0; u < kFoldILP; ++u) {
+        const long i = i0 + static_cast<long>(u) * blockDim.x;
+        ca[u] = -1;
+        cb[u] = -1;
+        if (i < a.N) {
+            const double x = fold1(a.pos[3 * i + 0], a.box[0]);
+            const double y = fold1(a.pos[3 * i + 1], a.box[1]);
+            const double z = fold1(a.pos[3 * i + 2], a.box[2]);
+            const double qi = a.q[i];
+            s1 += qi;
+            s2 += fabs(qi);
+            a.tmp[i] = make_double4(x, y, z, qi);
+            // fine pair cell (the reference's coarse cell ewald.hpp:479-482 split
+            // into fine columns and slices); nc = fine cells per dim here
+            const int cx = clampi(static_cast<int>(x / a.cw[0]), 0, a.nc[0] - 1);
+            const int cy = clampi(static_cast<int>(y / a.cw[1]), 0, a.nc[1] - 1);
+            const int cz = clampi(static_cast<int>(z / a.cw[2]), 0, a.nc[2] - 1);
+            ca[u] = (cx * a.nc[1] + cy) * a.nc[2] + cz;
+            // spread bin: S grid cells per side, by floor(x/h); atoms are ordered
+            // by bin and, inside a bin, by its sub-bins (large systems: single
+            // grid cells), z fastest: neighbouring K3 threads then gather
+            // overlapping footprint rows (a Morton order was measured slower)
+            const int lx = static_cast<int>(floor(x / a.h[0]));
+            const int ly = static_cast<int>(floor(y / a.h[1]));
+            const int lz = static_cast<int>(floor(z / a.h[2]));
+            const int bx = clampi(lx / a.S, 0, a.nb[0] - 1);
+            const int by = clampi(ly / a.S, 0, a.nb[1] - 1);
+            const int bz = clampi(lz / a.S, 0, a.nb[2] - 1);
+            const int D = a.sub;
+            const int sx = clampi((lx - bx * a.S) * D / a.S, 0, D - 1);
+            const int sy = clampi((ly - by * a.S) * D / a.S, 0, D - 1);
+            const int sz = clampi((lz - bz * a.S) * D / a.S, 0, D - 1);
+            cb[u] = ((bx * a.nb[1] + by) * a.nb[2] + bz) * (D * D * D) + (sx * D + sy) * D + sz;
+        }
+    }
+    int ra[kFoldILP], rb[kFoldILP];
+#pragma unroll
+    for (int u = 0; u < kFoldILP; ++u) {
+        ra[u] = ca[u] >= 0 ? atomicAdd(&a.countA[ca[u]], 1) : 0;
+        rb[u] = cb[u] >= 0 ? atomicAdd(&a.countB[cb[u]], 1) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kFoldILP; ++u) {
+        const long i = i0 + static_cast<long>(u) * blockDim.x;
+        if (ca[u] >= 0) {
+            a.cellA[i] = ca[u];
+            a.rankA[i] = ra[u];
+            a.cellB[i] = cb[u];
+            a.rankB[i] = rb[u];
+        }
     }
     // neutrality sums (system.hpp:39-47), one pair of atomics per warp
-    double s1 = qi, s2 = fabs(qi);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         s1 += __shfl_xor_sync(0xffffffffu, s1, o);
@@ -2323,6 +2353,17 @@ void Engine::ensure_capacity(long N) {
 
 void Engine::prepare(long N, const double* pos, const double* q, double* qsum_dev,
                      cudaStream_t s) {
+    // ESP_PREP_TIMING=1 (diagnostics, not under graph capture): event times of
+    // the binning steps on stderr
+    static const bool ptime = std::getenv("ESP_PREP_TIMING") != nullptr;
+    cudaEvent_t pe[6] = {};
+    int npe = 0;
+    auto mark = [&]() {
+        if (!ptime) return;
+        CK(cudaEventCreate(&pe[npe]));
+        CK(cudaEventRecord(pe[npe++], s));
+    };
+    mark();
     const Plan& p = plan_;
     const int nkeyB = nkeyB_;
     const bool small = ncellF_ + nkeyB + 2 <= kSmallScanMax;
@@ -2332,6 +2373,7 @@ void Engine::prepare(long N, const double* pos, const double* q, double* qsum_de
         CK(cudaMemsetAsync(d_countB_, 0, sizeof(int) * (nkeyB + 1), s));
     }
     if (qsum_dev) CK(cudaMemsetAsync(qsum_dev, 0, sizeof(double) * 2, s));
+    mark();
     BinArgs a{};
     a.N = N;
     a.pos = pos;
@@ -2354,10 +2396,14 @@ void Engine::prepare(long N, const double* pos, const double* q, double* qsum_de
     a.countB = d_countB_;
     a.qsum = qsum_dev;
     if (N > 0) {
-        k_fold_bin<<<grid1(N, 256), 256, 0, s>>>(a);
+        if (N >= kFoldILPMinN)
+            k_fold_bin<4><<<grid1(N, 256 * 4), 256, 0, s>>>(a);
+        else
+            k_fold_bin<1><<<grid1(N, 256), 256, 0, s>>>(a);
         CK(cudaGetLastError());
         ++launches_;
     }
+    mark();
     if (small) {
         const size_t sm = sizeof(int) * (ncellF_ + nkeyB + 2);
         if (sm > 48 * 1024)
@@ -2375,12 +2421,24 @@ void Engine::prepare(long N, const double* pos, const double* q, double* qsum_de
         CK(cub::DeviceScan::ExclusiveSum(d_scan_tmp_, tb, d_countB_, d_startB_, nkeyB + 1, s));
         launches_ += 2;
     }
+    mark();
     if (N > 0) {
         k_scatter<<<grid1(N, 256), 256, 0, s>>>(N, d_tmp_, d_cellA_, d_rankA_, d_startA_, d_xyzqA_,
                                                  d_origA_, d_cellB_, d_rankB_, d_startB_, d_xyzqB_,
                                                  d_origB_);
         CK(cudaGetLastError());
         ++launches_;
+    }
+    mark();
+    if (ptime) {
+        CK(cudaEventSynchronize(pe[npe - 1]));
+        const char* nm[5] = {"memsets", "fold_bin", "scans", "scatter", ""};
+        for (int i = 0; i + 1 < npe; ++i) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, pe[i], pe[i + 1]));
+            std::fprintf(stderr, "prepare %-9s %8.3f ms\n", nm[i], ms);
+        }
+        for (int i = 0; i < npe; ++i) cudaEventDestroy(pe[i]);
     }
 }
 
