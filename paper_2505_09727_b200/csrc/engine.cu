@@ -297,26 +297,26 @@ __device__ void block_exclusive_scan_smem(int* sm, int n, int* wsum) {
 }
 
 // counts staged in shared memory with coalesced loads (and zeroed in HBM),
-// scanned there, written back coalesced
+// scanned there, written back coalesced.  CTA 0 scans the pair-cell counts,
+// CTA 1 the spread-bin counts, concurrently; the staging loops are unrolled
+// so that each thread has several loads in flight (latency-bound otherwise).
 __global__ void __launch_bounds__(1024) k_scan_small(int* countA, int* startA, int nA, int* countB,
                                                      int* startB, int nB,
                                                      unsigned long long* npairs) {
     extern __shared__ int sm[];
     __shared__ int wsum[32];
-    for (int i = threadIdx.x; i < nA; i += blockDim.x) {
-        sm[i] = countA[i];
-        countA[i] = 0;
-    }
-    for (int i = threadIdx.x; i < nB; i += blockDim.x) {
-        sm[nA + i] = countB[i];
-        countB[i] = 0;
-    }
+    int* count = blockIdx.x == 0 ? countA : countB;
+    int* start = blockIdx.x == 0 ? startA : startB;
+    const int n = blockIdx.x == 0 ? nA : nB;
+#pragma unroll 8
+    for (int i = threadIdx.x; i < n; i += blockDim.x) sm[i] = count[i];
+#pragma unroll 8
+    for (int i = threadIdx.x; i < n; i += blockDim.x) count[i] = 0;
     __syncthreads();
-    block_exclusive_scan_smem(sm, nA, wsum);
-    block_exclusive_scan_smem(sm + nA, nB, wsum);
-    for (int i = threadIdx.x; i < nA; i += blockDim.x) startA[i] = sm[i];
-    for (int i = threadIdx.x; i < nB; i += blockDim.x) startB[i] = sm[nA + i];
-    if (threadIdx.x == 0) *npairs = 0ull;
+    block_exclusive_scan_smem(sm, n, wsum);
+#pragma unroll 8
+    for (int i = threadIdx.x; i < n; i += blockDim.x) start[i] = sm[i];
+    if (blockIdx.x == 0 && threadIdx.x == 0) *npairs = 0ull;
 }
 
 __global__ void __launch_bounds__(256) k_scatter(long N, const double4* __restrict__ tmp,
@@ -2405,11 +2405,11 @@ void Engine::prepare(long N, const double* pos, const double* q, double* qsum_de
     }
     mark();
     if (small) {
-        const size_t sm = sizeof(int) * (ncellF_ + nkeyB + 2);
+        const size_t sm = sizeof(int) * (std::max<long>(ncellF_, nkeyB) + 1);
         if (sm > 48 * 1024)
             CK(cudaFuncSetAttribute(k_scan_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(sm)));
-        k_scan_small<<<1, 1024, sm, s>>>(d_countA_, d_startA_, static_cast<int>(ncellF_ + 1),
+        k_scan_small<<<2, 1024, sm, s>>>(d_countA_, d_startA_, static_cast<int>(ncellF_ + 1),
                                          d_countB_, d_startB_, nkeyB + 1, d_npairs_);
         CK(cudaGetLastError());
         ++launches_;
