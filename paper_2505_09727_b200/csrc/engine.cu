@@ -1770,11 +1770,22 @@ __global__ void __launch_bounds__(256) k_combine(long N, const double4* __restri
 __global__ void __launch_bounds__(256) k_energy(const double* __restrict__ part, int n, double* out) {
     __shared__ double red[8];
     double s = 0.0, c = 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const double y = part[i] - c;
-        const double t = s + y;
-        c = (t - s) - y;
-        s = t;
+    // eight partials loaded ahead of the (sequential) compensated sum: one
+    // load latency per 8 elements instead of per element (cfg5: 31k partials)
+    for (int i0 = threadIdx.x; i0 < n; i0 += 8 * blockDim.x) {
+        double v8[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * blockDim.x;
+            v8[u] = i < n ? part[i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const double y = v8[u] - c;
+            const double t = s + y;
+            c = (t - s) - y;
+            s = t;
+        }
     }
     double v = s - c;
 #pragma unroll
