@@ -1358,19 +1358,44 @@ __global__ void __launch_bounds__(512) k_spread(GridArgs g, const double4* __res
     for (int t = threadIdx.x; t < tsize; t += nt) tile[t] = 0.0;
 
     const int P2 = P * P, P3 = P2 * P;
+    // each thread's first task of a chunk (atom ai = task / 3, coordinate d):
+    // its position is loaded one chunk ahead, during the previous chunk's
+    // atom loop, so the global latency is off the critical path
+    auto load_task = [&](int c0, int task, double& x, double& q) {
+        const int nc = min(kSpreadChunk, ie - c0);
+        x = 0.0;
+        q = 0.0;
+        if (c0 < ie && task < 3 * nc) {
+            const int ai = task / 3, d = task - 3 * ai;
+            const double* pv = reinterpret_cast<const double*>(xyzq + c0 + ai);
+            x = pv[d];
+            q = pv[3];
+        }
+    };
+    double nx_, nq_;
+    load_task(ib, threadIdx.x, nx_, nq_);
     for (int c0 = ib; c0 < ie; c0 += kSpreadChunk) {
         const int nc = min(kSpreadChunk, ie - c0);
         __syncthreads();  // previous chunk's last atom done with wch/fch
+        const double px = nx_, pq = nq_;
+        load_task(c0 + kSpreadChunk, threadIdx.x, nx_, nq_);
         for (int task = threadIdx.x; task < 3 * nc; task += nt) {
             const int ai = task / 3, d = task - 3 * ai;
-            const double4 v = xyzq[c0 + ai];
-            const double x = d == 0 ? v.x : (d == 1 ? v.y : v.z);
+            double x, vq;
+            if (task == threadIdx.x) {
+                x = px;
+                vq = pq;
+            } else {
+                const double* pv = reinterpret_cast<const double*>(xyzq + c0 + ai);
+                x = pv[d];
+                vq = pv[3];
+            }
             const Foot f = footprint(P, x, g.h[d], g.half[d]);
             const double* tab = g.win + static_cast<long>(d) * 4 * P * kNc;
             double* w = wch + (ai * 3 + d) * MP;
-            double scale = d == 0 ? v.w : 1.0;
+            double scale = d == 0 ? vq : 1.0;
             if (d == 0 && g.xslab) {  // distributed FFT: another rank's atom in a shared bin
-                const int l = clampi(static_cast<int>(floor(v.x / g.h[0])), 0, g.nf[0] - 1);
+                const int l = clampi(static_cast<int>(floor(x / g.h[0])), 0, g.nf[0] - 1);
                 if (l < g.own_x0 || l >= g.own_x1) scale = 0.0;
             }
 #pragma unroll
