@@ -383,6 +383,22 @@ struct PairArgs {
     double own_h;
 };
 
+// Candidate list of one column: list positions [p0, p1) (relative to the
+// piece start lb) get staged indices off + p.  Four at a time with one 64-bit
+// shared store (lists are 8-byte aligned per piece), scalar head and tail
+// (k_pair_half's list building was ~8 % of its instructions with one store
+// per entry; cfg5 K4 20.6 -> 20.3 ms).
+__device__ __forceinline__ void fill_range(unsigned short* lw, int lb, int p0, int p1, int off) {
+    int p = p0;
+    for (; p < p1 && (p & 3); ++p) lw[p - lb] = static_cast<unsigned short>(off + p);
+    for (; p + 4 <= p1; p += 4) {
+        const unsigned long long b = static_cast<unsigned long long>(off + p);
+        *reinterpret_cast<unsigned long long*>(lw + (p - lb)) =
+            b * 0x0001000100010001ull + 0x0003000200010000ull;
+    }
+    for (; p < p1; ++p) lw[p - lb] = static_cast<unsigned short>(off + p);
+}
+
 // d = (r_j - r_i) + image shift, in that order: the reference's min-image
 // displacement (ewald.hpp:436-443) bit for bit, hence F_ij = -F_ji exactly.
 template <int ND>
@@ -666,6 +682,8 @@ __global__ void __launch_bounds__(kPairThreads, kPairWarps >= 8 ? 3 : 6) k_pair(
                 const int le = min(T, lb + a.lcap - 32);
                 {
                     // this lane's columns cover stream positions [inc-cnt, inc)
+                    // (one store per entry: fill_range's packed stores measured
+                    // slower in this kernel, cfg5 42.1 -> 43.3 ms)
                     int p0 = max(inc0 - cnt0, lb), p1 = min(inc0, le);
                     int off = beg0 - (inc0 - cnt0);
 #pragma unroll 4
@@ -1134,10 +1152,8 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
         for (int lb = 0; lb < T; lb += a.lcap - 32) {
             const int le = min(T, lb + a.lcap - 32);
             {
-                const int p0 = max(inc - cnt, lb), p1 = min(inc, le);
-                const int off = beg - (inc - cnt);
-#pragma unroll 4
-                for (int p = p0; p < p1; ++p) lw[p - lb] = static_cast<unsigned short>(off + p);
+                // this lane's column: list positions [p0, p1)
+                fill_range(lw, lb, max(inc - cnt, lb), min(inc, le), beg - (inc - cnt));
             }
             const int n = le - lb;
             const int n32 = (n + 31) & ~31;
@@ -2232,7 +2248,7 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
     // pair kernel staging capacity (candidates per chunk); ESP_PAIR_CAP overrides
     pair_warps_ = 4;
     pair_cap_ = 2048;
-    if (const char* e = std::getenv("ESP_PAIR_CAP")) pair_cap_ = std::max(256, std::min(4096, std::atoi(e)));
+    if (const char* e = std::getenv("ESP_PAIR_CAP")) pair_cap_ = std::max(256, std::min(4096, std::atoi(e) / 32 * 32));
     if (const char* e = std::getenv("ESP_PAIR_HALF")) half_mode_ = std::atoi(e);
 }
 
@@ -2346,7 +2362,7 @@ void Engine::reconfigure(long N) {
         const double cand = pairs_per_atom * (want == 3 ? 1.8 : 2.2) * 1.2;
         pair_lcap_ = std::max(256, std::min(1024, (static_cast<int>(cand) + 127) / 128 * 128));
         if (const char* e = std::getenv("ESP_PAIR_LCAP"))
-            pair_lcap_ = std::max(128, std::min(2048, std::atoi(e) / 2 * 2));
+            pair_lcap_ = std::max(128, std::min(2048, std::atoi(e) / 32 * 32));
     }
     // finer sort sub-bins for large systems: better K3 locality, more keys
     // sort sub-bins: single grid cells for large systems (K3 cfg5 4.66 -> 3.50
@@ -2618,7 +2634,7 @@ bool Engine::run_pair_half(long N, cudaStream_t s) {
     double best_t = -1.0;
     const long want_blocks = 2L * 3 * sms;  // 3 CTAs per SM, 2 waves
     int cap_max = 4096;
-    if (const char* e = std::getenv("ESP_HALF_CAP")) cap_max = std::max(256, std::min(8192, std::atoi(e)));
+    if (const char* e = std::getenv("ESP_HALF_CAP")) cap_max = std::max(256, std::min(8192, std::atoi(e) / 32 * 32));
     for (int bx = 1; bx <= kHalfMaxBX; ++bx)
         for (int bz : {2, 3, 4, 6, 8}) {
             if (F_[0] < bx + 2 * M || F_[1] < bx + 2 * M || F_[2] < bz + 2 * Mz) continue;
@@ -2674,7 +2690,7 @@ bool Engine::run_pair_half(long N, cudaStream_t s) {
                            kPi * p.r_c * p.r_c * p.r_c;
         const double cand = ppa * (col_div_ == 3 ? 1.8 : 2.2) * 0.6;
         int l = std::max(128, std::min(1024, (static_cast<int>(cand) + 63) / 64 * 64));
-        if (const char* e = std::getenv("ESP_PAIR_LCAP")) l = std::max(128, std::min(2048, std::atoi(e) / 2 * 2));
+        if (const char* e = std::getenv("ESP_PAIR_LCAP")) l = std::max(128, std::min(2048, std::atoi(e) / 32 * 32));
         a.lcap = std::min(l, a.cap) + 32;
     }
     a.nent_max = (a.bx + M) * (a.bx + 2 * M) * (a.bz + 2 * Mz);
