@@ -851,6 +851,7 @@ struct HalfArgs {
     int nent_max;                // cell entries per CTA neighbourhood
     int M, Mz;                   // reach in columns / slices
     int bx, bz;                  // target block: bx x bx columns, bz slices
+    int blk0;                    // first block of this launch (slab decomposition)
     int F[3];                    // fine cells per dim
     double fw[3];
     double box[3];
@@ -972,7 +973,7 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
     const int M = a.M, Mz = a.Mz, BX = a.bx;
     const int nzb = (a.F[2] + a.bz - 1) / a.bz;
     const int nyb = (a.F[1] + BX - 1) / BX;
-    const int blk = blockIdx.x;
+    const int blk = blockIdx.x + a.blk0;
     const int bzi = blk % nzb;
     const int fy0 = ((blk / nzb) % nyb) * BX;
     const int fx0 = (blk / (nzb * nyb)) * BX;
@@ -2520,7 +2521,11 @@ void Engine::run_pair(long N, cudaStream_t s, int rank, int nranks, bool own_bin
     // half-shell K4 on the single-GPU path (tiny systems: the full-list kernel's
     // single launch is faster); ESP_PAIR_HALF=0 never, 2 always
     const bool half = half_mode_ == 2 || (half_mode_ == 1 && N >= kHalfMinN);
-    if (half && nranks == 1 && !own_bins && run_pair_half(N, s)) return;
+    // the slab decomposition (every rank holds all atoms, outputs all-reduced)
+    // takes the half-shell kernel for its x-range of blocks: partner terms on
+    // other ranks' atoms are summed by the all-reduce.  The distributed FFT
+    // (own_bins: plane-owned targets, possibly local inputs) keeps full lists.
+    if (half && !own_bins && run_pair_half(N, s, rank, nranks)) return;
     PairArgs a{};
     a.xyzq = d_xyzqA_;
     a.orig = d_origA_;
@@ -2622,7 +2627,7 @@ void Engine::run_pair(long N, cudaStream_t s, int rank, int nranks, bool own_bin
 // the most targets per CTA whose expected forward neighbourhood fits the
 // staging capacity while keeping >= 3 CTAs per SM in flight.  Returns false
 // (full-list kernel instead) when no block shape fits the period.
-bool Engine::run_pair_half(long N, cudaStream_t s) {
+bool Engine::run_pair_half(long N, cudaStream_t s, int rank, int nranks) {
     const Plan& p = plan_;
     int nd = 20;
     const PairConsts k = make_pair_consts(p, nd);
@@ -2694,10 +2699,16 @@ bool Engine::run_pair_half(long N, cudaStream_t s) {
         a.lcap = std::min(l, a.cap) + 32;
     }
     a.nent_max = (a.bx + M) * (a.bx + 2 * M) * (a.bz + 2 * Mz);
-    const long nblocks = static_cast<long>((F_[0] + a.bx - 1) / a.bx) *
-                         ((F_[1] + a.bx - 1) / a.bx) * ((F_[2] + a.bz - 1) / a.bz);
+    const long nblocks_all = static_cast<long>((F_[0] + a.bx - 1) / a.bx) *
+                             ((F_[1] + a.bx - 1) / a.bx) * ((F_[2] + a.bz - 1) / a.bz);
+    // slab decomposition: this rank's x-range of blocks (x-major block order)
+    const long nbx = (F_[0] + a.bx - 1) / a.bx;
+    const long per_x = nblocks_all / nbx;
+    const long xlo = nbx * rank / nranks, xhi = nbx * (rank + 1) / nranks;
+    a.blk0 = static_cast<int>(xlo * per_x);
+    const long nblocks = (xhi - xlo) * per_x;
     if (N >= (1L << 27)) throw InvalidArgument("pair kernel: N must be < 2^27");
-    if (nblocks + 1 > ovf_cap_) return false;  // sized in alloc_cells (no allocation under capture)
+    if (nblocks_all + 1 > ovf_cap_) return false;  // sized in alloc_cells (no allocation under capture)
     a.ovf = d_ovf_;
     CK(cudaMemsetAsync(d_ovf_, 0, sizeof(int), s));
     size_t sm = (a.cap + 1) * sizeof(float4) +
@@ -2707,7 +2718,7 @@ bool Engine::run_pair_half(long N, cudaStream_t s) {
     auto go = [&](auto kern, auto ovfk) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(sm)));
-        kern<<<static_cast<unsigned>(nblocks), kHalfThreads, sm, s>>>(a, k);
+        if (nblocks > 0) kern<<<static_cast<unsigned>(nblocks), kHalfThreads, sm, s>>>(a, k);
         CK(cudaGetLastError());
         ovfk<<<ovf_grid, 256, 0, s>>>(a, k);
         CK(cudaGetLastError());

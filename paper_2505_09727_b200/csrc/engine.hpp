@@ -145,7 +145,7 @@ private:
     void alloc_bins(int sub);
     void prepare(long N, const double* pos, const double* q, double* qsum_dev, cudaStream_t s);
     void run_pair(long N, cudaStream_t s, int rank, int nranks, bool own_bins = false);
-    bool run_pair_half(long N, cudaStream_t s);
+    bool run_pair_half(long N, cudaStream_t s, int rank = 0, int nranks = 1);
     void run_grid(long N, cudaStream_t s, StageTimes* t);
     void run_spread(long N, cudaStream_t s, int rank, int nranks, double* grid,
                     const GridArgs* gslab = nullptr, long nreals = -1, int b0 = -1,
