@@ -1603,15 +1603,27 @@ __global__ void __launch_bounds__(128) k_interp(GridArgs g, InterpArgs a) {
             // P <= 5 the jx loop is unrolled (w[0][jx] / idx[0][jx] stay in
             // registers instead of the local-memory stack: cfg4 0.394 -> 0.376
             // ms); for P = 6, 8 the rolled loop measured faster (fewer registers)
+            // For P > 5 the x weight and index are computed inside the loop (no
+            // runtime-indexed array, so no local-memory stack either).
             constexpr int kJxUnroll = (PT > 0 && PT <= 5) ? MP : 1;
             double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll kJxUnroll
             for (int jx = 0; jx < MP; ++jx) {
                 if (jx >= P) break;
+                double wxj;
+                int ixj;
+                if (kJxUnroll > 1) {
+                    wxj = w[0][jx];
+                    ixj = idx[0][jx];
+                } else {
+                    wxj = horner13(tab + (4 * (P - 1 - jx) + f[0].s) * kNc, f[0].t);
+                    if ((jx == 0 && f[0].zero_lo) || (jx == P - 1 && f[0].zero_hi)) wxj = 0.0;
+                    ixj = g.xslab ? f[0].first + jx - g.x_lo : wrapi(f[0].first + jx, g.nf[0]);
+                }
 #pragma unroll
                 for (int jy = 0; jy < MP; ++jy) {
                     if (jy < P) {
-                        const double* fld = a.fields + 4 * ((idx[0][jx] * ny + idx[1][jy]) * nz);
+                        const double* fld = a.fields + 4 * ((ixj * ny + idx[1][jy]) * nz);
                         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
                         for (int jz = 0; jz < MP; ++jz) {
@@ -1625,7 +1637,7 @@ __global__ void __launch_bounds__(128) k_interp(GridArgs g, InterpArgs a) {
                                 s3 = fma(wz, f3, s3);
                             }
                         }
-                        const double wxy = w[0][jx] * w[1][jy];
+                        const double wxy = wxj * w[1][jy];
                         a0 = fma(wxy, s0, a0);
                         a1 = fma(wxy, s1, a1);
                         a2 = fma(wxy, s2, a2);
