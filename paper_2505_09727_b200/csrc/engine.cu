@@ -1407,7 +1407,12 @@ __global__ void __launch_bounds__(512) k_spread(GridArgs g, const double4* __res
                 x = pv[d];
                 vq = pv[3];
             }
-            const Foot f = footprint(P, x, g.h[d], g.half[d]);
+            // per-dimension values by selection, not by a runtime index (which
+            // put g.h / g.half / lo in a local-memory stack frame)
+            const double hd = d == 0 ? g.h[0] : (d == 1 ? g.h[1] : g.h[2]);
+            const double halfd = d == 0 ? g.half[0] : (d == 1 ? g.half[1] : g.half[2]);
+            const int lod = d == 0 ? lo[0] : (d == 1 ? lo[1] : lo[2]);
+            const Foot f = footprint(P, x, hd, halfd);
             const double* tab = g.win + static_cast<long>(d) * 4 * P * kNc;
             double* w = wch + (ai * 3 + d) * MP;
             double scale = d == 0 ? vq : 1.0;
@@ -1424,7 +1429,7 @@ __global__ void __launch_bounds__(512) k_spread(GridArgs g, const double4* __res
                 }
             }
             // offsets are in [0, W-P] by construction; clamp for non-finite input
-            fch[ai * 3 + d] = clampi(f.first - lo[d], 0, W - P);
+            fch[ai * 3 + d] = clampi(f.first - lod, 0, W - P);
         }
         __syncthreads();
         if (P3 <= nt) {
