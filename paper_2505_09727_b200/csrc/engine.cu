@@ -140,6 +140,14 @@ __device__ __forceinline__ double horner13(const double* __restrict__ c, double 
     return r;
 }
 
+// weight of footprint node j in one dimension (the element of weights() below)
+__device__ __forceinline__ double weight1(int P, const double* __restrict__ tab, const Foot& f,
+                                          int j) {
+    double v = horner13(tab + (4 * (P - 1 - j) + f.s) * kNc, f.t);
+    if ((j == 0 && f.zero_lo) || (j == P - 1 && f.zero_hi)) v = 0.0;
+    return v;
+}
+
 template <int MP>
 __device__ __forceinline__ void weights(int P, const double* __restrict__ tab, const Foot& f,
                                         double* w) {
@@ -1587,18 +1595,21 @@ __global__ void __launch_bounds__(128) k_interp(GridArgs g, InterpArgs a) {
         double qi = v.w;
         double us = 0.0, Fx = 0.0, Fy = 0.0, Fz = 0.0;
         if (MODE == kValue) {
+            // x weight / index per jx inside the loop (no runtime-indexed array)
             double acc = 0.0;
 #pragma unroll 1
             for (int jx = 0; jx < P; ++jx) {
+                const double wxj = weight1(P, tab, f[0], jx);
+                const int ixj = g.xslab ? f[0].first + jx - g.x_lo : wrapi(f[0].first + jx, g.nf[0]);
 #pragma unroll
                 for (int jy = 0; jy < MP; ++jy) {
                     if (jy < P) {
-                        const double* fld = a.fields + (idx[0][jx] * ny + idx[1][jy]) * nz;
+                        const double* fld = a.fields + (ixj * ny + idx[1][jy]) * nz;
                         double sz = 0.0;
 #pragma unroll
                         for (int jz = 0; jz < MP; ++jz)
                             if (jz < P) sz = fma(w[2][jz], __ldg(fld + idx[2][jz]), sz);
-                        acc = fma(w[0][jx] * w[1][jy], sz, acc);
+                        acc = fma(wxj * w[1][jy], sz, acc);
                     }
                 }
             }
@@ -1621,8 +1632,7 @@ __global__ void __launch_bounds__(128) k_interp(GridArgs g, InterpArgs a) {
                     wxj = w[0][jx];
                     ixj = idx[0][jx];
                 } else {
-                    wxj = horner13(tab + (4 * (P - 1 - jx) + f[0].s) * kNc, f[0].t);
-                    if ((jx == 0 && f[0].zero_lo) || (jx == P - 1 && f[0].zero_hi)) wxj = 0.0;
+                    wxj = weight1(P, tab, f[0], jx);
                     ixj = g.xslab ? f[0].first + jx - g.x_lo : wrapi(f[0].first + jx, g.nf[0]);
                 }
 #pragma unroll
@@ -1658,14 +1668,18 @@ __global__ void __launch_bounds__(128) k_interp(GridArgs g, InterpArgs a) {
             // value + gradient from one field with derivative weights
             double dw[3][MP];
 #pragma unroll
-            for (int d = 0; d < 3; ++d) weights<MP>(P, tab + (3 + d) * 4 * P * kNc, f[d], dw[d]);
+            for (int d = 1; d < 3; ++d) weights<MP>(P, tab + (3 + d) * 4 * P * kNc, f[d], dw[d]);
             double val = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
 #pragma unroll 1
             for (int jx = 0; jx < P; ++jx) {
+                // x weights / index per jx inside the loop (no runtime-indexed array)
+                const double wxj = weight1(P, tab, f[0], jx);
+                const double dwxj = weight1(P, tab + 3 * 4 * P * kNc, f[0], jx);
+                const int ixj = g.xslab ? f[0].first + jx - g.x_lo : wrapi(f[0].first + jx, g.nf[0]);
 #pragma unroll
                 for (int jy = 0; jy < MP; ++jy) {
                     if (jy < P) {
-                        const long row = (idx[0][jx] * ny + idx[1][jy]) * nz;
+                        const long row = (ixj * ny + idx[1][jy]) * nz;
                         double sz = 0.0, sd = 0.0;
 #pragma unroll
                         for (int jz = 0; jz < MP; ++jz) {
@@ -1675,10 +1689,10 @@ __global__ void __launch_bounds__(128) k_interp(GridArgs g, InterpArgs a) {
                                 sd = fma(dw[2][jz], gv, sd);
                             }
                         }
-                        val = fma(w[0][jx] * w[1][jy], sz, val);
-                        gx = fma(dw[0][jx] * w[1][jy], sz, gx);
-                        gy = fma(w[0][jx] * dw[1][jy], sz, gy);
-                        gz = fma(w[0][jx] * w[1][jy], sd, gz);
+                        val = fma(wxj * w[1][jy], sz, val);
+                        gx = fma(dwxj * w[1][jy], sz, gx);
+                        gy = fma(wxj * dw[1][jy], sz, gy);
+                        gz = fma(wxj * w[1][jy], sd, gz);
                     }
                 }
             }
