@@ -330,6 +330,41 @@ def run_ours(args):
                            "round per target take ~40 % of the instructions; the partner terms go "
                            "to L2 as fire-and-forget fp64 REDs"}
 
+    # ---- every grid-pipeline kernel against the HBM roofline (SURVEY 8(d)
+    # algorithmic bytes; serialised stage times).  The grids fit in L2 (cfg5:
+    # 47 MB of 126 MB), so these kernels are L1/L2-bound and their HBM
+    # fractions are low by construction; the bytes are the algorithmic minimum.
+    hbm_peak, hbm_src = None, None
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            hbm_peak = float(json.load(f)["hbm_gbs"])
+        hbm_src = "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        hbm_peak, hbm_src = 7700.0, "nominal HBM3e (MEASURED_PEAKS.json absent)"
+    M = int(np.prod(plan.nf))
+    Mh = int(plan.nf[0] * plan.nf[1] * (plan.nf[2] // 2 + 1))
+    nfld = 4 if args.force_method == "ik" else 1
+    kbytes = {
+        "K1 k_spread": (32 * N + 8 * M, "spread"),
+        "K2 k_scale": ((24 + 16 * nfld) * Mh, "scale"),
+        "K3 k_interp": (8 * nfld * M + 64 * N, "interpolate"),
+        "cuFFT D2Z": (8 * M + 16 * Mh, "fft"),
+        f"cuFFT Z2D x{nfld}": (nfld * (16 * Mh + 8 * M), "ifft"),
+    }
+    kernels = {}
+    for name, (nbytes, stage) in kbytes.items():
+        kms = stages_ms.get(stage)
+        if not kms:
+            continue
+        gbs = nbytes / (kms * 1e-3) / 1e9
+        kernels[name] = {"bound": "hbm", "bytes": nbytes, "ms": kms, "GB/s": gbs,
+                         "frac": gbs / hbm_peak}
+    kernels["K4 " + roofline["kernel"].split(" ")[0]] = {
+        "bound": "fp64", "flops": pair_flops, "ms": stages_ms["local"],
+        "TFLOP/s": achieved, "frac": roofline["frac"]}
+    kernel_rooflines = {"hbm_peak_GBps": hbm_peak, "hbm_peak_source": hbm_src,
+                        "kernels": kernels}
+
     # ---- e2e through the public API on pinned host buffers
     pos_h = torch.from_numpy(pos).pin_memory().numpy()
     q_h = torch.from_numpy(q).pin_memory().numpy()
@@ -410,6 +445,7 @@ def run_ours(args):
             "launches_per_step": launches_per_step,
             "stages_ms": stages_ms,
             "roofline": roofline,
+            "kernel_rooflines": kernel_rooflines,
             "cpu_baseline": cpu,
             "e2e": {"value": (N / (e2e_ms * 1e-3)) if strong else weak_scaling_value(N, world, e2e_ms),
                     "unit": UNIT,
