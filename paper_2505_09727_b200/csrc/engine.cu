@@ -460,8 +460,6 @@ constexpr int kMaxBZ = 8;     // target slices per CTA (runtime a.bz <= kMaxBZ)
 constexpr int kMaxColDiv = 3;  // columns of edge >= r_c / col_div, col_div in {2, 3}
 constexpr int kMaxCol = (2 + 2 * kMaxColDiv) * (2 + 2 * kMaxColDiv);  // (BX+2M)^2, BX <= 2
 static_assert(kMaxCol <= 64, "two column passes per target");
-constexpr int kMaxSl = kMaxBZ + 8;  // bz + 2 Mz with Mz <= 4
-constexpr int kMaxEnt = kMaxCol * kMaxSl;
 #ifndef ESP_PAIR_WARPS
 #define ESP_PAIR_WARPS 8
 #endif
@@ -758,7 +756,6 @@ __global__ void __launch_bounds__(kPairThreads, kPairWarps >= 8 ? 3 : 6) k_pair(
                               u, fx, fy, fz, npair);
             }
             __syncwarp();
-#pragma unroll
             // transpose-reduce of (u, fx, fy, fz) over the warp: 6 double
             // shuffles instead of 20; lane 8c ends with component c
             {
