@@ -857,6 +857,13 @@ struct HalfArgs {
     int M, Mz;                   // reach in columns / slices
     int bx, bz;                  // target block: bx x bx columns, bz slices
     int blk0;                    // first block of this launch (slab decomposition)
+    // distributed FFT: targets are the atoms whose grid plane
+    // clamp(floor(x/own_h), 0, own_nx-1) lies in [own_lo, own_hi); own_lo < 0:
+    // every atom of the launched blocks is a target (as PairArgs).  Then the
+    // base of a same-cell pair is chosen by position (below), not by the
+    // sorted order, which differs between ranks (atomic counting-sort ranks).
+    int own_lo, own_hi, own_nx;
+    double own_h;
     int F[3];                    // fine cells per dim
     double fw[3];
     double box[3];
@@ -927,6 +934,14 @@ __device__ __forceinline__ bool pair_eval2(const PairConsts& k, double4 pj, doub
     const double b = qi * c;
     gj = make_double4(qi * pot, b * dx, b * dy, b * dz);
     return true;
+}
+
+// Same-cell pair base by position, for the distributed FFT: j's terms are
+// evaluated on i's side iff j lies after i in (z, x, y) order.  Positions are
+// identical on every rank (ghost copies carry the owner's folded coordinates),
+// unlike the sorted order inside a cell (atomic counting-sort ranks).
+__device__ __forceinline__ bool pos_after(const double4& pj, const double4& pi) {
+    return pj.z > pi.z || (pj.z == pi.z && (pj.x > pi.x || (pj.x == pi.x && pj.y > pi.y)));
 }
 
 // (u, F) terms of sorted atom j into the planar accumulators (global REDs;
@@ -1112,6 +1127,24 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
         const float4 ci = cand[si];
         const int gi = __float_as_int(ci.w) & 0x7ffffff;
         const double4 pi = a.xyzq[gi];
+        // distributed FFT: same-cell partners of i, as global sorted indices
+        // [cs, ce) (base by position, see HalfArgs); cs = ce = 0 otherwise
+        int cs = 0, ce = 0;
+        if (a.own_lo >= 0) {
+            const int l = clampi(static_cast<int>(floor(pi.x / a.own_h)), 0, a.own_nx - 1);
+            if (l < a.own_lo || l >= a.own_hi) {  // another rank's target
+                int nx = 0;
+                if (lane == 0) nx = atomicAdd(&tnext, 1);
+                ii = __shfl_sync(0xffffffffu, nx, 0);
+                continue;
+            }
+            const int cx = min(a.F[0] - 1, static_cast<int>(pi.x / a.fw[0]));
+            const int cy = min(a.F[1] - 1, static_cast<int>(pi.y / a.fw[1]));
+            const int cz = min(a.F[2] - 1, static_cast<int>(pi.z / a.fw[2]));
+            const int f = (cx * a.F[1] + cy) * a.F[2] + cz;
+            cs = a.start[f];
+            ce = a.start[f + 1];
+        }
         const float xf = ci.x, yf = ci.y, zf = ci.z;
         const int txy = tcxy[tc];
         const int tx = txy & 0xff, ty = txy >> 8;
@@ -1136,7 +1169,9 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
                 khi = max(0, min(nsl - 1, khi));
                 int lo = ent_off[col * nsl + klo];
                 const int hi = ent_off[col * nsl + khi + 1];
-                if (fc >> 8) lo = si + 1;  // own column: after i
+                // own column: after i (pencil mode: from i's cell start, the
+                // same-cell pairs being decided by position in the rounds)
+                if (fc >> 8) lo = a.own_lo >= 0 ? si - (gi - cs) : si + 1;
                 if (hi > lo) {
                     beg = lo;
                     cnt = hi - lo;
@@ -1183,7 +1218,9 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
                     qn -= 32;
                     if (have_pf) {
                         double4 g;
-                        if (pair_eval2<ND>(k, pf, shiftv[tf][0], shiftv[tf][1], shiftv[tf][2],
+                        const bool same = sf >= cs && sf < ce;  // pencil mode only
+                        if ((!same || pos_after(pf, pi)) &&
+                            pair_eval2<ND>(k, pf, shiftv[tf][0], shiftv[tf][1], shiftv[tf][2],
                                            pi.x, pi.y, pi.z, pi.w, u, fx, fy, fz, g)) {
                             ++npair;
                             red_acc(a.acc, a.nacc, sf, g.x, g.y, g.z, g.w);
@@ -1200,7 +1237,9 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
         }
         if (have_pf) {
             double4 g;
-            if (pair_eval2<ND>(k, pf, shiftv[tf][0], shiftv[tf][1], shiftv[tf][2], pi.x, pi.y,
+            const bool same = sf >= cs && sf < ce;
+            if ((!same || pos_after(pf, pi)) &&
+                pair_eval2<ND>(k, pf, shiftv[tf][0], shiftv[tf][1], shiftv[tf][2], pi.x, pi.y,
                                pi.z, pi.w, u, fx, fy, fz, g)) {
                 ++npair;
                 red_acc(a.acc, a.nacc, sf, g.x, g.y, g.z, g.w);
@@ -1212,7 +1251,10 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
             const double4 pj = a.xyzq[cd & 0x7ffffff];
             const int t = static_cast<unsigned>(cd) >> 27;
             double4 g;
-            if (pair_eval2<ND>(k, pj, shiftv[t][0], shiftv[t][1], shiftv[t][2], pi.x, pi.y, pi.z,
+            const int sj = cd & 0x7ffffff;
+            const bool same = sj >= cs && sj < ce;
+            if ((!same || pos_after(pj, pi)) &&
+                pair_eval2<ND>(k, pj, shiftv[t][0], shiftv[t][1], shiftv[t][2], pi.x, pi.y, pi.z,
                                pi.w, u, fx, fy, fz, g)) {
                 ++npair;
                 red_acc(a.acc, a.nacc, cd & 0x7ffffff, g.x, g.y, g.z, g.w);
@@ -1277,6 +1319,10 @@ __global__ void __launch_bounds__(256) k_pair_half_ovf(HalfArgs a, const __grid_
             const int i0 = a.start[fc + z0], i1 = a.start[fc + z1];
             for (int i = i0 + warp; i < i1; i += nw) {
                 const double4 pi = a.xyzq[i];
+                if (a.own_lo >= 0) {  // another rank's target (distributed FFT)
+                    const int l = clampi(static_cast<int>(floor(pi.x / a.own_h)), 0, a.own_nx - 1);
+                    if (l < a.own_lo || l >= a.own_hi) continue;
+                }
                 // own slice of i: the cell whose range holds i
                 int cz = z0;
                 while (cz + 1 < z1 && a.start[fc + cz + 1] <= i) ++cz;
@@ -1298,10 +1344,12 @@ __global__ void __launch_bounds__(256) k_pair_half_ovf(HalfArgs a, const __grid_
                         const int f = (gx * a.F[1] + gy) * a.F[2] + gz;
                         int j0 = a.start[f];
                         const int j1 = a.start[f + 1];
-                        if (own && dz == 0) j0 = i + 1;
+                        const bool bypos = own && dz == 0 && a.own_lo >= 0;
+                        if (own && dz == 0 && !bypos) j0 = i + 1;
                         for (int j = j0; j < j1; ++j) {
                             double4 g;
-                            if (pair_eval2<ND>(k, a.xyzq[j], shiftv[t][0], shiftv[t][1],
+                            if ((!bypos || pos_after(a.xyzq[j], pi)) &&
+                                pair_eval2<ND>(k, a.xyzq[j], shiftv[t][0], shiftv[t][1],
                                                shiftv[t][2], pi.x, pi.y, pi.z, pi.w, u, fx, fy,
                                                fz, g)) {
                                 ++npair;
@@ -2284,6 +2332,7 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
     pair_cap_ = 2048;
     if (const char* e = std::getenv("ESP_PAIR_CAP")) pair_cap_ = std::max(256, std::min(4096, std::atoi(e) / 32 * 32));
     if (const char* e = std::getenv("ESP_PAIR_HALF")) half_mode_ = std::atoi(e);
+    if (const char* e = std::getenv("ESP_PENCIL_HALF")) pencil_half_ = std::atoi(e) != 0;
 }
 
 Engine::~Engine() {
@@ -2558,7 +2607,8 @@ void Engine::run_pair(long N, cudaStream_t s, int rank, int nranks, bool own_bin
     // takes the half-shell kernel for its x-range of blocks: partner terms on
     // other ranks' atoms are summed by the all-reduce.  The distributed FFT
     // (own_bins: plane-owned targets, possibly local inputs) keeps full lists.
-    if (half && !own_bins && run_pair_half(N, s, rank, nranks)) return;
+    if (half && (!own_bins || pencil_half_) && run_pair_half(N, s, rank, nranks, own_bins))
+        return;
     PairArgs a{};
     a.xyzq = d_xyzqA_;
     a.orig = d_origA_;
@@ -2660,11 +2710,29 @@ void Engine::run_pair(long N, cudaStream_t s, int rank, int nranks, bool own_bin
 // the most targets per CTA whose expected forward neighbourhood fits the
 // staging capacity while keeping >= 3 CTAs per SM in flight.  Returns false
 // (full-list kernel instead) when no block shape fits the period.
-bool Engine::run_pair_half(long N, cudaStream_t s, int rank, int nranks) {
+bool Engine::run_pair_half(long N, cudaStream_t s, int rank, int nranks, bool own_bins) {
     const Plan& p = plan_;
     int nd = 20;
     const PairConsts k = make_pair_consts(p, nd);
-    const double per_cell = static_cast<double>(N) / ncellF_;
+    double per_cell = static_cast<double>(N) / ncellF_;
+    if (own_bins) {
+        // distributed FFT: the inputs may be the rank's own atoms + ghosts only,
+        // so the density behind the staging capacity is measured over the
+        // columns around the rank's planes (cell starts read back: one small
+        // synchronous copy; these phases are not graph-captured)
+        const PencilGeom G = pencil_geometry(p, rank, nranks);
+        const double fw0 = p.box[0] / F_[0];
+        const int c0 = std::max(0, static_cast<int>(std::floor(G.x0 * p.h[0] / fw0)) - 1);
+        const int c1 = std::min(F_[0] - 1, static_cast<int>(std::floor(G.x1 * p.h[0] / fw0)) + 1);
+        const long per_col = static_cast<long>(F_[1]) * F_[2];
+        int se[2] = {0, 0};
+        CK(cudaMemcpyAsync(&se[0], d_startA_ + c0 * per_col, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&se[1], d_startA_ + (c1 + 1) * per_col, sizeof(int),
+                           cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        per_cell = std::max(per_cell, static_cast<double>(se[1] - se[0]) /
+                                          (static_cast<double>(c1 - c0 + 1) * per_col));
+    }
     const int M = pM_, Mz = pMz_;
     int sms = 148;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
@@ -2737,7 +2805,23 @@ bool Engine::run_pair_half(long N, cudaStream_t s, int rank, int nranks) {
     // slab decomposition: this rank's x-range of blocks (x-major block order)
     const long nbx = (F_[0] + a.bx - 1) / a.bx;
     const long per_x = nblocks_all / nbx;
-    const long xlo = nbx * rank / nranks, xhi = nbx * (rank + 1) / nranks;
+    long xlo = nbx * rank / nranks, xhi = nbx * (rank + 1) / nranks;
+    a.own_lo = -1;
+    if (own_bins) {
+        // distributed FFT: the blocks covering this rank's x-planes (one column
+        // of margin each side), targets filtered by their plane in the kernel
+        const PencilGeom G = pencil_geometry(p, rank, nranks);
+        a.own_lo = G.x0;
+        a.own_hi = G.x1;
+        a.own_nx = p.nf[0];
+        a.own_h = p.h[0];
+        const double X0 = G.x0 * p.h[0], X1 = G.x1 * p.h[0];
+        const int c0 = std::max(0, static_cast<int>(std::floor(X0 / a.fw[0])) - 1);
+        const int c1 = std::min(F_[0] - 1, static_cast<int>(std::floor(X1 / a.fw[0])) + 1);
+        xlo = c0 / a.bx;
+        xhi = (G.x1 >= p.nf[0]) ? nbx : std::min(nbx, static_cast<long>(c1 / a.bx + 1));
+        if (a.own_lo >= a.own_hi) xhi = xlo;
+    }
     a.blk0 = static_cast<int>(xlo * per_x);
     const long nblocks = (xhi - xlo) * per_x;
     if (N >= (1L << 27)) throw InvalidArgument("pair kernel: N must be < 2^27");

@@ -145,7 +145,7 @@ private:
     void alloc_bins(int sub);
     void prepare(long N, const double* pos, const double* q, double* qsum_dev, cudaStream_t s);
     void run_pair(long N, cudaStream_t s, int rank, int nranks, bool own_bins = false);
-    bool run_pair_half(long N, cudaStream_t s, int rank = 0, int nranks = 1);
+    bool run_pair_half(long N, cudaStream_t s, int rank = 0, int nranks = 1, bool own_bins = false);
     void run_grid(long N, cudaStream_t s, StageTimes* t);
     void run_spread(long N, cudaStream_t s, int rank, int nranks, double* grid,
                     const GridArgs* gslab = nullptr, long nreals = -1, int b0 = -1,
@@ -214,6 +214,8 @@ private:
     int* d_ovf_ = nullptr;
     double* d_acc_ = nullptr;           // half-shell K4: planar pair-sorted (u, F) sums, 4 x cap_              // half-shell K4: overflowed blocks (count, ids)
     long ovf_cap_ = 0;
+    bool pencil_half_ = true;           // distributed FFT with half-shell K4 (ESP_PENCIL_HALF=0: full
+                                        // lists); local inputs return the ghost partner terms (dist.py)
     int half_mode_ = 1;                 // half-shell K4: 0 never, 1 from kHalfMinN atoms, 2 always (ESP_PAIR_HALF)
 
     cufftHandle fwd_ = 0, inv_ = 0;

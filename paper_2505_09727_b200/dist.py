@@ -418,21 +418,25 @@ def ghost_masks(layout, r, x, box_x, r_c):
     return (x - X0) <= reach, (X1 - x) <= reach
 
 
-def exchange_ghosts(layout, rank, pos_own, q_own, box, r_c, group=None):
+def exchange_ghosts(layout, rank, pos_own, q_own, box, r_c, group=None, return_plan=False):
     """Send this rank's atoms near its x-faces to the neighbours and receive
     theirs (NCCL send/recv on the GPU box, gloo in the CPU tests): returns the
-    ghost positions (k, 3) and charges (k,).  pos_own must be folded."""
+    ghost positions (k, 3) and charges (k,).  pos_own must be folded.  With
+    return_plan, also the bookkeeping return_ghost_terms needs (peers in
+    receive order, own indices sent to each peer, rows received from each)."""
     import torch
     import torch.distributed as dist
     left, right = layout.neighbours(rank)
     to_l, to_r = ghost_masks(layout, rank, pos_own[:, 0], box[0], r_c)
     packed = torch.cat([pos_own, q_own[:, None]], dim=1)
-    sends = {}
+    sends, sent_idx = {}, {}
     if left == right:
-        sends[left] = packed[to_l | to_r]
+        sent_idx[left] = torch.nonzero(to_l | to_r).flatten()
     else:
-        sends[left] = packed[to_l]
-        sends[right] = packed[to_r]
+        sent_idx[left] = torch.nonzero(to_l).flatten()
+        sent_idx[right] = torch.nonzero(to_r).flatten()
+    for p_, idx in sent_idx.items():
+        sends[p_] = packed[idx]
     peers = sorted(sends)
     cnt_out = {p: torch.tensor([sends[p].shape[0]], dtype=torch.int64, device=pos_own.device)
                for p in peers}
@@ -450,7 +454,43 @@ def exchange_ghosts(layout, rank, pos_own, q_own, box, r_c, group=None):
         for req in dist.batch_isend_irecv(ops):
             req.wait()
     g = torch.cat([recv[p] for p in peers], dim=0)
+    if return_plan:
+        plan = {"peers": peers, "sent_idx": sent_idx,
+                "recv_cnt": {p: recv[p].shape[0] for p in peers}}
+        return g[:, :3].contiguous(), g[:, 3].contiguous(), plan
     return g[:, :3].contiguous(), g[:, 3].contiguous()
+
+
+def return_ghost_terms(plan, ghost_rows, own_rows, group=None):
+    """Reverse of exchange_ghosts for the half-shell pair sum
+    (ESP_PENCIL_HALF=1): a rank's evaluation leaves partner terms
+    (u, Fx, Fy, Fz) on its ghost atoms; each ghost row goes back to the rank
+    that owns the atom and is added to that atom's row there.  ghost_rows:
+    (k, 4) in receive order; own_rows: (n, 4), updated in place."""
+    import torch
+    import torch.distributed as dist
+    peers = plan["peers"]
+    segs, o = {}, 0
+    for p in peers:
+        segs[p] = ghost_rows[o:o + plan["recv_cnt"][p]].contiguous()
+        o += plan["recv_cnt"][p]
+    back = {p: torch.empty((plan["sent_idx"][p].numel(), 4), dtype=own_rows.dtype,
+                           device=own_rows.device) for p in peers}
+    ops = [dist.P2POp(dist.isend, segs[p], p, group) for p in peers if segs[p].shape[0] > 0]
+    ops += [dist.P2POp(dist.irecv, back[p], p, group) for p in peers if back[p].shape[0] > 0]
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    for p in peers:
+        if back[p].shape[0] > 0:
+            own_rows.index_add_(0, plan["sent_idx"][p].to(own_rows.device), back[p])
+
+
+def pencil_half_enabled() -> bool:
+    """The distributed FFT's K4 runs half-shell unless ESP_PENCIL_HALF=0 (read
+    by the engine when a plan is built); local inputs then return ghost terms."""
+    import os
+    return os.environ.get("ESP_PENCIL_HALF", "1") != "0"
 
 
 def evaluate_pencil_local(plan, box, pos_own, q_own, layout, rank, r_c, stream=0, group=None,
@@ -465,7 +505,8 @@ def evaluate_pencil_local(plan, box, pos_own, q_own, layout, rank, r_c, stream=0
     import torch.distributed as dist
     check_ghost_reach(layout, box[0], r_c)
     pos_own = fold_positions(pos_own, box)
-    gpos, gq = exchange_ghosts(layout, rank, pos_own, q_own, box, r_c, group)
+    gpos, gq, gplan = exchange_ghosts(layout, rank, pos_own, q_own, box, r_c, group,
+                                      return_plan=True)
     pos_l = torch.cat([pos_own, gpos], dim=0).contiguous()
     q_l = torch.cat([q_own, gq]).contiguous()
     n_own, n = q_own.numel(), q_l.numel()
@@ -476,6 +517,16 @@ def evaluate_pencil_local(plan, box, pos_own, q_own, layout, rank, r_c, stream=0
             cache["bufs"] = bufs
     out = evaluate_pencil(plan, box, n, pos_l.reshape(-1), q_l, bufs, layout, rank, stream,
                           group, engine, reduce_outputs=False)
+    if pencil_half_enabled():
+        # half-shell K4: the ghost rows hold partner terms owed to their owners;
+        # return them, then E = 1/2 sum q u over the owned atoms (ewald.hpp:641-647)
+        rows = torch.cat([out[:n, None], out[n:4 * n].reshape(n, 3)], dim=1)
+        own_rows = rows[:n_own].clone()
+        return_ghost_terms(gplan, rows[n_own:], own_rows, group)
+        e = (0.5 * torch.dot(q_own.to(own_rows.dtype), own_rows[:, 0])).reshape(1)
+        if dist.is_available() and dist.is_initialized():
+            dist.all_reduce(e, group=group)
+        return own_rows[:, 0].contiguous(), own_rows[:, 1:].contiguous(), e
     e = out[4 * n:].clone()
     if dist.is_available() and dist.is_initialized():
         dist.all_reduce(e, group=group)

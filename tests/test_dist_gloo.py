@@ -389,3 +389,54 @@ def test_ghost_selection_host():
             inside = (posf[:, 0] >= X0) & (posf[:, 0] < X1)
             need = inside | (d < 1.0)
             assert (have | ~need).all()
+
+
+def _ghost_return_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2505_09727_b200.dist import return_ghost_terms
+    # ring: each rank sent atoms sent_idx[p] to peer p and received ghosts from p
+    left, right = (rank - 1) % world, (rank + 1) % world
+    peers = sorted({left, right})
+    n_own = 10
+    sent_idx = {p: torch.tensor([(3 * p + k) % n_own for k in range(2 + p)]) for p in peers}
+    # the ghosts this rank holds from peer p are the atoms p sent to this rank:
+    # p's sent_idx[rank] has 2 + rank entries
+    recv_cnt = {p: 2 + rank for p in peers}
+    rows = []
+    for p in peers:
+        for k in range(recv_cnt[p]):
+            # term owed to atom k of p's send list to `rank`, tagged by (sender, k)
+            rows.append([1000.0 * rank + k, p, k, 1.0])
+    ghost_rows = torch.tensor(rows, dtype=torch.float64)
+    own_rows = torch.zeros((n_own, 4), dtype=torch.float64)
+    return_ghost_terms({"peers": peers, "sent_idx": sent_idx, "recv_cnt": recv_cnt},
+                       ghost_rows, own_rows)
+    out[rank] = (own_rows.numpy().copy(), {p: sent_idx[p].numpy().copy() for p in peers})
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_return_ghost_terms_gloo(world):
+    """dist.return_ghost_terms (the half-shell distributed FFT's reverse ghost
+    exchange): every ghost row reaches the rank that owns the atom and is added
+    at the index that rank sent it from."""
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_ghost_return_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    for r in range(world):
+        own, sent = out[r]
+        expect = np.zeros((10, 4))
+        for p, idx in sent.items():
+            for k, i in enumerate(idx):
+                expect[i] += [1000.0 * p + k, r, k, 1.0]
+        assert np.array_equal(own, expect)
+
+
+@pytest.mark.parametrize("world", [2])
+def test_pencil_local_inputs_full_list_mode_gloo(world, monkeypatch):
+    """ESP_PENCIL_HALF=0 path of evaluate_pencil_local (no reverse exchange,
+    the engine's energy); the default path (half-shell: reverse ghost exchange,
+    energy from the owned rows) is test_pencil_local_inputs_gloo."""
+    monkeypatch.setenv("ESP_PENCIL_HALF", "0")
+    test_pencil_local_inputs_gloo(world)

@@ -81,12 +81,17 @@ def test_pencil_refuses_thin_slabs(esp, gpu):
         esp.pencil_geometry(plan, 0, 8)
 
 
-def _pencil_local(esp, box, pos, q, eps, r_c, nranks):
+def _pencil_local(esp, box, pos, q, eps, r_c, nranks, half=None):
     """Local inputs: each emulated rank gets only its own atoms plus the
-    ghosts its x-neighbours would send it (dist.ghost_masks)."""
+    ghosts its x-neighbours would send it (dist.ghost_masks).  Ghost rows
+    (partner terms of a half-shell K4; zero with full lists) are added to
+    their owners' rows, as dist.return_ghost_terms does; with half=True the
+    energy is 1/2 sum q u over the gathered owned rows."""
     from paper_2505_09727_b200.dist import (PencilBuffers, PencilLayout, atom_owner,
                                             evaluate_pencil_emulated, fold_positions,
-                                            ghost_masks)
+                                            ghost_masks, pencil_half_enabled)
+    if half is None:
+        half = pencil_half_enabled()
     dev = torch.device("cuda", 0)
     N = q.size
     plans = [esp.build_plan(box, "pswf", eps, r_c, device=0) for _ in range(nranks)]
@@ -100,7 +105,7 @@ def _pencil_local(esp, box, pos, q, eps, r_c, nranks):
         mine = np.nonzero(own == r)[0]
         gh = (own == left) & masks[left][1] | (own == right) & masks[right][0]
         loc = np.concatenate([mine, np.nonzero(gh & (own != r))[0]])
-        idx.append(mine)
+        idx.append(loc)
         Ns.append(loc.size)
         poss.append(torch.from_numpy(np.ascontiguousarray(pos[loc]).ravel()).to(dev))
         qs.append(torch.from_numpy(q[loc]).to(dev))
@@ -111,10 +116,12 @@ def _pencil_local(esp, box, pos, q, eps, r_c, nranks):
     u, F, E = np.zeros(N), np.zeros((N, 3)), 0.0
     for r in range(nranks):
         o = outs[r].cpu().numpy()
-        n, m = Ns[r], idx[r].size
-        u[idx[r]] = o[:m]
-        F[idx[r]] = o[n:4 * n].reshape(n, 3)[:m]
+        n = Ns[r]
+        np.add.at(u, idx[r], o[:n])                       # own rows + returned ghost rows
+        np.add.at(F, idx[r], o[n:4 * n].reshape(n, 3))
         E += float(o[4 * n])
+    if half:
+        E = 0.5 * float(np.dot(q, u))
     return u, F, E
 
 

@@ -22,7 +22,7 @@ import paper_2505_09727_b200 as E  # noqa: E402
 from paper_2505_09727_b200 import systems as S  # noqa: E402
 from paper_2505_09727_b200.dist import (PencilBuffers, PencilLayout, _Lib,  # noqa: E402
                                         atom_owner, evaluate_pencil_emulated, fold_positions,
-                                        ghost_masks)
+                                        ghost_masks, pencil_half_enabled)
 
 
 def main():
@@ -100,8 +100,10 @@ def main():
             halo_bytes = 2 * lay.halo * pl * (1 + lay.nfields)          # out: slab + field halos
             a2a = 8 * (sum(lay.fwd_send_splits(r)) - lay.fwd_send_splits(r)[r]) * \
                 (1 + (2 if lay.nfields == 4 else 1))                    # fwd + A (+B), off-rank
-            if local:  # ghosts out (32 B each, about the ghosts received) + energy
-                t["bytes_out"] = halo_bytes + a2a + 32 * (Nr - nown[r]) + 8
+            if local:  # ghosts out (32 B each, about the ghosts received) + energy;
+                # half-shell K4: plus the ghost rows' partner terms returned (32 B each)
+                back = 32 * (Nr - nown[r]) if pencil_half_enabled() else 0
+                t["bytes_out"] = halo_bytes + a2a + 32 * (Nr - nown[r]) + back + 8
                 t["atoms_own"], t["atoms_ghost"] = nown[r], Nr - nown[r]
             else:      # + output all-reduce
                 t["bytes_out"] = halo_bytes + a2a + 8 * (4 * N + 1)
