@@ -970,7 +970,9 @@ __device__ __forceinline__ void fwd_col(int l, int M, int& dx, int& dy) {
     }
 }
 
-template <int ND>
+// OWN: distributed-FFT instantiation (plane-ownership targets, position-based
+// same-cell base); the single-GPU one carries none of those checks.
+template <int ND, bool OWN>
 __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const __grid_constant__ PairConsts k) {
     extern __shared__ __align__(16) unsigned char smem[];
     float4* cand = reinterpret_cast<float4*>(smem);                 // a.cap + 1 (sentinel)
@@ -1130,7 +1132,7 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
         // distributed FFT: same-cell partners of i, as global sorted indices
         // [cs, ce) (base by position, see HalfArgs); cs = ce = 0 otherwise
         int cs = 0, ce = 0;
-        if (a.own_lo >= 0) {
+        if (OWN) {
             const int l = clampi(static_cast<int>(floor(pi.x / a.own_h)), 0, a.own_nx - 1);
             if (l < a.own_lo || l >= a.own_hi) {  // another rank's target
                 int nx = 0;
@@ -1171,7 +1173,7 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
                 const int hi = ent_off[col * nsl + khi + 1];
                 // own column: after i (pencil mode: from i's cell start, the
                 // same-cell pairs being decided by position in the rounds)
-                if (fc >> 8) lo = a.own_lo >= 0 ? si - (gi - cs) : si + 1;
+                if (fc >> 8) lo = OWN ? si - (gi - cs) : si + 1;
                 if (hi > lo) {
                     beg = lo;
                     cnt = hi - lo;
@@ -1218,7 +1220,7 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
                     qn -= 32;
                     if (have_pf) {
                         double4 g;
-                        const bool same = sf >= cs && sf < ce;  // pencil mode only
+                        const bool same = OWN && sf >= cs && sf < ce;
                         if ((!same || pos_after(pf, pi)) &&
                             pair_eval2<ND>(k, pf, shiftv[tf][0], shiftv[tf][1], shiftv[tf][2],
                                            pi.x, pi.y, pi.z, pi.w, u, fx, fy, fz, g)) {
@@ -1237,7 +1239,7 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
         }
         if (have_pf) {
             double4 g;
-            const bool same = sf >= cs && sf < ce;
+            const bool same = OWN && sf >= cs && sf < ce;
             if ((!same || pos_after(pf, pi)) &&
                 pair_eval2<ND>(k, pf, shiftv[tf][0], shiftv[tf][1], shiftv[tf][2], pi.x, pi.y,
                                pi.z, pi.w, u, fx, fy, fz, g)) {
@@ -1252,7 +1254,7 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
             const int t = static_cast<unsigned>(cd) >> 27;
             double4 g;
             const int sj = cd & 0x7ffffff;
-            const bool same = sj >= cs && sj < ce;
+            const bool same = OWN && sj >= cs && sj < ce;
             if ((!same || pos_after(pj, pi)) &&
                 pair_eval2<ND>(k, pj, shiftv[t][0], shiftv[t][1], shiftv[t][2], pi.x, pi.y, pi.z,
                                pi.w, u, fx, fy, fz, g)) {
@@ -2843,14 +2845,14 @@ bool Engine::run_pair_half(long N, cudaStream_t s, int rank, int nranks, bool ow
         CK(cudaGetLastError());
     };
     switch (nd) {
-        case 14: go(k_pair_half<14>, k_pair_half_ovf<14>); break;
-        case 15: go(k_pair_half<15>, k_pair_half_ovf<15>); break;
-        case 16: go(k_pair_half<16>, k_pair_half_ovf<16>); break;
-        case 17: go(k_pair_half<17>, k_pair_half_ovf<17>); break;
-        case 18: go(k_pair_half<18>, k_pair_half_ovf<18>); break;
-        case 20: go(k_pair_half<20>, k_pair_half_ovf<20>); break;
-        case 28: go(k_pair_half<28>, k_pair_half_ovf<28>); break;
-        default: go(k_pair_half<kMaxPoly>, k_pair_half_ovf<kMaxPoly>); break;
+        case 14: (own_bins ? go(k_pair_half<14, true>, k_pair_half_ovf<14>) : go(k_pair_half<14, false>, k_pair_half_ovf<14>)); break;
+        case 15: (own_bins ? go(k_pair_half<15, true>, k_pair_half_ovf<15>) : go(k_pair_half<15, false>, k_pair_half_ovf<15>)); break;
+        case 16: (own_bins ? go(k_pair_half<16, true>, k_pair_half_ovf<16>) : go(k_pair_half<16, false>, k_pair_half_ovf<16>)); break;
+        case 17: (own_bins ? go(k_pair_half<17, true>, k_pair_half_ovf<17>) : go(k_pair_half<17, false>, k_pair_half_ovf<17>)); break;
+        case 18: (own_bins ? go(k_pair_half<18, true>, k_pair_half_ovf<18>) : go(k_pair_half<18, false>, k_pair_half_ovf<18>)); break;
+        case 20: (own_bins ? go(k_pair_half<20, true>, k_pair_half_ovf<20>) : go(k_pair_half<20, false>, k_pair_half_ovf<20>)); break;
+        case 28: (own_bins ? go(k_pair_half<28, true>, k_pair_half_ovf<28>) : go(k_pair_half<28, false>, k_pair_half_ovf<28>)); break;
+        default: (own_bins ? go(k_pair_half<kMaxPoly, true>, k_pair_half_ovf<kMaxPoly>) : go(k_pair_half<kMaxPoly, false>, k_pair_half_ovf<kMaxPoly>)); break;
     }
     launches_ += 3;
     return true;
