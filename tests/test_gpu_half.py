@@ -114,3 +114,27 @@ def test_half_evaluate_repeated_and_resized(esp, gpu, monkeypatch):
     assert max_rel(l2.u, r2.u) <= 1e-12 and rel_rms(l2.F, r2.F) <= 1e-12
     c1 = esp.evaluate(plan, s1)
     assert rel_rms(c1.F, a.F) <= 1e-13
+
+
+def test_half_gaussian_family(esp, gpu, monkeypatch):
+    """Gaussian (Ewald) split: the pair polynomial is the erf kernel's (longer)
+    -- half-shell against full lists at N >= 4096."""
+    rng = np.random.default_rng(5)
+    L = 40.0
+    n = 8000
+    pos = rng.uniform(0.0, L, size=(n, 3))
+    q = np.where(np.arange(n) % 2 == 0, 1.0, -1.0)
+    box = np.array([L, L, L])
+    sysm = esp.ParticleSystem(box, q, pos)
+    monkeypatch.setenv("ESP_PAIR_HALF", "0")
+    full = esp.build_plan(box, "gaussian", 1e-4, 5.0, device=gpu)
+    lf = esp.local_sum(full, sysm)
+    nf = full.last_pair_count()
+    monkeypatch.setenv("ESP_PAIR_HALF", "2")
+    half = esp.build_plan(box, "gaussian", 1e-4, 5.0, device=gpu)
+    lh = esp.local_sum(half, sysm)
+    assert half.last_pair_count() == nf > 0
+    assert max_rel(lh.u, lf.u) <= 1e-12
+    assert rel_rms(lh.F, lf.F) <= 1e-12
+    a, b = esp.evaluate(full, sysm), esp.evaluate(half, sysm)
+    assert abs(a.energy - b.energy) <= 1e-12 * abs(a.energy)
