@@ -1,21 +1,31 @@
 #!/usr/bin/env python
 """ESP force-evaluation benchmark (BASELINE.json metric: atoms*evals/s).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg5]
     python bench.py --impl reference ...      # the reference CPU arm
 
-One step = one full ESP evaluation (real-space pair sum + spread + FFT +
-influence/ik multiply + 4 inverse FFTs + interpolation + energy) of the
-workload, with positions/charges already resident in HBM (`value`).  `e2e`
-is the same metric through the public API on pinned HOST buffers
-(H2D of positions+charges and D2H of potentials, forces and energy inside
-the timed region).  Under torchrun each rank evaluates its own seeded replica
-(weak scaling, no data-path collective).
+Workload: cfg5 by default -- BASELINE configs[4], the 8,000,001-atom water box
+the metric is quoted on at 1/2/4/8 B200 (it fits one GPU).  One step = one
+full ESP evaluation (real-space pair sum + spread + FFT + influence/ik
+multiply + 4 inverse FFTs + interpolation + energy) with positions/charges
+already resident in HBM (`value`).  `e2e` is the same metric through the
+public API on pinned HOST buffers (H2D of positions+charges and D2H of
+potentials, forces and energy inside the timed region).
+
+--gpus N > 1: bench.py launches itself under torch.distributed.run when
+WORLD_SIZE is unset (one rank per GPU, NCCL).  The default decomposition for
+cfg3/cfg4/cfg5 is ONE system sharded over the ranks (distributed FFT with
+local atoms + ghosts, strong scaling, value = N_atoms / max-over-ranks step
+time); cfg1/cfg2 (too small to shard) run replicas (weak scaling).
 
 Timing: W >= 3 warm-up steps; then K steps, each preceded by a 256 MiB L2
 flush (outside the event pair) and bracketed by CUDA events on the stream
 the kernels run on; barrier + synchronize around the timed loop; the max
 over ranks is reported.  nvidia-smi clocks are sampled while it runs.
+
+The reference arm (--impl reference) runs the compiled, unmodified reference
+(oracle/_ref/libesp_ref.so) on all host cores; it never loads this repo's
+CUDA library (systems.py is loaded by file path, not through the package).
 """
 from __future__ import annotations
 
@@ -41,30 +51,86 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--workload", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--force-method", default="ik", choices=["ik", "ad"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
-                    help="budget of the cpu_baseline sample (rank 0, N=1)")
+                    help="budget of the cpu_baseline sample (rank 0, N=1; at least one "
+                         "full evaluate)")
+    ap.add_argument("--ref-seconds", type=float, default=240.0,
+                    help="--impl reference: timed-step budget (at least one step, at most "
+                         "--steps)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--decomp", choices=["replicas", "slab", "pencil", "pencil-local"],
-                    default="replicas",
+    ap.add_argument("--decomp", choices=["auto", "replicas", "slab", "pencil", "pencil-local"],
+                    default="auto",
                     help="N>1: replicas = one independent system per rank (weak scaling); "
                          "slab = ONE system, x-slabs, NCCL all-reduce of the charge grid and "
                          "outputs; pencil = ONE system with the grid/spectrum/fields split too "
                          "(halo exchanges + all-to-all transposes); pencil-local = the same "
                          "with every rank holding only its own atoms (ghost exchange, energy "
-                         "all-reduce)")
+                         "all-reduce); auto = pencil-local for cfg3/4/5, replicas for "
+                         "cfg1/2")
     ap.add_argument("--strong", action="store_true", help="alias of --decomp slab")
     args = ap.parse_args()
     if args.strong:
         args.decomp = "slab"
+    if args.decomp == "auto":
+        args.decomp = "pencil-local" if args.workload in ("cfg3", "cfg4", "cfg5") else "replicas"
     args.warmup = max(args.warmup, 3)
     return args
 
 
 def dist_env():
-    from paper_2505_09727_b200.dist import env
-    return env()
+    """(rank, world_size, local_rank) from the torchrun environment."""
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def load_systems():
+    """paper_2505_09727_b200/systems.py loaded by file path: pure numpy, and
+    importing it this way does not run the package __init__ (which dlopens
+    libesp_b200.so) -- the reference arm must not load the repo's library."""
+    import importlib.util
+    name = "_esp_bench_systems"
+    if name in sys.modules:
+        return sys.modules[name]
+    spec = importlib.util.spec_from_file_location(
+        name, os.path.join(ROOT, "paper_2505_09727_b200", "systems.py"))
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules[name] = mod
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def parallelism(decomp: str, world: int) -> str:
+    if world <= 1:
+        return "single GPU"
+    return {"slab": f"x-slabs x{world} (NCCL all-reduce of grid + outputs)",
+            "pencil": f"distributed FFT x{world} (NCCL halo send/recv + all-to-all transposes)",
+            "pencil-local": f"distributed FFT x{world}, local atoms + ghosts (NCCL ghost/halo "
+                            "send/recv, all-to-all transposes, energy all-reduce)",
+            }.get(decomp, f"replicas x{world}")
+
+
+def bench_config(c, N, box, nf, P, force_method, decomp, world) -> dict:
+    """The `config` dict, identical in both arms (same workload, same keys)."""
+    return {"workload": c.name, "N": int(N), "box_L": box[0], "r_c": c.r_c, "eps": c.eps,
+            "nf": [int(v) for v in nf], "P": int(P), "force_method": force_method,
+            "parallelism": parallelism(decomp, world),
+            "l2": "GPU arm: 256 MiB flush write before every timed step (outside the events); "
+                  "inputs (32 B/atom) also exceed L2 at cfg3-5"}
+
+
+def spawn_ranks(args) -> int:
+    """--gpus N > 1 without a torchrun environment: relaunch this script under
+    torch.distributed.run (one rank per GPU, rendezvous on 127.0.0.1)."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 class ClockSampler:
@@ -126,73 +192,98 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_reference_rate(c, pos, q, box, budget_s: float, min_evals: int = 1):
-    """Time the compiled reference (oracle/_ref) on the host cores."""
+def _ref_lib():
+    """oracle/ref.py (ctypes binding of oracle/_ref/libesp_ref.so)."""
     from oracle import ref
+    return ref
+
+
+def cpu_reference_rate(c, pos, q, box, budget_s: float):
+    """cpu_baseline: the compiled reference (oracle/_ref) on the host cores,
+    a bounded sample -- evaluate() calls of the full workload until about
+    budget_s of CPU time has been spent (at least one; no warm-up call when
+    one evaluation alone exceeds the budget)."""
+    ref = _ref_lib()
     if not ref.available():
         return None
     cores = os.cpu_count() or 1
     ref.set_threads(cores)
     plan = ref.RefPlan(box, "pswf", c.eps, c.r_c)
     t0 = time.perf_counter()
-    r = plan.evaluate(pos, q)  # warm-up (first-touch, thread start-up)
+    r = plan.evaluate(pos, q)
     first = time.perf_counter() - t0
     times, stages = [], []
+    warm = first < 0.5 * budget_s
+    if not warm:
+        times.append(first)
+        stages.append(r.timings)
     t_end = time.perf_counter() + budget_s
-    while len(times) < min_evals or (time.perf_counter() + first < t_end):
+    while not times or (time.perf_counter() + statistics.mean(times) < t_end and len(times) < 50):
         t0 = time.perf_counter()
         r = plan.evaluate(pos, q)
         times.append(time.perf_counter() - t0)
         stages.append(r.timings)
-        if len(times) >= 50:
-            break
     mean = statistics.mean(times)
     st = {k: statistics.mean(s[k] for s in stages) for k in stages[0]}
     return {"value": q.size / mean, "unit": UNIT, "cores": cores, "kind": "reference",
-            "sample": f"{c.name}: full system, {len(times)} evaluate() calls after 1 warm-up, "
+            "sample": f"{c.name}: full system, {len(times)} evaluate() call(s)"
+                      f"{' after 1 warm-up' if warm else ' (no warm-up)'}, "
                       f"esp::thread_count()={cores}; FFT stage uses the oracle's FFTW3 shim",
             "s_per_eval": mean, "stage_s": st, "energy": r.energy}
 
 
 def run_reference(args):
+    """--impl reference: the compiled, unmodified reference evaluate()
+    (ewald.hpp:619-649 via oracle/_ref) on all host cores, same workload and
+    config as the GPU arm.  Under torchrun only rank 0 runs.  Each step is one
+    full evaluate(); one untimed warm-up (a CPU code has no JIT/caches to
+    warm beyond first touch), then timed steps until --steps or the
+    --ref-seconds budget is reached (at least one) -- a cfg5 evaluate takes
+    ~40 s on 16 host threads."""
     rank, world, local = dist_env()
     if rank != 0:
         return 0
-    from oracle import ref
-    from paper_2505_09727_b200 import systems as S
+    S = load_systems()
+    ref = _ref_lib()
     c = S.config(args.workload)
-    pos, q, box = c.system()
-    cfg = {"workload": c.name, "N": int(q.size), "box_L": box[0], "r_c": c.r_c, "eps": c.eps,
-           "force_method": "ik"}
     if not ref.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libesp_ref.so not built"}))
         return 0
+    pos, q, box = c.system()
     cores = os.cpu_count() or 1
     ref.set_threads(cores)
     plan = ref.RefPlan(box, "pswf", c.eps, c.r_c)
-    cfg.update(nf=list(plan.nf), P=plan.P)
-    for _ in range(args.warmup):
-        plan.evaluate(pos, q)
+    cfg = bench_config(c, q.size, box, plan.nf, plan.P, "ik", args.decomp, world)
+    t0 = time.perf_counter()
+    plan.evaluate(pos, q)
+    t_warm = time.perf_counter() - t0
     times = []
-    for _ in range(args.steps):
+    t_end = time.perf_counter() + args.ref_seconds
+    while len(times) < args.steps and (not times or time.perf_counter() + t_warm < t_end):
         t0 = time.perf_counter()
         plan.evaluate(pos, q)
         times.append(time.perf_counter() - t0)
     s = statistics.mean(times)
     value = q.size / s
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": s * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded generators, SURVEY.md 8(d))", "config": cfg,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": len(times), "steps_requested": args.steps, "warmup": 1,
+        "warmup_requested": args.warmup, "ms_per_step": s * 1e3,
+        "higher_is_better": True,
+        "scaling": "strong" if (world > 1 and args.decomp != "replicas") else "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generators, SURVEY.md 8(d); water-like boxes by "
+                "paper_2505_09727_b200/systems.py water_box)",
+        "config": cfg,
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": f"{c.name}: one full evaluate() per step on all "
                                    f"{cores} host threads (oracle/_ref, unmodified headers + "
-                                   "FFTW3 shim)"},
+                                   f"FFTW3 shim); {len(times)} timed step(s) after 1 warm-up "
+                                   f"(budget {args.ref_seconds:g} s)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
     return 0
 
 
@@ -206,7 +297,7 @@ def run_ours(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2505_09727_b200 as E
-    from paper_2505_09727_b200 import systems as S
+    S = load_systems()
 
     from paper_2505_09727_b200.dist import max_over_ranks, replica_seed, weak_scaling_value
     base = S.config(args.workload)
@@ -298,7 +389,7 @@ def run_ours(args):
     for _ in range(5):
         ef = E.evaluate(plan, E.ParticleSystem(box, q, pos), timings=True)
         tim.append(ef.timings)
-    stages_ms = {k: statistics.median(t[k] for t in tim) * 1e3 for k in tim[0]}
+    stages_ms = {k: statistics.median(t[k] for t in tim) * 1e3 for k in tim[0] if k != "total"}
     ordered_pairs = plan.last_pair_count()
     pair_flops = FLOPS_PER_UNORDERED_PAIR * ordered_pairs / 2.0
     t_pair = stages_ms["local"] * 1e-3
@@ -397,7 +488,7 @@ def run_ours(args):
             torch.cuda.synchronize()
     else:
         def e2e_step():
-            E.evaluate(plan, sysh, out=(u_h, F_h))
+            E.evaluate(plan, sysh, timings=False, out=(u_h, F_h))
     for _ in range(2):
         e2e_step()
     if dist:
@@ -427,17 +518,8 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generators, SURVEY.md 8(d); water-like boxes by "
                     "paper_2505_09727_b200/systems.py water_box)",
-            "config": {"workload": c.name, "N": N, "box_L": box[0], "r_c": c.r_c, "eps": c.eps,
-                       "nf": list(plan.nf), "P": plan.P, "force_method": plan.force_method,
-                       "parallelism": (f"x-slabs x{world} (NCCL all-reduce of grid + outputs)"
-                                       if decomp == "slab" else
-                                       f"distributed FFT x{world} (NCCL halo send/recv + "
-                                       "all-to-all transposes)" if decomp == "pencil" else
-                                       f"distributed FFT x{world}, local atoms + ghosts "
-                                       "(NCCL ghost/halo send/recv, all-to-all transposes, "
-                                       "energy all-reduce)" if decomp == "pencil-local" else
-                                       f"replicas x{world}" if world > 1 else "single GPU"),
-                       "l2": "256 MiB flush write before every timed step (outside the events)"},
+            "config": bench_config(c, N, box, plan.nf, plan.P, plan.force_method, decomp,
+                                   world),
             "impl": "ours",
             "energy": energy,
             "clocks": clk,
@@ -461,6 +543,8 @@ def run_ours(args):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -31,6 +31,7 @@
 
 #include <algorithm>
 #include <array>
+#include <chrono>
 #include <cmath>
 #include <complex>
 #include <limits>
@@ -86,6 +87,8 @@ struct EnergyForces {  // system.hpp:49-55
     std::vector<double> u;
     std::vector<Vec3> F;
     std::map<std::string, double> timings;
+    // GPU-only stage times (not in the reference's struct): "bin", "total"
+    std::map<std::string, double> device_timings;
 };
 
 struct PartialField {  // ewald.hpp:411-414
@@ -326,23 +329,38 @@ inline void require_neutral(const ParticleSystem& s) {
     detail::check(esp_check_neutral(static_cast<long>(s.size()), s.q.data()));
 }
 
-// ewald.hpp:619-649 (GPU)
-inline EnergyForces evaluate(const EwaldPlan& plan, const ParticleSystem& s) {
+// ewald.hpp:619-649 (GPU).  Like the reference, `timings` holds the per-stage
+// wall times (seconds) under exactly its keys {local, spread, fft, scale,
+// ifft, interpolate}: CUDA events around each stage, the stages serialised on
+// one stream as the reference runs them.  GPU-only times go to
+// `device_timings` ("bin": fold, cell keys and sorts; "total": host wall time
+// of the call).  stage_timings = false selects the overlapped CUDA-graph path
+// (real-space sum concurrent with the grid pipeline); the six keys are then
+// 0 and only device_timings["total"] is measured.
+inline EnergyForces evaluate(const EwaldPlan& plan, const ParticleSystem& s,
+                             bool stage_timings = true) {
     const long N = static_cast<long>(s.size());
     if (s.pos.size() != s.q.size()) throw std::invalid_argument("evaluate: pos/q length mismatch");
     EnergyForces out;
     out.u.resize(N);
     out.F.resize(N);
     esp_timings t{};
+    const auto t0 = std::chrono::steady_clock::now();
     {
         std::lock_guard<std::mutex> lk(plan.mutex());
         detail::check(esp_evaluate(plan.handle(), s.box.data(), N, detail::flat(s.pos),
                                    s.q.data(), out.u.data(), detail::flat(out.F), &out.energy,
-                                   nullptr));
+                                   stage_timings ? &t : nullptr));
     }
-    for (const char* k : {"local", "spread", "fft", "scale", "ifft", "interpolate"})
-        out.timings[k] = 0.0;  // per-stage times: esp_evaluate(..., &timings)
-    (void)t;
+    out.timings["local"] = t.local;
+    out.timings["spread"] = t.spread;
+    out.timings["fft"] = t.fft;
+    out.timings["scale"] = t.scale;
+    out.timings["ifft"] = t.ifft;
+    out.timings["interpolate"] = t.interpolate;
+    out.device_timings["bin"] = t.bin;
+    out.device_timings["total"] =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return out;
 }
 
@@ -363,12 +381,18 @@ inline PartialField spectral_sum(const EwaldPlan& plan, const ParticleSystem& s,
     PartialField f;
     f.u.resize(s.size());
     f.F.resize(s.size());
+    esp_timings t{};
     std::lock_guard<std::mutex> lk(plan.mutex());
     detail::check(esp_spectral_sum(plan.handle(), s.box.data(), static_cast<long>(s.size()),
                                    detail::flat(s.pos), s.q.data(), f.u.data(),
-                                   detail::flat(f.F)));
-    if (timings)
-        for (const char* k : {"spread", "fft", "scale", "ifft", "interpolate"}) (*timings)[k] += 0.0;
+                                   detail::flat(f.F), timings ? &t : nullptr));
+    if (timings) {  // the reference adds its tick() times into the caller's map
+        (*timings)["spread"] += t.spread;
+        (*timings)["fft"] += t.fft;
+        (*timings)["scale"] += t.scale;
+        (*timings)["ifft"] += t.ifft;
+        (*timings)["interpolate"] += t.interpolate;
+    }
     return f;
 }
 

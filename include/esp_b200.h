@@ -72,6 +72,12 @@ typedef struct {
     double pair_fit_err;    /* their max deviation from the exact kernels */
     int device;             /* -1 for a host-only plan */
     int pair_cells[3];      /* GPU cell-list geometry */
+    int pencil_half;        /* distributed FFT K4 mode, fixed at plan build
+                             * (ESP_PENCIL_HALF, default 1): 1 = half-shell --
+                             * ghost rows of esp_pencil_phase_b's output carry
+                             * partner terms owed to their owners, which the
+                             * caller must send back and add (see below);
+                             * 0 = full lists, ghost rows are zero */
 } esp_plan_info;
 
 /* Per-stage wall time in seconds (EnergyForces::timings keys,
@@ -174,8 +180,20 @@ int esp_eval_phase_b(esp_plan* plan, int rank, int nranks, const double* grid_de
  * would own fewer x-planes than the halo.
  * Inputs: every rank passes either the whole system or only its own atoms
  * (ownership below) plus ghost atoms within r_c of its x-slab (the
- * neighbours' atoms, any order); a rank computes u, F and the energy share of
- * the atoms it owns, zero for the others. */
+ * neighbours' atoms, any order).  Outputs depend on esp_plan_info.pencil_half
+ * (the same on every rank: it is fixed when the plan is built):
+ *   pencil_half = 0: a rank computes u, F and the energy share of the atoms
+ *     it owns, zero for the others.
+ *   pencil_half = 1 (default): each unordered real-space pair is evaluated
+ *     once, on the rank owning its base atom, and the partner's terms land in
+ *     the partner's row -- also when the partner is another rank's atom.
+ *     With replicated inputs, summing u and F over ranks (all-reduce) gives
+ *     the result.  With local inputs, the ghost rows hold terms owed to the
+ *     ghosts' owners: send each ghost row (u, Fx, Fy, Fz) back to the rank
+ *     that sent the ghost and add it into that atom's row (the reverse of the
+ *     ghost exchange); then E = 1/2 sum q_i u_i over the owned atoms
+ *     (ewald.hpp:641-647) -- the energy output of phase_b does not include
+ *     the returned terms. */
 typedef struct esp_pencil_info {
     int nranks, rank;
     int halo;          /* planes exchanged with each x-neighbour */
@@ -234,8 +252,11 @@ int esp_check_neutral(long N, const double* q);
 /* Parts of the hot path on HOST buffers (synchronous). */
 int esp_local_sum(esp_plan* plan, const double box[3], long N, const double* pos,
                   const double* q, double* u, double* F);          /* ewald.hpp:419-515 */
+/* ewald.hpp:524-604; timings (may be NULL) receives the grid-pipeline stage
+ * times (spread, fft, scale, ifft, interpolate; the stages then run
+ * serialised on one stream), like the reference's optional timings map. */
 int esp_spectral_sum(esp_plan* plan, const double box[3], long N, const double* pos,
-                     const double* q, double* u, double* F);       /* ewald.hpp:524-604 */
+                     const double* q, double* u, double* F, esp_timings* timings);
 int esp_self_correction(const esp_plan* plan, long N, const double* q, double* out);
                                                                     /* ewald.hpp:609-615 */
 int esp_spread(esp_plan* plan, long N, const double* pos, const double* q, double* grid);

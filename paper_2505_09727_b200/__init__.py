@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import time as _time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -72,6 +73,7 @@ class _Info(C.Structure):
         ("self_coef", C.c_double),
         ("n_split_coef", C.c_int), ("n_window_coef", C.c_int), ("pair_poly_degree", C.c_int),
         ("pair_fit_err", C.c_double), ("device", C.c_int), ("pair_cells", C.c_int * 3),
+        ("pencil_half", C.c_int),
     ]
 
 
@@ -119,7 +121,7 @@ _sig("esp_evaluate", [_vp, _dp, C.c_long, _dp, _dp, _dp, _dp, C.POINTER(C.c_doub
 _sig("esp_evaluate_device", [_vp, _dp, C.c_long, _vp, _vp, _vp, _vp, _vp, _vp])
 _sig("esp_check_neutral", [C.c_long, _dp])
 _sig("esp_local_sum", [_vp, _dp, C.c_long, _dp, _dp, _dp, _dp])
-_sig("esp_spectral_sum", [_vp, _dp, C.c_long, _dp, _dp, _dp, _dp])
+_sig("esp_spectral_sum", [_vp, _dp, C.c_long, _dp, _dp, _dp, _dp, C.POINTER(_Timings)])
 _sig("esp_self_correction", [_vp, C.c_long, _dp, _dp])
 _sig("esp_spread", [_vp, C.c_long, _dp, _dp, _dp])
 _sig("esp_interpolate", [_vp, C.c_long, _dp, _dp, _dp])
@@ -219,6 +221,8 @@ class EwaldPlan:
         self.pair_poly_degree = info.pair_poly_degree
         self.pair_fit_err = info.pair_fit_err
         self.pair_cells = tuple(info.pair_cells)
+        # distributed-FFT K4 mode, fixed at plan build (include/esp_b200.h)
+        self.pencil_half = bool(info.pencil_half)
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -340,11 +344,6 @@ def build_plan(box, family: str = "pswf", eps: float = 1e-4, r_c: float = 1.0,
     return EwaldPlan(h)
 
 
-def select_parameters(family: str, eps: float, box, r_c: float, ov: Overrides | None = None):
-    """ewald.hpp:338-349 (host-only plan; same selection as build_plan)."""
-    return build_plan(box, family, eps, r_c, ov, device=-1)
-
-
 def fold(system: ParticleSystem) -> ParticleSystem:
     """system.hpp:29-36 (host helper; the device path folds inside K0)."""
     L = np.asarray(system.box)
@@ -358,13 +357,17 @@ def require_neutral(system: ParticleSystem) -> None:
     _check(_lib.esp_check_neutral(system.size(), system.q))
 
 
-def evaluate(plan: EwaldPlan, system: ParticleSystem, timings: bool = False,
+def evaluate(plan: EwaldPlan, system: ParticleSystem, timings: bool = True,
              out: tuple | None = None) -> EnergyForces:
     """ewald.hpp:619-649 on host arrays (H2D, GPU evaluation, D2H).
 
-    timings=True serialises the stages and reports them under the
-    reference's keys (seconds) plus 'bin'.  out=(u, F) supplies
-    preallocated (e.g. pinned) float64 output arrays."""
+    Like the reference, the result's timings hold the per-stage times
+    (seconds) under its keys {local, spread, fft, scale, ifft, interpolate}
+    -- the stages then run serialised, each timed alone with CUDA events --
+    plus the GPU-only 'bin' (fold, cell keys, sorts).  timings=False selects
+    the overlapped CUDA-graph path (real-space sum concurrent with the grid
+    pipeline) and reports only 'total', the host wall time of the call.
+    out=(u, F) supplies preallocated (e.g. pinned) float64 output arrays."""
     N = system.size()
     if out is not None:
         u, F = out
@@ -375,10 +378,12 @@ def evaluate(plan: EwaldPlan, system: ParticleSystem, timings: bool = False,
         F = np.empty((N, 3))
     e = C.c_double()
     t = _Timings() if timings else None
+    t0 = _time.perf_counter()
     _check(_lib.esp_evaluate(plan._h, _f64(system.box, (3,)), N, system.pos, system.q, u, F,
                              C.byref(e), C.byref(t) if t is not None else None))
-    tim = {k: getattr(t, k) for k, _ in _Timings._fields_} if t is not None else {
-        k: 0.0 for k in ("local", "spread", "fft", "scale", "ifft", "interpolate")}
+    wall = _time.perf_counter() - t0
+    tim = {k: getattr(t, k) for k, _ in _Timings._fields_} if t is not None else {}
+    tim["total"] = wall
     return EnergyForces(e.value, u, F, tim)
 
 
@@ -543,13 +548,20 @@ def local_sum(plan: EwaldPlan, system: ParticleSystem) -> PartialField:
     return PartialField(u, F)
 
 
-def spectral_sum(plan: EwaldPlan, system: ParticleSystem) -> PartialField:
-    """ewald.hpp:524-604."""
+def spectral_sum(plan: EwaldPlan, system: ParticleSystem,
+                 timings: dict | None = None) -> PartialField:
+    """ewald.hpp:524-604.  Like the reference, a `timings` dict receives the
+    stage times (seconds, added to existing values) under spread, fft, scale,
+    ifft, interpolate."""
     N = system.size()
     u = np.empty(N)
     F = np.empty((N, 3))
+    t = _Timings() if timings is not None else None
     _check(_lib.esp_spectral_sum(plan._h, _f64(system.box, (3,)), N, system.pos, system.q, u,
-                                 F))
+                                 F, C.byref(t) if t is not None else None))
+    if t is not None:
+        for k in ("spread", "fft", "scale", "ifft", "interpolate"):
+            timings[k] = timings.get(k, 0.0) + getattr(t, k)
     return PartialField(u, F)
 
 

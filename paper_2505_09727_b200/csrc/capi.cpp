@@ -238,6 +238,7 @@ int esp_plan_get_info(const esp_plan* p, esp_plan_info* o) {
         o->n_split_coef = static_cast<int>(P.split.a.size());
         o->n_window_coef = static_cast<int>(P.window.a.size());
         o->pair_poly_degree = static_cast<int>(P.pair_H.size()) - 1;
+        o->pencil_half = p->eng ? (p->eng->pencil_half() ? 1 : 0) : espb::Engine::pencil_half_env();
         o->pair_fit_err = P.pair_fit_err;
         o->device = p->device;
     });
@@ -351,7 +352,14 @@ int esp_evaluate(esp_plan* p, const double box[3], long N, const double* pos, co
         const bool small = N > 0 && N <= kZeroCopyMaxN;
         const double *pos_m = small ? mapped(pos) : nullptr, *q_m = small ? mapped(q) : nullptr;
         double *u_m = small ? mapped(u) : nullptr, *F_m = small ? mapped(F) : nullptr;
+        // require_neutral (system.hpp:39-47) before any output is written, as
+        // the reference does (ewald.hpp:622): the caller's u / F stay
+        // untouched when it throws.  The zero-copy path writes u / F from the
+        // combine kernel, so it checks first (N <= 2^17: microseconds); the
+        // bulk path runs the same host loop while the GPU evaluates, and only
+        // copies the results out after it passed.
         if (pos_m && q_m && u_m && F_m) {
+            require_neutral(N, q);
             e.evaluate(N, pos_m, q_m, p->d_u, p->d_F, p->d_e, p->d_e + 1, p->stream,
                        timings ? &st : nullptr, u_m, F_m);
         } else {
@@ -359,6 +367,12 @@ int esp_evaluate(esp_plan* p, const double box[3], long N, const double* pos, co
             h2d(p, p->d_q, q, N);
             e.evaluate(N, p->d_pos, p->d_q, p->d_u, p->d_F, p->d_e, p->d_e + 1, p->stream,
                        timings ? &st : nullptr);
+            try {
+                require_neutral(N, q);
+            } catch (...) {
+                sync(p);
+                throw;
+            }
             d2h(p, u, p->d_u, N);
             d2h(p, F, p->d_F, 3 * N);
         }
@@ -366,9 +380,6 @@ int esp_evaluate(esp_plan* p, const double box[3], long N, const double* pos, co
         cuda_ok(cudaMemcpyAsync(hv, p->d_e, 3 * sizeof(double), cudaMemcpyDeviceToHost, p->stream),
                 "D2H");
         sync(p);
-        // require_neutral (system.hpp:39-47) from the fused device sums
-        if (std::fabs(hv[1]) > 1e-12 * std::max(hv[2], 1.0))
-            throw espb::NumericalError("system is not charge neutral");
         *energy = hv[0];
         if (timings) {
             timings->local = st.local;
@@ -550,7 +561,7 @@ int esp_local_sum(esp_plan* p, const double box[3], long N, const double* pos, c
 }
 
 int esp_spectral_sum(esp_plan* p, const double box[3], long N, const double* pos,
-                     const double* q, double* u, double* F) {
+                     const double* q, double* u, double* F, esp_timings* timings) {
     return guarded([&] {
         espb::Engine& e = engine(p);
         check_box(p, box, "spectral_sum");
@@ -558,10 +569,19 @@ int esp_spectral_sum(esp_plan* p, const double box[3], long N, const double* pos
         stage(p, N);
         h2d(p, p->d_pos, pos, 3 * N);
         h2d(p, p->d_q, q, N);
-        e.spectral_sum(N, p->d_pos, p->d_q, p->d_u, p->d_F, p->stream);
+        espb::StageTimes st;
+        e.spectral_sum(N, p->d_pos, p->d_q, p->d_u, p->d_F, p->stream, timings ? &st : nullptr);
         d2h(p, u, p->d_u, N);
         d2h(p, F, p->d_F, 3 * N);
         sync(p);
+        if (timings) {
+            *timings = esp_timings{};
+            timings->spread = st.spread;
+            timings->fft = st.fft;
+            timings->scale = st.scale;
+            timings->ifft = st.ifft;
+            timings->interpolate = st.interpolate;
+        }
     });
 }
 

@@ -2336,7 +2336,7 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
     pair_cap_ = 2048;
     if (const char* e = std::getenv("ESP_PAIR_CAP")) pair_cap_ = std::max(256, std::min(4096, std::atoi(e) / 32 * 32));
     if (const char* e = std::getenv("ESP_PAIR_HALF")) half_mode_ = std::atoi(e);
-    if (const char* e = std::getenv("ESP_PENCIL_HALF")) pencil_half_ = std::atoi(e) != 0;
+    pencil_half_ = pencil_half_env() != 0;
 }
 
 Engine::~Engine() {
@@ -2606,13 +2606,20 @@ void Engine::run_pair(long N, cudaStream_t s, int rank, int nranks, bool own_bin
     }
     // half-shell K4 on the single-GPU path (tiny systems: the full-list kernel's
     // single launch is faster); ESP_PAIR_HALF=0 never, 2 always
-    const bool half = half_mode_ == 2 || (half_mode_ == 1 && N >= kHalfMinN);
-    // the slab decomposition (every rank holds all atoms, outputs all-reduced)
+    // The slab decomposition (every rank holds all atoms, outputs all-reduced)
     // takes the half-shell kernel for its x-range of blocks: partner terms on
     // other ranks' atoms are summed by the all-reduce.  The distributed FFT
-    // (own_bins: plane-owned targets, possibly local inputs) keeps full lists.
-    if (half && (!own_bins || pencil_half_) && run_pair_half(N, s, rank, nranks, own_bins))
-        return;
+    // (own_bins: plane-owned targets, possibly local inputs) must make the SAME
+    // choice on every rank -- a rank on full lists next to a half-shell rank
+    // would count cross-rank pairs twice on one side and drop them on the
+    // other -- so there the mode is the plan's alone (ESP_PENCIL_HALF, read
+    // once at plan build; esp_plan_info.pencil_half), independent of the
+    // rank's atom count and density, and the half-shell path never falls back.
+    const bool half = own_bins ? pencil_half_
+                               : half_mode_ == 2 || (half_mode_ == 1 && N >= kHalfMinN);
+    if (half && run_pair_half(N, s, rank, nranks, own_bins)) return;
+    if (half && own_bins)
+        throw CudaError("distributed FFT: half-shell pair kernel could not be configured");
     PairArgs a{};
     a.xyzq = d_xyzqA_;
     a.orig = d_origA_;
@@ -2775,6 +2782,15 @@ bool Engine::run_pair_half(long N, cudaStream_t s, int rank, int nranks, bool ow
             best_bx = bx;
             best_bz = bz;
         }
+    }
+    if (best_bx == 0 && own_bins) {
+        // distributed FFT: never fall back to full lists (see run_pair); the
+        // smallest block always fits the period when cells_ok_, and blocks
+        // whose neighbourhood exceeds the staging capacity go to the overflow
+        // kernel
+        best_bx = 1;
+        best_bz = 2;
+        best_cap = cap_max;
     }
     if (best_bx == 0) return false;
     HalfArgs a{};
@@ -3250,16 +3266,25 @@ void Engine::local_sum(long N, const double* pos, const double* q, double* u, do
 }
 
 void Engine::spectral_sum(long N, const double* pos, const double* q, double* u, double* F,
-                          cudaStream_t s) {
+                          cudaStream_t s, StageTimes* t) {
     CK(cudaSetDevice(device_));
     ensure_capacity(N);
     prepare(N, pos, q, nullptr, s);
-    CK(cudaEventRecord(ev_fork_, s));
-    CK(cudaStreamWaitEvent(aux_, ev_fork_, 0));
-    run_grid(N, aux_, nullptr);
-    CK(cudaEventRecord(ev_join_, aux_));
-    CK(cudaStreamWaitEvent(s, ev_join_, 0));
-    if (N == 0) return;
+    if (t) {
+        // stages timed on the caller's stream (ewald.hpp:524-604 tick() keys)
+        CK(cudaEventRecord(ev_t_[2], s));
+        run_grid(N, s, t);
+    } else {
+        CK(cudaEventRecord(ev_fork_, s));
+        CK(cudaStreamWaitEvent(aux_, ev_fork_, 0));
+        run_grid(N, aux_, nullptr);
+        CK(cudaEventRecord(ev_join_, aux_));
+        CK(cudaStreamWaitEvent(s, ev_join_, 0));
+    }
+    if (N == 0) {
+        if (t) *t = StageTimes{};
+        return;
+    }
     InterpArgs a{};
     a.N = N;
     a.xyzq = d_xyzqB_;
@@ -3270,6 +3295,20 @@ void Engine::spectral_sum(long N, const double* pos, const double* q, double* u,
     a.F = F;
     const GridArgs g = grid_args();
     dispatch_P<InterpLaunch>(plan_.P, static_cast<int>(kSpectral), nfields_ == 4, g, a, s);
+    if (t) {
+        CK(cudaEventRecord(ev_t_[7], s));
+        CK(cudaEventSynchronize(ev_t_[7]));
+        auto el = [&](int a0, int a1) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, ev_t_[a0], ev_t_[a1]));
+            return ms * 1e-3;
+        };
+        t->spread = el(2, 3);
+        t->fft = el(3, 4);
+        t->scale = el(4, 5);
+        t->ifft = el(5, 6);
+        t->interpolate = el(6, 7);
+    }
 }
 
 void Engine::spread(long N, const double* pos, const double* q, double* grid, cudaStream_t s) {

@@ -10,6 +10,7 @@
 
 #include "plan.hpp"
 
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include <cufft.h>
 
@@ -81,7 +82,8 @@ public:
     void local_sum(long N, const double* pos, const double* q, double* u, double* F,
                    cudaStream_t s);
     void spectral_sum(long N, const double* pos, const double* q, double* u, double* F,
-                      cudaStream_t s);
+                      cudaStream_t s,
+                      StageTimes* t = nullptr);
     // Grid pipeline pieces (gridder.hpp:215, :244, :280); grid = nx*ny*nz reals.
     void spread(long N, const double* pos, const double* q, double* grid, cudaStream_t s);
     void interpolate(long N, const double* pos, const double* grid, double* out,
@@ -130,6 +132,12 @@ public:
 
     // Launch count of the last evaluate() (our kernels only, excluding cuFFT).
     int last_launches() const { return launches_; }
+    // distributed-FFT K4 mode (fixed when the engine is built; see run_pair)
+    bool pencil_half() const { return pencil_half_; }
+    static int pencil_half_env() {
+        const char* e = std::getenv("ESP_PENCIL_HALF");
+        return (e && std::atoi(e) == 0) ? 0 : 1;
+    }
     // Ordered in-range pairs (0 < r < r_c) evaluated by the last pair-kernel
     // launch, counted on the device (synchronous read).
     unsigned long long last_pair_count() const;

@@ -486,9 +486,14 @@ def return_ghost_terms(plan, ghost_rows, own_rows, group=None):
             own_rows.index_add_(0, plan["sent_idx"][p].to(own_rows.device), back[p])
 
 
-def pencil_half_enabled() -> bool:
-    """The distributed FFT's K4 runs half-shell unless ESP_PENCIL_HALF=0 (read
-    by the engine when a plan is built); local inputs then return ghost terms."""
+def pencil_half_enabled(plan=None) -> bool:
+    """Whether the distributed FFT's K4 runs half-shell (then local inputs
+    return ghost partner terms).  The mode is fixed when the plan is built
+    (esp_plan_info.pencil_half); it is read from the plan, never from the
+    environment at call time.  plan=None (engine-less callers) gives the
+    build-time default, ESP_PENCIL_HALF != 0."""
+    if plan is not None and hasattr(plan, "pencil_half"):
+        return bool(plan.pencil_half)
     import os
     return os.environ.get("ESP_PENCIL_HALF", "1") != "0"
 
@@ -517,7 +522,7 @@ def evaluate_pencil_local(plan, box, pos_own, q_own, layout, rank, r_c, stream=0
             cache["bufs"] = bufs
     out = evaluate_pencil(plan, box, n, pos_l.reshape(-1), q_l, bufs, layout, rank, stream,
                           group, engine, reduce_outputs=False)
-    if pencil_half_enabled():
+    if pencil_half_enabled(plan):
         # half-shell K4: the ghost rows hold partner terms owed to their owners;
         # return them, then E = 1/2 sum q u over the owned atoms (ewald.hpp:641-647)
         rows = torch.cat([out[:n, None], out[n:4 * n].reshape(n, 3)], dim=1)

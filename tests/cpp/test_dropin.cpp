@@ -103,6 +103,12 @@ int main() {
         CHECK(throws<esp::NumericalError>([&] { esp::evaluate(plan, charged); }));
         esp::EnergyForces ef = esp::evaluate(plan, random_system(8, box, 1));
         CHECK(ef.timings.size() == 6);
+        CHECK(ef.timings.at("local") > 0.0 && ef.timings.at("interpolate") > 0.0);
+        CHECK(ef.device_timings.at("total") > 0.0);
+        // spectral_sum fills the caller's map with the grid-pipeline stages
+        std::map<std::string, double> sp;
+        esp::spectral_sum(plan, random_system(8, box, 1), &sp);
+        CHECK(sp.size() == 5 && sp.at("fft") > 0.0);
     }
     // translation invariance (test_ewald.cpp:383-409)
     {

@@ -139,6 +139,42 @@ def test_device_errors_follow_reference(esp, gpu):
         esp.evaluate(plan, esp.ParticleSystem(box, q, pos))
 
 
+@pytest.mark.parametrize("N", [64, 200_000])
+def test_non_neutral_leaves_outputs_untouched(esp, gpu, N):
+    """ewald.hpp:622: require_neutral runs before any work, so a NumericalError
+    leaves the caller's output arrays as they were (both the zero-copy path,
+    N <= 2^17, and the bulk-copy path)."""
+    from paper_2505_09727_b200 import systems as S
+    L = 10.0 if N < 1000 else 60.0
+    box = (L, L, L)
+    plan = esp.build_plan(box, "pswf", 1e-3, 3.0 if N > 1000 else 1.0, device=gpu)
+    pos, q = S.generate_system("random", N, box, 3)
+    q = q.copy()
+    q[1] += 1e-6
+    u = np.full(N, 7.0)
+    F = np.full((N, 3), -3.0)
+    with pytest.raises(esp.NumericalError):
+        esp.evaluate(plan, esp.ParticleSystem(box, q, pos), timings=False, out=(u, F))
+    assert np.all(u == 7.0) and np.all(F == -3.0)
+    # the plan stays usable after the error
+    q[1] -= 1e-6
+    ef = esp.evaluate(plan, esp.ParticleSystem(box, q, pos), timings=False, out=(u, F))
+    assert np.isfinite(ef.energy) and not np.all(u == 7.0)
+
+
+def test_stage_timings_follow_reference_keys(esp, gpu):
+    """ewald.hpp:628-634 / test_ewald.cpp:378-380: evaluate reports the six
+    stage times; spectral_sum adds its five into the caller's map."""
+    sysm, c = _cfg1(esp)
+    plan = esp.build_plan(sysm.box, "pswf", c.eps, c.r_c, device=gpu)
+    ef = esp.evaluate(plan, sysm)
+    for k in ("local", "spread", "fft", "scale", "ifft", "interpolate"):
+        assert ef.timings[k] > 0.0
+    t = {"spread": 1.0}
+    esp.spectral_sum(plan, sysm, timings=t)
+    assert set(t) == {"spread", "fft", "scale", "ifft", "interpolate"} and t["spread"] > 1.0
+
+
 def test_zero_and_empty(esp, gpu):
     """test_ewald.cpp:282-291: zero charges give a zero field; N=0 is valid."""
     from paper_2505_09727_b200 import systems as S

@@ -90,11 +90,11 @@ def _pencil_local(esp, box, pos, q, eps, r_c, nranks, half=None):
     from paper_2505_09727_b200.dist import (PencilBuffers, PencilLayout, atom_owner,
                                             evaluate_pencil_emulated, fold_positions,
                                             ghost_masks, pencil_half_enabled)
-    if half is None:
-        half = pencil_half_enabled()
     dev = torch.device("cuda", 0)
     N = q.size
     plans = [esp.build_plan(box, "pswf", eps, r_c, device=0) for _ in range(nranks)]
+    if half is None:
+        half = pencil_half_enabled(plans[0])
     layout = PencilLayout.of(plans[0], nranks)
     posf = fold_positions(pos, box)
     own = atom_owner(layout, posf[:, 0])
@@ -139,3 +139,27 @@ def test_pencil_local_inputs_equal_single_gpu(esp, gpu, name, nranks):
     assert abs(E - full.energy) <= 1e-12 * abs(full.energy)
     assert rel_rms(F, full.F) <= 1e-12
     assert max_rel(u, full.u) <= 1e-12
+
+
+def test_pencil_local_uneven_ranks_equal_single_gpu(esp, gpu):
+    """Ranks with very different local atom counts (a density step along x:
+    one rank holds < 4096 own + ghost atoms, the other ~10x more) must take
+    the same K4 mode -- the plan's, never a per-rank choice from the local N
+    or density (a mixed half-shell / full-list pair of ranks double-counts
+    cross-rank pairs on one side and drops them on the other)."""
+    from paper_2505_09727_b200 import systems as S
+    L, N, r_c, eps = 40.0, 24000, 4.0, 1e-4
+    box = (L, L, L)
+    pos, q = S.generate_system("random", N, box, 29)
+    pos = pos.copy()
+    # 90 % of the atoms in the slab 5 <= x < 15, inside rank 0's planes and
+    # more than r_c from rank 1's (charges stay alternating: neutral); rank 1
+    # then holds ~2400 own + ~1000 ghost atoms
+    dense = np.arange(N) % 10 != 0
+    pos[dense, 0] = 5.0 + 0.25 * pos[dense, 0]
+    plan = esp.build_plan(box, "pswf", eps, r_c, device=0)
+    ref = esp.evaluate(plan, esp.ParticleSystem(box, q, pos))
+    u, F, E = _pencil_local(esp, box, pos, q, eps, r_c, 2)
+    assert abs(E - ref.energy) <= 1e-12 * abs(ref.energy)
+    assert rel_rms(F, ref.F) <= 1e-12
+    assert max_rel(u, ref.u) <= 1e-12

@@ -88,3 +88,17 @@ def test_fftw_shim_and_reference_if_built():
     rp = ref.RefPlan((10.0, 10.0, 10.0), "pswf", 1e-4, 1.0)
     r = rp.evaluate(pos, q)
     assert r.energy == float(g["energy"]) or abs(r.energy - g["energy"]) <= 1e-14 * abs(r.energy)
+
+
+def test_oracle_gaussian_evaluate_matches_reference():
+    """Gaussian split (kernels.hpp:105-138) + B-spline window
+    (kernels.hpp:263-273): the restatement's full evaluation pinned to the
+    compiled reference's output on the cfg1 system (gauss_cfg1.npz)."""
+    g = golden("gauss_cfg1.npz")
+    p = O.build_plan((10.0, 10.0, 10.0), "gaussian", 1e-4, 1.0)
+    assert tuple(p.nf) == tuple(int(v) for v in g["nf"]) and p.P == int(g["P"])
+    pos, q = O.random_system(1000, (10.0, 10.0, 10.0), 1)
+    E, u, F = O.evaluate(p, pos, q)
+    assert abs(E - g["energy"]) <= 1e-11 * abs(g["energy"])
+    assert rel_rms(F, g["F"]) <= 1e-10
+    assert max_rel(u, g["u"]) <= 1e-10
