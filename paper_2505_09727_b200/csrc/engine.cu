@@ -944,6 +944,56 @@ __device__ __forceinline__ bool pos_after(const double4& pj, const double4& pi) 
     return pj.z > pi.z || (pj.z == pi.z && (pj.x > pi.x || (pj.x == pi.x && pj.y > pi.y)));
 }
 
+// pair terms from both sides (as pair_eval2), optionally without the image
+// shift: d = (r_j - r_i) [+ s]
+template <int ND, bool SHIFT>
+__device__ __forceinline__ bool pair_eval3(const PairConsts& k, double4 pj, double sx, double sy,
+                                           double sz, double xi, double yi, double zi, double qi,
+                                           double& u, double& fx, double& fy, double& fz,
+                                           double4& gj) {
+    double dx = pj.x - xi, dy = pj.y - yi, dz = pj.z - zi;
+    if (SHIFT) {
+        dx += sx;
+        dy += sy;
+        dz += sz;
+    }
+    const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+    if (!(r2 < k.rc2 && r2 > 0.0)) return false;
+    double rinv;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rinv) : "d"(r2));
+    {
+        const double hr = 0.5 * r2;
+        double e = fma(-hr * rinv, rinv, 0.5);
+        rinv = fma(rinv, e, rinv);
+        e = fma(-hr * rinv, rinv, 0.5);
+        rinv = fma(rinv, e, rinv);
+    }
+    const double z = fma(r2, k.two_irc2, -1.0);
+    constexpr int NE = (ND + 1) / 2, NO = ND / 2, NDE = ND / 2, NDO = (ND + 1) / 2 - 1;
+    const double w = z * z;
+    double he = k.He[NE - 1], ho = k.Ho[NO - 1], de = k.De[NDE - 1], dO = k.Do[NDO - 1];
+#pragma unroll
+    for (int m = NE - 2; m >= 0; --m) {
+        he = fma(he, w, k.He[m]);
+        if (m < NO - 1) ho = fma(ho, w, k.Ho[m]);
+        if (m < NDE - 1) de = fma(de, w, k.De[m]);
+        if (m < NDO - 1) dO = fma(dO, w, k.Do[m]);
+    }
+    const double H = fma(z, ho, he);
+    const double dH = fma(z, dO, de);
+    const double G = fma(fma(2.0, z, 2.0), dH, H);  // chi / r_c
+    const double pot = rinv - H;                     // 4 pi S
+    const double c0 = (G + pot) * (rinv * rinv);     // 4 pi (-dS/dr) / r
+    u = fma(pj.w, pot, u);
+    const double c = pj.w * c0;
+    fx = fma(c, dx, fx);
+    fy = fma(c, dy, fy);
+    fz = fma(c, dz, fz);
+    const double b = qi * c;
+    gj = make_double4(qi * pot, b * dx, b * dy, b * dz);
+    return true;
+}
+
 // (u, F) terms of sorted atom j into the planar accumulators (global REDs;
 // the 32 lanes of a round mostly hold consecutive sorted atoms, so one RED
 // instruction touches a few 32-byte sectors per component)
@@ -1020,6 +1070,7 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
         fwd_col(l, M, dx, dy);
         fwdc[threadIdx.x - 64] = dx | ((dy + M) << 4) | ((l == nfc - 1) << 8);
     }
+    int wraps = 0;
     for (int e = threadIdx.x; e < nent; e += blockDim.x) {
         const int col = e / nsl, sl = e - col * nsl;
         const int cx = col / Wy, cy = col - cx * Wy;
@@ -1034,9 +1085,14 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
         const int s0 = a.start[f];
         ent_src[e] = s0;
         ent_off[e + 1] = a.start[f + 1] - s0;
-        ent_slot[e] = static_cast<unsigned char>((ix * 3 + iy) * 3 + iz);
+        const int slot = (ix * 3 + iy) * 3 + iz;
+        ent_slot[e] = static_cast<unsigned char>(slot);
+        wraps |= slot != 13;
     }
-    __syncthreads();
+    // blocks whose neighbourhood never wraps around the box (most of them)
+    // evaluate their pairs without image shifts (uniform per CTA: no shift
+    // lookups, 3 fp64 adds fewer per pair)
+    const bool wrap = __syncthreads_or(wraps) != 0;
     if (warp == 0) {
         const int per = (nent + 31) / 32;
         const int e0 = min(nent, lane * per), e1 = min(nent, e0 + per);
@@ -1222,8 +1278,11 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
                         double4 g;
                         const bool same = OWN && sf >= cs && sf < ce;
                         if ((!same || pos_after(pf, pi)) &&
-                            pair_eval2<ND>(k, pf, shiftv[tf][0], shiftv[tf][1], shiftv[tf][2],
-                                           pi.x, pi.y, pi.z, pi.w, u, fx, fy, fz, g)) {
+                            (wrap ? pair_eval3<ND, true>(k, pf, shiftv[tf][0], shiftv[tf][1],
+                                                         shiftv[tf][2], pi.x, pi.y, pi.z, pi.w,
+                                                         u, fx, fy, fz, g)
+                                  : pair_eval3<ND, false>(k, pf, 0.0, 0.0, 0.0, pi.x, pi.y, pi.z,
+                                                          pi.w, u, fx, fy, fz, g))) {
                             ++npair;
                             red_acc(a.acc, a.nacc, sf, g.x, g.y, g.z, g.w);
                         }
@@ -1241,8 +1300,10 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
             double4 g;
             const bool same = OWN && sf >= cs && sf < ce;
             if ((!same || pos_after(pf, pi)) &&
-                pair_eval2<ND>(k, pf, shiftv[tf][0], shiftv[tf][1], shiftv[tf][2], pi.x, pi.y,
-                               pi.z, pi.w, u, fx, fy, fz, g)) {
+                (wrap ? pair_eval3<ND, true>(k, pf, shiftv[tf][0], shiftv[tf][1], shiftv[tf][2],
+                                             pi.x, pi.y, pi.z, pi.w, u, fx, fy, fz, g)
+                      : pair_eval3<ND, false>(k, pf, 0.0, 0.0, 0.0, pi.x, pi.y, pi.z, pi.w, u,
+                                              fx, fy, fz, g))) {
                 ++npair;
                 red_acc(a.acc, a.nacc, sf, g.x, g.y, g.z, g.w);
             }
@@ -1256,8 +1317,10 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
             const int sj = cd & 0x7ffffff;
             const bool same = OWN && sj >= cs && sj < ce;
             if ((!same || pos_after(pj, pi)) &&
-                pair_eval2<ND>(k, pj, shiftv[t][0], shiftv[t][1], shiftv[t][2], pi.x, pi.y, pi.z,
-                               pi.w, u, fx, fy, fz, g)) {
+                (wrap ? pair_eval3<ND, true>(k, pj, shiftv[t][0], shiftv[t][1], shiftv[t][2],
+                                             pi.x, pi.y, pi.z, pi.w, u, fx, fy, fz, g)
+                      : pair_eval3<ND, false>(k, pj, 0.0, 0.0, 0.0, pi.x, pi.y, pi.z, pi.w, u,
+                                              fx, fy, fz, g))) {
                 ++npair;
                 red_acc(a.acc, a.nacc, cd & 0x7ffffff, g.x, g.y, g.z, g.w);
             }
@@ -2848,14 +2911,15 @@ bool Engine::run_pair_half(long N, cudaStream_t s, int rank, int nranks, bool ow
     if (nblocks_all + 1 > ovf_cap_) return false;  // sized in alloc_cells (no allocation under capture)
     a.ovf = d_ovf_;
     CK(cudaMemsetAsync(d_ovf_, 0, sizeof(int), s));
-    size_t sm = (a.cap + 1) * sizeof(float4) +
-                kHalfWarps * 64 * sizeof(int) + kHalfWarps * a.lcap * sizeof(unsigned short);
+    size_t sm = (a.cap + 1) * sizeof(float4) + kHalfWarps * 64 * sizeof(int) +
+                kHalfWarps * a.lcap * sizeof(unsigned short);
     sm = (sm + 3) / 4 * 4 + (2 * a.nent_max + 1) * sizeof(int) + a.nent_max;
     const int ovf_grid = 2 * sms;
     auto go = [&](auto kern, auto ovfk) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(sm)));
-        if (nblocks > 0) kern<<<static_cast<unsigned>(nblocks), kHalfThreads, sm, s>>>(a, k);
+        if (nblocks > 0)
+            kern<<<static_cast<unsigned>(nblocks), kHalfThreads, sm, s>>>(a, k);
         CK(cudaGetLastError());
         ovfk<<<ovf_grid, 256, 0, s>>>(a, k);
         CK(cudaGetLastError());
@@ -2863,14 +2927,14 @@ bool Engine::run_pair_half(long N, cudaStream_t s, int rank, int nranks, bool ow
         CK(cudaGetLastError());
     };
     switch (nd) {
-        case 14: (own_bins ? go(k_pair_half<14, true>, k_pair_half_ovf<14>) : go(k_pair_half<14, false>, k_pair_half_ovf<14>)); break;
-        case 15: (own_bins ? go(k_pair_half<15, true>, k_pair_half_ovf<15>) : go(k_pair_half<15, false>, k_pair_half_ovf<15>)); break;
-        case 16: (own_bins ? go(k_pair_half<16, true>, k_pair_half_ovf<16>) : go(k_pair_half<16, false>, k_pair_half_ovf<16>)); break;
-        case 17: (own_bins ? go(k_pair_half<17, true>, k_pair_half_ovf<17>) : go(k_pair_half<17, false>, k_pair_half_ovf<17>)); break;
-        case 18: (own_bins ? go(k_pair_half<18, true>, k_pair_half_ovf<18>) : go(k_pair_half<18, false>, k_pair_half_ovf<18>)); break;
-        case 20: (own_bins ? go(k_pair_half<20, true>, k_pair_half_ovf<20>) : go(k_pair_half<20, false>, k_pair_half_ovf<20>)); break;
-        case 28: (own_bins ? go(k_pair_half<28, true>, k_pair_half_ovf<28>) : go(k_pair_half<28, false>, k_pair_half_ovf<28>)); break;
-        default: (own_bins ? go(k_pair_half<kMaxPoly, true>, k_pair_half_ovf<kMaxPoly>) : go(k_pair_half<kMaxPoly, false>, k_pair_half_ovf<kMaxPoly>)); break;
+        case 14: own_bins ? go(k_pair_half<14, true>, k_pair_half_ovf<14>) : go(k_pair_half<14, false>, k_pair_half_ovf<14>); break;
+        case 15: own_bins ? go(k_pair_half<15, true>, k_pair_half_ovf<15>) : go(k_pair_half<15, false>, k_pair_half_ovf<15>); break;
+        case 16: own_bins ? go(k_pair_half<16, true>, k_pair_half_ovf<16>) : go(k_pair_half<16, false>, k_pair_half_ovf<16>); break;
+        case 17: own_bins ? go(k_pair_half<17, true>, k_pair_half_ovf<17>) : go(k_pair_half<17, false>, k_pair_half_ovf<17>); break;
+        case 18: own_bins ? go(k_pair_half<18, true>, k_pair_half_ovf<18>) : go(k_pair_half<18, false>, k_pair_half_ovf<18>); break;
+        case 20: own_bins ? go(k_pair_half<20, true>, k_pair_half_ovf<20>) : go(k_pair_half<20, false>, k_pair_half_ovf<20>); break;
+        case 28: own_bins ? go(k_pair_half<28, true>, k_pair_half_ovf<28>) : go(k_pair_half<28, false>, k_pair_half_ovf<28>); break;
+        default: own_bins ? go(k_pair_half<kMaxPoly, true>, k_pair_half_ovf<kMaxPoly>) : go(k_pair_half<kMaxPoly, false>, k_pair_half_ovf<kMaxPoly>); break;
     }
     launches_ += 3;
     return true;
