@@ -168,8 +168,9 @@ def test_stage_timings_follow_reference_keys(esp, gpu):
     sysm, c = _cfg1(esp)
     plan = esp.build_plan(sysm.box, "pswf", c.eps, c.r_c, device=gpu)
     ef = esp.evaluate(plan, sysm)
-    for k in ("local", "spread", "fft", "scale", "ifft", "interpolate"):
+    for k in ("local", "spread", "fft", "ifft", "interpolate"):
         assert ef.timings[k] > 0.0
+    assert ef.timings["scale"] >= 0.0  # fused into the FFT callbacks: ~0
     t = {"spread": 1.0}
     esp.spectral_sum(plan, sysm, timings=t)
     assert set(t) == {"spread", "fft", "scale", "ifft", "interpolate"} and t["spread"] > 1.0
