@@ -283,6 +283,71 @@ int esp_fp64_peak(int device, double* tflops);
  * registers, no neighbour search): the ceiling of K4's inner work. */
 int esp_pair_eval_rate(esp_plan* plan, double* pairs_per_s);
 
+/* ---- Sharded evaluation over the GPUs of one box -----------
+ * One process per GPU, each with its own plan (same box / eps / r_c / family
+ * / overrides on every rank, device = that process's GPU).  The system is
+ * split into x-slabs by grid plane (the distributed-FFT decomposition of
+ * esp_pencil_geometry): rank r passes ONLY the atoms it owns (partition with
+ * esp_shard_owner) and gets back u and F of those atoms and the total energy.
+ * Inside one esp_shard_evaluate call: ghost atoms within r_c of the slab
+ * faces are exchanged with the two x-neighbours (fixed-capacity NCCL
+ * send/recv), the pencil phases run, the spread halos and field halos go to
+ * the neighbours, the half spectrum is transposed twice by grouped NCCL
+ * send/recv (all-to-all), the half-shell real-space partner terms of the
+ * ghosts go back to their owners, and the energy is all-reduced.  Everything
+ * is asynchronous on `stream`, with no host synchronisation: the call can be
+ * captured in a CUDA graph.  Replaces the single-process esp::evaluate
+ * (ewald.hpp:619-649) for systems sharded over GPUs; API shape README.md:58-64.
+ * The results equal esp_evaluate on the whole system up to summation order.
+ *
+ * NCCL is loaded at run time (libnccl.so.2). */
+typedef struct esp_shard esp_shard;
+typedef struct esp_shard_info_t {
+    int rank, nranks;
+    int x0, x1;             /* owned grid planes */
+    double X0, X1;          /* owned slab in x (folded coordinates) */
+    long max_own_atoms;     /* capacity for own atoms */
+    long ghost_capacity;    /* ghost atoms per slab face (2x for two ranks) */
+    long local_atoms;       /* own + ghost capacity: the rank's local system */
+    int pencil_half;        /* real-space pairs once (ghost terms returned) */
+    int nccl;               /* 1: NCCL communicator, 0: emulation member */
+} esp_shard_info_t;
+
+/* A new NCCL unique id (128 bytes) -- made on one rank and shared with the
+ * others by the caller (e.g. a torch.distributed broadcast). */
+int esp_shard_unique_id(void* id128);
+/* Collective over nranks >= 2 processes when nccl_id != NULL
+ * (ncclCommInitRank on the plan's device).  nccl_id == NULL makes an
+ * emulation member for esp_shard_evaluate_emulated (all ranks' shards in one
+ * process on one GPU, messages moved by device copies: tests).
+ * max_own_atoms: upper bound of the atoms this rank will pass;
+ * ghost_capacity: atoms per slab face (0 = from max_own_atoms and the slab
+ * width, +30 %).  INVALID_ARGUMENT when a slab is narrower than r_c. */
+int esp_shard_create(esp_plan* plan, const void* nccl_id, int rank, int nranks,
+                     long max_own_atoms, long ghost_capacity, esp_shard** out);
+void esp_shard_destroy(esp_shard* shard);
+int esp_shard_info(const esp_shard* shard, esp_shard_info_t* info);
+/* Owner rank of each atom (host positions N x 3, any image): the rank whose
+ * planes hold clamp(floor(fold(x) / hx), 0, nx - 1). */
+int esp_shard_owner(const esp_plan* plan, int nranks, long N, const double* pos, int* owner);
+/* One sharded evaluation (collective: every rank calls it for the same step).
+ * Device pointers: pos (n_own x 3), q (n_own) of this rank's atoms; out u
+ * (n_own), F (n_own x 3), energy (1 double: the TOTAL energy, all-reduced).
+ * A ghost-capacity overflow or a non-owned input atom is detected on the
+ * device and reported by the next call (or esp_shard_check) as
+ * ESP_ERR_NUMERICAL / ESP_ERR_INVALID_ARGUMENT. */
+int esp_shard_evaluate(esp_shard* shard, const double box[3], long n_own, const double* pos_dev,
+                       const double* q_dev, double* u_dev, double* F_dev, double* energy_dev,
+                       void* stream);
+/* All ranks of a decomposition in this process (emulation members, one GPU),
+ * executed in lockstep; per-rank argument arrays. */
+int esp_shard_evaluate_emulated(esp_shard* const* shards, int nranks, const double box[3],
+                                const long* n_own, const double* const* pos_dev,
+                                const double* const* q_dev, double* const* u_dev,
+                                double* const* F_dev, double* const* energy_dev, void* stream);
+/* Synchronises and reports the device-side error flags of the last call. */
+int esp_shard_check(esp_shard* shard);
+
 #ifdef __cplusplus
 }
 #endif

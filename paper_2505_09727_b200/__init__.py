@@ -30,7 +30,7 @@ __all__ = [
     "evaluate_device", "local_sum", "spectral_sum", "self_correction", "spread",
     "interpolate", "interpolate_gradient", "require_neutral", "fold", "device_count",
     "direct_ewald", "ReferenceResult", "fft_forward", "fft_inverse", "select_parameters",
-    "LIB_PATH",
+    "LIB_PATH", "Shard", "shard_owner", "shard_unique_id", "evaluate_sharded_emulated",
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
@@ -87,6 +87,13 @@ class _PencilInfo(C.Structure):
     ]
 
 
+class _ShardInfo(C.Structure):
+    _fields_ = [("rank", C.c_int), ("nranks", C.c_int), ("x0", C.c_int), ("x1", C.c_int),
+                ("X0", C.c_double), ("X1", C.c_double), ("max_own_atoms", C.c_long),
+                ("ghost_capacity", C.c_long), ("local_atoms", C.c_long),
+                ("pencil_half", C.c_int), ("nccl", C.c_int)]
+
+
 class _DirectInfo(C.Structure):
     _fields_ = [("lambda_", C.c_double), ("real_shells", C.c_int), ("recip_kmax", C.c_int),
                 ("tail_bound", C.c_double)]
@@ -120,6 +127,14 @@ _sig("esp_evaluate", [_vp, _dp, C.c_long, _dp, _dp, _dp, _dp, C.POINTER(C.c_doub
                       C.POINTER(_Timings)])
 _sig("esp_evaluate_device", [_vp, _dp, C.c_long, _vp, _vp, _vp, _vp, _vp, _vp])
 _sig("esp_check_neutral", [C.c_long, _dp])
+_sig("esp_shard_unique_id", [_vp])
+_sig("esp_shard_create", [_vp, _vp, C.c_int, C.c_int, C.c_long, C.c_long, C.POINTER(_vp)])
+_sig("esp_shard_destroy", [_vp], None)
+_sig("esp_shard_info", [_vp, C.POINTER(_ShardInfo)])
+_sig("esp_shard_owner", [_vp, C.c_int, C.c_long, _dp, _vp])
+_sig("esp_shard_evaluate", [_vp, _dp, C.c_long, _vp, _vp, _vp, _vp, _vp, _vp])
+_sig("esp_shard_evaluate_emulated", [_vp, C.c_int, _dp, _vp, _vp, _vp, _vp, _vp, _vp, _vp])
+_sig("esp_shard_check", [_vp])
 _sig("esp_local_sum", [_vp, _dp, C.c_long, _dp, _dp, _dp, _dp])
 _sig("esp_spectral_sum", [_vp, _dp, C.c_long, _dp, _dp, _dp, _dp, C.POINTER(_Timings)])
 _sig("esp_self_correction", [_vp, C.c_long, _dp, _dp])
@@ -593,3 +608,71 @@ def interpolate_gradient(plan: EwaldPlan, grid, system: ParticleSystem) -> np.nd
     _check(_lib.esp_interpolate_gradient(plan._h, system.size(), system.pos,
                                          _f64(grid).ravel(), out))
     return out
+
+
+# ---- sharded evaluation over the GPUs of one box (include/esp_b200.h esp_shard_*)
+
+
+def shard_unique_id() -> bytes:
+    """A new NCCL unique id (128 bytes), to be shared with every rank."""
+    buf = C.create_string_buffer(128)
+    _check(_lib.esp_shard_unique_id(buf))
+    return buf.raw
+
+
+def shard_owner(plan: EwaldPlan, nranks: int, pos) -> np.ndarray:
+    """Owner rank of every atom (host (N, 3) positions, any image)."""
+    pos = _f64(pos).reshape(-1, 3)
+    out = np.empty(pos.shape[0], dtype=np.int32)
+    _check(_lib.esp_shard_owner(plan._h, int(nranks), pos.shape[0], pos, out.ctypes.data))
+    return out
+
+
+class Shard:
+    """One rank of a sharded evaluation (esp_shard_create).  nccl_id=None
+    makes an emulation member for evaluate_sharded_emulated."""
+
+    def __init__(self, plan: EwaldPlan, rank: int, nranks: int, max_own_atoms: int,
+                 nccl_id: bytes | None = None, ghost_capacity: int = 0):
+        self.plan = plan  # keeps the plan alive
+        h = C.c_void_p()
+        idb = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        _check(_lib.esp_shard_create(plan._h, idb, int(rank), int(nranks), int(max_own_atoms),
+                                     int(ghost_capacity), C.byref(h)))
+        self._h = h
+        info = _ShardInfo()
+        _check(_lib.esp_shard_info(self._h, C.byref(info)))
+        self.info = {k: getattr(info, k) for k, _ in _ShardInfo._fields_}
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                _lib.esp_shard_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    def evaluate(self, box, n_own: int, pos_ptr: int, q_ptr: int, u_ptr: int, F_ptr: int,
+                 energy_ptr: int, stream: int = 0) -> None:
+        """esp_shard_evaluate (collective; device pointers, asynchronous)."""
+        _check(_lib.esp_shard_evaluate(self._h, _f64(box, (3,)), int(n_own), C.c_void_p(pos_ptr),
+                                       C.c_void_p(q_ptr), C.c_void_p(u_ptr), C.c_void_p(F_ptr),
+                                       C.c_void_p(energy_ptr), C.c_void_p(stream)))
+
+    def check(self) -> None:
+        _check(_lib.esp_shard_check(self._h))
+
+
+def evaluate_sharded_emulated(shards, box, n_own, pos_ptrs, q_ptrs, u_ptrs, F_ptrs, e_ptrs,
+                              stream: int = 0) -> None:
+    """All ranks of one decomposition in this process, in lockstep on one GPU
+    (esp_shard_evaluate_emulated); per-rank lists of counts and device
+    pointers."""
+    G = len(shards)
+    arr = lambda vals: (C.c_void_p * G)(*[C.c_void_p(v) for v in vals])  # noqa: E731
+    hs = (C.c_void_p * G)(*[s._h for s in shards])
+    ns = (C.c_long * G)(*[int(v) for v in n_own])
+    _check(_lib.esp_shard_evaluate_emulated(hs, G, _f64(box, (3,)), ns, arr(pos_ptrs),
+                                            arr(q_ptrs), arr(u_ptrs), arr(F_ptrs), arr(e_ptrs),
+                                            C.c_void_p(stream)))

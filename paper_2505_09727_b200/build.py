@@ -28,8 +28,8 @@ NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-pthread",
           "-I" + os.path.join(ROOT, "include")]
-SOURCES = ["plan.cpp", "plan_device.cu", "engine.cu", "direct.cu", "capi.cpp"]
-HEADERS = ["plan.hpp", "engine.hpp", "direct.hpp", os.path.join("..", "..", "include", "esp_b200.h")]
+SOURCES = ["plan.cpp", "plan_device.cu", "engine.cu", "direct.cu", "capi.cpp", "shard.cu"]
+HEADERS = ["plan.hpp", "engine.hpp", "direct.hpp", "capi_internal.hpp", os.path.join("..", "..", "include", "esp_b200.h")]
 
 
 def _newest_header() -> float:
@@ -66,7 +66,7 @@ def build(force: bool = False, verbose: bool = True) -> str:
         objs = list(ex.map(_compile, SOURCES))
     if (not os.path.exists(LIB)) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcufft", "-cudart", "static",
-               "-Xlinker", "-rpath=" + os.path.join(CUDA, "lib64"), "-Xcompiler", "-pthread"]
+               "-Xlinker", "-rpath=" + os.path.join(CUDA, "lib64"), "-Xcompiler", "-pthread", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -2,9 +2,8 @@
 
 #include "../../include/esp_b200.h"
 
+#include "capi_internal.hpp"
 #include "direct.hpp"
-#include "engine.hpp"
-#include "plan.hpp"
 
 #include <cuda_runtime.h>
 #include <cufft.h>
@@ -17,71 +16,18 @@
 #include <string>
 #include <vector>
 
-struct esp_plan {
-    espb::Plan plan;
-    std::unique_ptr<espb::Engine> eng;
-    int device = -1;
-    // device staging for the host-pointer entry points
-    double* d_pos = nullptr;
-    double* d_q = nullptr;
-    double* d_u = nullptr;
-    double* d_F = nullptr;
-    double* d_e = nullptr;  // energy + qsum[2]
-    double* h_e = nullptr;  // pinned host copy of d_e
-    long cap = 0;
-    cudaStream_t stream = nullptr;
-
-    ~esp_plan() {
-        if (device >= 0) {
-            cudaSetDevice(device);
-            cudaFree(d_pos);
-            cudaFree(d_q);
-            cudaFree(d_u);
-            cudaFree(d_F);
-            cudaFree(d_e);
-            if (h_e) cudaFreeHost(h_e);
-            if (stream) cudaStreamDestroy(stream);
-        }
-    }
-};
+namespace espc {
+std::string& last_error() {
+    static thread_local std::string e;
+    return e;
+}
+}  // namespace espc
 
 namespace {
 
-thread_local std::string g_err;
-
-template <class F>
-int guarded(F&& f) {
-    try {
-        f();
-        return ESP_OK;
-    } catch (const espb::InvalidArgument& e) {
-        g_err = e.what();
-        return ESP_ERR_INVALID_ARGUMENT;
-    } catch (const std::invalid_argument& e) {
-        g_err = e.what();
-        return ESP_ERR_INVALID_ARGUMENT;
-    } catch (const espb::NumericalError& e) {
-        g_err = e.what();
-        return ESP_ERR_NUMERICAL;
-    } catch (const espb::CudaError& e) {
-        g_err = e.what();
-        return ESP_ERR_CUDA;
-    } catch (const std::exception& e) {
-        g_err = e.what();
-        return ESP_ERR_INTERNAL;
-    }
-}
-
-void cuda_ok(cudaError_t e, const char* what) {
-    if (e != cudaSuccess)
-        throw espb::CudaError(std::string(what) + ": " + cudaGetErrorString(e));
-}
-
-espb::Engine& engine(esp_plan* p) {
-    if (!p) throw espb::InvalidArgument("null plan");
-    if (!p->eng) throw espb::CudaError("plan was created host-only (device < 0)");
-    return *p->eng;
-}
+using espc::cuda_ok;
+using espc::engine;
+using espc::guarded;
 
 void check_box(const esp_plan* p, const double* box, const char* who) {
     // evaluate / spectral_sum require box == plan.box exactly (ewald.hpp:620-621)
@@ -156,7 +102,7 @@ void check_n(long N) {
 
 extern "C" {
 
-const char* esp_last_error(void) { return g_err.c_str(); }
+const char* esp_last_error(void) { return espc::last_error().c_str(); }
 const char* esp_version(void) { return "esp-b200 0.1 (sm_100a)"; }
 
 int esp_device_count(void) {

@@ -2501,9 +2501,9 @@ void Engine::reconfigure(long N) {
     ensure_capacity(N);
     int want = kColDivDefault;
     const Plan& p = plan_;
-    const double pairs_per_atom =
-        static_cast<double>(N) / (p.box[0] * p.box[1] * p.box[2]) * 4.0 / 3.0 * kPi * p.r_c *
-        p.r_c * p.r_c;
+    const double rho = density_hint_ > 0.0 ? density_hint_
+                                           : static_cast<double>(N) / (p.box[0] * p.box[1] * p.box[2]);
+    const double pairs_per_atom = rho * 4.0 / 3.0 * kPi * p.r_c * p.r_c * p.r_c;
     if (pairs_per_atom >= kColDiv3MinPairs) want = 3;
     if (const char* e = std::getenv("ESP_COL_DIV")) want = std::max(2, std::min(kMaxColDiv, std::atoi(e)));
     // per-warp list pieces: the expected candidates per target (~1.8 / 2.2 per
@@ -2789,7 +2789,12 @@ bool Engine::run_pair_half(long N, cudaStream_t s, int rank, int nranks, bool ow
     int nd = 20;
     const PairConsts k = make_pair_consts(p, nd);
     double per_cell = static_cast<double>(N) / ncellF_;
-    if (own_bins) {
+    if (own_bins && density_hint_ > 0.0) {
+        // sharded evaluation: the system's mean density (plus 20 %) instead of
+        // a read-back of the rank's cell counts; denser blocks overflow to
+        // k_pair_half_ovf
+        per_cell = 1.2 * density_hint_ * p.box[0] * p.box[1] * p.box[2] / ncellF_;
+    } else if (own_bins) {
         // distributed FFT: the inputs may be the rank's own atoms + ghosts only,
         // so the density behind the staging capacity is measured over the
         // columns around the rank's planes (cell starts read back: one small
@@ -2875,8 +2880,10 @@ bool Engine::run_pair_half(long N, cudaStream_t s, int rank, int nranks, bool ow
     a.cap = best_cap;
     {
         // forward list per target: about half the full-list estimate
-        const double ppa = static_cast<double>(N) / (p.box[0] * p.box[1] * p.box[2]) * 4.0 / 3.0 *
-                           kPi * p.r_c * p.r_c * p.r_c;
+        const double ppa = (density_hint_ > 0.0 ? density_hint_
+                                                 : static_cast<double>(N) /
+                                                       (p.box[0] * p.box[1] * p.box[2])) *
+                           4.0 / 3.0 * kPi * p.r_c * p.r_c * p.r_c;
         const double cand = ppa * (col_div_ == 3 ? 1.8 : 2.2) * 0.6;
         int l = std::max(128, std::min(1024, (static_cast<int>(cand) + 63) / 64 * 64));
         if (const char* e = std::getenv("ESP_PAIR_LCAP")) l = std::max(128, std::min(2048, std::atoi(e) / 32 * 32));

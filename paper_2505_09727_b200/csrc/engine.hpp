@@ -130,6 +130,14 @@ public:
     void pencil_phase_b(int rank, int nranks, const double* fslab, double* u, double* F,
                         double* energy_dev, cudaStream_t s);
 
+    // Distributed FFT with local inputs (esp_shard): the rank's atoms cover
+    // only its slab, so N / box volume underestimates the density.  A hint
+    // (atoms per unit volume of the whole system) replaces it in the cell-list
+    // and staging-capacity choices, and the half-shell kernel then sizes its
+    // staging without reading cell counts back (no host synchronisation:
+    // the sharded evaluation can be captured in a CUDA graph).  0 = none.
+    void set_density_hint(double rho) { density_hint_ = rho; }
+
     // Launch count of the last evaluate() (our kernels only, excluding cuFFT).
     int last_launches() const { return launches_; }
     // distributed-FFT K4 mode (fixed when the engine is built; see run_pair)
@@ -222,6 +230,7 @@ private:
     int* d_ovf_ = nullptr;
     double* d_acc_ = nullptr;           // half-shell K4: planar pair-sorted (u, F) sums, 4 x cap_              // half-shell K4: overflowed blocks (count, ids)
     long ovf_cap_ = 0;
+    double density_hint_ = 0.0;        // set_density_hint
     bool pencil_half_ = true;           // distributed FFT with half-shell K4 (ESP_PENCIL_HALF=0: full
                                         // lists); local inputs return the ghost partner terms (dist.py)
     int half_mode_ = 1;                 // half-shell K4: 0 never, 1 from kHalfMinN atoms, 2 always (ESP_PAIR_HALF)

@@ -111,3 +111,26 @@ def test_plan_info_layout_matches_the_header():
     assert g["nf"] == p.nf and g["rank"] == 1 and g["nranks"] == 2
     assert abs(g["hx"] - p.h[0]) < 1e-15 and g["x1"] == p.nf[0]
     assert g["slab_reals"] == (g["x1"] - g["x0"] + 2 * g["halo"]) * p.nf[1] * p.nf[2]
+
+
+def test_shard_owner_matches_pencil_geometry(esp):
+    """esp_shard_owner: the rank whose planes hold clamp(floor(fold(x)/hx)),
+    the same ownership rule as the distributed FFT (esp_pencil_geometry)."""
+    from paper_2505_09727_b200 import systems as S
+    c = S.config("cfg2")
+    pos, q, box = c.system()
+    p = esp.build_plan(box, "pswf", c.eps, c.r_c, device=-1)
+    for G in (2, 3, 4):
+        own = esp.shard_owner(p, G, pos - box[0] * 0.5)  # unfolded images
+        geo = [esp.pencil_geometry(p, r, G) for r in range(G)]
+        x = np.mod(pos[:, 0] - box[0] * 0.5, box[0])
+        pl = np.clip(np.floor(x / geo[0]["hx"]).astype(int), 0, p.nf[0] - 1)
+        want = np.searchsorted([g["x1"] for g in geo], pl, side="right")
+        assert np.array_equal(own, want)
+        assert np.bincount(own, minlength=G).min() > 0
+
+
+def test_shard_needs_a_device_plan(esp):
+    p = esp.build_plan((40.0, 40.0, 40.0), "pswf", 1e-3, 4.0, device=-1)
+    with pytest.raises(esp.CudaError):
+        esp.Shard(p, 0, 2, 1000)
