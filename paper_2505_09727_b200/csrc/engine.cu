@@ -1633,6 +1633,202 @@ __global__ void __launch_bounds__(256) k_scale(long Mh, int ny, int nzh, const d
 }
 
 // ----------------------------------------------------------------------------
+// K2 fused into the FFT (the x pass of the 3-D transforms)
+//
+// The 3-D forward DFT is a batched 2-D D2Z over (y, z) per x-plane (cuFFT)
+// followed by 1-D DFTs along x; the inverse is 1-D DFTs along x followed by
+// batched 2-D Z2D per field.  k_xpass does the x-direction work of BOTH
+// transforms in one pass over the half spectrum, with the influence multiply
+// and the ik derivatives in between (ewald.hpp:545-548, 567-595;
+// gridder.hpp:162-210):
+//   for a block of CW consecutive kz columns at one ky (loaded once):
+//     X = DFT_x(b)                (forward, e^{-i})
+//     C = p(kx, ky, kz) X         (influence; p includes the 1/M scaling)
+//     A = IDFT_x(C), B = IDFT_x(i xi_x C)      (inverse, e^{+i}, ik only)
+//     out = {A, B, i xi_y A, i xi_z A}          (xi := 0 at Nyquist)
+// i xi_y and i xi_z are constant along x, so they commute with IDFT_x and
+// are applied on the way out.  The spectra never make a round trip through
+// HBM between the transforms and the multiply: the separate k_scale pass
+// (read b, p; write 4 spectra) and the x-stages of the five cuFFT transforms
+// are replaced by one read of b and p and one write of the 4 half-transformed
+// fields.  The 1-D DFTs are self-sorting Stockham passes of radix 4, 2, 3, 5
+// in shared memory (n_x even 5-smooth, the reference's auto grids,
+// ewald.hpp:261-273), fp64 throughout, twiddles from a long-double table.
+// Grids with other n_x (explicit overrides) or n_x < 128 (where the 3-D
+// path's fewer launches are faster) keep cuFFT 3-D + k_scale.
+// ----------------------------------------------------------------------------
+
+constexpr int kXpCols = 4;          // kz columns per CTA
+constexpr int kXpThreads = 256;
+constexpr int kXpMaxPass = 16;
+constexpr int kXpMaxN = 720;        // shared memory: n_x * (2 * 2 * kXpCols + 1) * 16 B
+constexpr int kXpAutoMinN = 128;    // k_xpass by default from this n_x
+
+struct XPassArgs {
+    int nx, ny, nzh;
+    int npass;
+    int rad[kXpMaxPass];            // radix of each Stockham pass (product nx)
+    int ns[kXpMaxPass];             // product of the radices before the pass
+    float invns[kXpMaxPass];        // 1 / ns
+    long Mh;
+    int nfields;                    // 4 (ik) or 1 (ad)
+    const double2* tw;              // nx twiddles e^{-2 pi i t / nx}
+    const double* p;                // influence, half spectrum [kx][ky][kz]
+    const double* xi;               // nx + ny + nz derivative multipliers
+    const double2* in;              // 2-D transformed planes [x][ky][kz]
+    double2* out;                   // nfields x [x][ky][kz]
+};
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+// s i z (s = +1 / -1)
+template <int S>
+__device__ __forceinline__ double2 cmuli(double2 z) {
+    return S > 0 ? make_double2(-z.y, z.x) : make_double2(z.y, -z.x);
+}
+
+// radix-R DFT of v in place; S = -1 forward (e^{-i}), +1 inverse
+template <int R, int S>
+__device__ __forceinline__ void dft_small(double2* v) {
+    if (R == 2) {
+        const double2 a = v[0], b = v[1];
+        v[0] = cadd(a, b);
+        v[1] = csub(a, b);
+    } else if (R == 4) {
+        const double2 t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]);
+        const double2 t2 = cadd(v[1], v[3]), t3 = cmuli<S>(csub(v[1], v[3]));
+        v[0] = cadd(t0, t2);
+        v[2] = csub(t0, t2);
+        v[1] = cadd(t1, t3);
+        v[3] = csub(t1, t3);
+    } else if (R == 3) {
+        constexpr double h = 0.86602540378443864676;  // sin(2 pi / 3)
+        const double2 s = cadd(v[1], v[2]), d = csub(v[1], v[2]);
+        const double2 m = make_double2(fma(-0.5, s.x, v[0].x), fma(-0.5, s.y, v[0].y));
+        const double2 e = cmuli<S>(make_double2(h * d.x, h * d.y));
+        v[0] = cadd(v[0], s);
+        v[1] = cadd(m, e);
+        v[2] = csub(m, e);
+    } else if (R == 5) {
+        constexpr double c1 = 0.30901699437494742410, c2 = -0.80901699437494742410;
+        constexpr double s1 = 0.95105651629515357212, s2 = 0.58778525229247312917;
+        const double2 a1 = cadd(v[1], v[4]), b1 = csub(v[1], v[4]);
+        const double2 a2 = cadd(v[2], v[3]), b2 = csub(v[2], v[3]);
+        const double2 x0 = v[0];
+        const double2 m1 = make_double2(x0.x + c1 * a1.x + c2 * a2.x, x0.y + c1 * a1.y + c2 * a2.y);
+        const double2 m2 = make_double2(x0.x + c2 * a1.x + c1 * a2.x, x0.y + c2 * a1.y + c1 * a2.y);
+        const double2 e1 = cmuli<S>(make_double2(s1 * b1.x + s2 * b2.x, s1 * b1.y + s2 * b2.y));
+        const double2 e2 = cmuli<S>(make_double2(s2 * b1.x - s1 * b2.x, s2 * b1.y - s1 * b2.y));
+        v[0] = cadd(x0, cadd(a1, a2));
+        v[1] = cadd(m1, e1);
+        v[4] = csub(m1, e1);
+        v[2] = cadd(m2, e2);
+        v[3] = csub(m2, e2);
+    }
+}
+
+// one Stockham pass of radix R over NC columns (row stride CW2) from `in` to
+// `out`: butterfly j of n/R takes in[j + r n/R], twiddles e^{S 2 pi i
+// (j mod Ns) r / (Ns R)}, writes out[(j / Ns) Ns R + j mod Ns + r Ns].  The
+// per-pass constants come from the host (no integer divisions by runtime
+// values: j / Ns in fp32, exact for j, Ns < 2^12)
+template <int R, int S, int NC, int CW2>
+__device__ __forceinline__ void xp_pass(const double2* __restrict__ in, double2* __restrict__ out,
+                                        int nb, int Ns, int tstep0, float invNs,
+                                        const double2* tw) {
+    for (int e = threadIdx.x; e < nb * NC; e += blockDim.x) {
+        const int j = e / NC, c = e - j * NC;
+        const int q = static_cast<int>((static_cast<float>(j) + 0.5f) * invNs);
+        const int k = j - q * Ns;
+        double2 v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = in[(j + r * nb) * CW2 + c];
+        const int ts = k * tstep0;
+#pragma unroll
+        for (int r = 1; r < R; ++r) {
+            double2 w = tw[ts * r];
+            if (S > 0) w.y = -w.y;
+            v[r] = cmul(v[r], w);
+        }
+        dft_small<R, S>(v);
+        const int d = q * Ns * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) out[(d + r * Ns) * CW2 + c] = v[r];
+    }
+}
+
+// all passes; returns the buffer holding the result
+template <int S, int NC, int CW2>
+__device__ double2* xp_fft(const XPassArgs& a, double2* b0, double2* b1, const double2* tw) {
+    for (int q = 0; q < a.npass; ++q) {
+        const int R = a.rad[q], Ns = a.ns[q], nb = a.nx / R, ts = a.nx / (Ns * R);
+        const float inv = a.invns[q];
+        if (R == 4) xp_pass<4, S, NC, CW2>(b0, b1, nb, Ns, ts, inv, tw);
+        else if (R == 2) xp_pass<2, S, NC, CW2>(b0, b1, nb, Ns, ts, inv, tw);
+        else if (R == 3) xp_pass<3, S, NC, CW2>(b0, b1, nb, Ns, ts, inv, tw);
+        else xp_pass<5, S, NC, CW2>(b0, b1, nb, Ns, ts, inv, tw);
+        double2* t = b0;
+        b0 = b1;
+        b1 = t;
+        __syncthreads();
+    }
+    return b0;
+}
+
+__global__ void __launch_bounds__(kXpThreads) k_xpass(XPassArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int CW = kXpCols, CW2 = 2 * kXpCols;
+    const int nx = a.nx;
+    double2* tw = reinterpret_cast<double2*>(smem);
+    double2* b0 = tw + nx;
+    double2* b1 = b0 + nx * CW2;
+    const int nzb = (a.nzh + CW - 1) / CW;
+    const int ky = blockIdx.x / nzb;
+    const int kz0 = (blockIdx.x - ky * nzb) * CW;
+    const long rowst = static_cast<long>(a.ny) * a.nzh;  // x stride of [x][ky][kz]
+    const long base = static_cast<long>(ky) * a.nzh + kz0;
+    for (int t = threadIdx.x; t < nx; t += blockDim.x) tw[t] = a.tw[t];
+    for (int e = threadIdx.x; e < nx * CW; e += blockDim.x) {
+        const int x = e / CW, c = e - x * CW;
+        b0[x * CW2 + c] = kz0 + c < a.nzh ? a.in[x * rowst + base + c] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    double2* X = xp_fft<-1, CW, CW2>(a, b0, b1, tw);
+    double2* Y = X == b0 ? b1 : b0;
+    // influence multiply (and i xi_x for the x-derivative field)
+    const bool ik = a.nfields == 4;
+    for (int e = threadIdx.x; e < nx * CW; e += blockDim.x) {
+        const int kx = e / CW, c = e - kx * CW;
+        const double pk = kz0 + c < a.nzh ? a.p[kx * rowst + base + c] : 0.0;
+        const double2 v = X[kx * CW2 + c];
+        const double2 cv = make_double2(v.x * pk, v.y * pk);
+        X[kx * CW2 + c] = cv;
+        if (ik) {
+            const double f = a.xi[kx];
+            X[kx * CW2 + CW + c] = make_double2(-cv.y * f, cv.x * f);
+        }
+    }
+    __syncthreads();
+    double2* Z = ik ? xp_fft<1, CW2, CW2>(a, X, Y, tw) : xp_fft<1, CW, CW2>(a, X, Y, tw);
+    for (int e = threadIdx.x; e < nx * CW; e += blockDim.x) {
+        const int x = e / CW, c = e - x * CW;
+        if (kz0 + c >= a.nzh) continue;
+        const long m = x * rowst + base + c;
+        const double2 A = Z[x * CW2 + c];
+        a.out[m] = A;
+        if (ik) {
+            const double fy = a.xi[nx + ky], fz = a.xi[nx + a.ny + kz0 + c];
+            a.out[a.Mh + m] = Z[x * CW2 + CW + c];
+            a.out[2 * a.Mh + m] = make_double2(-A.y * fy, A.x * fy);
+            a.out[3 * a.Mh + m] = make_double2(-A.y * fz, A.x * fz);
+        }
+    }
+}
+
+// ----------------------------------------------------------------------------
 // K3: interpolation + combine (gridder.hpp:244-314, ewald.hpp:571-647)
 // ----------------------------------------------------------------------------
 
@@ -2350,12 +2546,50 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
     dalloc(d_qsum_, 2);
     dalloc(d_npairs_, 1);
 
-    // cuFFT: forward D2Z, batched inverse Z2D
+    // cuFFT.  Even 5-smooth n_x (every auto-selected grid): batched 2-D D2Z /
+    // Z2D over (y, z) planes, the x direction + influence + ik in k_xpass;
+    // otherwise 3-D D2Z, k_scale, batched 3-D Z2D.
     CF(cufftCreate(&fwd_));
     CF(cufftCreate(&inv_));
     CF(cufftSetAutoAllocation(fwd_, 0));
     CF(cufftSetAutoAllocation(inv_, 0));
     size_t w1 = 0, w2 = 0;
+    {
+        int n = p.nf[0];
+        std::vector<int> rad;
+        for (int r : {4, 2, 3, 5})
+            while (n % r == 0 && static_cast<int>(rad.size()) < kXpMaxPass) {
+                rad.push_back(r);
+                n /= r;
+            }
+        // auto from n_x >= 128 (cfg5, n_x = 180: fft + multiply + ifft 0.655 ->
+        // 0.588 ms); below that the 3-D path's fewer launches win (cfg2-4:
+        // +15-25 us).  ESP_XPASS=1 forces it (even 5-smooth n_x), 0 disables.
+        const char* e = std::getenv("ESP_XPASS");
+        const int want = e ? std::atoi(e) : (p.nf[0] >= kXpAutoMinN ? 1 : 0);
+        xpass_ = want != 0 && n == 1 && p.nf[0] % 2 == 0 && p.nf[0] <= kXpMaxN;
+        if (xpass_) {
+            xp_rad_ = rad;
+            std::vector<double2> tw(p.nf[0]);
+            for (int t = 0; t < p.nf[0]; ++t) {
+                const long double ang = -2.0L * 3.141592653589793238462643383279502884L * t / p.nf[0];
+                tw[t] = make_double2(static_cast<double>(cosl(ang)), static_cast<double>(sinl(ang)));
+            }
+            dalloc(d_xtw_, tw.size());
+            CK(cudaMemcpy(d_xtw_, tw.data(), sizeof(double2) * tw.size(), cudaMemcpyHostToDevice));
+        }
+    }
+    if (xpass_) {
+        const int ny = p.nf[1], nz = p.nf[2], nzh = nz / 2 + 1;
+        int n2[2] = {ny, nz};
+        int re[2] = {ny, nz}, ce[2] = {ny, nzh};
+        CF(cufftMakePlanMany(fwd_, 2, n2, re, 1, ny * nz, ce, 1, ny * nzh, CUFFT_D2Z, p.nf[0], &w1));
+        // one field per execution: planar half-transformed input, planar
+        // fields out (interleaved for K3 afterwards, see spectral())
+        CF(cufftMakePlanMany(inv_, 2, n2, ce, 1, ny * nzh, re, 1, ny * nz, CUFFT_Z2D, p.nf[0],
+                             &w2));
+        dalloc(d_fplanar_, nfields_ * M_);
+    } else {
     CF(cufftMakePlan3d(fwd_, p.nf[0], p.nf[1], p.nf[2], CUFFT_D2Z, &w1));
     int n3[3] = {p.nf[0], p.nf[1], p.nf[2]};
     int inembed[3] = {p.nf[0], p.nf[1], p.nf[2] / 2 + 1};
@@ -2369,6 +2603,7 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
     } else {
         CF(cufftMakePlanMany(inv_, 3, n3, inembed, 1, static_cast<int>(Mh_), onembed, 1,
                              static_cast<int>(M_), CUFFT_Z2D, 1, &w2));
+    }
     }
     CK(cudaMalloc(&d_cufft_work_, std::max<size_t>(std::max(w1, w2), 16)));
     CF(cufftSetWorkArea(fwd_, d_cufft_work_));
@@ -2414,6 +2649,8 @@ Engine::~Engine() {
     dfree(d_win_);
     dfree(d_influence_);
     dfree(d_xi_);
+    dfree(d_xtw_);
+    dfree(d_fplanar_);
     dfree(d_tmp_);
     dfree(d_cellA_);
     dfree(d_rankA_);
@@ -2989,15 +3226,7 @@ void Engine::phase_b(int rank, int nranks, const double* grid_in, double* u, dou
         CK(cudaMemsetAsync(u, 0, sizeof(double) * N, s));
         CK(cudaMemsetAsync(F, 0, sizeof(double) * 3 * N, s));
     }
-    CF(cufftSetStream(fwd_, s));
-    CF(cufftExecD2Z(fwd_, const_cast<double*>(grid_in), d_spec_));
-    k_scale<<<grid1(Mh_, 256), 256, 0, s>>>(Mh_, plan_.nf[1], plan_.nf[2] / 2 + 1, d_influence_,
-                                            d_xi_, plan_.nf[0], plan_.nf[2], d_spec_, d_spec4_,
-                                            nfields_);
-    CK(cudaGetLastError());
-    ++launches_;
-    CF(cufftSetStream(inv_, s));
-    CF(cufftExecZ2D(inv_, d_spec4_, d_fields_));
+    spectral(grid_in, s, nullptr);
     finish(N, rank, nranks, d_fields_, grid_args(), u, F, energy_dev, s);
 }
 
@@ -3040,17 +3269,70 @@ void Engine::finish(long N, int rank, int nranks, const double* fields, const Gr
 void Engine::run_grid(long N, cudaStream_t s, StageTimes* t) {
     run_spread(N, s, 0, 1, nullptr);
     if (t) CK(cudaEventRecord(ev_t_[3], s));
+    spectral(d_grid_, s, t);
+}
+
+// grid -> the nfields interleaved fields (stage events 4, 5, 6 after the
+// forward transform, the multiply and the inverse transform).  With k_xpass
+// "fft" is the 2-D forward planes, "scale" the fused x pass (forward x DFTs,
+// influence, ik, inverse x DFTs) and "ifft" the 2-D inverse planes.
+void Engine::spectral(const double* grid_in, cudaStream_t s, StageTimes* t) {
     CF(cufftSetStream(fwd_, s));
-    CF(cufftExecD2Z(fwd_, d_grid_, d_spec_));
+    CF(cufftExecD2Z(fwd_, const_cast<double*>(grid_in), d_spec_));
     if (t) CK(cudaEventRecord(ev_t_[4], s));
-    k_scale<<<grid1(Mh_, 256), 256, 0, s>>>(Mh_, plan_.nf[1], plan_.nf[2] / 2 + 1, d_influence_,
-                                            d_xi_, plan_.nf[0], plan_.nf[2], d_spec_, d_spec4_,
-                                            nfields_);
-    CK(cudaGetLastError());
-    ++launches_;
-    if (t) CK(cudaEventRecord(ev_t_[5], s));
-    CF(cufftSetStream(inv_, s));
-    CF(cufftExecZ2D(inv_, d_spec4_, d_fields_));
+    if (xpass_) {
+        XPassArgs a{};
+        a.nx = plan_.nf[0];
+        a.ny = plan_.nf[1];
+        a.nzh = plan_.nf[2] / 2 + 1;
+        a.npass = static_cast<int>(xp_rad_.size());
+        for (int q = 0, ns = 1; q < a.npass; ++q) {
+            a.rad[q] = xp_rad_[q];
+            a.ns[q] = ns;
+            a.invns[q] = 1.0f / static_cast<float>(ns);
+            ns *= xp_rad_[q];
+        }
+        a.Mh = Mh_;
+        a.nfields = nfields_;
+        a.tw = d_xtw_;
+        a.p = d_influence_;
+        a.xi = d_xi_;
+        a.in = reinterpret_cast<const double2*>(d_spec_);
+        a.out = reinterpret_cast<double2*>(d_spec4_);
+        const size_t sm = sizeof(double2) * a.nx * (1 + 2 * 2 * kXpCols);
+        if (sm > 48 * 1024)
+            CK(cudaFuncSetAttribute(k_xpass, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(sm)));
+        const int nzb = (a.nzh + kXpCols - 1) / kXpCols;
+        k_xpass<<<static_cast<unsigned>(a.ny * nzb), kXpThreads, sm, s>>>(a);
+        CK(cudaGetLastError());
+        ++launches_;
+        if (t) CK(cudaEventRecord(ev_t_[5], s));
+        CF(cufftSetStream(inv_, s));
+        // planar fields (cuFFT rejects the 8-byte-offset output bases of an
+        // interleaved layout), then interleaved [node][4] for K3's 256-bit
+        // node loads (K3 reading the planar fields, four 64-bit loads per
+        // node: cfg5 3.35 -> 4.16 ms)
+        for (int f = 0; f < nfields_; ++f)
+            CF(cufftExecZ2D(inv_, d_spec4_ + f * Mh_, d_fplanar_ + f * M_));
+        if (nfields_ == 4) {
+            k_pencil_interleave<<<grid1(M_, 256), 256, 0, s>>>(M_, 4, d_fplanar_, d_fields_);
+            CK(cudaGetLastError());
+            ++launches_;
+        } else {
+            CK(cudaMemcpyAsync(d_fields_, d_fplanar_, sizeof(double) * M_,
+                               cudaMemcpyDeviceToDevice, s));
+        }
+    } else {
+        k_scale<<<grid1(Mh_, 256), 256, 0, s>>>(Mh_, plan_.nf[1], plan_.nf[2] / 2 + 1,
+                                                d_influence_, d_xi_, plan_.nf[0], plan_.nf[2],
+                                                d_spec_, d_spec4_, nfields_);
+        CK(cudaGetLastError());
+        ++launches_;
+        if (t) CK(cudaEventRecord(ev_t_[5], s));
+        CF(cufftSetStream(inv_, s));
+        CF(cufftExecZ2D(inv_, d_spec4_, d_fields_));
+    }
     if (t) CK(cudaEventRecord(ev_t_[6], s));
 }
 

@@ -15,6 +15,7 @@
 #include <cufft.h>
 
 #include <array>
+#include <vector>
 #include <string>
 
 namespace espb {
@@ -163,6 +164,7 @@ private:
     void run_pair(long N, cudaStream_t s, int rank, int nranks, bool own_bins = false);
     bool run_pair_half(long N, cudaStream_t s, int rank = 0, int nranks = 1, bool own_bins = false);
     void run_grid(long N, cudaStream_t s, StageTimes* t);
+    void spectral(const double* grid_in, cudaStream_t s, StageTimes* t);
     void run_spread(long N, cudaStream_t s, int rank, int nranks, double* grid,
                     const GridArgs* gslab = nullptr, long nreals = -1, int b0 = -1,
                     int b1 = -1);
@@ -201,6 +203,10 @@ private:
     double* d_win_ = nullptr;        // 3 x 4P x 13 phi, then 3 x 4P x 13 dphi
     double* d_influence_ = nullptr;  // Mh
     double* d_xi_ = nullptr;         // nx + ny + nz derivative multipliers (Nyquist = 0)
+    bool xpass_ = false;             // 2-D cuFFT planes + k_xpass (x DFTs fused with K2)
+    std::vector<int> xp_rad_;        // k_xpass Stockham radices (product n_x)
+    double2* d_xtw_ = nullptr;       // n_x twiddles e^{-2 pi i t / n_x}
+    double* d_fplanar_ = nullptr;    // k_xpass path: planar fields before interleaving
 
     // scratch
     long cap_ = 0;
