@@ -414,12 +414,12 @@ def run_ours(args):
                 "work": f"{FLOPS_PER_UNORDERED_PAIR} flops x {ordered_pairs // 2} unordered "
                         "in-range pairs (counted on device)",
                 "kernel_ms": stages_ms["local"],
-                "limiter": "instruction issue and fp64 dependency latency (profiles/r01_full_cfg*.md): "
-                           "the fp64 rounds (~68 fp64 ops per pair, both sides' terms) run at "
-                           "~2x the issue rate they need, while the neighbour search (forward "
-                           "columns, list, fp32 screen, ballot compaction) and the last partial "
-                           "round per target take ~40 % of the instructions; the partner terms go "
-                           "to L2 as fire-and-forget fp64 REDs"}
+                "limiter": "instruction issue (profiles/r02_k4_lines_cfg5.md, cfg5: 68 % issue "
+                           "active, fp64 pipe 33 %): ~290 warp instructions per 32 pairs, of "
+                           "which the fp64 pair terms of both sides are ~32 % and the "
+                           "neighbour search the rest -- fp32 screen + ballot compaction 16 %, "
+                           "queue flushes 10 %, candidate-list fill 10 %, staging and "
+                           "per-target setup 12 %, partial rounds 5 %, partner REDs 7 %"}
 
     # ---- every grid-pipeline kernel against the HBM roofline (SURVEY 8(d)
     # algorithmic bytes; serialised stage times).  The grids fit in L2 (cfg5:
@@ -435,13 +435,26 @@ def run_ours(args):
     M = int(np.prod(plan.nf))
     Mh = int(plan.nf[0] * plan.nf[1] * (plan.nf[2] // 2 + 1))
     nfld = 4 if args.force_method == "ik" else 1
-    kbytes = {
-        "K1 k_spread": (32 * N + 8 * M, "spread"),
-        "K2 k_scale": ((24 + 16 * nfld) * Mh, "scale"),
-        "K3 k_interp": (8 * nfld * M + 64 * N, "interpolate"),
-        "cuFFT D2Z": (8 * M + 16 * Mh, "fft"),
-        f"cuFFT Z2D x{nfld}": (nfld * (16 * Mh + 8 * M), "ifft"),
-    }
+    if plan.fused_xpass:
+        # 2-D cuFFT planes + K2 fused into the x pass (read b and p, write the
+        # nfld half-transformed fields); the inverse planes write planar
+        # fields that are interleaved for K3 (read + write)
+        kbytes = {
+            "K1 k_spread": (32 * N + 8 * M, "spread"),
+            "K2+x-DFTs k_xpass (fused)": ((24 + 16 * nfld) * Mh, "scale"),
+            "K3 k_interp": (8 * nfld * M + 64 * N, "interpolate"),
+            "cuFFT D2Z 2-D planes": (8 * M + 16 * Mh, "fft"),
+            f"cuFFT Z2D 2-D planes x{nfld} + interleave":
+                (nfld * (16 * Mh + 8 * M) + (16 * nfld * M if nfld == 4 else 0), "ifft"),
+        }
+    else:
+        kbytes = {
+            "K1 k_spread": (32 * N + 8 * M, "spread"),
+            "K2 k_scale": ((24 + 16 * nfld) * Mh, "scale"),
+            "K3 k_interp": (8 * nfld * M + 64 * N, "interpolate"),
+            "cuFFT D2Z": (8 * M + 16 * Mh, "fft"),
+            f"cuFFT Z2D x{nfld}": (nfld * (16 * Mh + 8 * M), "ifft"),
+        }
     kernels = {}
     for name, (nbytes, stage) in kbytes.items():
         kms = stages_ms.get(stage)

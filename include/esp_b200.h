@@ -78,6 +78,10 @@ typedef struct {
                              * partner terms owed to their owners, which the
                              * caller must send back and add (see below);
                              * 0 = full lists, ghost rows are zero */
+    int fused_xpass;        /* 1: the influence multiply and ik derivatives run
+                             * inside the FFT's x pass (2-D cuFFT planes +
+                             * k_xpass; even 5-smooth n_x >= 128, ESP_XPASS);
+                             * 0: 3-D cuFFT + separate multiply pass */
 } esp_plan_info;
 
 /* Per-stage wall time in seconds (EnergyForces::timings keys,

@@ -73,7 +73,7 @@ class _Info(C.Structure):
         ("self_coef", C.c_double),
         ("n_split_coef", C.c_int), ("n_window_coef", C.c_int), ("pair_poly_degree", C.c_int),
         ("pair_fit_err", C.c_double), ("device", C.c_int), ("pair_cells", C.c_int * 3),
-        ("pencil_half", C.c_int),
+        ("pencil_half", C.c_int), ("fused_xpass", C.c_int),
     ]
 
 
@@ -91,7 +91,7 @@ class _ShardInfo(C.Structure):
     _fields_ = [("rank", C.c_int), ("nranks", C.c_int), ("x0", C.c_int), ("x1", C.c_int),
                 ("X0", C.c_double), ("X1", C.c_double), ("max_own_atoms", C.c_long),
                 ("ghost_capacity", C.c_long), ("local_atoms", C.c_long),
-                ("pencil_half", C.c_int), ("nccl", C.c_int)]
+                ("pencil_half", C.c_int), ("fused_xpass", C.c_int), ("nccl", C.c_int)]
 
 
 class _DirectInfo(C.Structure):
@@ -238,6 +238,8 @@ class EwaldPlan:
         self.pair_cells = tuple(info.pair_cells)
         # distributed-FFT K4 mode, fixed at plan build (include/esp_b200.h)
         self.pencil_half = bool(info.pencil_half)
+        # K2 inside the FFT's x pass (include/esp_b200.h)
+        self.fused_xpass = bool(info.fused_xpass)
 
     def __del__(self):
         h = getattr(self, "_h", None)

@@ -185,6 +185,7 @@ int esp_plan_get_info(const esp_plan* p, esp_plan_info* o) {
         o->n_window_coef = static_cast<int>(P.window.a.size());
         o->pair_poly_degree = static_cast<int>(P.pair_H.size()) - 1;
         o->pencil_half = p->eng ? (p->eng->pencil_half() ? 1 : 0) : espb::Engine::pencil_half_env();
+        o->fused_xpass = p->eng && p->eng->fused_xpass() ? 1 : 0;
         o->pair_fit_err = P.pair_fit_err;
         o->device = p->device;
     });

@@ -1852,6 +1852,8 @@ struct InterpArgs {
     double* epart;         // per-block energy partial sums
     const int* startB;     // if set: only atoms of spread bins [bin_lo, bin_hi)
     int bin_lo, bin_hi;
+    double4* S;            // kSpectral: if set, (u_s, F_s) per atom (original order) go
+                           // here as one 32-byte store instead of into u / F
 };
 
 // Thread per atom (spread-bin order, so neighbouring threads share grid
@@ -2015,10 +2017,16 @@ __global__ void __launch_bounds__(128) k_interp(GridArgs g, InterpArgs a) {
         }
         if (MODE == kSpectral) {
             us -= qi * a.self_coef;  // self term (0 for the spectral_sum API)
-            a.u[o] = us;
-            a.F[3 * o + 0] = Fx;
-            a.F[3 * o + 1] = Fy;
-            a.F[3 * o + 2] = Fz;
+            if (a.S) {
+                // one full 32-byte sector per atom: the scattered 8/24-byte
+                // u / F stores were partial sectors, filled from DRAM
+                a.S[o] = make_double4(us, Fx, Fy, Fz);
+            } else {
+                a.u[o] = us;
+                a.F[3 * o + 0] = Fx;
+                a.F[3 * o + 1] = Fy;
+                a.F[3 * o + 2] = Fz;
+            }
         }
     }
 }
@@ -2104,10 +2112,14 @@ __global__ void __launch_bounds__(128) k_interp8(GridArgs g, InterpArgs a) {
     if (j == 0) {
         const int o = a.orig[k];
         const double qi = v.w;
-        a.u[o] = a0 - qi * a.self_coef;
-        a.F[3 * o + 0] = -qi * a1;
-        a.F[3 * o + 1] = -qi * a2;
-        a.F[3 * o + 2] = -qi * a3;
+        if (a.S) {
+            a.S[o] = make_double4(a0 - qi * a.self_coef, -qi * a1, -qi * a2, -qi * a3);
+        } else {
+            a.u[o] = a0 - qi * a.self_coef;
+            a.F[3 * o + 0] = -qi * a1;
+            a.F[3 * o + 1] = -qi * a2;
+            a.F[3 * o + 2] = -qi * a3;
+        }
     }
 }
 
@@ -2116,7 +2128,8 @@ __global__ void __launch_bounds__(128) k_interp8(GridArgs g, InterpArgs a) {
 // partial sums of q u feed the energy.
 __global__ void __launch_bounds__(256) k_combine(long N, const double4* __restrict__ loc,
                                                  const double4* __restrict__ xyzq_orig,
-                                                 double self_coef, double* __restrict__ u,
+                                                 const double4* __restrict__ spec,
+                                                 double* __restrict__ u,
                                                  double* __restrict__ F, double* __restrict__ epart,
                                                  double* __restrict__ u_out,
                                                  double* __restrict__ F_out) {
@@ -2127,11 +2140,15 @@ __global__ void __launch_bounds__(256) k_combine(long N, const double4* __restri
     if (i < N) {
         const double4 l = loc[i];
         const double qi = xyzq_orig[i].w;
-        const double ui = l.x + u[i];  // u holds u_s - q s0 (self folded in K3)
+        // spectral part u_s - q s0 (self folded in K3) and F_s: from spec if
+        // set, else from u / F
+        const double4 sp = spec ? spec[i] : make_double4(u[i], F[3 * i + 0], F[3 * i + 1],
+                                                         F[3 * i + 2]);
+        const double ui = l.x + sp.x;
         double* uo = u_out ? u_out : u;
         double* Fo = F_out ? F_out : F;
         uo[i] = ui;
-        const double fx = F[3 * i + 0] + l.y, fy = F[3 * i + 1] + l.z, fz = F[3 * i + 2] + l.w;
+        const double fx = sp.y + l.y, fy = sp.z + l.z, fz = sp.w + l.w;
         Fo[3 * i + 0] = fx;
         Fo[3 * i + 1] = fy;
         Fo[3 * i + 2] = fz;
@@ -2661,6 +2678,7 @@ Engine::~Engine() {
     dfree(d_xyzqB_);
     dfree(d_origB_);
     dfree(d_loc_);
+    dfree(d_specres_);
     dfree(d_epart_);
     dfree(d_countA_);
     dfree(d_startA_);
@@ -2784,6 +2802,7 @@ void Engine::ensure_capacity(long N) {
     dalloc(d_xyzqB_, c);
     dalloc(d_origB_, c);
     dalloc(d_loc_, c);
+    dalloc(d_specres_, c);
     dalloc(d_acc_, 4 * c);  // half-shell K4 accumulators: zero at rest
     CK(cudaMemset(d_acc_, 0, sizeof(double) * 4 * c));
     dalloc(d_epart_, grid1(c, 128) + 1);
@@ -3255,8 +3274,8 @@ void Engine::finish(long N, int rank, int nranks, const double* fields, const Gr
     }
     const int nblk = static_cast<int>(grid1(std::max<long>(N, 1), 256));
     if (N > 0) {
-        k_combine<<<nblk, 256, 0, s>>>(N, d_loc_, d_tmp_, plan_.self_coef, u, F, d_epart_,
-                                       nullptr, nullptr);
+        k_combine<<<nblk, 256, 0, s>>>(N, d_loc_, d_tmp_, nullptr, u, F, d_epart_, nullptr,
+                                       nullptr);
         CK(cudaGetLastError());
         k_energy<<<1, 256, 0, s>>>(d_epart_, nblk, energy_dev);
         CK(cudaGetLastError());
@@ -3543,8 +3562,9 @@ void Engine::enqueue(long N, const double* pos, const double* q, double* u, doub
     a.orig = d_origB_;
     a.fields = d_fields_;
     a.M = M_;
-    a.u = u;  // spectral part (minus self) lands in the caller's arrays, combined below
+    a.u = u;
     a.F = F;
+    a.S = d_specres_;  // spectral part (minus self) per atom, combined below
     a.self_coef = plan_.self_coef;
     const GridArgs g = grid_args();
     if (t) {
@@ -3578,8 +3598,8 @@ void Engine::enqueue(long N, const double* pos, const double* q, double* u, doub
     }
     const int nblk = static_cast<int>(grid1(std::max<long>(N, 1), 256));
     if (N > 0) {
-        k_combine<<<nblk, 256, 0, s>>>(N, d_loc_, d_tmp_, plan_.self_coef, u, F, d_epart_,
-                                       u_out, F_out);
+        k_combine<<<nblk, 256, 0, s>>>(N, d_loc_, d_tmp_, d_specres_, u, F, d_epart_, u_out,
+                                       F_out);
         CK(cudaGetLastError());
         ++launches_;
         k_energy<<<1, 256, 0, s>>>(d_epart_, nblk, energy_dev);

@@ -143,6 +143,7 @@ public:
     int last_launches() const { return launches_; }
     // distributed-FFT K4 mode (fixed when the engine is built; see run_pair)
     bool pencil_half() const { return pencil_half_; }
+    bool fused_xpass() const { return xpass_; }
     static int pencil_half_env() {
         const char* e = std::getenv("ESP_PENCIL_HALF");
         return (e && std::atoi(e) == 0) ? 0 : 1;
@@ -220,6 +221,7 @@ private:
     double4* d_xyzqB_ = nullptr;
     int* d_origB_ = nullptr;
     double4* d_loc_ = nullptr;   // (u_l, F_l) in original order
+    double4* d_specres_ = nullptr;  // (u_s - q s0, F_s) in original order (K3 -> combine)
     double* d_epart_ = nullptr;  // energy partials
     int* d_countA_ = nullptr;    // ncell + 1
     int* d_startA_ = nullptr;

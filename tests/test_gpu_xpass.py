@@ -90,3 +90,19 @@ def test_non_smooth_override_keeps_3d_path(esp, gpu, monkeypatch):
     fused pass has radices 2-5 only, so the 3-D path runs even when forced."""
     monkeypatch.setenv("ESP_XPASS", "1")
     _vs_oracle(esp, gpu, (10.0, 10.0, 10.0), 500, 5, 1e-4, 1.0, nf=42)
+
+
+def test_mode_reported_by_plan(esp, gpu, monkeypatch):
+    """esp_plan_info.fused_xpass: auto from n_x >= 128 (cfg5's 180), forced by
+    ESP_XPASS=1 on smooth grids, never for non-smooth n_x."""
+    from paper_2505_09727_b200 import systems as S
+    monkeypatch.delenv("ESP_XPASS", raising=False)
+    c5 = S.config("cfg5")
+    assert esp.build_plan((c5.L,) * 3, "pswf", c5.eps, c5.r_c, device=gpu).fused_xpass
+    assert not esp.build_plan((10.0,) * 3, "pswf", 1e-4, 1.0, device=gpu).fused_xpass
+    monkeypatch.setenv("ESP_XPASS", "1")
+    assert esp.build_plan((10.0,) * 3, "pswf", 1e-4, 1.0, device=gpu).fused_xpass
+    assert not esp.build_plan((10.0,) * 3, "pswf", 1e-4, 1.0, esp.Overrides(nf=42),
+                              device=gpu).fused_xpass
+    monkeypatch.setenv("ESP_XPASS", "0")
+    assert not esp.build_plan((c5.L,) * 3, "pswf", c5.eps, c5.r_c, device=gpu).fused_xpass
