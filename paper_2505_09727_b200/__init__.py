@@ -34,7 +34,10 @@ __all__ = [
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libesp_b200.so")
+# ESP_B200_CHECKED=1 loads the checked build (device-side bounds checks,
+# build.py --checked): a diagnostics variant of the same library
+LIB_PATH = os.path.join(_PKG, "libesp_b200_checked.so" if os.environ.get("ESP_B200_CHECKED") == "1"
+                        else "libesp_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -36,13 +36,22 @@ def _newest_header() -> float:
     return max(os.path.getmtime(os.path.join(CSRC, h)) for h in HEADERS)
 
 
-def _compile(src: str) -> str:
+def _paths(checked: bool):
+    """(object directory, library) of the product or the checked build."""
+    if checked:
+        return BUILD + "_checked", os.path.join(PKG, "libesp_b200_checked.so")
+    return BUILD, LIB
+
+
+def _compile(src: str, checked: bool = False) -> str:
     path = os.path.join(CSRC, src)
-    obj = os.path.join(BUILD, src + ".o")
+    obj = os.path.join(_paths(checked)[0], src + ".o")
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(path),
                                                             _newest_header()):
         return obj
     cmd = [NVCC, *ARCH, *COMMON, "-c", path, "-o", obj]
+    if checked:
+        cmd += ["-DESP_DEVICE_CHECKS"]
     if src.endswith(".cu"):
         cmd += ["-Xptxas", "-warn-spills"]
     else:
@@ -55,15 +64,19 @@ def _compile(src: str) -> str:
     return obj
 
 
-def build(force: bool = False, verbose: bool = True) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = True, checked: bool = False) -> str:
+    """Compile libesp_b200.so (or, checked=True, libesp_b200_checked.so with
+    the device-side bounds checks ESP_DCHECK compiled in, loaded by the
+    package when ESP_B200_CHECKED=1)."""
+    bdir, LIB = _paths(checked)
+    os.makedirs(bdir, exist_ok=True)
     if force:
         for s in SOURCES:
-            o = os.path.join(BUILD, s + ".o")
+            o = os.path.join(bdir, s + ".o")
             if os.path.exists(o):
                 os.remove(o)
     with ThreadPoolExecutor(len(SOURCES)) as ex:
-        objs = list(ex.map(_compile, SOURCES))
+        objs = list(ex.map(lambda src: _compile(src, checked), SOURCES))
     if (not os.path.exists(LIB)) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcufft", "-cudart", "static",
                "-Xlinker", "-rpath=" + os.path.join(CUDA, "lib64"), "-Xcompiler", "-pthread", "-ldl"]
@@ -76,4 +89,4 @@ def build(force: bool = False, verbose: bool = True) -> str:
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv)
+    build(force="--force" in sys.argv, checked="--checked" in sys.argv)

@@ -340,9 +340,11 @@ __global__ void __launch_bounds__(256) k_scatter(long N, const double4* __restri
     if (i >= N) return;
     double4 v = tmp[i];
     int da = startA[cellA[i]] + rankA[i];
+    ESP_DCHECK(da >= 0 && da < N);
     xyzqA[da] = v;
     origA[da] = static_cast<int>(i);
     int db = startB[cellB[i]] + rankB[i];
+    ESP_DCHECK(db >= 0 && db < N);
     xyzqB[db] = v;
     origB[db] = static_cast<int>(i);
 }
@@ -397,6 +399,7 @@ struct PairArgs {
 // (k_pair_half's list building was ~8 % of its instructions with one store
 // per entry; cfg5 K4 20.6 -> 20.3 ms).
 __device__ __forceinline__ void fill_range(unsigned short* lw, int lb, int p0, int p1, int off) {
+    ESP_DCHECK(p1 <= p0 || (p0 >= lb && off + p1 - 1 < 65536));
     int p = p0;
     for (; p < p1 && (p & 3); ++p) lw[p - lb] = static_cast<unsigned short>(off + p);
     for (; p + 4 <= p1; p += 4) {
@@ -1056,6 +1059,7 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
     const int nsl = bze + 2 * Mz;
     const int nent = ncol * nsl;
     const double ox = fx0 * a.fw[0], oy = fy0 * a.fw[1], oz = z0 * a.fw[2];
+    ESP_DCHECK(nent <= a.nent_max && bxe * bye <= kHalfMaxBX * kHalfMaxBX);
 
     if (threadIdx.x < 27) {
         const int t = threadIdx.x;
@@ -1082,6 +1086,7 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
         fy += (1 - iy) * a.F[1];
         fz += (1 - iz) * a.F[2];
         const int f = (fx * a.F[1] + fy) * a.F[2] + fz;
+        ESP_DCHECK(f >= 0 && f < a.F[0] * a.F[1] * a.F[2]);
         const int s0 = a.start[f];
         ent_src[e] = s0;
         ent_off[e + 1] = a.start[f + 1] - s0;
@@ -1159,6 +1164,7 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
                          shz = shiftv[sl][2] - oz;
             for (int g = g0 + lane; g < g1; g += 32) {
                 const int src = g + src0;
+                ESP_DCHECK(g < a.cap && src >= 0 && src < a.nacc);
                 const double4 v = a.xyzq[src];
                 cand[g] = make_float4(static_cast<float>(v.x + shx), static_cast<float>(v.y + shy),
                                       static_cast<float>(v.z + shz),
@@ -1256,15 +1262,18 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
             }
             const int n = le - lb;
             const int n32 = (n + 31) & ~31;
+            ESP_DCHECK(n32 <= a.lcap);
             if (n + lane < n32) lw[n + lane] = static_cast<unsigned short>(a.cap);
             __syncwarp();
             const unsigned short* lend = lw + n32;
             for (const unsigned short* lp = lw + lane; lp < lend; lp += 32) {
                 const int s = *lp;
+                ESP_DCHECK(s >= 0 && s <= a.cap);
                 const float4 c4 = cand[s];
                 const float dx = c4.x - xf, dy = c4.y - yf, dz = c4.z - zf;
                 const bool in = fmaf(dz, dz, fmaf(dy, dy, dx * dx)) < R2;
                 const unsigned m = __ballot_sync(0xffffffffu, in);
+                ESP_DCHECK(qn + __popc(m) <= 64);
                 if (in) qw[qn + __popc(m & lt_mask)] = s;
                 qn += __popc(m);
                 if (qn >= 32) {
@@ -1288,6 +1297,7 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
                         }
                     }
                     const int cd = __float_as_int(cand[sq].w);
+                    ESP_DCHECK((cd & 0x7ffffff) < a.nacc && (static_cast<unsigned>(cd) >> 27) < 27);
                     pf = a.xyzq[cd & 0x7ffffff];
                     tf = static_cast<unsigned>(cd) >> 27;
                     sf = cd & 0x7ffffff;
@@ -1547,6 +1557,7 @@ __global__ void __launch_bounds__(512) k_spread(GridArgs g, const double4* __res
                 }
             }
             // offsets are in [0, W-P] by construction; clamp for non-finite input
+            ESP_DCHECK(!isfinite(x) || (f.first - lod >= 0 && f.first - lod <= W - P));
             fch[ai * 3 + d] = clampi(f.first - lod, 0, W - P);
         }
         __syncthreads();
@@ -1596,6 +1607,8 @@ __global__ void __launch_bounds__(512) k_spread(GridArgs g, const double4* __res
             const int gx = g.xslab ? lo[0] + ix - g.x_lo : wrapi(lo[0] + ix, g.nf[0]);
             const int gy = wrapi(lo[1] + iy, g.nf[1]);
             const int gz = wrapi(lo[2] + iz, g.nf[2]);
+            ESP_DCHECK(gx >= 0 && gy >= 0 && gy < g.nf[1] && gz >= 0 && gz < g.nf[2] &&
+                       (g.xslab || gx < g.nf[0]));
             atomicAdd(&grid[(static_cast<long>(gx) * g.nf[1] + gy) * g.nf[2] + gz], val);
         }
     }
@@ -1755,6 +1768,7 @@ __device__ __forceinline__ void xp_pass(const double2* __restrict__ in, double2*
         }
         dft_small<R, S>(v);
         const int d = q * Ns * R + k;
+        ESP_DCHECK(k >= 0 && k < Ns && d + (R - 1) * Ns < nb * R && j + (R - 1) * nb < nb * R);
 #pragma unroll
         for (int r = 0; r < R; ++r) out[(d + r * Ns) * CW2 + c] = v[r];
     }
@@ -1946,6 +1960,7 @@ __global__ void __launch_bounds__(128) k_interp(GridArgs g, InterpArgs a) {
 #pragma unroll
                 for (int jy = 0; jy < MP; ++jy) {
                     if (jy < P) {
+                        ESP_DCHECK(g.xslab ? ixj >= 0 : (ixj >= 0 && ixj < g.nf[0]));
                         const double* fld = a.fields + 4 * ((ixj * ny + idx[1][jy]) * nz);
                         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll

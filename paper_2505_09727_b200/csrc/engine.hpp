@@ -14,9 +14,31 @@
 #include <cuda_runtime.h>
 #include <cufft.h>
 
+#include <cstdio>
 #include <array>
 #include <vector>
 #include <string>
+
+// Device-side bounds checks of the checked build (build.py --checked,
+// -DESP_DEVICE_CHECKS; loaded with ESP_B200_CHECKED=1): a failed check prints
+// the condition and traps, failing the evaluation with a CUDA error.  The
+// product build compiles them out.  (compute-sanitizer is not available on
+// the GPU pool; these checks and the reference-parity tests stand in for it.)
+#ifdef ESP_DEVICE_CHECKS
+#define ESP_DCHECK(c)                                                                  \
+    do {                                                                               \
+        if (!(c)) {                                                                    \
+            printf("ESP_DCHECK failed: %s at %s:%d (block %d thread %d)\n", #c,        \
+                   __FILE__, __LINE__, static_cast<int>(blockIdx.x),                   \
+                   static_cast<int>(threadIdx.x));                                     \
+            __trap();                                                                  \
+        }                                                                              \
+    } while (0)
+#else
+#define ESP_DCHECK(c) \
+    do {              \
+    } while (0)
+#endif
 
 namespace espb {
 
