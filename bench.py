@@ -60,21 +60,23 @@ def parse():
                     help="--impl reference: timed-step budget (at least one step, at most "
                          "--steps)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--decomp", choices=["auto", "replicas", "slab", "pencil", "pencil-local"],
+    ap.add_argument("--decomp", choices=["auto", "replicas", "slab", "pencil", "pencil-local",
+                                         "shard"],
                     default="auto",
                     help="N>1: replicas = one independent system per rank (weak scaling); "
                          "slab = ONE system, x-slabs, NCCL all-reduce of the charge grid and "
                          "outputs; pencil = ONE system with the grid/spectrum/fields split too "
                          "(halo exchanges + all-to-all transposes); pencil-local = the same "
                          "with every rank holding only its own atoms (ghost exchange, energy "
-                         "all-reduce); auto = pencil-local for cfg3/4/5, replicas for "
-                         "cfg1/2")
+                         "all-reduce); shard = the same decomposition behind the C ABI "
+                         "(esp_shard_evaluate: NCCL inside the library, no host "
+                         "synchronisation); auto = shard for cfg3/4/5, replicas for cfg1/2")
     ap.add_argument("--strong", action="store_true", help="alias of --decomp slab")
     args = ap.parse_args()
     if args.strong:
         args.decomp = "slab"
     if args.decomp == "auto":
-        args.decomp = "pencil-local" if args.workload in ("cfg3", "cfg4", "cfg5") else "replicas"
+        args.decomp = "shard" if args.workload in ("cfg3", "cfg4", "cfg5") else "replicas"
     args.warmup = max(args.warmup, 3)
     return args
 
@@ -108,6 +110,9 @@ def parallelism(decomp: str, world: int) -> str:
             "pencil": f"distributed FFT x{world} (NCCL halo send/recv + all-to-all transposes)",
             "pencil-local": f"distributed FFT x{world}, local atoms + ghosts (NCCL ghost/halo "
                             "send/recv, all-to-all transposes, energy all-reduce)",
+            "shard": f"sharded x{world} behind the C ABI (esp_shard_evaluate: x-slabs by grid "
+                     "plane, local atoms + ghosts, NCCL send/recv halos and all-to-all "
+                     "transposes inside the library, energy all-reduce)",
             }.get(decomp, f"replicas x{world}")
 
 
@@ -346,6 +351,25 @@ def run_ours(args):
         def step():
             res["u"], res["F"], res["e"] = evaluate_pencil_local(
                 plan, box, pos_d, q_d, layout, rank, c.r_c, stream.cuda_stream, cache=res)
+    elif decomp == "shard":
+        # each rank passes only its own atoms; the exchanges run inside the
+        # library on a NCCL communicator made from a broadcast unique id
+        own_idx = np.nonzero(E.shard_owner(plan, world, pos) == rank)[0]
+        counts = [None] * world
+        dist.all_gather_object(counts, int(own_idx.size))
+        uid = [E.shard_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        shard = E.Shard(plan, rank, world, max(counts), nccl_id=uid[0])
+        pos_d = torch.from_numpy(np.ascontiguousarray(pos[own_idx])).to(dev)
+        q_d = torch.from_numpy(q[own_idx]).to(dev)
+        res = {"u": torch.empty(own_idx.size, dtype=torch.float64, device=dev),
+               "F": torch.empty((own_idx.size, 3), dtype=torch.float64, device=dev),
+               "e": torch.empty(1, dtype=torch.float64, device=dev)}
+
+        def step():
+            shard.evaluate(box, own_idx.size, pos_d.data_ptr(), q_d.data_ptr(),
+                           res["u"].data_ptr(), res["F"].data_ptr(), res["e"].data_ptr(),
+                           stream.cuda_stream)
     else:
         def step():
             E.evaluate_device(plan, box, N, pos_d.data_ptr(), q_d.data_ptr(), u_d.data_ptr(),
@@ -373,7 +397,9 @@ def run_ours(args):
     if dist:
         dist.barrier()
     ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev0, ev1))
-    energy = (float(res["e"].item()) if decomp == "pencil-local" else
+    if decomp == "shard":
+        shard.check()
+    energy = (float(res["e"].item()) if decomp in ("pencil-local", "shard") else
               float(out_d[4 * N].item()) if strong else float(e_d.item()))
 
     # keep the GPU busy (untimed) until the clock sampler has a few samples
@@ -385,12 +411,16 @@ def run_ours(args):
     clk = clocks.stop()
 
     # ---- per-stage breakdown and the dominant kernel's roofline
+    # (whole system on this GPU; a separate plan for the sharded modes, whose
+    # shard keeps using its own plan's engine buffers afterwards)
+    tplan = plan if not strong else E.build_plan(
+        box, "pswf", c.eps, c.r_c, E.Overrides(force_method=args.force_method), device=local)
     tim = []
     for _ in range(5):
-        ef = E.evaluate(plan, E.ParticleSystem(box, q, pos), timings=True)
+        ef = E.evaluate(tplan, E.ParticleSystem(box, q, pos), timings=True)
         tim.append(ef.timings)
     stages_ms = {k: statistics.median(t[k] for t in tim) * 1e3 for k in tim[0] if k != "total"}
-    ordered_pairs = plan.last_pair_count()
+    ordered_pairs = tplan.last_pair_count()
     pair_flops = FLOPS_PER_UNORDERED_PAIR * ordered_pairs / 2.0
     t_pair = stages_ms["local"] * 1e-3
     peak64 = E.fp64_peak_tflops(local)
@@ -475,7 +505,7 @@ def run_ours(args):
     u_h = torch.empty(N, dtype=torch.float64).pin_memory().numpy()
     F_h = torch.empty((N, 3), dtype=torch.float64).pin_memory().numpy()
     sysh = E.ParticleSystem(box, q_h, pos_h)
-    if decomp == "pencil-local":
+    if decomp in ("pencil-local", "shard"):
         pos_ht = torch.from_numpy(np.ascontiguousarray(pos[own_idx])).pin_memory()
         q_ht = torch.from_numpy(q[own_idx]).pin_memory()
         uo_h = torch.empty(own_idx.size, dtype=torch.float64).pin_memory()
@@ -544,8 +574,8 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": {"value": (N / (e2e_ms * 1e-3)) if strong else weak_scaling_value(N, world, e2e_ms),
                     "unit": UNIT,
-                    "h2d_bytes_per_step": int((own_idx.size if decomp == "pencil-local" else N) * 32),
-                    "d2h_bytes_per_step": int((own_idx.size if decomp == "pencil-local" else N) * 32 + 8),
+                    "h2d_bytes_per_step": int((own_idx.size if decomp in ("pencil-local", "shard") else N) * 32),
+                    "d2h_bytes_per_step": int((own_idx.size if decomp in ("pencil-local", "shard") else N) * 32 + 8),
                     "ms_per_step": e2e_ms},
         }
         print(json.dumps(line))
