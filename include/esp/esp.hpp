@@ -529,6 +529,102 @@ inline ReferenceResult direct_ewald(const ParticleSystem& system, double tol) {
     return r;
 }
 
+// ---- evaluate() sharded over the GPUs of one box (esp_shard_*) ------------
+// One process per GPU; every rank builds its own plan (same arguments, its own
+// device via set_device) and a Shard on it.  Rank 0's unique_id() is shared
+// with the other ranks by the caller (MPI, a file, ...).  Each rank passes only
+// the atoms it owns (owner(), the x-slab decomposition by grid plane) and gets
+// back their u and F and the TOTAL energy; the ghost, halo, transpose and
+// reduction traffic is NCCL inside the library.  Same results as
+// evaluate(plan, whole system) up to summation order.
+class Shard {
+public:
+    using Id = std::array<unsigned char, 128>;
+    static Id unique_id() {
+        Id id{};
+        detail::check(esp_shard_unique_id(id.data()));
+        return id;
+    }
+    // owner rank of every atom (any image)
+    static std::vector<int> owner(const EwaldPlan& plan, int nranks, const std::vector<Vec3>& pos) {
+        std::vector<int> o(pos.size());
+        detail::check(esp_shard_owner(plan.handle(), nranks, static_cast<long>(pos.size()),
+                                      detail::flat(pos), o.data()));
+        return o;
+    }
+    // collective over nranks processes (id != nullptr), or an emulation
+    // member (id == nullptr) for evaluate_emulated below
+    Shard(const EwaldPlan& plan, const Id* id, int rank, int nranks, long max_own_atoms,
+          long ghost_capacity = 0)
+        : plan_(plan) {
+        detail::check(esp_shard_create(plan.handle(), id ? id->data() : nullptr, rank, nranks,
+                                       max_own_atoms, ghost_capacity, &h_));
+    }
+    ~Shard() { esp_shard_destroy(h_); }
+    Shard(const Shard&) = delete;
+    Shard& operator=(const Shard&) = delete;
+
+    // this rank's atoms (host; collective: every rank calls it for the step)
+    EnergyForces evaluate(const ParticleSystem& own) {
+        EnergyForces out;
+        const long n = static_cast<long>(own.size());
+        if (own.pos.size() != own.q.size())
+            throw std::invalid_argument("evaluate: pos/q length mismatch");
+        out.u.resize(n);
+        out.F.resize(n);
+        std::lock_guard<std::mutex> lk(plan_.mutex());
+        detail::check(esp_shard_evaluate_host(h_, own.box.data(), n, detail::flat(own.pos),
+                                              own.q.data(), out.u.data(), detail::flat(out.F),
+                                              &out.energy));
+        return out;
+    }
+    // device pointers, asynchronous on `stream` (graph-capturable)
+    void evaluate_device(const Vec3& box, long n_own, const double* pos, const double* q,
+                         double* u, double* F, double* energy, void* stream) {
+        detail::check(esp_shard_evaluate(h_, box.data(), n_own, pos, q, u, F, energy, stream));
+    }
+    void check() { detail::check(esp_shard_check(h_)); }
+    esp_shard_info_t info() const {
+        esp_shard_info_t i{};
+        detail::check(esp_shard_info(h_, &i));
+        return i;
+    }
+    esp_shard* handle() const { return h_; }
+
+    // all ranks of one decomposition in this process on one GPU (emulation
+    // members, messages moved by device copies): tests and single-GPU runs
+    static std::vector<EnergyForces> evaluate_emulated(std::vector<Shard*> shards,
+                                                       const std::vector<ParticleSystem>& own) {
+        const int G = static_cast<int>(shards.size());
+        if (static_cast<int>(own.size()) != G) throw std::invalid_argument("one system per shard");
+        std::vector<esp_shard*> hs(G);
+        std::vector<long> n(G);
+        std::vector<const double*> P(G), Q(G);
+        std::vector<double*> U(G), F(G);
+        std::vector<EnergyForces> out(G);
+        for (int r = 0; r < G; ++r) {
+            hs[r] = shards[r]->h_;
+            n[r] = static_cast<long>(own[r].size());
+            out[r].u.resize(n[r]);
+            out[r].F.resize(n[r]);
+            P[r] = detail::flat(own[r].pos);
+            Q[r] = own[r].q.data();
+            U[r] = out[r].u.data();
+            F[r] = detail::flat(out[r].F);
+        }
+        double e = 0.0;
+        detail::check(esp_shard_evaluate_emulated_host(hs.data(), G, own[0].box.data(), n.data(),
+                                                       P.data(), Q.data(), U.data(), F.data(),
+                                                       &e));
+        for (auto& o : out) o.energy = e;
+        return out;
+    }
+
+private:
+    const EwaldPlan& plan_;
+    esp_shard* h_ = nullptr;
+};
+
 // reference.hpp:241-255
 inline double relative_force_error(const std::vector<Vec3>& test, const std::vector<Vec3>& ref) {
     if (test.size() != ref.size())

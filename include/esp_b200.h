@@ -351,6 +351,17 @@ int esp_shard_evaluate_emulated(esp_shard* const* shards, int nranks, const doub
                                 double* const* F_dev, double* const* energy_dev, void* stream);
 /* Synchronises and reports the device-side error flags of the last call. */
 int esp_shard_check(esp_shard* shard);
+/* Host-buffer forms of the two above (synchronous): the own atoms are copied
+ * into device buffers held by the shard (n_own <= max_own_atoms), the
+ * evaluation runs, u / F / the total energy are copied back, and the device
+ * flags are reported as by esp_shard_check.  The emulated form takes per-rank
+ * host arrays and one energy. */
+int esp_shard_evaluate_host(esp_shard* shard, const double box[3], long n_own, const double* pos,
+                            const double* q, double* u, double* F, double* energy);
+int esp_shard_evaluate_emulated_host(esp_shard* const* shards, int nranks, const double box[3],
+                                     const long* n_own, const double* const* pos,
+                                     const double* const* q, double* const* u,
+                                     double* const* F, double* energy);
 
 #ifdef __cplusplus
 }

@@ -300,6 +300,17 @@ struct esp_shard {
     double *A = nullptr, *B = nullptr, *A2 = nullptr, *B2 = nullptr, *fslab = nullptr;
     double *ul = nullptr, *Fl = nullptr, *e_part = nullptr;
     double *bRu = nullptr, *bRF = nullptr, *bLu = nullptr, *bLF = nullptr;
+    // host-buffer entry points: device copies of the own atoms and outputs
+    // (allocated on first use, n_own_cap atoms)
+    double *hpos = nullptr, *hq = nullptr, *hu = nullptr, *hF = nullptr, *he = nullptr;
+    void host_buffers() {
+        if (hpos) return;
+        hpos = dmalloc(3 * n_own_cap);
+        hq = dmalloc(n_own_cap);
+        hu = dmalloc(n_own_cap);
+        hF = dmalloc(3 * n_own_cap);
+        he = dmalloc(1);
+    }
     // current call
     long n_own = 0;
     const double *pos = nullptr, *q = nullptr;
@@ -308,7 +319,7 @@ struct esp_shard {
     ~esp_shard() {
         if (plan && plan->device >= 0) cudaSetDevice(plan->device);
         for (double* p : {pos_l, q_l, sendL, sendR, gR, gL, slab, hR, hL, send, recv, A, B, A2, B2,
-                          fslab, ul, Fl, e_part, bRu, bRF, bLu, bLF})
+                          fslab, ul, Fl, e_part, bRu, bRF, bLu, bLF, hpos, hq, hu, hF, he})
             cudaFree(p);
         for (int* p : {idxL, idxR, cnt, flags}) cudaFree(p);
         if (h_flags) cudaFreeHost(h_flags);
@@ -763,6 +774,74 @@ int esp_shard_evaluate_emulated(esp_shard* const* shards, int nranks, const doub
                     "energy copy");
         cuda_ok(cudaGetLastError(), "emulated all-reduce");
     });
+}
+
+// Host-buffer forms: copy the own atoms in, evaluate, copy u / F / energy out
+// (synchronous), then report the device flags like esp_shard_check.
+int esp_shard_evaluate_host(esp_shard* sh, const double box[3], long n_own, const double* pos,
+                            const double* q, double* u, double* F, double* energy) {
+    int rc = guarded([&] {
+        if (!sh) throw espb::InvalidArgument("null shard");
+        if (n_own < 0 || n_own > sh->n_own_cap)
+            throw espb::InvalidArgument("n_own exceeds the shard's max_own_atoms");
+        if (n_own > 0 && (!pos || !q || !u || !F)) throw espb::InvalidArgument("null argument");
+        if (!energy) throw espb::InvalidArgument("null energy");
+        cuda_ok(cudaSetDevice(sh->plan->device), "cudaSetDevice");
+        sh->host_buffers();
+        cuda_ok(cudaMemcpy(sh->hpos, pos, sizeof(double) * 3 * n_own, cudaMemcpyHostToDevice), "H2D");
+        cuda_ok(cudaMemcpy(sh->hq, q, sizeof(double) * n_own, cudaMemcpyHostToDevice), "H2D");
+    });
+    if (rc) return rc;
+    rc = esp_shard_evaluate(sh, box, n_own, sh->hpos, sh->hq, sh->hu, sh->hF, sh->he, nullptr);
+    if (rc) return rc;
+    rc = guarded([&] {
+        cuda_ok(cudaMemcpy(u, sh->hu, sizeof(double) * n_own, cudaMemcpyDeviceToHost), "D2H");
+        cuda_ok(cudaMemcpy(F, sh->hF, sizeof(double) * 3 * n_own, cudaMemcpyDeviceToHost), "D2H");
+        cuda_ok(cudaMemcpy(energy, sh->he, sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    });
+    return rc ? rc : esp_shard_check(sh);
+}
+
+int esp_shard_evaluate_emulated_host(esp_shard* const* shards, int nranks, const double box[3],
+                                     const long* n_own, const double* const* pos,
+                                     const double* const* q, double* const* u, double* const* F,
+                                     double* energy) {
+    std::vector<const double*> P(nranks > 0 ? nranks : 0), Q(P.size());
+    std::vector<double*> U(P.size()), Fd(P.size()), Ed(P.size());
+    int rc = guarded([&] {
+        if (!shards || nranks < 2 || !n_own || !energy) throw espb::InvalidArgument("null argument");
+        for (int r = 0; r < nranks; ++r) {
+            esp_shard* sh = shards[r];
+            if (!sh) throw espb::InvalidArgument("null shard");
+            if (n_own[r] < 0 || n_own[r] > sh->n_own_cap)
+                throw espb::InvalidArgument("n_own exceeds the shard's max_own_atoms");
+            cuda_ok(cudaSetDevice(sh->plan->device), "cudaSetDevice");
+            sh->host_buffers();
+            cuda_ok(cudaMemcpy(sh->hpos, pos[r], sizeof(double) * 3 * n_own[r],
+                               cudaMemcpyHostToDevice), "H2D");
+            cuda_ok(cudaMemcpy(sh->hq, q[r], sizeof(double) * n_own[r], cudaMemcpyHostToDevice),
+                    "H2D");
+            P[r] = sh->hpos;
+            Q[r] = sh->hq;
+            U[r] = sh->hu;
+            Fd[r] = sh->hF;
+            Ed[r] = sh->he;
+        }
+    });
+    if (rc) return rc;
+    rc = esp_shard_evaluate_emulated(shards, nranks, box, n_own, P.data(), Q.data(), U.data(),
+                                     Fd.data(), Ed.data(), nullptr);
+    if (rc) return rc;
+    rc = guarded([&] {
+        for (int r = 0; r < nranks; ++r) {
+            cuda_ok(cudaMemcpy(u[r], U[r], sizeof(double) * n_own[r], cudaMemcpyDeviceToHost), "D2H");
+            cuda_ok(cudaMemcpy(F[r], Fd[r], sizeof(double) * 3 * n_own[r], cudaMemcpyDeviceToHost),
+                    "D2H");
+        }
+        cuda_ok(cudaMemcpy(energy, Ed[0], sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    });
+    for (int r = 0; r < nranks && !rc; ++r) rc = esp_shard_check(shards[r]);
+    return rc;
 }
 
 int esp_shard_check(esp_shard* sh) {

@@ -9,7 +9,9 @@
 #include <complex>
 #include <cstdint>
 #include <cstdio>
+#include <memory>
 #include <stdexcept>
+#include <vector>
 
 static int failures = 0;
 #define CHECK(cond)                                                                  \
@@ -271,6 +273,60 @@ int main() {
         CHECK(esp::relative_force_error(ef.F, d.F) <= 1e-4);
         CHECK(std::fabs(ef.energy - d.energy) <= 1e-4 * std::fabs(d.energy));
         CHECK(d.real_shells >= 1 && d.recip_kmax >= 1 && d.lambda > 0.0);
+    }
+    // evaluate() sharded over 2 and 3 ranks (esp::Shard, emulation members on
+    // this GPU): each rank holds only its own atoms; equal to the
+    // single-process evaluation up to summation order
+    {
+        const esp::Vec3 bx{24.0, 20.0, 22.0};
+        esp::ParticleSystem s = random_system(4000, bx, 5);
+        esp::EwaldPlan whole = esp::build_plan(bx, esp::SplitFamily::pswf, 1e-4, 2.0);
+        esp::EnergyForces ref = esp::evaluate(whole, s, false);
+        for (int G : {2, 3}) {
+            std::vector<esp::EwaldPlan> plans;
+            for (int r = 0; r < G; ++r) plans.push_back(esp::build_plan(bx, esp::SplitFamily::pswf, 1e-4, 2.0));
+            const std::vector<int> own = esp::Shard::owner(plans[0], G, s.pos);
+            std::vector<esp::ParticleSystem> parts(G);
+            std::vector<std::vector<std::size_t>> idx(G);
+            for (int r = 0; r < G; ++r) parts[r].box = bx;
+            for (std::size_t i = 0; i < s.size(); ++i) {
+                parts[own[i]].pos.push_back(s.pos[i]);
+                parts[own[i]].q.push_back(s.q[i]);
+                idx[own[i]].push_back(i);
+            }
+            long nmax = 0;
+            for (auto& p : parts) nmax = std::max(nmax, static_cast<long>(p.size()));
+            std::vector<std::unique_ptr<esp::Shard>> sh;
+            std::vector<esp::Shard*> raw;
+            for (int r = 0; r < G; ++r) {
+                sh.emplace_back(new esp::Shard(plans[r], nullptr, r, G, nmax));
+                raw.push_back(sh.back().get());
+            }
+            const std::vector<esp::EnergyForces> out = esp::Shard::evaluate_emulated(raw, parts);
+            std::vector<esp::Vec3> F(s.size());
+            double du = 0.0, umax = 0.0;
+            for (int r = 0; r < G; ++r)
+                for (std::size_t k = 0; k < idx[r].size(); ++k) {
+                    F[idx[r][k]] = out[r].F[k];
+                    du = std::max(du, std::fabs(out[r].u[k] - ref.u[idx[r][k]]));
+                    umax = std::max(umax, std::fabs(ref.u[idx[r][k]]));
+                }
+            CHECK(std::fabs(out[0].energy - ref.energy) <= 1e-12 * std::fabs(ref.energy));
+            CHECK(esp::relative_force_error(F, ref.F) <= 1e-12);
+            CHECK(du <= 1e-12 * umax);
+            CHECK(raw[0]->info().nranks == G && raw[0]->info().nccl == 0);
+        }
+        // an atom passed to the wrong rank is reported (esp_shard_check flags)
+        esp::EwaldPlan p0 = esp::build_plan(bx, esp::SplitFamily::pswf, 1e-4, 2.0);
+        esp::EwaldPlan p1 = esp::build_plan(bx, esp::SplitFamily::pswf, 1e-4, 2.0);
+        esp::Shard a(p0, nullptr, 0, 2, 10), b(p1, nullptr, 1, 2, 10);
+        esp::ParticleSystem s0, s1;
+        s0.box = s1.box = bx;
+        s0.pos = {{22.0, 1.0, 1.0}, {1.0, 2.0, 3.0}};   // the first atom is rank 1's
+        s0.q = {1.0, -1.0};
+        s1.pos = {{13.0, 5.0, 5.0}};
+        s1.q = {0.0};
+        CHECK(throws<std::invalid_argument>([&] { esp::Shard::evaluate_emulated({&a, &b}, {s0, s1}); }));
     }
     std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "PASSED", failures);
     return failures ? 1 : 0;
