@@ -324,6 +324,14 @@ inline void fold(ParticleSystem& s) {
         }
 }
 
+// Deterministic mode of a plan (esp_plan_set_deterministic): bitwise
+// reproducible evaluations, like the reference for any thread count
+// (README.md:87-94); slower.
+inline void set_deterministic(const EwaldPlan& plan, bool on) {
+    std::lock_guard<std::mutex> lk(plan.mutex());
+    detail::check(esp_plan_set_deterministic(plan.handle(), on ? 1 : 0));
+}
+
 // system.hpp:39-47
 inline void require_neutral(const ParticleSystem& s) {
     detail::check(esp_check_neutral(static_cast<long>(s.size()), s.q.data()));

@@ -82,6 +82,7 @@ typedef struct {
                              * inside the FFT's x pass (2-D cuFFT planes +
                              * k_xpass; even 5-smooth n_x >= 128, ESP_XPASS);
                              * 0: 3-D cuFFT + separate multiply pass */
+    int deterministic;      /* esp_plan_set_deterministic */
 } esp_plan_info;
 
 /* Per-stage wall time in seconds (EnergyForces::timings keys,
@@ -103,6 +104,16 @@ int esp_plan_create(const double box[3], int family, double eps, double r_c,
                     const esp_overrides* ov, int device, esp_plan** out);
 void esp_plan_destroy(esp_plan* plan);
 int esp_plan_get_info(const esp_plan* plan, esp_plan_info* out);
+/* Deterministic mode (default off): results bitwise identical run to run for
+ * the same inputs on the same device, like the reference's results for any
+ * thread count (README.md:87-94, test_cli.cpp:174-188).  Costs speed: stable
+ * radix sorts instead of atomic counting-sort ranks, the full-list real-space
+ * kernel (each atom's sum in a fixed order, no partner atomics), spreading
+ * tiles flushed bin colour by colour with plain adds.  Single-GPU evaluation
+ * entry points (esp_evaluate*, esp_local_sum, esp_spectral_sum, esp_spread);
+ * the decompositions (phases, pencil, shard) keep their atomics.  Needs
+ * n_f >= S + P + 2 (spread bin edge S, window P) in every dimension. */
+int esp_plan_set_deterministic(esp_plan* plan, int on);
 
 /* Plan tables (for parity checks).  influence: full nx*ny*nz reference
  * layout (gridder.hpp:162-210).  which: 0 Psi, 1 chi (16 x 13 Chebyshev-T

@@ -76,7 +76,7 @@ class _Info(C.Structure):
         ("self_coef", C.c_double),
         ("n_split_coef", C.c_int), ("n_window_coef", C.c_int), ("pair_poly_degree", C.c_int),
         ("pair_fit_err", C.c_double), ("device", C.c_int), ("pair_cells", C.c_int * 3),
-        ("pencil_half", C.c_int), ("fused_xpass", C.c_int),
+        ("pencil_half", C.c_int), ("fused_xpass", C.c_int), ("deterministic", C.c_int),
     ]
 
 
@@ -94,7 +94,7 @@ class _ShardInfo(C.Structure):
     _fields_ = [("rank", C.c_int), ("nranks", C.c_int), ("x0", C.c_int), ("x1", C.c_int),
                 ("X0", C.c_double), ("X1", C.c_double), ("max_own_atoms", C.c_long),
                 ("ghost_capacity", C.c_long), ("local_atoms", C.c_long),
-                ("pencil_half", C.c_int), ("fused_xpass", C.c_int), ("nccl", C.c_int)]
+                ("pencil_half", C.c_int), ("fused_xpass", C.c_int), ("deterministic", C.c_int), ("nccl", C.c_int)]
 
 
 class _DirectInfo(C.Structure):
@@ -122,6 +122,7 @@ _sig("esp_plan_create", [_dp, C.c_int, C.c_double, C.c_double, C.POINTER(_Overri
                          C.POINTER(_vp)])
 _sig("esp_plan_destroy", [_vp], None)
 _sig("esp_plan_get_info", [_vp, C.POINTER(_Info)])
+_sig("esp_plan_set_deterministic", [_vp, C.c_int])
 _sig("esp_plan_get_influence", [_vp, _dp])
 _sig("esp_plan_get_table", [_vp, C.c_int, C.c_int, _vp, C.POINTER(C.c_int)])
 _sig("esp_plan_get_prolate", [_vp, C.c_int, _vp, C.POINTER(C.c_int)])
@@ -287,6 +288,16 @@ class EwaldPlan:
         y = np.empty_like(x)
         _check(_lib.esp_plan_eval_kernel(self._h, sel, x.size, x, y))
         return y
+
+    def set_deterministic(self, on: bool = True) -> None:
+        """esp_plan_set_deterministic: bitwise-reproducible evaluations (slower)."""
+        _check(_lib.esp_plan_set_deterministic(self._h, 1 if on else 0))
+
+    @property
+    def deterministic(self) -> bool:
+        info = _Info()
+        _check(_lib.esp_plan_get_info(self._h, C.byref(info)))
+        return bool(info.deterministic)
 
     def last_launch_count(self) -> int:
         return int(_lib.esp_last_launch_count(self._h))

@@ -186,9 +186,14 @@ int esp_plan_get_info(const esp_plan* p, esp_plan_info* o) {
         o->pair_poly_degree = static_cast<int>(P.pair_H.size()) - 1;
         o->pencil_half = p->eng ? (p->eng->pencil_half() ? 1 : 0) : espb::Engine::pencil_half_env();
         o->fused_xpass = p->eng && p->eng->fused_xpass() ? 1 : 0;
+        o->deterministic = p->eng && p->eng->deterministic() ? 1 : 0;
         o->pair_fit_err = P.pair_fit_err;
         o->device = p->device;
     });
+}
+
+int esp_plan_set_deterministic(esp_plan* p, int on) {
+    return guarded([&] { engine(p).set_deterministic(on != 0); });
 }
 
 int esp_plan_get_influence(const esp_plan* p, double* out) {

@@ -16,6 +16,7 @@
 
 #include "engine.hpp"
 
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
@@ -40,6 +41,12 @@ struct GridArgs {
     int kpb;            // sort keys per spread bin (start[] has kpb entries per bin)
     int xslab;          // 1: x indexes a rank's plane slab starting at plane x_lo
     int x_lo;           //    (unwrapped; the slab's halos hold the periodic images)
+    // deterministic mode: the launch covers one colour of bins (no two of
+    // its tiles share a grid node): bin_d = coff[d] + cstr[d] * (index along
+    // d over ccnt[d]); the tile is flushed with plain adds, colours in a fixed
+    // order.  det = 0: bins bin0 + blockIdx.x, flushed with fp64 REDs.
+    int det;
+    int coff[3], cstr[3], ccnt[3];
     int own_x0, own_x1; // xslab: only atoms with clamp(floor(x/h), 0, nx-1) in
                         //    [own_x0, own_x1) are spread / interpolated
     const double* win;  // 3 x 4P x 13 (phi) then 3 x 4P x 13 (dphi)
@@ -347,6 +354,24 @@ __global__ void __launch_bounds__(256) k_scatter(long N, const double4* __restri
     ESP_DCHECK(db >= 0 && db < N);
     xyzqB[db] = v;
     origB[db] = static_cast<int>(i);
+}
+
+// deterministic mode: sorted position k takes atom perm[k] (a stable radix
+// sort by key: inside a cell, atoms stay in their input order)
+__global__ void __launch_bounds__(256) k_gather_perm(long N, const double4* __restrict__ tmp,
+                                                     const int* __restrict__ perm,
+                                                     double4* __restrict__ xyzq,
+                                                     int* __restrict__ orig) {
+    const long k = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+    if (k >= N) return;
+    const int i = perm[k];
+    xyzq[k] = tmp[i];
+    orig[k] = i;
+}
+
+__global__ void k_iota(long N, int* __restrict__ v) {
+    const long k = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+    if (k < N) v[k] = static_cast<int>(k);
 }
 
 // ----------------------------------------------------------------------------
@@ -1494,8 +1519,20 @@ __global__ void __launch_bounds__(512) k_spread(GridArgs g, const double4* __res
     double* tile = reinterpret_cast<double*>(smem) + kSpreadChunk * 3 * MP + kSpreadChunk * 2;
     const int W = g.W, RS = g.RS, PS = g.PS;
     const int nt = blockDim.x;
-    const int bin = blockIdx.x + g.bin0;
-    const int bz = bin % g.nb[2], by = (bin / g.nb[2]) % g.nb[1], bx = bin / (g.nb[1] * g.nb[2]);
+    int bin, bx, by, bz;
+    if (g.det) {
+        const int k = blockIdx.x % g.ccnt[2], j = (blockIdx.x / g.ccnt[2]) % g.ccnt[1],
+                  i = blockIdx.x / (g.ccnt[1] * g.ccnt[2]);
+        bx = g.coff[0] + g.cstr[0] * i;
+        by = g.coff[1] + g.cstr[1] * j;
+        bz = g.coff[2] + g.cstr[2] * k;
+        bin = (bx * g.nb[1] + by) * g.nb[2] + bz;
+    } else {
+        bin = blockIdx.x + g.bin0;
+        bz = bin % g.nb[2];
+        by = (bin / g.nb[2]) % g.nb[1];
+        bx = bin / (g.nb[1] * g.nb[2]);
+    }
     const int ib = start[bin * g.kpb], ie = start[(bin + 1) * g.kpb];
     if (ib == ie) return;
     const int lo[3] = {bx * g.S - P / 2, by * g.S - P / 2, bz * g.S - P / 2};
@@ -1609,7 +1646,11 @@ __global__ void __launch_bounds__(512) k_spread(GridArgs g, const double4* __res
             const int gz = wrapi(lo[2] + iz, g.nf[2]);
             ESP_DCHECK(gx >= 0 && gy >= 0 && gy < g.nf[1] && gz >= 0 && gz < g.nf[2] &&
                        (g.xslab || gx < g.nf[0]));
-            atomicAdd(&grid[(static_cast<long>(gx) * g.nf[1] + gy) * g.nf[2] + gz], val);
+            double* dst = &grid[(static_cast<long>(gx) * g.nf[1] + gy) * g.nf[2] + gz];
+            if (g.det)
+                *dst += val;  // this colour's tiles are disjoint
+            else
+                atomicAdd(dst, val);
         }
     }
 }
@@ -2694,6 +2735,10 @@ Engine::~Engine() {
     dfree(d_origB_);
     dfree(d_loc_);
     dfree(d_specres_);
+    dfree(d_det_keys_);
+    dfree(d_det_iota_);
+    dfree(d_det_perm_);
+    if (d_det_tmp_) cudaFree(d_det_tmp_);
     dfree(d_epart_);
     dfree(d_countA_);
     dfree(d_startA_);
@@ -2822,6 +2867,7 @@ void Engine::ensure_capacity(long N) {
     CK(cudaMemset(d_acc_, 0, sizeof(double) * 4 * c));
     dalloc(d_epart_, grid1(c, 128) + 1);
     cap_ = c;
+    if (deterministic_) alloc_det(c);
 }
 
 void Engine::prepare(long N, const double* pos, const double* q, double* qsum_dev,
@@ -2895,7 +2941,31 @@ void Engine::prepare(long N, const double* pos, const double* q, double* qsum_de
         launches_ += 2;
     }
     mark();
-    if (N > 0) {
+    if (N > 0 && deterministic_) {
+        // stable sorts instead of the atomic ranks: the order inside a cell /
+        // sort key is the input order on every run
+        auto bits = [](long n) {
+            int b = 1;
+            while ((1L << b) < n) ++b;
+            return b;
+        };
+        if (det_cap_ < N) throw CudaError("deterministic mode: sort scratch not sized");
+        k_iota<<<grid1(N, 256), 256, 0, s>>>(N, d_det_iota_);
+        CK(cudaGetLastError());
+        size_t tb = det_tmp_bytes_;
+        CK(cub::DeviceRadixSort::SortPairs(d_det_tmp_, tb, d_cellA_, d_det_keys_, d_det_iota_,
+                                           d_det_perm_, static_cast<int>(N), 0,
+                                           bits(ncellF_ + 1), s));
+        k_gather_perm<<<grid1(N, 256), 256, 0, s>>>(N, d_tmp_, d_det_perm_, d_xyzqA_, d_origA_);
+        CK(cudaGetLastError());
+        tb = det_tmp_bytes_;
+        CK(cub::DeviceRadixSort::SortPairs(d_det_tmp_, tb, d_cellB_, d_det_keys_, d_det_iota_,
+                                           d_det_perm_, static_cast<int>(N), 0,
+                                           bits(nkeyB + 1), s));
+        k_gather_perm<<<grid1(N, 256), 256, 0, s>>>(N, d_tmp_, d_det_perm_, d_xyzqB_, d_origB_);
+        CK(cudaGetLastError());
+        launches_ += 5;
+    } else if (N > 0) {
         k_scatter<<<grid1(N, 256), 256, 0, s>>>(N, d_tmp_, d_cellA_, d_rankA_, d_startA_, d_xyzqA_,
                                                  d_origA_, d_cellB_, d_rankB_, d_startB_, d_xyzqB_,
                                                  d_origB_);
@@ -2949,8 +3019,11 @@ void Engine::run_pair(long N, cudaStream_t s, int rank, int nranks, bool own_bin
     // other -- so there the mode is the plan's alone (ESP_PENCIL_HALF, read
     // once at plan build; esp_plan_info.pencil_half), independent of the
     // rank's atom count and density, and the half-shell path never falls back.
+    // deterministic mode: full lists (each atom's sum in a fixed order, no
+    // partner REDs)
     const bool half = own_bins ? pencil_half_
-                               : half_mode_ == 2 || (half_mode_ == 1 && N >= kHalfMinN);
+                               : !deterministic_ &&
+                                     (half_mode_ == 2 || (half_mode_ == 1 && N >= kHalfMinN));
     if (half && run_pair_half(N, s, rank, nranks, own_bins)) return;
     if (half && own_bins)
         throw CudaError("distributed FFT: half-shell pair kernel could not be configured");
@@ -3225,11 +3298,72 @@ void Engine::run_spread(long N, cudaStream_t s, int rank, int nranks, double* gr
     CK(cudaMemsetAsync(grid, 0, sizeof(double) * (nreals >= 0 ? nreals : M_), s));
     if (N == 0) return;
     GridArgs g = gslab ? *gslab : grid_args();
+    if (deterministic_ && !gslab && nranks == 1) {
+        // bins coloured so that no two tiles of a colour share a grid node:
+        // per dimension residue c of bin mod C over the first C*floor(nb/C)
+        // bins (stride C >= W/S, so same-colour tiles are >= W nodes apart,
+        // also across the periodic boundary), the remaining nb mod C bins
+        // one colour each; colours in a fixed order, plain adds
+        for (int d = 0; d < 3; ++d)
+            if (p.nf[d] < W_)
+                throw InvalidArgument("deterministic mode needs n_f >= S + P + 2 in every dimension");
+        const int C = (W_ + S_ - 1) / S_;
+        std::vector<std::array<int, 3>> cols[3];  // (offset, stride, count)
+        for (int d = 0; d < 3; ++d) {
+            const int m = nb_[d] / C, r = nb_[d] - m * C;
+            if (m >= 1)
+                for (int c = 0; c < C; ++c) cols[d].push_back({c, C, m});
+            for (int e = 0; e < r; ++e) cols[d].push_back({m * C + e, 1, 1});
+        }
+        g.det = 1;
+        for (const auto& cx : cols[0])
+            for (const auto& cy : cols[1])
+                for (const auto& cz : cols[2]) {
+                    const std::array<int, 3> c3[3] = {cx, cy, cz};
+                    for (int d = 0; d < 3; ++d) {
+                        g.coff[d] = c3[d][0];
+                        g.cstr[d] = c3[d][1];
+                        g.ccnt[d] = c3[d][2];
+                    }
+                    dispatch_P<SpreadLaunch>(p.P, g, g.ccnt[0] * g.ccnt[1] * g.ccnt[2], d_xyzqB_,
+                                             d_startB_, grid, s);
+                    ++launches_;
+                }
+        return;
+    }
     if (b0 < 0) slab_bins(rank, nranks, &b0, &b1);
     if (b1 <= b0) return;
     g.bin0 = b0;
     dispatch_P<SpreadLaunch>(p.P, g, b1 - b0, d_xyzqB_, d_startB_, grid, s);
     ++launches_;
+}
+
+void Engine::set_deterministic(bool on) {
+    if (on == deterministic_) return;
+    CK(cudaSetDevice(device_));
+    CK(cudaDeviceSynchronize());
+    if (gexec_) {  // the captured graph has the other mode's launches
+        cudaGraphExecDestroy(gexec_);
+        gexec_ = nullptr;
+    }
+    deterministic_ = on;
+    if (on) alloc_det(std::max<long>(cap_, 1));
+}
+
+// stable-sort scratch for n atoms (outside any stream capture)
+void Engine::alloc_det(long n) {
+    if (det_cap_ >= n) return;
+    dalloc(d_det_keys_, n);
+    dalloc(d_det_iota_, n);
+    dalloc(d_det_perm_, n);
+    size_t t = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, t, d_cellA_, d_det_keys_, d_det_iota_,
+                                       d_det_perm_, static_cast<int>(n), 0, 31));
+    if (d_det_tmp_) cudaFree(d_det_tmp_);
+    d_det_tmp_ = nullptr;
+    CK(cudaMalloc(&d_det_tmp_, std::max<size_t>(t, 16)));
+    det_tmp_bytes_ = t;
+    det_cap_ = n;
 }
 
 void Engine::slab_bins(int rank, int nranks, int* b0, int* b1) const {

@@ -166,6 +166,13 @@ public:
     // distributed-FFT K4 mode (fixed when the engine is built; see run_pair)
     bool pencil_half() const { return pencil_half_; }
     bool fused_xpass() const { return xpass_; }
+    // Deterministic mode: bitwise-identical results run to run for the same
+    // inputs (stable sorts instead of atomic ranks, full-list K4 without
+    // partner REDs, K1 tiles flushed by bin colours with plain adds); the
+    // reference's results are bit-identical for any thread count
+    // (README.md:87-94).  Single-GPU evaluation paths.
+    void set_deterministic(bool on);
+    bool deterministic() const { return deterministic_; }
     static int pencil_half_env() {
         const char* e = std::getenv("ESP_PENCIL_HALF");
         return (e && std::atoi(e) == 0) ? 0 : 1;
@@ -179,6 +186,7 @@ private:
                  double* energy_dev, double* qsum_dev, cudaStream_t s, StageTimes* t,
                  double* u_out, double* F_out);
     void ensure_capacity(long N);
+    void alloc_det(long n);
     void reconfigure(long N);
     void set_cells(int col_div);
     void alloc_cells();
@@ -244,6 +252,11 @@ private:
     int* d_origB_ = nullptr;
     double4* d_loc_ = nullptr;   // (u_l, F_l) in original order
     double4* d_specres_ = nullptr;  // (u_s - q s0, F_s) in original order (K3 -> combine)
+    bool deterministic_ = false;
+    long det_cap_ = 0;              // deterministic mode: stable-sort scratch (atoms)
+    int *d_det_keys_ = nullptr, *d_det_iota_ = nullptr, *d_det_perm_ = nullptr;
+    void* d_det_tmp_ = nullptr;
+    size_t det_tmp_bytes_ = 0;
     double* d_epart_ = nullptr;  // energy partials
     int* d_countA_ = nullptr;    // ncell + 1
     int* d_startA_ = nullptr;
