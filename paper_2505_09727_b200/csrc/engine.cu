@@ -2661,7 +2661,7 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
         // fields out (interleaved for K3 afterwards, see spectral())
         CF(cufftMakePlanMany(inv_, 2, n2, ce, 1, ny * nzh, re, 1, ny * nz, CUFFT_Z2D, p.nf[0],
                              &w2));
-        dalloc(d_fplanar_, nfields_ * M_);
+        if (nfields_ == 4) dalloc(d_fplanar_, nfields_ * M_);
     } else {
     CF(cufftMakePlan3d(fwd_, p.nf[0], p.nf[1], p.nf[2], CUFFT_D2Z, &w1));
     int n3[3] = {p.nf[0], p.nf[1], p.nf[2]};
@@ -3481,15 +3481,14 @@ void Engine::spectral(const double* grid_in, cudaStream_t s, StageTimes* t) {
         // interleaved layout), then interleaved [node][4] for K3's 256-bit
         // node loads (K3 reading the planar fields, four 64-bit loads per
         // node: cfg5 3.35 -> 4.16 ms)
-        for (int f = 0; f < nfields_; ++f)
-            CF(cufftExecZ2D(inv_, d_spec4_ + f * Mh_, d_fplanar_ + f * M_));
         if (nfields_ == 4) {
+            for (int f = 0; f < nfields_; ++f)
+                CF(cufftExecZ2D(inv_, d_spec4_ + f * Mh_, d_fplanar_ + f * M_));
             k_pencil_interleave<<<grid1(M_, 256), 256, 0, s>>>(M_, 4, d_fplanar_, d_fields_);
             CK(cudaGetLastError());
             ++launches_;
         } else {
-            CK(cudaMemcpyAsync(d_fields_, d_fplanar_, sizeof(double) * M_,
-                               cudaMemcpyDeviceToDevice, s));
+            CF(cufftExecZ2D(inv_, d_spec4_, d_fields_));  // one field: planar is the layout
         }
     } else {
         k_scale<<<grid1(Mh_, 256), 256, 0, s>>>(Mh_, plan_.nf[1], plan_.nf[2] / 2 + 1,
