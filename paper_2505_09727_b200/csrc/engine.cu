@@ -101,6 +101,13 @@ __device__ __forceinline__ int wrapi(int l, int n) {
     return r < 0 ? r + n : r;
 }
 
+// wrap l into [0, n): one conditional add/subtract covers [-n, 2n) (tile
+// nodes of grids with n > S + P/2), wrapi otherwise
+__device__ __forceinline__ int wrap_once(int l, int n) {
+    l = l < 0 ? l + n : (l >= n ? l - n : l);
+    return static_cast<unsigned>(l) < static_cast<unsigned>(n) ? l : wrapi(l, n);
+}
+
 // Per-dimension footprint (gridder.hpp:108-139): first node and the shared
 // window-piece coordinate.  Node j's argument x - h(first+j) lies in window
 // piece 4(P-1-j)+s at the same local coordinate t for every j.
@@ -1909,6 +1916,8 @@ struct InterpArgs {
     int bin_lo, bin_hi;
     double4* S;            // kSpectral: if set, (u_s, F_s) per atom (original order) go
                            // here as one 32-byte store instead of into u / F
+    const int* tstart;     // k_interp_tile: spread-bin starts (kpb keys per bin)
+    int nbin;
 };
 
 // Thread per atom (spread-bin order, so neighbouring threads share grid
@@ -2083,6 +2092,110 @@ __global__ void __launch_bounds__(128) k_interp(GridArgs g, InterpArgs a) {
                 a.F[3 * o + 1] = Fy;
                 a.F[3 * o + 2] = Fz;
             }
+        }
+    }
+}
+
+// Padded row / plane strides (16-byte elements) of k_interp_tile's field
+// tile: RS = S and PS = S^2 (mod 8), so the tile element of a warp's
+// consecutive atoms -- consecutive grid cells of the bin, z fastest -- is
+// their linear cell index mod 8: eight consecutive cells fill the eight
+// 16-byte slots of a 128-byte wavefront without a bank conflict.
+__host__ __device__ __forceinline__ void tile_strides(int S, int W, int& RS, int& PS) {
+    RS = W;
+    while ((RS - S) % 8 != 0) ++RS;
+    PS = RS * W;
+    while ((PS - S * S) % 8 != 0) ++PS;
+}
+
+// K3 for large systems (ik, spectral mode): one CTA per x-half of a spread
+// bin (the bin's atoms are sorted by grid cell, x slowest, so each half is a
+// contiguous range), the half's field tile (S/2 + P by S + P by S + P nodes:
+// the footprints of all its atoms) staged in shared memory as two double2
+// planes -- (u, E_x) and (E_y, E_z) per node -- with padded row / plane
+// strides, then thread per atom from the tile.  Every node read is a
+// shared-memory hit: no L1/L2-miss latency (k_interp is bound by it, 23 %
+// occupancy at 128 registers).  XH = number of x-parts per bin (1 or 2).
+template <int PT>
+__global__ void __launch_bounds__(256) k_interp_tile(GridArgs g, InterpArgs a, int XH) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int P = PT;
+    const int SX = g.S / XH;                     // cells of this part in x
+    const int Wx = SX + P, W = g.S + P;          // tile edges (footprints start 0..S nodes in)
+    int RS, PS;
+    tile_strides(g.S, W, RS, PS);
+    const int TS = PS * Wx;
+    double2* t0 = reinterpret_cast<double2*>(smem);  // (u, Ex)
+    double2* t1 = t0 + TS;                           // (Ey, Ez)
+    double* tab = reinterpret_cast<double*>(t1 + TS);  // phi (3 x 4P x 13)
+    const int bin = blockIdx.x / XH, h = blockIdx.x - bin * XH;
+    const int kb = bin * g.kpb + h * (g.kpb / XH);
+    const int ib = a.tstart[kb], ie = a.tstart[kb + g.kpb / XH];
+    if (ib == ie) return;
+    const int bz = bin % g.nb[2], by = (bin / g.nb[2]) % g.nb[1], bx = bin / (g.nb[1] * g.nb[2]);
+    const int lo0 = bx * g.S + h * SX - P / 2, lo1 = by * g.S - P / 2, lo2 = bz * g.S - P / 2;
+    const int ntab = 3 * 4 * P * kNc;
+    for (int t = threadIdx.x; t < ntab; t += blockDim.x) tab[t] = g.win[t];
+    const long ny = g.nf[1], nz = g.nf[2];
+    const int W2 = W * W, n3 = Wx * W2;
+    for (int t = threadIdx.x; t < n3; t += blockDim.x) {
+        const int ix = t / W2, r = t - ix * W2;
+        const int iy = r / W, iz = r - iy * W;
+        const int gx = wrap_once(lo0 + ix, g.nf[0]), gy = wrap_once(lo1 + iy, g.nf[1]),
+                  gz = wrap_once(lo2 + iz, g.nf[2]);
+        double f0, f1, f2, f3;
+        ldg4(a.fields + 4 * ((gx * ny + gy) * nz + gz), f0, f1, f2, f3);
+        const int e = ix * PS + iy * RS + iz;
+        t0[e] = make_double2(f0, f1);
+        t1[e] = make_double2(f2, f3);
+    }
+    __syncthreads();
+    for (int k = ib + threadIdx.x; k < ie; k += blockDim.x) {
+        const double4 v = a.xyzq[k];
+        const Foot fx = footprint(P, v.x, g.h[0], g.half[0]);
+        const Foot fy = footprint(P, v.y, g.h[1], g.half[1]);
+        const Foot fz = footprint(P, v.z, g.h[2], g.half[2]);
+        double wy[P], wz[P];
+        weights<P>(P, tab + 1 * 4 * P * kNc, fy, wy);
+        weights<P>(P, tab + 2 * 4 * P * kNc, fz, wz);
+        // footprint offsets inside the tile (0..SX / 0..S by construction;
+        // clamped for non-finite input)
+        const int ox = clampi(fx.first - lo0, 0, Wx - P), oy = clampi(fy.first - lo1, 0, W - P),
+                  oz = clampi(fz.first - lo2, 0, W - P);
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll 1
+        for (int jx = 0; jx < P; ++jx) {
+            const double wxj = weight1(P, tab, fx, jx);
+            const int rowx = (ox + jx) * PS + oy * RS + oz;
+#pragma unroll
+            for (int jy = 0; jy < P; ++jy) {
+                const int row = rowx + jy * RS;
+                double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+                for (int jz = 0; jz < P; ++jz) {
+                    const double2 p0 = t0[row + jz], p1 = t1[row + jz];
+                    s0 = fma(wz[jz], p0.x, s0);
+                    s1 = fma(wz[jz], p0.y, s1);
+                    s2 = fma(wz[jz], p1.x, s2);
+                    s3 = fma(wz[jz], p1.y, s3);
+                }
+                const double wxy = wxj * wy[jy];
+                a0 = fma(wxy, s0, a0);
+                a1 = fma(wxy, s1, a1);
+                a2 = fma(wxy, s2, a2);
+                a3 = fma(wxy, s3, a3);
+            }
+        }
+        const int o = a.orig[k];
+        const double qi = v.w;
+        const double us = a0 - qi * a.self_coef;
+        if (a.S) {
+            a.S[o] = make_double4(us, -qi * a1, -qi * a2, -qi * a3);
+        } else {
+            a.u[o] = us;
+            a.F[3 * o + 0] = -qi * a1;
+            a.F[3 * o + 1] = -qi * a2;
+            a.F[3 * o + 2] = -qi * a3;
         }
     }
 }
@@ -2346,6 +2459,17 @@ struct SpreadLaunch {
     }
 };
 
+// atoms from which K3 stages each bin's field tile in shared memory
+// (ESP_INTERP_TILE_MIN_N overrides; 0 disables)
+inline long interp_tile_min_n() {
+    static const long v = [] {
+        const char* e = std::getenv("ESP_INTERP_TILE_MIN_N");
+        const long n = e ? std::atol(e) : (1L << 19);
+        return n > 0 ? n : (1L << 62);
+    }();
+    return v;
+}
+
 // atoms up to which K3 runs eight lanes per atom (ESP_INTERP8_MAX_N overrides)
 inline long interp8_max_n() {
     static const long v = [] {
@@ -2370,6 +2494,35 @@ struct InterpLaunch {
             CK(cudaGetLastError());
         };
         if constexpr (P > 0 && P <= 8) {
+            // large systems: the bin's field tile in shared memory
+            if (mode == kSpectral && ik && !a.startB && !g.xslab && a.tstart &&
+                a.N >= interp_tile_min_n()) {
+                // one CTA of 256 threads per whole bin (cfg5 K3, ms: whole
+                // bins 2.60, x-halves 2.89, x-quarters 2.75; 128 threads
+                // 3.00-3.26); XH > 1 (x-parts of a bin sorted by single grid
+                // cells) is kept for bins whose tile would not fit
+                int XH = 1;
+                const int NT = 256;
+                const int W = g.S + P, Wx = g.S / XH + P;
+                int RS, PS;
+                tile_strides(g.S, W, RS, PS);
+                size_t smt = 2 * sizeof(double2) * static_cast<size_t>(PS) * Wx +
+                             sizeof(double) * 3 * 4 * P * kNc;
+                if (smt > 120 * 1024 && g.kpb == g.S * g.S * g.S && g.S % 2 == 0) {
+                    XH = 2;  // x-halves: smaller tiles
+                    const int Wx2 = g.S / 2 + P;
+                    smt = 2 * sizeof(double2) * static_cast<size_t>(PS) * Wx2 +
+                          sizeof(double) * 3 * 4 * P * kNc;
+                }
+                if (smt <= 120 * 1024) {
+                    CK(cudaFuncSetAttribute(k_interp_tile<P>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(smt)));
+                    k_interp_tile<P><<<a.nbin * XH, NT, smt, s>>>(g, a, XH);
+                    CK(cudaGetLastError());
+                    return;
+                }
+            }
             // small systems: eight lanes per atom (more gathers in flight)
             if (mode == kSpectral && ik && !a.startB && !g.xslab && a.N <= interp8_max_n()) {
                 const size_t sm8 = sizeof(double) * 3 * 4 * P * kNc;
@@ -3713,6 +3866,8 @@ void Engine::enqueue(long N, const double* pos, const double* q, double* u, doub
     a.u = u;
     a.F = F;
     a.S = d_specres_;  // spectral part (minus self) per atom, combined below
+    a.tstart = d_startB_;
+    a.nbin = nbin_;
     a.self_coef = plan_.self_coef;
     const GridArgs g = grid_args();
     if (t) {
