@@ -1918,6 +1918,8 @@ struct InterpArgs {
                            // here as one 32-byte store instead of into u / F
     const int* tstart;     // k_interp_tile: spread-bin starts (kpb keys per bin)
     int nbin;
+    const double* fplanar; // k_interp_tile: if set, the fields planar [4][node] (the
+                           // interleaving pass is skipped) instead of a.fields
 };
 
 // Thread per atom (spread-bin order, so neighbouring threads share grid
@@ -2144,7 +2146,15 @@ __global__ void __launch_bounds__(256) k_interp_tile(GridArgs g, InterpArgs a, i
         const int gx = wrap_once(lo0 + ix, g.nf[0]), gy = wrap_once(lo1 + iy, g.nf[1]),
                   gz = wrap_once(lo2 + iz, g.nf[2]);
         double f0, f1, f2, f3;
-        ldg4(a.fields + 4 * ((gx * ny + gy) * nz + gz), f0, f1, f2, f3);
+        const long node = (gx * ny + gy) * nz + gz;
+        if (a.fplanar) {
+            f0 = __ldg(a.fplanar + node);
+            f1 = __ldg(a.fplanar + a.M + node);
+            f2 = __ldg(a.fplanar + 2 * a.M + node);
+            f3 = __ldg(a.fplanar + 3 * a.M + node);
+        } else {
+            ldg4(a.fields + 4 * node, f0, f1, f2, f3);
+        }
         const int e = ix * PS + iy * RS + iz;
         t0[e] = make_double2(f0, f1);
         t1[e] = make_double2(f2, f3);
@@ -2470,6 +2480,28 @@ inline long interp_tile_min_n() {
     return v;
 }
 
+// k_interp_tile for this grid / window / N (ik spectral mode): the number of
+// x-parts per bin (1: whole bins, the fastest; 2: x-halves when a whole-bin
+// tile does not fit) and its shared memory, or 0 when k_interp runs.  cfg5
+// sweep (K3 ms): whole bins 2.60, x-halves 2.89, x-quarters 2.75, 128
+// threads per CTA 3.00-3.26.
+inline int interp_tile_parts(const GridArgs& g, int P, long N, size_t* smem) {
+    if (P < 5 || P > 8 || g.xslab || N < interp_tile_min_n()) return 0;
+    const int W = g.S + P;
+    int RS, PS;
+    tile_strides(g.S, W, RS, PS);
+    const size_t tab = sizeof(double) * 3 * 4 * P * kNc;
+    for (int XH : {1, 2}) {
+        if (XH == 2 && !(g.kpb == g.S * g.S * g.S && g.S % 2 == 0)) break;
+        const size_t smt = 2 * sizeof(double2) * static_cast<size_t>(PS) * (g.S / XH + P) + tab;
+        if (smt <= 120 * 1024) {
+            if (smem) *smem = smt;
+            return XH;
+        }
+    }
+    return 0;
+}
+
 // atoms up to which K3 runs eight lanes per atom (ESP_INTERP8_MAX_N overrides)
 inline long interp8_max_n() {
     static const long v = [] {
@@ -2495,34 +2527,18 @@ struct InterpLaunch {
         };
         if constexpr (P > 0 && P <= 8) {
             // large systems: the bin's field tile in shared memory
-            if (mode == kSpectral && ik && !a.startB && !g.xslab && a.tstart &&
-                a.N >= interp_tile_min_n()) {
-                // one CTA of 256 threads per whole bin (cfg5 K3, ms: whole
-                // bins 2.60, x-halves 2.89, x-quarters 2.75; 128 threads
-                // 3.00-3.26); XH > 1 (x-parts of a bin sorted by single grid
-                // cells) is kept for bins whose tile would not fit
-                int XH = 1;
-                const int NT = 256;
-                const int W = g.S + P, Wx = g.S / XH + P;
-                int RS, PS;
-                tile_strides(g.S, W, RS, PS);
-                size_t smt = 2 * sizeof(double2) * static_cast<size_t>(PS) * Wx +
-                             sizeof(double) * 3 * 4 * P * kNc;
-                if (smt > 120 * 1024 && g.kpb == g.S * g.S * g.S && g.S % 2 == 0) {
-                    XH = 2;  // x-halves: smaller tiles
-                    const int Wx2 = g.S / 2 + P;
-                    smt = 2 * sizeof(double2) * static_cast<size_t>(PS) * Wx2 +
-                          sizeof(double) * 3 * 4 * P * kNc;
-                }
-                if (smt <= 120 * 1024) {
-                    CK(cudaFuncSetAttribute(k_interp_tile<P>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            static_cast<int>(smt)));
-                    k_interp_tile<P><<<a.nbin * XH, NT, smt, s>>>(g, a, XH);
-                    CK(cudaGetLastError());
-                    return;
-                }
+            size_t smt = 0;
+            const int XH = mode == kSpectral && ik && !a.startB && a.tstart
+                               ? interp_tile_parts(g, P, a.N, &smt) : 0;
+            if (XH > 0) {
+                CK(cudaFuncSetAttribute(k_interp_tile<P>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smt)));
+                k_interp_tile<P><<<a.nbin * XH, 256, smt, s>>>(g, a, XH);
+                CK(cudaGetLastError());
+                return;
             }
+            if (a.fplanar) throw CudaError("K3: planar fields without the tiled kernel");
             // small systems: eight lanes per atom (more gathers in flight)
             if (mode == kSpectral && ik && !a.startB && !g.xslab && a.N <= interp8_max_n()) {
                 const size_t sm8 = sizeof(double) * 3 * 4 * P * kNc;
@@ -2531,6 +2547,7 @@ struct InterpLaunch {
                 return;
             }
         }
+        if (a.fplanar) throw CudaError("K3: planar fields without the tiled kernel");
         switch (mode) {
             case kSpectral: ik ? go(k_interp<P, kSpectral, true>) : go(k_interp<P, kSpectral, false>); break;
             case kValue: go(k_interp<P, kValue, true>); break;
@@ -3547,7 +3564,7 @@ void Engine::phase_b(int rank, int nranks, const double* grid_in, double* u, dou
         CK(cudaMemsetAsync(u, 0, sizeof(double) * N, s));
         CK(cudaMemsetAsync(F, 0, sizeof(double) * 3 * N, s));
     }
-    spectral(grid_in, s, nullptr);
+    spectral(grid_in, s, nullptr, -1);
     finish(N, rank, nranks, d_fields_, grid_args(), u, F, energy_dev, s);
 }
 
@@ -3590,14 +3607,15 @@ void Engine::finish(long N, int rank, int nranks, const double* fields, const Gr
 void Engine::run_grid(long N, cudaStream_t s, StageTimes* t) {
     run_spread(N, s, 0, 1, nullptr);
     if (t) CK(cudaEventRecord(ev_t_[3], s));
-    spectral(d_grid_, s, t);
+    spectral(d_grid_, s, t, N);
 }
 
 // grid -> the nfields interleaved fields (stage events 4, 5, 6 after the
 // forward transform, the multiply and the inverse transform).  With k_xpass
 // "fft" is the 2-D forward planes, "scale" the fused x pass (forward x DFTs,
 // influence, ik, inverse x DFTs) and "ifft" the 2-D inverse planes.
-void Engine::spectral(const double* grid_in, cudaStream_t s, StageTimes* t) {
+void Engine::spectral(const double* grid_in, cudaStream_t s, StageTimes* t, long n_k3) {
+    k3_planar_ = false;
     CF(cufftSetStream(fwd_, s));
     CF(cufftExecD2Z(fwd_, const_cast<double*>(grid_in), d_spec_));
     if (t) CK(cudaEventRecord(ev_t_[4], s));
@@ -3637,9 +3655,13 @@ void Engine::spectral(const double* grid_in, cudaStream_t s, StageTimes* t) {
         if (nfields_ == 4) {
             for (int f = 0; f < nfields_; ++f)
                 CF(cufftExecZ2D(inv_, d_spec4_ + f * Mh_, d_fplanar_ + f * M_));
-            k_pencil_interleave<<<grid1(M_, 256), 256, 0, s>>>(M_, 4, d_fplanar_, d_fields_);
-            CK(cudaGetLastError());
-            ++launches_;
+            // the tiled K3 stages its tiles from the planar fields itself
+            k3_planar_ = n_k3 > 0 && interp_tile_parts(grid_args(), plan_.P, n_k3, nullptr) > 0;
+            if (!k3_planar_) {
+                k_pencil_interleave<<<grid1(M_, 256), 256, 0, s>>>(M_, 4, d_fplanar_, d_fields_);
+                CK(cudaGetLastError());
+                ++launches_;
+            }
         } else {
             CF(cufftExecZ2D(inv_, d_spec4_, d_fields_));  // one field: planar is the layout
         }
@@ -3878,6 +3900,7 @@ void Engine::enqueue(long N, const double* pos, const double* q, double* u, doub
         run_pair(N, s, 0, 1);
         CK(cudaEventRecord(ev_t_[2], s));
         run_grid(N, s, t);
+        a.fplanar = k3_planar_ ? d_fplanar_ : nullptr;
         if (N > 0) {
             dispatch_P<InterpLaunch>(plan_.P, static_cast<int>(kSpectral), nfields_ == 4, g, a, s);
             ++launches_;
@@ -3890,6 +3913,7 @@ void Engine::enqueue(long N, const double* pos, const double* q, double* u, doub
         CK(cudaEventRecord(ev_fork_, s));
         CK(cudaStreamWaitEvent(aux, ev_fork_, 0));
         run_grid(N, aux, nullptr);
+        a.fplanar = k3_planar_ ? d_fplanar_ : nullptr;
         if (N > 0) {
             dispatch_P<InterpLaunch>(plan_.P, static_cast<int>(kSpectral), nfields_ == 4, g, a,
                                      aux);
@@ -3969,6 +3993,9 @@ void Engine::spectral_sum(long N, const double* pos, const double* q, double* u,
     a.M = M_;
     a.u = u;
     a.F = F;
+    a.tstart = d_startB_;  // the tiled K3 when run_grid chose it (planar fields)
+    a.nbin = nbin_;
+    a.fplanar = k3_planar_ ? d_fplanar_ : nullptr;
     const GridArgs g = grid_args();
     dispatch_P<InterpLaunch>(plan_.P, static_cast<int>(kSpectral), nfields_ == 4, g, a, s);
     if (t) {

@@ -195,7 +195,10 @@ private:
     void run_pair(long N, cudaStream_t s, int rank, int nranks, bool own_bins = false);
     bool run_pair_half(long N, cudaStream_t s, int rank = 0, int nranks = 1, bool own_bins = false);
     void run_grid(long N, cudaStream_t s, StageTimes* t);
-    void spectral(const double* grid_in, cudaStream_t s, StageTimes* t);
+    // n_k3 > 0: the K3 launch that follows is the enqueue's (N atoms), so the
+    // tiled K3 may take the planar fields; -1 otherwise
+    void spectral(const double* grid_in, cudaStream_t s, StageTimes* t, long n_k3);
+    bool k3_planar_ = false;
     void run_spread(long N, cudaStream_t s, int rank, int nranks, double* grid,
                     const GridArgs* gslab = nullptr, long nreals = -1, int b0 = -1,
                     int b1 = -1);
