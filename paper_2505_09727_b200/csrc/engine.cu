@@ -2827,10 +2827,12 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
         int n2[2] = {ny, nz};
         int re[2] = {ny, nz}, ce[2] = {ny, nzh};
         CF(cufftMakePlanMany(fwd_, 2, n2, re, 1, ny * nz, ce, 1, ny * nzh, CUFFT_D2Z, p.nf[0], &w1));
-        // one field per execution: planar half-transformed input, planar
-        // fields out (interleaved for K3 afterwards, see spectral())
-        CF(cufftMakePlanMany(inv_, 2, n2, ce, 1, ny * nzh, re, 1, ny * nz, CUFFT_Z2D, p.nf[0],
-                             &w2));
+        // planar half-transformed input, planar fields out (interleaved for
+        // K3 afterwards unless the tiled K3 reads them planar, see
+        // spectral()); all fields' planes in one batch: the [f][x] planes
+        // are consecutive in both layouts
+        CF(cufftMakePlanMany(inv_, 2, n2, ce, 1, ny * nzh, re, 1, ny * nz, CUFFT_Z2D,
+                             p.nf[0] * nfields_, &w2));
         if (nfields_ == 4) dalloc(d_fplanar_, nfields_ * M_);
     } else {
     CF(cufftMakePlan3d(fwd_, p.nf[0], p.nf[1], p.nf[2], CUFFT_D2Z, &w1));
@@ -3653,8 +3655,7 @@ void Engine::spectral(const double* grid_in, cudaStream_t s, StageTimes* t, long
         // node loads (K3 reading the planar fields, four 64-bit loads per
         // node: cfg5 3.35 -> 4.16 ms)
         if (nfields_ == 4) {
-            for (int f = 0; f < nfields_; ++f)
-                CF(cufftExecZ2D(inv_, d_spec4_ + f * Mh_, d_fplanar_ + f * M_));
+            CF(cufftExecZ2D(inv_, d_spec4_, d_fplanar_));
             // the tiled K3 stages its tiles from the planar fields itself
             k3_planar_ = n_k3 > 0 && interp_tile_parts(grid_args(), plan_.P, n_k3, nullptr) > 0;
             if (!k3_planar_) {
