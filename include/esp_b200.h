@@ -80,8 +80,8 @@ typedef struct {
                              * 0 = full lists, ghost rows are zero */
     int fused_xpass;        /* 1: the influence multiply and ik derivatives run
                              * inside the FFT's x pass (2-D cuFFT planes +
-                             * k_xpass; even 5-smooth n_x >= 128, ESP_XPASS);
-                             * 0: 3-D cuFFT + separate multiply pass */
+                             * k_xpass; even 5-smooth n_x <= 720, unless
+                             * ESP_XPASS=0); 0: 3-D cuFFT + a multiply pass */
     int deterministic;      /* esp_plan_set_deterministic */
 } esp_plan_info;
 

@@ -1715,15 +1715,15 @@ __global__ void __launch_bounds__(256) k_scale(long Mh, int ny, int nzh, const d
 // fields.  The 1-D DFTs are self-sorting Stockham passes of radix 4, 2, 3, 5
 // in shared memory (n_x even 5-smooth, the reference's auto grids,
 // ewald.hpp:261-273), fp64 throughout, twiddles from a long-double table.
-// Grids with other n_x (explicit overrides) or n_x < 128 (where the 3-D
-// path's fewer launches are faster) keep cuFFT 3-D + k_scale.
+// Grids with other n_x (explicit overrides, n_x > 720) keep cuFFT 3-D +
+// k_scale.
 // ----------------------------------------------------------------------------
 
 constexpr int kXpCols = 4;          // kz columns per CTA
 constexpr int kXpThreads = 256;
 constexpr int kXpMaxPass = 16;
 constexpr int kXpMaxN = 720;        // shared memory: n_x * (2 * 2 * kXpCols + 1) * 16 B
-constexpr int kXpAutoMinN = 128;    // k_xpass by default from this n_x
+constexpr int kXpAutoMinN = 2;      // k_xpass by default from this n_x (all even grids)
 
 struct XPassArgs {
     int nx, ny, nzh;
@@ -2805,9 +2805,9 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
                 rad.push_back(r);
                 n /= r;
             }
-        // auto from n_x >= 128 (cfg5, n_x = 180: fft + multiply + ifft 0.655 ->
-        // 0.588 ms); below that the 3-D path's fewer launches win (cfg2-4:
-        // +15-25 us).  ESP_XPASS=1 forces it (even 5-smooth n_x), 0 disables.
+        // on for every even 5-smooth n_x <= kXpMaxN (fft + multiply + ifft,
+        // ms: cfg5 0.655 -> 0.50, cfg4 0.088 -> 0.072, cfg2 0.043 -> 0.037);
+        // ESP_XPASS=0 keeps 3-D cuFFT + k_scale.
         const char* e = std::getenv("ESP_XPASS");
         const int want = e ? std::atoi(e) : (p.nf[0] >= kXpAutoMinN ? 1 : 0);
         xpass_ = want != 0 && n == 1 && p.nf[0] % 2 == 0 && p.nf[0] <= kXpMaxN;

@@ -1,10 +1,9 @@
 """K2 fused into the FFT's x pass (k_xpass, engine.cu): the 2-D cuFFT
 planes + fused x DFTs / influence multiply / ik derivatives must reproduce
 the reference (ewald.hpp:545-548, 567-595; gridder.hpp:162-210) like the
-3-D cuFFT + k_scale path.  ESP_XPASS=1 forces the fused path on the small
-configs (auto only from n_x >= 128, i.e. cfg5, whose parity is checked in
-test_gpu_golden_large.py), ESP_XPASS=0 forces the 3-D path; both are
-compared with the compiled reference's fixtures and with each other."""
+3-D cuFFT + k_scale path.  The fused path is the default for every even
+5-smooth n_x; ESP_XPASS=0 forces the 3-D path; both are compared with the
+compiled reference's fixtures and with each other."""
 import numpy as np
 import pytest
 
@@ -93,13 +92,13 @@ def test_non_smooth_override_keeps_3d_path(esp, gpu, monkeypatch):
 
 
 def test_mode_reported_by_plan(esp, gpu, monkeypatch):
-    """esp_plan_info.fused_xpass: auto from n_x >= 128 (cfg5's 180), forced by
-    ESP_XPASS=1 on smooth grids, never for non-smooth n_x."""
+    """esp_plan_info.fused_xpass: on by default for even 5-smooth n_x (every
+    auto-selected grid), never for non-smooth n_x, off with ESP_XPASS=0."""
     from paper_2505_09727_b200 import systems as S
     monkeypatch.delenv("ESP_XPASS", raising=False)
     c5 = S.config("cfg5")
     assert esp.build_plan((c5.L,) * 3, "pswf", c5.eps, c5.r_c, device=gpu).fused_xpass
-    assert not esp.build_plan((10.0,) * 3, "pswf", 1e-4, 1.0, device=gpu).fused_xpass
+    assert esp.build_plan((10.0,) * 3, "pswf", 1e-4, 1.0, device=gpu).fused_xpass
     monkeypatch.setenv("ESP_XPASS", "1")
     assert esp.build_plan((10.0,) * 3, "pswf", 1e-4, 1.0, device=gpu).fused_xpass
     assert not esp.build_plan((10.0,) * 3, "pswf", 1e-4, 1.0, esp.Overrides(nf=42),
