@@ -1648,9 +1648,9 @@ __global__ void __launch_bounds__(512) k_spread(GridArgs g, const double4* __res
             const int ix = t / PS, rem = t - ix * PS;
             const int iy = rem / RS, iz = rem - iy * RS;
             if (iy >= W || iz >= W) continue;  // padding
-            const int gx = g.xslab ? lo[0] + ix - g.x_lo : wrapi(lo[0] + ix, g.nf[0]);
-            const int gy = wrapi(lo[1] + iy, g.nf[1]);
-            const int gz = wrapi(lo[2] + iz, g.nf[2]);
+            const int gx = g.xslab ? lo[0] + ix - g.x_lo : wrap_once(lo[0] + ix, g.nf[0]);
+            const int gy = wrap_once(lo[1] + iy, g.nf[1]);
+            const int gz = wrap_once(lo[2] + iz, g.nf[2]);
             ESP_DCHECK(gx >= 0 && gy >= 0 && gy < g.nf[1] && gz >= 0 && gz < g.nf[2] &&
                        (g.xslab || gx < g.nf[0]));
             double* dst = &grid[(static_cast<long>(gx) * g.nf[1] + gy) * g.nf[2] + gz];
