@@ -467,15 +467,17 @@ def run_ours(args):
     nfld = 4 if args.force_method == "ik" else 1
     if plan.fused_xpass:
         # 2-D cuFFT planes + K2 fused into the x pass (read b and p, write the
-        # nfld half-transformed fields); the inverse planes write planar
-        # fields that are interleaved for K3 (read + write)
+        # nfld half-transformed fields); the inverse planes write planar fields
         kbytes = {
             "K1 k_spread": (32 * N + 8 * M, "spread"),
             "K2+x-DFTs k_xpass (fused)": ((24 + 16 * nfld) * Mh, "scale"),
             "K3 k_interp": (8 * nfld * M + 64 * N, "interpolate"),
             "cuFFT D2Z 2-D planes": (8 * M + 16 * Mh, "fft"),
-            f"cuFFT Z2D 2-D planes x{nfld} + interleave":
-                (nfld * (16 * Mh + 8 * M) + (16 * nfld * M if nfld == 4 else 0), "ifft"),
+            # (the tiled K3, N >= 2^19, reads the planar fields; smaller
+            # systems add an interleaving pass, 16 B per field and node)
+            f"cuFFT Z2D 2-D planes, {nfld} field(s) in one batch":
+                (nfld * (16 * Mh + 8 * M) + (16 * nfld * M if nfld == 4 and N < (1 << 19) else 0),
+                 "ifft"),
         }
     else:
         kbytes = {
@@ -496,7 +498,28 @@ def run_ours(args):
     kernels["K4 " + roofline["kernel"].split(" ")[0]] = {
         "bound": "fp64", "flops": pair_flops, "ms": stages_ms["local"],
         "TFLOP/s": achieved, "frac": roofline["frac"]}
+    # K1 and K3 move their footprint nodes through shared memory (K1: the
+    # tile read-modify-write, 16 B per node; tiled K3: 32 B per node read),
+    # so their bound is the SM-wide shared-memory bandwidth: 128 B per clock
+    # per SM at the SM clock sampled during the run
+    try:
+        import torch as _t
+        n_sm = _t.cuda.get_device_properties(local).multi_processor_count
+    except Exception:
+        n_sm = 148
+    sm_mhz = (clk or {}).get("sm_mhz") or 1965.0
+    smem_peak = n_sm * 128.0 * sm_mhz * 1e6 / 1e9  # GB/s
+    P3 = int(plan.P) ** 3
+    for name, (nbytes, stage) in {"K1 k_spread (shared-memory tile RMW)": (16 * P3 * N, "spread"),
+                                  "K3 (footprint node reads)": (32 * P3 * N, "interpolate")}.items():
+        kms = stages_ms.get(stage)
+        if kms:
+            gbs = nbytes / (kms * 1e-3) / 1e9
+            kernels[name] = {"bound": "smem", "bytes": nbytes, "ms": kms, "GB/s": gbs,
+                             "frac": gbs / smem_peak}
     kernel_rooflines = {"hbm_peak_GBps": hbm_peak, "hbm_peak_source": hbm_src,
+                        "smem_peak_GBps": smem_peak,
+                        "smem_peak_source": f"{n_sm} SMs x 128 B/clock x {sm_mhz:g} MHz (sampled)",
                         "kernels": kernels}
 
     # ---- e2e through the public API on pinned host buffers
