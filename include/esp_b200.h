@@ -83,6 +83,11 @@ typedef struct {
                              * k_xpass; even 5-smooth n_x <= 720, unless
                              * ESP_XPASS=0); 0: 3-D cuFFT + a multiply pass */
     int deterministic;      /* esp_plan_set_deterministic */
+    int pair_kernel;        /* real-space kernel of the plan's last evaluation
+                             * (selected per call from N and the density):
+                             * -1 none yet, 0 full lists (k_pair), 1 half-shell
+                             * (k_pair_half), 2 cluster pairs (k_pair_tile),
+                             * 3 all pairs (box too small for the cell list) */
 } esp_plan_info;
 
 /* Per-stage wall time in seconds (EnergyForces::timings keys,

@@ -77,6 +77,7 @@ class _Info(C.Structure):
         ("n_split_coef", C.c_int), ("n_window_coef", C.c_int), ("pair_poly_degree", C.c_int),
         ("pair_fit_err", C.c_double), ("device", C.c_int), ("pair_cells", C.c_int * 3),
         ("pencil_half", C.c_int), ("fused_xpass", C.c_int), ("deterministic", C.c_int),
+        ("pair_kernel", C.c_int),
     ]
 
 
@@ -244,6 +245,14 @@ class EwaldPlan:
         self.pencil_half = bool(info.pencil_half)
         # K2 inside the FFT's x pass (include/esp_b200.h)
         self.fused_xpass = bool(info.fused_xpass)
+
+    @property
+    def pair_kernel(self) -> str:
+        """Real-space kernel of the plan's last evaluation (esp_plan_info.pair_kernel):
+        "none", "full", "half", "tile" (cluster pairs) or "allpairs"."""
+        info = _Info()
+        _check(_lib.esp_plan_get_info(self._h, C.byref(info)))
+        return {-1: "none", 0: "full", 1: "half", 2: "tile", 3: "allpairs"}[info.pair_kernel]
 
     def __del__(self):
         h = getattr(self, "_h", None)

@@ -1393,6 +1393,399 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
         atomicAdd(a.npairs, 2ull * static_cast<unsigned long long>(npair));
 }
 
+// ----------------------------------------------------------------------------
+// K4, cluster-pair form (single GPU): a warp evaluates 2 targets x 16 partners
+// ----------------------------------------------------------------------------
+//
+// k_pair_half spends ~2/3 of its instructions on the neighbour search: per
+// target a candidate list (~1.9 candidates per in-range pair), an fp32 screen
+// and a ballot compaction into full 32-lane rounds.  Here a warp takes a
+// CLUSTER of two consecutive sorted atoms of a target column (i0, i1, ~1 A
+// apart in z) and one candidate list for both (the union of their spheres
+// over the forward columns, own column from i0 + 1).  A candidate is screened
+// against both targets at once and kept if either is in range; the survivors
+// queue up, and every 16 of them form one 2 x 16 tile: lane (isub, jsub) =
+// (lane >> 4, lane & 15) evaluates pair (i_isub, j_jsub) in fp64 with the
+// out-of-range lanes masked by selects (~86 % of a tile's lanes are in range,
+// by a Monte Carlo estimate at water density and r_c = 10 A).  The j-side
+// terms of the two targets are summed with one shuffle and sent with the
+// same REDs as k_pair_half; the i-side sums stay in registers and are
+// transpose-reduced over the 16 lanes once per cluster.  Per in-range pair
+// this halves the screening, list and per-target work, and removes the
+// per-pair compaction.  The pair terms are those of pair_eval3, operation for
+// operation, so only the summation order differs.
+
+// pair terms as pair_eval3 with the out-of-range / invalid lanes masked by
+// selects (r2 replaced by r_c^2 before the square root, so every lane's
+// arithmetic is finite); returns whether the pair counted
+template <int ND, bool SHIFT>
+__device__ __forceinline__ bool pair_tile(const PairConsts& k, const double4& pj, double sx,
+                                          double sy, double sz, const double4& pi, bool ok,
+                                          double& u, double& fx, double& fy, double& fz,
+                                          double4& gj) {
+    double dx = pj.x - pi.x, dy = pj.y - pi.y, dz = pj.z - pi.z;
+    if (SHIFT) {
+        dx += sx;
+        dy += sy;
+        dz += sz;
+    }
+    const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+    const bool in = ok && r2 < k.rc2 && r2 > 0.0;
+    const double r2s = in ? r2 : k.rc2;
+    double rinv;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rinv) : "d"(r2s));
+    {
+        const double hr = 0.5 * r2s;
+        double e = fma(-hr * rinv, rinv, 0.5);
+        rinv = fma(rinv, e, rinv);
+        e = fma(-hr * rinv, rinv, 0.5);
+        rinv = fma(rinv, e, rinv);
+    }
+    const double z = fma(r2s, k.two_irc2, -1.0);
+    constexpr int NE = (ND + 1) / 2, NO = ND / 2, NDE = ND / 2, NDO = (ND + 1) / 2 - 1;
+    const double w = z * z;
+    double he = k.He[NE - 1], ho = k.Ho[NO - 1], de = k.De[NDE - 1], dO = k.Do[NDO - 1];
+#pragma unroll
+    for (int m = NE - 2; m >= 0; --m) {
+        he = fma(he, w, k.He[m]);
+        if (m < NO - 1) ho = fma(ho, w, k.Ho[m]);
+        if (m < NDE - 1) de = fma(de, w, k.De[m]);
+        if (m < NDO - 1) dO = fma(dO, w, k.Do[m]);
+    }
+    const double H = fma(z, ho, he);
+    const double dH = fma(z, dO, de);
+    const double G = fma(fma(2.0, z, 2.0), dH, H);  // chi / r_c
+    double pot = rinv - H;                           // 4 pi S
+    double c0 = (G + pot) * (rinv * rinv);           // 4 pi (-dS/dr) / r
+    pot = in ? pot : 0.0;
+    c0 = in ? c0 : 0.0;
+    u = fma(pj.w, pot, u);
+    const double c = pj.w * c0;
+    fx = fma(c, dx, fx);
+    fy = fma(c, dy, fy);
+    fz = fma(c, dz, fz);
+    const double b = pi.w * c;
+    gj = make_double4(pi.w * pot, b * dx, b * dy, b * dz);
+    return in;
+}
+
+template <int ND>
+__global__ void __launch_bounds__(kHalfThreads, 3) k_pair_tile(HalfArgs a, const __grid_constant__ PairConsts k) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    float4* cand = reinterpret_cast<float4*>(smem);                 // a.cap + 1 (sentinel)
+    int* qall = reinterpret_cast<int*>(cand + a.cap + 1);           // 64 per warp
+    unsigned short* lall = reinterpret_cast<unsigned short*>(qall + kHalfWarps * 64);
+    int* ent_src = reinterpret_cast<int*>(lall + kHalfWarps * a.lcap);
+    int* ent_off = ent_src + a.nent_max;                            // nent_max + 1
+    unsigned char* ent_slot = reinterpret_cast<unsigned char*>(ent_off + a.nent_max + 1);
+    __shared__ double shiftv[27][3];
+    __shared__ int tbeg[kHalfMaxBX * kHalfMaxBX], tcnt[kHalfMaxBX * kHalfMaxBX];
+    __shared__ int cpre[kHalfMaxBX * kHalfMaxBX + 1];  // cluster prefix per target column
+    __shared__ int tnext;  // next unassigned cluster
+    __shared__ int tcxy[kHalfMaxBX * kHalfMaxBX];
+    __shared__ int fwdc[64];
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int* qw = qall + warp * 64;
+    unsigned short* lw = lall + warp * a.lcap;
+    const unsigned lt_mask = (1u << lane) - 1u;
+
+    const int M = a.M, Mz = a.Mz, BX = a.bx;
+    const int nzb = (a.F[2] + a.bz - 1) / a.bz;
+    const int nyb = (a.F[1] + BX - 1) / BX;
+    const int blk = blockIdx.x + a.blk0;
+    const int bzi = blk % nzb;
+    const int fy0 = ((blk / nzb) % nyb) * BX;
+    const int fx0 = (blk / (nzb * nyb)) * BX;
+    const int bxe = min(BX, a.F[0] - fx0), bye = min(BX, a.F[1] - fy0);
+    const int z0 = bzi * a.bz, z1 = min(a.F[2], z0 + a.bz), bze = z1 - z0;
+    const int Wx = bxe + M, Wy = bye + 2 * M;
+    const int ncol = Wx * Wy;
+    const int nsl = bze + 2 * Mz;
+    const int nent = ncol * nsl;
+    const double ox = fx0 * a.fw[0], oy = fy0 * a.fw[1], oz = z0 * a.fw[2];
+    ESP_DCHECK(nent <= a.nent_max && bxe * bye <= kHalfMaxBX * kHalfMaxBX);
+
+    if (threadIdx.x < 27) {
+        const int t = threadIdx.x;
+        shiftv[t][0] = (t / 9 - 1) * a.box[0];
+        shiftv[t][1] = ((t / 3) % 3 - 1) * a.box[1];
+        shiftv[t][2] = (t % 3 - 1) * a.box[2];
+    }
+    if (threadIdx.x >= 64 && threadIdx.x < 128) {
+        const int nfc = M * (2 * M + 1) + M + 1;
+        const int l = (threadIdx.x - 64) % nfc;
+        int dx, dy;
+        fwd_col(l, M, dx, dy);
+        fwdc[threadIdx.x - 64] = dx | ((dy + M) << 4) | ((l == nfc - 1) << 8);
+    }
+    int wraps = 0;
+    for (int e = threadIdx.x; e < nent; e += blockDim.x) {
+        const int col = e / nsl, sl = e - col * nsl;
+        const int cx = col / Wy, cy = col - cx * Wy;
+        int fx = fx0 + cx, fy = fy0 - M + cy, fz = z0 - Mz + sl;
+        const int ix = fx < 0 ? 0 : (fx >= a.F[0] ? 2 : 1);
+        const int iy = fy < 0 ? 0 : (fy >= a.F[1] ? 2 : 1);
+        const int iz = fz < 0 ? 0 : (fz >= a.F[2] ? 2 : 1);
+        fx += (1 - ix) * a.F[0];
+        fy += (1 - iy) * a.F[1];
+        fz += (1 - iz) * a.F[2];
+        const int f = (fx * a.F[1] + fy) * a.F[2] + fz;
+        ESP_DCHECK(f >= 0 && f < a.F[0] * a.F[1] * a.F[2]);
+        const int s0 = a.start[f];
+        ent_src[e] = s0;
+        ent_off[e + 1] = a.start[f + 1] - s0;
+        const int slot = (ix * 3 + iy) * 3 + iz;
+        ent_slot[e] = static_cast<unsigned char>(slot);
+        wraps |= slot != 13;
+    }
+    const bool wrap = __syncthreads_or(wraps) != 0;
+    if (warp == 0) {
+        const int per = (nent + 31) / 32;
+        const int e0 = min(nent, lane * per), e1 = min(nent, e0 + per);
+        int sum = 0;
+        for (int e = e0; e < e1; ++e) sum += ent_off[e + 1];
+        int incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const int last = e1 > e0 ? ent_off[e1] : 0;
+        __syncwarp();
+        int run = incl - sum;
+        for (int e = e0; e < e1; ++e) {
+            const int c = e == e1 - 1 ? last : ent_off[e + 1];
+            ent_off[e] = run;
+            run += c;
+        }
+        __syncwarp();
+        if (lane == 31) ent_off[nent] = incl;
+    }
+    __syncthreads();
+    const int total = ent_off[nent];
+    if (total > a.cap) {
+        if (threadIdx.x == 0) {
+            const int q = atomicAdd(a.ovf, 1);
+            a.ovf[1 + q] = blk;
+        }
+        return;
+    }
+    if (threadIdx.x == 32) {
+        int accn = 0;
+        const int ntc = bxe * bye;
+        for (int c = 0; c < ntc; ++c) {
+            const int tx = c / bye, ty = M + c % bye;
+            const int col = tx * Wy + ty;
+            const int b = ent_off[col * nsl + Mz], e = ent_off[col * nsl + Mz + bze];
+            tbeg[c] = b;
+            tcnt[c] = e - b;
+            cpre[c] = accn;
+            tcxy[c] = tx | (ty << 8);
+            accn += (e - b + 1) >> 1;
+        }
+        cpre[ntc] = accn;
+        tnext = kHalfWarps;
+    }
+    {
+        const int lo_in = max(0, min(nsl, Mz - z0));
+        const int hi_in = max(0, min(nsl, a.F[2] - z0 + Mz));
+        for (int task = warp; task < ncol * 3; task += kHalfWarps) {
+            const int col = task / 3, part = task - 3 * (task / 3);
+            const int sa = part == 0 ? 0 : (part == 1 ? lo_in : hi_in);
+            const int sb = part == 0 ? lo_in : (part == 1 ? hi_in : nsl);
+            if (sb <= sa) continue;
+            const int e0 = col * nsl + sa;
+            const int g0 = ent_off[e0], g1 = ent_off[col * nsl + sb];
+            const int src0 = ent_src[e0] - g0;
+            const int sl = ent_slot[e0];
+            const double shx = shiftv[sl][0] - ox, shy = shiftv[sl][1] - oy,
+                         shz = shiftv[sl][2] - oz;
+            for (int g = g0 + lane; g < g1; g += 32) {
+                const int src = g + src0;
+                ESP_DCHECK(g < a.cap && src >= 0 && src < a.nacc);
+                const double4 v = a.xyzq[src];
+                cand[g] = make_float4(static_cast<float>(v.x + shx), static_cast<float>(v.y + shy),
+                                      static_cast<float>(v.z + shz),
+                                      __int_as_float(src | (sl << 27)));
+            }
+        }
+        if (threadIdx.x == 0) cand[a.cap] = make_float4(1e30f, 1e30f, 1e30f, __int_as_float(0));
+    }
+    __syncthreads();
+    const int ntc = bxe * bye;
+    const int ncl = cpre[ntc];
+    const float R2 = k.rc2_test;
+    const float fwx = static_cast<float>(a.fw[0]), fwy = static_cast<float>(a.fw[1]);
+    const float ifwz = 1.0f / static_cast<float>(a.fw[2]);
+    const int nfc = M * (2 * M + 1) + M + 1;
+    const int isub = lane >> 4, jsub = lane & 15;
+    int npair = 0;
+
+    for (int cc = warp;;) {
+        if (cc >= ncl) break;
+        const int tc = __popc(__ballot_sync(0xffffffffu, lane >= 1 && lane < ntc && cpre[lane] <= cc));
+        const int k0 = 2 * (cc - cpre[tc]);
+        const int si0 = tbeg[tc] + k0;
+        const bool two = k0 + 1 < tcnt[tc];
+        const int si1 = two ? si0 + 1 : si0;
+        const float4 c0 = cand[si0], c1 = cand[si1];
+        // this lane's target (lanes of a missing second target are masked)
+        const bool vi = isub == 0 || two;
+        const int gi = __float_as_int(isub ? c1.w : c0.w) & 0x7ffffff;
+        const double4 pi = a.xyzq[gi];
+        const int txy = tcxy[tc];
+        const int tx = txy & 0xff, ty = txy >> 8;
+        int beg = 0, cnt = 0;
+        if (lane < nfc) {
+            const int fc = fwdc[lane + ((5 * cc) & 31)];
+            const int dx = fc & 15, dy = ((fc >> 4) & 15) - M;
+            const int ca = tx + dx, cb = ty + dy;
+            const int col = ca * Wy + cb;
+            const float x0 = ca * fwx, y0 = (cb - M) * fwy;
+            // z-extent of the union of the two spheres in this column
+            float zlo = 1e30f, zhi = -1e30f;
+            {
+                const float gx = fmaxf(0.f, fmaxf(x0 - c0.x, c0.x - (x0 + fwx)));
+                const float gy = fmaxf(0.f, fmaxf(y0 - c0.y, c0.y - (y0 + fwy)));
+                const float g2 = fmaf(gx, gx, gy * gy);
+                if (g2 < R2) {
+                    const float zm = sqrtf(R2 - g2);
+                    zlo = c0.z - zm;
+                    zhi = c0.z + zm;
+                }
+            }
+            {
+                const float gx = fmaxf(0.f, fmaxf(x0 - c1.x, c1.x - (x0 + fwx)));
+                const float gy = fmaxf(0.f, fmaxf(y0 - c1.y, c1.y - (y0 + fwy)));
+                const float g2 = fmaf(gx, gx, gy * gy);
+                if (g2 < R2) {
+                    const float zm = sqrtf(R2 - g2);
+                    zlo = fminf(zlo, c1.z - zm);
+                    zhi = fmaxf(zhi, c1.z + zm);
+                }
+            }
+            if (zlo <= zhi) {
+                int klo = static_cast<int>(floorf(zlo * ifwz)) + Mz;
+                int khi = static_cast<int>(floorf(zhi * ifwz)) + Mz;
+                klo = max(0, min(nsl - 1, klo));
+                khi = max(0, min(nsl - 1, khi));
+                int lo = ent_off[col * nsl + klo];
+                const int hi = ent_off[col * nsl + khi + 1];
+                if (fc >> 8) lo = si0 + 1;  // own column: after i0 (i1 meets itself at r = 0)
+                if (hi > lo) {
+                    beg = lo;
+                    cnt = hi - lo;
+                }
+            }
+        }
+        int inc = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
+        }
+        const int T = __shfl_sync(0xffffffffu, inc, 31);
+        double u = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
+        int qn = 0;
+        bool have_pf = false;
+        // partners: the final partial pop (a), the previous pop (b, prefetched)
+        double4 pfa = make_double4(0.0, 0.0, 0.0, 0.0), pfb = pfa;
+        int tfa = 13, sfa = 0, tfb = 13, sfb = 0;
+        // one 2 x 16 tile; j-side terms of both targets summed across the
+        // halves, sent by the lower half; in-range pairs counted by ballot
+        auto tile = [&](const double4& pf, int tf, int sf, bool jv) {
+            double4 g;
+            const bool in = wrap ? pair_tile<ND, true>(k, pf, shiftv[tf][0], shiftv[tf][1],
+                                                       shiftv[tf][2], pi, vi && jv, u, fx, fy, fz, g)
+                                 : pair_tile<ND, false>(k, pf, 0.0, 0.0, 0.0, pi, vi && jv, u, fx,
+                                                        fy, fz, g);
+            npair += __popc(__ballot_sync(0xffffffffu, in));
+            g.x += __shfl_xor_sync(0xffffffffu, g.x, 16);
+            g.y += __shfl_xor_sync(0xffffffffu, g.y, 16);
+            g.z += __shfl_xor_sync(0xffffffffu, g.z, 16);
+            g.w += __shfl_xor_sync(0xffffffffu, g.w, 16);
+            if (isub == 0 && jv) red_acc(a.acc, a.nacc, sf, g.x, g.y, g.z, g.w);
+        };
+        auto fetch = [&](int sq, double4& pf, int& tf, int& sf) {
+            const int cd = __float_as_int(cand[sq].w);
+            ESP_DCHECK((cd & 0x7ffffff) < a.nacc && (static_cast<unsigned>(cd) >> 27) < 27);
+            sf = cd & 0x7ffffff;
+            tf = static_cast<unsigned>(cd) >> 27;
+            pf = a.xyzq[sf];
+        };
+        for (int lb = 0; lb < T; lb += a.lcap - 32) {
+            const int le = min(T, lb + a.lcap - 32);
+            fill_range(lw, lb, max(inc - cnt, lb), min(inc, le), beg - (inc - cnt));
+            const int n = le - lb;
+            const int n32 = (n + 31) & ~31;
+            ESP_DCHECK(n32 <= a.lcap);
+            if (n + lane < n32) lw[n + lane] = static_cast<unsigned short>(a.cap);
+            __syncwarp();
+            const unsigned short* lend = lw + n32;
+            for (const unsigned short* lp = lw + lane; lp < lend; lp += 32) {
+                const int s = *lp;
+                ESP_DCHECK(s >= 0 && s <= a.cap);
+                const float4 c4 = cand[s];
+                const float ax = c4.x - c0.x, ay = c4.y - c0.y, az = c4.z - c0.z;
+                const float bx = c4.x - c1.x, by = c4.y - c1.y, bz = c4.z - c1.z;
+                const bool in = fminf(fmaf(az, az, fmaf(ay, ay, ax * ax)),
+                                      fmaf(bz, bz, fmaf(by, by, bx * bx))) < R2;
+                const unsigned m = __ballot_sync(0xffffffffu, in);
+                ESP_DCHECK(qn + __popc(m) <= 64);
+                if (in) qw[qn + __popc(m & lt_mask)] = s;
+                qn += __popc(m);
+                while (qn >= 16) {
+                    __syncwarp();
+                    const int sqa = qw[jsub];
+                    const int extra = qw[16 + lane];
+                    __syncwarp();
+                    qw[lane] = extra;
+                    qn -= 16;
+                    // evaluate the previous pop's partner, prefetch this one
+                    if (have_pf) tile(pfb, tfb, sfb, true);
+                    fetch(sqa, pfb, tfb, sfb);
+                    have_pf = true;
+                }
+            }
+            __syncwarp();
+        }
+        if (have_pf) tile(pfb, tfb, sfb, true);
+        if (qn > 0) {
+            const bool ja = jsub < qn;
+            fetch(ja ? qw[jsub] : qw[0], pfa, tfa, sfa);
+            tile(pfa, tfa, sfa, ja);
+            if (qn > 16) {
+                const bool jb = 16 + jsub < qn;
+                fetch(jb ? qw[16 + jsub] : qw[0], pfb, tfb, sfb);
+                tile(pfb, tfb, sfb, jb);
+            }
+        }
+        __syncwarp();
+        {
+            // i-side sums over the 16 lanes of each half (transposed reduce)
+            const bool h8 = lane & 8, h4 = lane & 4;
+            const double s0 = h8 ? u : fy, s1 = h8 ? fx : fz;
+            const double k0d = h8 ? fy : u, k1d = h8 ? fz : fx;
+            const double v0 = k0d + __shfl_xor_sync(0xffffffffu, s0, 8);
+            const double v1 = k1d + __shfl_xor_sync(0xffffffffu, s1, 8);
+            double w = (h4 ? v1 : v0) + __shfl_xor_sync(0xffffffffu, h4 ? v0 : v1, 4);
+            w += __shfl_xor_sync(0xffffffffu, w, 2);
+            w += __shfl_xor_sync(0xffffffffu, w, 1);
+            if ((lane & 3) == 0 && vi) {
+                const int comp = (lane >> 2) & 3;  // 0 u, 1 Fx, 2 Fy, 3 Fz
+                atomicAdd(a.acc + comp * a.nacc + gi, comp == 0 ? w : -pi.w * w);
+            }
+        }
+        int nx = 0;
+        if (lane == 0) nx = atomicAdd(&tnext, 1);
+        cc = __shfl_sync(0xffffffffu, nx, 0);
+    }
+    // npair is warp-uniform here (ballot counts)
+    if (lane == 0 && a.npairs && npair)
+        atomicAdd(a.npairs, 2ull * static_cast<unsigned long long>(npair));
+}
+
 // Blocks whose forward neighbourhood did not fit the staging area: warp per
 // target, lane per forward column, exact tests only, both sides with global
 // REDs.  Rare (strongly non-uniform systems); correctness path.
@@ -2879,6 +3272,7 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
     pair_cap_ = 2048;
     if (const char* e = std::getenv("ESP_PAIR_CAP")) pair_cap_ = std::max(256, std::min(4096, std::atoi(e) / 32 * 32));
     if (const char* e = std::getenv("ESP_PAIR_HALF")) half_mode_ = std::atoi(e);
+    if (const char* e = std::getenv("ESP_PAIR_TILE")) tile_mode_ = std::atoi(e);
     pencil_half_ = pencil_half_env() != 0;
 }
 
@@ -3197,6 +3591,7 @@ void Engine::run_pair(long N, cudaStream_t s, int rank, int nranks, bool own_bin
                                : !deterministic_ &&
                                      (half_mode_ == 2 || (half_mode_ == 1 && N >= kHalfMinN));
     if (half && run_pair_half(N, s, rank, nranks, own_bins)) return;
+    pair_kernel_ = cells_ok_ ? 0 : 3;
     if (half && own_bins)
         throw CudaError("distributed FFT: half-shell pair kernel could not be configured");
     PairArgs a{};
@@ -3335,7 +3730,8 @@ bool Engine::run_pair_half(long N, cudaStream_t s, int rank, int nranks, bool ow
     double best_t = -1.0;
     const long want_blocks = 2L * 3 * sms;  // 3 CTAs per SM, 2 waves
     int cap_max = 4096;
-    if (const char* e = std::getenv("ESP_HALF_CAP")) cap_max = std::max(256, std::min(8192, std::atoi(e) / 32 * 32));
+    const char* cap_env = std::getenv("ESP_HALF_CAP");  // tests: force the overflow kernel
+    if (cap_env) cap_max = std::max(256, std::min(8192, std::atoi(cap_env) / 32 * 32));
     for (int bx = 1; bx <= kHalfMaxBX; ++bx)
         for (int bz : {2, 3, 4, 6, 8}) {
             if (F_[0] < bx + 2 * M || F_[1] < bx + 2 * M || F_[2] < bz + 2 * Mz) continue;
@@ -3367,7 +3763,7 @@ bool Engine::run_pair_half(long N, cudaStream_t s, int rank, int nranks, bool ow
             best_bz = bz;
         }
     }
-    if (best_bx == 0 && own_bins) {
+    if (best_bx == 0 && (own_bins || cap_env)) {
         // distributed FFT: never fall back to full lists (see run_pair); the
         // smallest block always fits the period when cells_ok_, and blocks
         // whose neighbourhood exceeds the staging capacity go to the overflow
@@ -3438,6 +3834,11 @@ bool Engine::run_pair_half(long N, cudaStream_t s, int rank, int nranks, bool ow
                 kHalfWarps * a.lcap * sizeof(unsigned short);
     sm = (sm + 3) / 4 * 4 + (2 * a.nent_max + 1) * sizeof(int) + a.nent_max;
     const int ovf_grid = 2 * sms;
+    // cluster-pair kernel: measured faster at ~200 in-range pairs per atom
+    // (cfg4: 1.69 vs 1.76 ms), slower at ~400 (cfg5: 20.5 vs 20.1 ms), where
+    // the per-target search work it amortises is a smaller share
+    const bool tile = tile_mode_ == 1 || (tile_mode_ < 0 && col_div_ == 2);
+    pair_kernel_ = (!own_bins && tile) ? 2 : 1;
     auto go = [&](auto kern, auto ovfk) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(sm)));
@@ -3450,14 +3851,14 @@ bool Engine::run_pair_half(long N, cudaStream_t s, int rank, int nranks, bool ow
         CK(cudaGetLastError());
     };
     switch (nd) {
-        case 14: own_bins ? go(k_pair_half<14, true>, k_pair_half_ovf<14>) : go(k_pair_half<14, false>, k_pair_half_ovf<14>); break;
-        case 15: own_bins ? go(k_pair_half<15, true>, k_pair_half_ovf<15>) : go(k_pair_half<15, false>, k_pair_half_ovf<15>); break;
-        case 16: own_bins ? go(k_pair_half<16, true>, k_pair_half_ovf<16>) : go(k_pair_half<16, false>, k_pair_half_ovf<16>); break;
-        case 17: own_bins ? go(k_pair_half<17, true>, k_pair_half_ovf<17>) : go(k_pair_half<17, false>, k_pair_half_ovf<17>); break;
-        case 18: own_bins ? go(k_pair_half<18, true>, k_pair_half_ovf<18>) : go(k_pair_half<18, false>, k_pair_half_ovf<18>); break;
-        case 20: own_bins ? go(k_pair_half<20, true>, k_pair_half_ovf<20>) : go(k_pair_half<20, false>, k_pair_half_ovf<20>); break;
-        case 28: own_bins ? go(k_pair_half<28, true>, k_pair_half_ovf<28>) : go(k_pair_half<28, false>, k_pair_half_ovf<28>); break;
-        default: own_bins ? go(k_pair_half<kMaxPoly, true>, k_pair_half_ovf<kMaxPoly>) : go(k_pair_half<kMaxPoly, false>, k_pair_half_ovf<kMaxPoly>); break;
+        case 14: own_bins ? go(k_pair_half<14, true>, k_pair_half_ovf<14>) : (tile ? go(k_pair_tile<14>, k_pair_half_ovf<14>) : go(k_pair_half<14, false>, k_pair_half_ovf<14>)); break;
+        case 15: own_bins ? go(k_pair_half<15, true>, k_pair_half_ovf<15>) : (tile ? go(k_pair_tile<15>, k_pair_half_ovf<15>) : go(k_pair_half<15, false>, k_pair_half_ovf<15>)); break;
+        case 16: own_bins ? go(k_pair_half<16, true>, k_pair_half_ovf<16>) : (tile ? go(k_pair_tile<16>, k_pair_half_ovf<16>) : go(k_pair_half<16, false>, k_pair_half_ovf<16>)); break;
+        case 17: own_bins ? go(k_pair_half<17, true>, k_pair_half_ovf<17>) : (tile ? go(k_pair_tile<17>, k_pair_half_ovf<17>) : go(k_pair_half<17, false>, k_pair_half_ovf<17>)); break;
+        case 18: own_bins ? go(k_pair_half<18, true>, k_pair_half_ovf<18>) : (tile ? go(k_pair_tile<18>, k_pair_half_ovf<18>) : go(k_pair_half<18, false>, k_pair_half_ovf<18>)); break;
+        case 20: own_bins ? go(k_pair_half<20, true>, k_pair_half_ovf<20>) : (tile ? go(k_pair_tile<20>, k_pair_half_ovf<20>) : go(k_pair_half<20, false>, k_pair_half_ovf<20>)); break;
+        case 28: own_bins ? go(k_pair_half<28, true>, k_pair_half_ovf<28>) : (tile ? go(k_pair_tile<28>, k_pair_half_ovf<28>) : go(k_pair_half<28, false>, k_pair_half_ovf<28>)); break;
+        default: own_bins ? go(k_pair_half<kMaxPoly, true>, k_pair_half_ovf<kMaxPoly>) : (tile ? go(k_pair_tile<kMaxPoly>, k_pair_half_ovf<kMaxPoly>) : go(k_pair_half<kMaxPoly, false>, k_pair_half_ovf<kMaxPoly>)); break;
     }
     launches_ += 3;
     return true;

@@ -166,6 +166,7 @@ public:
     // distributed-FFT K4 mode (fixed when the engine is built; see run_pair)
     bool pencil_half() const { return pencil_half_; }
     bool fused_xpass() const { return xpass_; }
+    int pair_kernel() const { return pair_kernel_; }
     // Deterministic mode: bitwise-identical results run to run for the same
     // inputs (stable sorts instead of atomic ranks, full-list K4 without
     // partner REDs, K1 tiles flushed by bin colours with plain adds); the
@@ -279,6 +280,8 @@ private:
     double density_hint_ = 0.0;        // set_density_hint
     bool pencil_half_ = true;           // distributed FFT with half-shell K4 (ESP_PENCIL_HALF=0: full
                                         // lists); local inputs return the ghost partner terms (dist.py)
+    int tile_mode_ = -1;                // cluster-pair K4 (k_pair_tile) on one GPU: -1 auto (col_div 2), 0 never, 1 always (ESP_PAIR_TILE)
+    int pair_kernel_ = -1;              // K4 kernel of the last launch (esp_plan_info.pair_kernel)
     int half_mode_ = 1;                 // half-shell K4: 0 never, 1 from kHalfMinN atoms, 2 always (ESP_PAIR_HALF)
 
     cufftHandle fwd_ = 0, inv_ = 0;

@@ -7,7 +7,9 @@ non-uniform / non-cubic systems.
 
 ESP_PAIR_HALF (read when a plan is built): 0 = full lists, 1 = half-shell from
 4096 atoms (default), 2 = half-shell always.  ESP_HALF_CAP (read per launch)
-bounds the staging capacity."""
+bounds the staging capacity (and forces the half-shell form with the
+smallest block, so that the overflow kernel runs).  ESP_PAIR_TILE=0 keeps the
+warp-per-target kernel where the cluster-pair one would be chosen."""
 import numpy as np
 import pytest
 
@@ -18,6 +20,7 @@ pytestmark = pytest.mark.gpu
 
 def _plan(esp, monkeypatch, mode, box, eps, r_c, gpu):
     monkeypatch.setenv("ESP_PAIR_HALF", str(mode))
+    monkeypatch.setenv("ESP_PAIR_TILE", "0")  # warp-per-target kernel (test_gpu_tile.py: clusters)
     return esp.build_plan(box, "pswf", eps, r_c, device=gpu)
 
 
@@ -31,6 +34,7 @@ def _compare_to_full(esp, monkeypatch, gpu, sysm, eps, r_c, tol=1e-12):
     lf, nf = _local(esp, full, sysm)
     half = _plan(esp, monkeypatch, 2, sysm.box, eps, r_c, gpu)
     lh, nh = _local(esp, half, sysm)
+    assert full.pair_kernel == "full" and half.pair_kernel == "half"
     assert nh == nf and nf > 0
     assert max_rel(lh.u, lf.u) <= tol
     assert rel_rms(lh.F, lf.F) <= tol
@@ -127,6 +131,7 @@ def test_half_gaussian_family(esp, gpu, monkeypatch):
     box = np.array([L, L, L])
     sysm = esp.ParticleSystem(box, q, pos)
     monkeypatch.setenv("ESP_PAIR_HALF", "0")
+    monkeypatch.setenv("ESP_PAIR_TILE", "0")
     full = esp.build_plan(box, "gaussian", 1e-4, 5.0, device=gpu)
     lf = esp.local_sum(full, sysm)
     nf = full.last_pair_count()
