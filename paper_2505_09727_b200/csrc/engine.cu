@@ -195,6 +195,7 @@ struct BinArgs {
     int* countB;
     int sub;             // sort sub-bins per spread-bin edge (keys per bin: sub^3)
     double* qsum;  // [2]
+    int write_tmp;       // keep the folded original-order copy (small systems, all-pairs, deterministic)
 };
 
 // Fold, keys and ranks.  A rank is the return value of an atomic on the
@@ -223,7 +224,7 @@ __global__ void __launch_bounds__(256) k_fold_bin(BinArgs a) {
             const double qi = a.q[i];
             s1 += qi;
             s2 += fabs(qi);
-            a.tmp[i] = make_double4(x, y, z, qi);
+            if (a.write_tmp) a.tmp[i] = make_double4(x, y, z, qi);
             // fine pair cell (the reference's coarse cell ewald.hpp:479-482 split
             // into fine columns and slices); nc = fine cells per dim here
             const int cx = clampi(static_cast<int>(x / a.cw[0]), 0, a.nc[0] - 1);
@@ -341,26 +342,63 @@ __global__ void __launch_bounds__(1024) k_scan_small(int* countA, int* startA, i
     if (blockIdx.x == 0 && threadIdx.x == 0) *npairs = 0ull;
 }
 
+// Counting-sort scatter, in two passes.  The index arrays (orig) take 4-byte
+// writes at random positions: issued together with the 32-byte xyzq records,
+// their partially written sectors were evicted from L2 by the record stream
+// and merged in DRAM (read-modify-write: 0.32 of 0.68 ms at cfg5).  Alone,
+// both index arrays (8 bytes per atom) stay L2-resident until every sector
+// is complete; the records are full sectors either way.
+__device__ __forceinline__ void scatter_dest(long i, const int* __restrict__ cellA,
+                                             const int* __restrict__ rankA,
+                                             const int* __restrict__ startA,
+                                             const int* __restrict__ cellB,
+                                             const int* __restrict__ rankB,
+                                             const int* __restrict__ startB, int& da, int& db) {
+    da = startA[cellA[i]] + rankA[i];
+    db = startB[cellB[i]] + rankB[i];
+}
+
+__global__ void __launch_bounds__(256) k_scatter_orig(long N, const int* __restrict__ cellA,
+                                                      const int* __restrict__ rankA,
+                                                      const int* __restrict__ startA,
+                                                      int* __restrict__ origA,
+                                                      const int* __restrict__ cellB,
+                                                      const int* __restrict__ rankB,
+                                                      const int* __restrict__ startB,
+                                                      int* __restrict__ origB) {
+    const long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+    if (i >= N) return;
+    int da, db;
+    scatter_dest(i, cellA, rankA, startA, cellB, rankB, startB, da, db);
+    ESP_DCHECK(da >= 0 && da < N && db >= 0 && db < N);
+    origA[da] = static_cast<int>(i);
+    origB[db] = static_cast<int>(i);
+}
+
+// The records come from the folded copy (tmp) or, for large systems, are
+// folded again from the caller's positions (fold1, bitwise the same values as
+// k_fold_bin's): the 32-byte copy is then neither written nor read back.
 __global__ void __launch_bounds__(256) k_scatter(long N, const double4* __restrict__ tmp,
+                                                 const double* __restrict__ pos,
+                                                 const double* __restrict__ q, double3 box,
                                                  const int* __restrict__ cellA,
                                                  const int* __restrict__ rankA,
                                                  const int* __restrict__ startA,
-                                                 double4* __restrict__ xyzqA, int* __restrict__ origA,
+                                                 double4* __restrict__ xyzqA,
                                                  const int* __restrict__ cellB,
                                                  const int* __restrict__ rankB,
                                                  const int* __restrict__ startB,
-                                                 double4* __restrict__ xyzqB, int* __restrict__ origB) {
-    long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+                                                 double4* __restrict__ xyzqB) {
+    const long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
     if (i >= N) return;
-    double4 v = tmp[i];
-    int da = startA[cellA[i]] + rankA[i];
-    ESP_DCHECK(da >= 0 && da < N);
+    const double4 v = tmp ? tmp[i]
+                          : make_double4(fold1(pos[3 * i + 0], box.x), fold1(pos[3 * i + 1], box.y),
+                                         fold1(pos[3 * i + 2], box.z), q[i]);
+    int da, db;
+    scatter_dest(i, cellA, rankA, startA, cellB, rankB, startB, da, db);
+    ESP_DCHECK(da >= 0 && da < N && db >= 0 && db < N);
     xyzqA[da] = v;
-    origA[da] = static_cast<int>(i);
-    int db = startB[cellB[i]] + rankB[i];
-    ESP_DCHECK(db >= 0 && db < N);
     xyzqB[db] = v;
-    origB[db] = static_cast<int>(i);
 }
 
 // deterministic mode: sorted position k takes atom perm[k] (a stable radix
@@ -2700,6 +2738,7 @@ __global__ void __launch_bounds__(128) k_interp8(GridArgs g, InterpArgs a) {
 // partial sums of q u feed the energy.
 __global__ void __launch_bounds__(256) k_combine(long N, const double4* __restrict__ loc,
                                                  const double4* __restrict__ xyzq_orig,
+                                                 const double* __restrict__ qv,
                                                  const double4* __restrict__ spec,
                                                  double* __restrict__ u,
                                                  double* __restrict__ F, double* __restrict__ epart,
@@ -2711,7 +2750,7 @@ __global__ void __launch_bounds__(256) k_combine(long N, const double4* __restri
     double e = 0.0;
     if (i < N) {
         const double4 l = loc[i];
-        const double qi = xyzq_orig[i].w;
+        const double qi = xyzq_orig ? xyzq_orig[i].w : qv[i];
         // spectral part u_s - q s0 (self folded in K3) and F_s: from spec if
         // set, else from u / F
         const double4 sp = spec ? spec[i] : make_double4(u[i], F[3 * i + 0], F[3 * i + 1],
@@ -3437,7 +3476,7 @@ void Engine::ensure_capacity(long N) {
 }
 
 void Engine::prepare(long N, const double* pos, const double* q, double* qsum_dev,
-                     cudaStream_t s) {
+                     cudaStream_t s, bool lean) {
     // ESP_PREP_TIMING=1 (diagnostics, not under graph capture): event times of
     // the binning steps on stderr
     static const bool ptime = std::getenv("ESP_PREP_TIMING") != nullptr;
@@ -3480,6 +3519,14 @@ void Engine::prepare(long N, const double* pos, const double* q, double* qsum_de
     a.rankB = d_rankB_;
     a.countB = d_countB_;
     a.qsum = qsum_dev;
+    // the folded original-order copy: read by the all-pairs kernel, the
+    // deterministic gathers, the phase entry points (whose inputs need not
+    // outlive the call) and, for small systems (zero-copy host inputs), the
+    // combine; a large single-call evaluation (lean) re-folds in the scatter
+    // and the combine reads q directly
+    tmp_written_ = !lean || deterministic_ || !cells_ok_ || N < kFoldILPMinN;
+    a.write_tmp = tmp_written_ ? 1 : 0;
+    prep_q_ = q;
     if (N > 0) {
         if (N >= kFoldILPMinN)
             k_fold_bin<4><<<grid1(N, 256 * 4), 256, 0, s>>>(a);
@@ -3532,11 +3579,14 @@ void Engine::prepare(long N, const double* pos, const double* q, double* qsum_de
         CK(cudaGetLastError());
         launches_ += 5;
     } else if (N > 0) {
-        k_scatter<<<grid1(N, 256), 256, 0, s>>>(N, d_tmp_, d_cellA_, d_rankA_, d_startA_, d_xyzqA_,
-                                                 d_origA_, d_cellB_, d_rankB_, d_startB_, d_xyzqB_,
-                                                 d_origB_);
+        k_scatter_orig<<<grid1(N, 256), 256, 0, s>>>(N, d_cellA_, d_rankA_, d_startA_, d_origA_,
+                                                      d_cellB_, d_rankB_, d_startB_, d_origB_);
         CK(cudaGetLastError());
-        ++launches_;
+        k_scatter<<<grid1(N, 256), 256, 0, s>>>(
+            N, tmp_written_ ? d_tmp_ : nullptr, pos, q, make_double3(p.box[0], p.box[1], p.box[2]),
+            d_cellA_, d_rankA_, d_startA_, d_xyzqA_, d_cellB_, d_rankB_, d_startB_, d_xyzqB_);
+        CK(cudaGetLastError());
+        launches_ += 2;
     }
     mark();
     if (ptime) {
@@ -3996,7 +4046,8 @@ void Engine::finish(long N, int rank, int nranks, const double* fields, const Gr
     }
     const int nblk = static_cast<int>(grid1(std::max<long>(N, 1), 256));
     if (N > 0) {
-        k_combine<<<nblk, 256, 0, s>>>(N, d_loc_, d_tmp_, nullptr, u, F, d_epart_, nullptr,
+        k_combine<<<nblk, 256, 0, s>>>(N, d_loc_, tmp_written_ ? d_tmp_ : nullptr, prep_q_,
+                                       nullptr, u, F, d_epart_, nullptr,
                                        nullptr);
         CK(cudaGetLastError());
         k_energy<<<1, 256, 0, s>>>(d_epart_, nblk, energy_dev);
@@ -4297,7 +4348,7 @@ void Engine::enqueue(long N, const double* pos, const double* q, double* u, doub
     if (t) {
         // serialised on the caller's stream so that each stage is timed alone
         CK(cudaEventRecord(ev_t_[0], s));
-        prepare(N, pos, q, qsum_dev, s);
+        prepare(N, pos, q, qsum_dev, s, true);
         CK(cudaEventRecord(ev_t_[1], s));
         run_pair(N, s, 0, 1);
         CK(cudaEventRecord(ev_t_[2], s));
@@ -4310,7 +4361,7 @@ void Engine::enqueue(long N, const double* pos, const double* q, double* u, doub
     } else {
         // K4 on the caller's stream overlaps the whole grid pipeline (K1, FFT,
         // K2, inverse FFT, K3) on aux_; the combine joins them
-        prepare(N, pos, q, qsum_dev, s);
+        prepare(N, pos, q, qsum_dev, s, true);
         cudaStream_t aux = N <= kHighPriorityMaxN ? aux_hi_ : aux_;
         CK(cudaEventRecord(ev_fork_, s));
         CK(cudaStreamWaitEvent(aux, ev_fork_, 0));
@@ -4327,7 +4378,8 @@ void Engine::enqueue(long N, const double* pos, const double* q, double* u, doub
     }
     const int nblk = static_cast<int>(grid1(std::max<long>(N, 1), 256));
     if (N > 0) {
-        k_combine<<<nblk, 256, 0, s>>>(N, d_loc_, d_tmp_, d_specres_, u, F, d_epart_, u_out,
+        k_combine<<<nblk, 256, 0, s>>>(N, d_loc_, tmp_written_ ? d_tmp_ : nullptr, prep_q_,
+                                       d_specres_, u, F, d_epart_, u_out,
                                        F_out);
         CK(cudaGetLastError());
         ++launches_;

@@ -192,7 +192,8 @@ private:
     void set_cells(int col_div);
     void alloc_cells();
     void alloc_bins(int sub);
-    void prepare(long N, const double* pos, const double* q, double* qsum_dev, cudaStream_t s);
+    void prepare(long N, const double* pos, const double* q, double* qsum_dev, cudaStream_t s,
+                 bool lean = false);
     void run_pair(long N, cudaStream_t s, int rank, int nranks, bool own_bins = false);
     bool run_pair_half(long N, cudaStream_t s, int rank = 0, int nranks = 1, bool own_bins = false);
     void run_grid(long N, cudaStream_t s, StageTimes* t);
@@ -281,6 +282,8 @@ private:
     bool pencil_half_ = true;           // distributed FFT with half-shell K4 (ESP_PENCIL_HALF=0: full
                                         // lists); local inputs return the ghost partner terms (dist.py)
     int tile_mode_ = -1;                // cluster-pair K4 (k_pair_tile) on one GPU: -1 auto (col_div 2), 0 never, 1 always (ESP_PAIR_TILE)
+    bool tmp_written_ = true;           // prepare() wrote the folded original-order copy d_tmp_
+    const double* prep_q_ = nullptr;    // charges of the last prepare() (combine reads them when !tmp_written_)
     int pair_kernel_ = -1;              // K4 kernel of the last launch (esp_plan_info.pair_kernel)
     int half_mode_ = 1;                 // half-shell K4: 0 never, 1 from kHalfMinN atoms, 2 always (ESP_PAIR_HALF)
 
