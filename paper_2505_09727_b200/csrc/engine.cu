@@ -1095,7 +1095,18 @@ __device__ __forceinline__ void fwd_col(int l, int M, int& dx, int& dy) {
 
 // OWN: distributed-FFT instantiation (plane-ownership targets, position-based
 // same-cell base); the single-GPU one carries none of those checks.
-template <int ND, bool OWN>
+//
+// TWO (two-phase targets, round 2): instead of flushing a 64-entry queue from
+// inside the screening loop, a target's whole candidate list piece is screened
+// first -- 64 candidates per iteration, no flush branch, the survivors
+// compacted IN PLACE over the list (the write position never passes the chunk
+// being read: lw[0, 32) is the carry zone, the list piece starts at lw + 32)
+// -- and then evaluated in a tight loop of fp64 rounds (operands of the next
+// round fetched before the current one is evaluated; the last round of the
+// target is the only partial one and is predicated, so the pair terms are
+// inlined once instead of three times).  Survivors that do not fill a round at
+// the end of a non-final piece are carried to the next piece.
+template <int ND, bool OWN, bool TWO>
 __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const __grid_constant__ PairConsts k) {
     extern __shared__ __align__(16) unsigned char smem[];
     float4* cand = reinterpret_cast<float4*>(smem);                 // a.cap + 1 (sentinel)
@@ -1324,6 +1335,83 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
         bool have_pf = false;
         double4 pf = make_double4(0.0, 0.0, 0.0, 0.0);
         int tf = 13, sf = 0;
+        if constexpr (TWO) {
+            const int piece = (a.lcap - 32) & ~63;
+            unsigned short* lin = lw + 32;
+            for (int lb = 0; lb < T; lb += piece) {
+                const int le = min(T, lb + piece);
+                fill_range(lin, lb, max(inc - cnt, lb), min(inc, le), beg - (inc - cnt));
+                const int n = le - lb;
+                const int n64 = (n + 63) & ~63;
+                ESP_DCHECK(32 + n64 <= a.lcap);
+                if (n + lane < n64) lin[n + lane] = static_cast<unsigned short>(a.cap);
+                if (n + 32 + lane < n64) lin[n + 32 + lane] = static_cast<unsigned short>(a.cap);
+                __syncwarp();
+                // phase 1: screen 64 candidates per iteration, compact in place
+                for (const unsigned short* lp = lin + lane; lp < lin + n64; lp += 64) {
+                    const int s0 = lp[0], s1 = lp[32];
+                    ESP_DCHECK(s0 <= a.cap && s1 <= a.cap);
+                    const float4 a0 = cand[s0], a1 = cand[s1];
+                    const float dx0 = a0.x - xf, dy0 = a0.y - yf, dz0 = a0.z - zf;
+                    const float dx1 = a1.x - xf, dy1 = a1.y - yf, dz1 = a1.z - zf;
+                    const bool in0 = fmaf(dz0, dz0, fmaf(dy0, dy0, dx0 * dx0)) < R2;
+                    const bool in1 = fmaf(dz1, dz1, fmaf(dy1, dy1, dx1 * dx1)) < R2;
+                    const unsigned m0 = __ballot_sync(0xffffffffu, in0);
+                    const unsigned m1 = __ballot_sync(0xffffffffu, in1);
+                    const int q1 = qn + __popc(m0);
+                    if (in0) lw[qn + __popc(m0 & lt_mask)] = static_cast<unsigned short>(s0);
+                    if (in1) lw[q1 + __popc(m1 & lt_mask)] = static_cast<unsigned short>(s1);
+                    qn = q1 + __popc(m1);
+                }
+                __syncwarp();
+                // phase 2: fp64 rounds over lw[0, qn); the partial round only
+                // at the end of the target
+                const bool last = le == T;
+                const int nr = last ? (qn + 31) >> 5 : qn >> 5;
+                if (nr > 0) {
+                    double4 pn;
+                    int tn, sn;
+                    {
+                        const int cd = __float_as_int(cand[lw[min(lane, qn - 1)]].w);
+                        sn = cd & 0x7ffffff;
+                        tn = static_cast<unsigned>(cd) >> 27;
+                        pn = a.xyzq[sn];
+                    }
+                    for (int r = 0; r < nr; ++r) {
+                        const double4 pj = pn;
+                        const int tj = tn, sj = sn;
+                        const bool valid = r * 32 + lane < qn;
+                        if (r + 1 < nr) {
+                            const int cd = __float_as_int(cand[lw[min(r * 32 + 32 + lane, qn - 1)]].w);
+                            ESP_DCHECK((cd & 0x7ffffff) < a.nacc && (static_cast<unsigned>(cd) >> 27) < 27);
+                            sn = cd & 0x7ffffff;
+                            tn = static_cast<unsigned>(cd) >> 27;
+                            pn = a.xyzq[sn];
+                        }
+                        double4 g;
+                        const bool same = OWN && sj >= cs && sj < ce;
+                        if (valid && (!same || pos_after(pj, pi)) &&
+                            (wrap ? pair_eval3<ND, true>(k, pj, shiftv[tj][0], shiftv[tj][1],
+                                                         shiftv[tj][2], pi.x, pi.y, pi.z, pi.w,
+                                                         u, fx, fy, fz, g)
+                                  : pair_eval3<ND, false>(k, pj, 0.0, 0.0, 0.0, pi.x, pi.y, pi.z,
+                                                          pi.w, u, fx, fy, fz, g))) {
+                            ++npair;
+                            red_acc(a.acc, a.nacc, sj, g.x, g.y, g.z, g.w);
+                        }
+                    }
+                }
+                if (!last) {
+                    // carry the survivors that do not fill a round
+                    const int rem = qn & 31;
+                    const unsigned short v = lw[(qn & ~31) + (lane < rem ? lane : 0)];
+                    __syncwarp();
+                    if (lane < rem) lw[lane] = v;
+                    qn = rem;
+                }
+                __syncwarp();
+            }
+        } else {
         for (int lb = 0; lb < T; lb += a.lcap - 32) {
             const int le = min(T, lb + a.lcap - 32);
             {
@@ -1405,6 +1493,7 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
                 red_acc(a.acc, a.nacc, cd & 0x7ffffff, g.x, g.y, g.z, g.w);
             }
         }
+        }  // !TWO
         __syncwarp();
         {
             const bool h16 = lane & 16, h8 = lane & 8;
@@ -3312,6 +3401,7 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
     if (const char* e = std::getenv("ESP_PAIR_CAP")) pair_cap_ = std::max(256, std::min(4096, std::atoi(e) / 32 * 32));
     if (const char* e = std::getenv("ESP_PAIR_HALF")) half_mode_ = std::atoi(e);
     if (const char* e = std::getenv("ESP_PAIR_TILE")) tile_mode_ = std::atoi(e);
+    if (const char* e = std::getenv("ESP_PAIR_PHASED")) phased_mode_ = std::atoi(e);
     pencil_half_ = pencil_half_env() != 0;
 }
 
@@ -3888,6 +3978,7 @@ bool Engine::run_pair_half(long N, cudaStream_t s, int rank, int nranks, bool ow
     // (cfg4: 1.69 vs 1.76 ms), slower at ~400 (cfg5: 20.5 vs 20.1 ms), where
     // the per-target search work it amortises is a smaller share
     const bool tile = tile_mode_ == 1 || (tile_mode_ < 0 && col_div_ == 2);
+    const bool phased = phased_mode_ != 0;
     pair_kernel_ = (!own_bins && tile) ? 2 : 1;
     auto go = [&](auto kern, auto ovfk) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -3900,16 +3991,23 @@ bool Engine::run_pair_half(long N, cudaStream_t s, int rank, int nranks, bool ow
         k_acc_to_loc<<<grid1(N, 256), 256, 0, s>>>(N, d_acc_, d_origA_, d_loc_);
         CK(cudaGetLastError());
     };
+#define ESP_HALF_CASE(D)                                                                  \
+    (own_bins ? (phased ? go(k_pair_half<D, true, true>, k_pair_half_ovf<D>)                \
+                        : go(k_pair_half<D, true, false>, k_pair_half_ovf<D>))              \
+              : (tile ? go(k_pair_tile<D>, k_pair_half_ovf<D>)                              \
+                      : (phased ? go(k_pair_half<D, false, true>, k_pair_half_ovf<D>)       \
+                                : go(k_pair_half<D, false, false>, k_pair_half_ovf<D>))))
     switch (nd) {
-        case 14: own_bins ? go(k_pair_half<14, true>, k_pair_half_ovf<14>) : (tile ? go(k_pair_tile<14>, k_pair_half_ovf<14>) : go(k_pair_half<14, false>, k_pair_half_ovf<14>)); break;
-        case 15: own_bins ? go(k_pair_half<15, true>, k_pair_half_ovf<15>) : (tile ? go(k_pair_tile<15>, k_pair_half_ovf<15>) : go(k_pair_half<15, false>, k_pair_half_ovf<15>)); break;
-        case 16: own_bins ? go(k_pair_half<16, true>, k_pair_half_ovf<16>) : (tile ? go(k_pair_tile<16>, k_pair_half_ovf<16>) : go(k_pair_half<16, false>, k_pair_half_ovf<16>)); break;
-        case 17: own_bins ? go(k_pair_half<17, true>, k_pair_half_ovf<17>) : (tile ? go(k_pair_tile<17>, k_pair_half_ovf<17>) : go(k_pair_half<17, false>, k_pair_half_ovf<17>)); break;
-        case 18: own_bins ? go(k_pair_half<18, true>, k_pair_half_ovf<18>) : (tile ? go(k_pair_tile<18>, k_pair_half_ovf<18>) : go(k_pair_half<18, false>, k_pair_half_ovf<18>)); break;
-        case 20: own_bins ? go(k_pair_half<20, true>, k_pair_half_ovf<20>) : (tile ? go(k_pair_tile<20>, k_pair_half_ovf<20>) : go(k_pair_half<20, false>, k_pair_half_ovf<20>)); break;
-        case 28: own_bins ? go(k_pair_half<28, true>, k_pair_half_ovf<28>) : (tile ? go(k_pair_tile<28>, k_pair_half_ovf<28>) : go(k_pair_half<28, false>, k_pair_half_ovf<28>)); break;
-        default: own_bins ? go(k_pair_half<kMaxPoly, true>, k_pair_half_ovf<kMaxPoly>) : (tile ? go(k_pair_tile<kMaxPoly>, k_pair_half_ovf<kMaxPoly>) : go(k_pair_half<kMaxPoly, false>, k_pair_half_ovf<kMaxPoly>)); break;
+        case 14: ESP_HALF_CASE(14); break;
+        case 15: ESP_HALF_CASE(15); break;
+        case 16: ESP_HALF_CASE(16); break;
+        case 17: ESP_HALF_CASE(17); break;
+        case 18: ESP_HALF_CASE(18); break;
+        case 20: ESP_HALF_CASE(20); break;
+        case 28: ESP_HALF_CASE(28); break;
+        default: ESP_HALF_CASE(kMaxPoly); break;
     }
+#undef ESP_HALF_CASE
     launches_ += 3;
     return true;
 }
