@@ -38,6 +38,9 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 # build.py --checked): a diagnostics variant of the same library
 LIB_PATH = os.path.join(_PKG, "libesp_b200_checked.so" if os.environ.get("ESP_B200_CHECKED") == "1"
                         else "libesp_b200.so")
+# experiments: an A/B build made by `build.py --variant NAME -D...`
+if os.environ.get("ESP_B200_LIB"):
+    LIB_PATH = os.path.join(_PKG, os.environ["ESP_B200_LIB"])
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

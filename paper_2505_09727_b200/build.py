@@ -36,8 +36,14 @@ def _newest_header() -> float:
     return max(os.path.getmtime(os.path.join(CSRC, h)) for h in HEADERS)
 
 
+VARIANT = None   # experiments: --variant NAME -DX=Y ... -> libesp_b200_NAME.so (ESP_B200_LIB loads it)
+DEFINES: list = []
+
+
 def _paths(checked: bool):
     """(object directory, library) of the product or the checked build."""
+    if VARIANT:
+        return BUILD + "_" + VARIANT, os.path.join(PKG, f"libesp_b200_{VARIANT}.so")
     if checked:
         return BUILD + "_checked", os.path.join(PKG, "libesp_b200_checked.so")
     return BUILD, LIB
@@ -49,7 +55,7 @@ def _compile(src: str, checked: bool = False) -> str:
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(path),
                                                             _newest_header()):
         return obj
-    cmd = [NVCC, *ARCH, *COMMON, "-c", path, "-o", obj]
+    cmd = [NVCC, *ARCH, *COMMON, *DEFINES, "-c", path, "-o", obj]
     if checked:
         cmd += ["-DESP_DEVICE_CHECKS"]
     if src.endswith(".cu"):
@@ -89,4 +95,7 @@ def build(force: bool = False, verbose: bool = True, checked: bool = False) -> s
 
 
 if __name__ == "__main__":
+    if "--variant" in sys.argv:
+        VARIANT = sys.argv[sys.argv.index("--variant") + 1]
+        DEFINES = [a for a in sys.argv if a.startswith("-D")]
     build(force="--force" in sys.argv, checked="--checked" in sys.argv)

@@ -942,6 +942,15 @@ struct HalfArgs {
     double box[3];
 };
 
+#ifndef ESP_K4_P2
+#define ESP_K4_P2 1  // rounds loop of the two-phase targets: 0 no prefetch, 1 one round ahead, 2 ping-pong x2
+#endif
+#ifndef ESP_K4_ABLATE
+#define ESP_K4_ABLATE 0  // timing builds (wrong results): 1 staging only, 2 + target setup and list fill, 3 + screening, 4 all but the partner REDs
+#endif
+#ifndef ESP_K4_MINB
+#define ESP_K4_MINB 3  // resident CTAs per SM k_pair_half is compiled for (80 registers)
+#endif
 constexpr int kHalfMaxBX = 4;
 constexpr int kHalfWarps = 8;
 constexpr int kHalfThreads = 32 * kHalfWarps;
@@ -1107,11 +1116,12 @@ __device__ __forceinline__ void fwd_col(int l, int M, int& dx, int& dy) {
 // inlined once instead of three times).  Survivors that do not fill a round at
 // the end of a non-final piece are carried to the next piece.
 template <int ND, bool OWN, bool TWO>
-__global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const __grid_constant__ PairConsts k) {
+__global__ void __launch_bounds__(kHalfThreads, ESP_K4_MINB) k_pair_half(HalfArgs a, const __grid_constant__ PairConsts k) {
     extern __shared__ __align__(16) unsigned char smem[];
     float4* cand = reinterpret_cast<float4*>(smem);                 // a.cap + 1 (sentinel)
-    int* qall = reinterpret_cast<int*>(cand + a.cap + 1);           // 64 per warp
-    unsigned short* lall = reinterpret_cast<unsigned short*>(qall + kHalfWarps * 64);
+    constexpr int kQueue = TWO ? 0 : 64;  // the two-phase targets compact in place: no queue
+    int* qall = reinterpret_cast<int*>(cand + a.cap + 1);           // kQueue per warp
+    unsigned short* lall = reinterpret_cast<unsigned short*>(qall + kHalfWarps * kQueue);
     int* ent_src = reinterpret_cast<int*>(lall + kHalfWarps * a.lcap);
     int* ent_off = ent_src + a.nent_max;                            // nent_max + 1
     unsigned char* ent_slot = reinterpret_cast<unsigned char*>(ent_off + a.nent_max + 1);
@@ -1122,7 +1132,7 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
     __shared__ int fwdc[64];  // l -> forward column (l mod nfc): dx | (dy + M) << 4 | own << 8
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int* qw = qall + warp * 64;
+    int* qw = qall + warp * kQueue;
     unsigned short* lw = lall + warp * a.lcap;
     const unsigned lt_mask = (1u << lane) - 1u;
 
@@ -1255,6 +1265,7 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
         if (threadIdx.x == 0) cand[a.cap] = make_float4(1e30f, 1e30f, 1e30f, __int_as_float(0));
     }
     __syncthreads();
+    if (ESP_K4_ABLATE == 1) return;
     const int ntc = bxe * bye;
     const int ni = tpre[ntc];
     const float R2 = k.rc2_test;
@@ -1336,17 +1347,18 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
         double4 pf = make_double4(0.0, 0.0, 0.0, 0.0);
         int tf = 13, sf = 0;
         if constexpr (TWO) {
-            const int piece = (a.lcap - 32) & ~63;
+            const int piece = (a.lcap - 128) & ~63;  // carry zone + padding rounds
             unsigned short* lin = lw + 32;
             for (int lb = 0; lb < T; lb += piece) {
                 const int le = min(T, lb + piece);
                 fill_range(lin, lb, max(inc - cnt, lb), min(inc, le), beg - (inc - cnt));
                 const int n = le - lb;
                 const int n64 = (n + 63) & ~63;
-                ESP_DCHECK(32 + n64 <= a.lcap);
+                ESP_DCHECK(32 + n64 + 96 <= a.lcap);
                 if (n + lane < n64) lin[n + lane] = static_cast<unsigned short>(a.cap);
                 if (n + 32 + lane < n64) lin[n + 32 + lane] = static_cast<unsigned short>(a.cap);
                 __syncwarp();
+                if (ESP_K4_ABLATE == 2) continue;
                 // phase 1: screen 64 candidates per iteration, compact in place
                 for (const unsigned short* lp = lin + lane; lp < lin + n64; lp += 64) {
                     const int s0 = lp[0], s1 = lp[32];
@@ -1364,49 +1376,83 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_half(HalfArgs a, const
                     qn = q1 + __popc(m1);
                 }
                 __syncwarp();
-                // phase 2: fp64 rounds over lw[0, qn); the partial round only
-                // at the end of the target
+                if (ESP_K4_ABLATE == 3) { u += qn; qn = 0; continue; }
+                // phase 2: fp64 rounds over lw[0, qn).  The list is padded
+                // with the target's own staged index (r = 0: rejected by the
+                // range test), so no round needs a validity predicate or a
+                // clamped index, and the loop may fetch up to two rounds past
+                // the end.  Two rounds per iteration with ping-pong operands
+                // (the next round's loads are issued before a round is
+                // evaluated; no register copies).  The partial round only at
+                // the end of the target: survivors that do not fill a round
+                // of a non-final piece are carried to the next piece.
                 const bool last = le == T;
                 const int nr = last ? (qn + 31) >> 5 : qn >> 5;
+                const int qe = last ? qn : (qn & ~31);
+                const int rem = qn - qe;
+                const unsigned short carry = lw[qe + (lane < rem ? lane : 0)];
+                __syncwarp();
+                ESP_DCHECK(qe + 96 <= a.lcap);
+                lw[qe + lane] = static_cast<unsigned short>(si);
+                lw[qe + 32 + lane] = static_cast<unsigned short>(si);
+                lw[qe + 64 + lane] = static_cast<unsigned short>(si);
+                __syncwarp();
                 if (nr > 0) {
-                    double4 pn;
-                    int tn, sn;
-                    {
-                        const int cd = __float_as_int(cand[lw[min(lane, qn - 1)]].w);
-                        sn = cd & 0x7ffffff;
-                        tn = static_cast<unsigned>(cd) >> 27;
-                        pn = a.xyzq[sn];
-                    }
-                    for (int r = 0; r < nr; ++r) {
-                        const double4 pj = pn;
-                        const int tj = tn, sj = sn;
-                        const bool valid = r * 32 + lane < qn;
-                        if (r + 1 < nr) {
-                            const int cd = __float_as_int(cand[lw[min(r * 32 + 32 + lane, qn - 1)]].w);
-                            ESP_DCHECK((cd & 0x7ffffff) < a.nacc && (static_cast<unsigned>(cd) >> 27) < 27);
-                            sn = cd & 0x7ffffff;
-                            tn = static_cast<unsigned>(cd) >> 27;
-                            pn = a.xyzq[sn];
-                        }
+                    auto fetch = [&](const unsigned short* lp, double4& p, int& t, int& sj) {
+                        const int cd = __float_as_int(cand[*lp].w);
+                        ESP_DCHECK((cd & 0x7ffffff) < a.nacc && (static_cast<unsigned>(cd) >> 27) < 27);
+                        sj = cd & 0x7ffffff;
+                        t = static_cast<unsigned>(cd) >> 27;
+                        p = a.xyzq[sj];
+                    };
+                    auto evalr = [&](const double4& pj, int tj, int sj) {
                         double4 g;
                         const bool same = OWN && sj >= cs && sj < ce;
-                        if (valid && (!same || pos_after(pj, pi)) &&
+                        if ((!same || pos_after(pj, pi)) &&
                             (wrap ? pair_eval3<ND, true>(k, pj, shiftv[tj][0], shiftv[tj][1],
                                                          shiftv[tj][2], pi.x, pi.y, pi.z, pi.w,
                                                          u, fx, fy, fz, g)
                                   : pair_eval3<ND, false>(k, pj, 0.0, 0.0, 0.0, pi.x, pi.y, pi.z,
                                                           pi.w, u, fx, fy, fz, g))) {
                             ++npair;
+                            if (ESP_K4_ABLATE == 4) { u += g.x + g.y + g.z + g.w; } else
                             red_acc(a.acc, a.nacc, sj, g.x, g.y, g.z, g.w);
                         }
+                    };
+                    const unsigned short* lp = lw + lane;
+                    const unsigned short* lend = lp + 32 * nr;
+#if ESP_K4_P2 == 2
+                    double4 pa, pb;
+                    int ta, tb, sa, sb;
+                    fetch(lp, pa, ta, sa);
+                    for (; lp < lend; lp += 64) {
+                        fetch(lp + 32, pb, tb, sb);
+                        evalr(pa, ta, sa);
+                        fetch(lp + 64, pa, ta, sa);
+                        evalr(pb, tb, sb);
                     }
+#elif ESP_K4_P2 == 1
+                    double4 pn;
+                    int tn, sn;
+                    fetch(lp, pn, tn, sn);
+                    for (; lp < lend; lp += 32) {
+                        const double4 pj = pn;
+                        const int tj = tn, sj = sn;
+                        fetch(lp + 32, pn, tn, sn);
+                        evalr(pj, tj, sj);
+                    }
+#else
+                    for (; lp < lend; lp += 32) {
+                        double4 pj;
+                        int tj, sj;
+                        fetch(lp, pj, tj, sj);
+                        evalr(pj, tj, sj);
+                    }
+#endif
                 }
+                __syncwarp();
                 if (!last) {
-                    // carry the survivors that do not fill a round
-                    const int rem = qn & 31;
-                    const unsigned short v = lw[(qn & ~31) + (lane < rem ? lane : 0)];
-                    __syncwarp();
-                    if (lane < rem) lw[lane] = v;
+                    if (lane < rem) lw[lane] = carry;
                     qn = rem;
                 }
                 __syncwarp();
@@ -3939,7 +3985,7 @@ bool Engine::run_pair_half(long N, cudaStream_t s, int rank, int nranks, bool ow
         const double cand = ppa * (col_div_ == 3 ? 1.8 : 2.2) * 0.6;
         int l = std::max(128, std::min(1024, (static_cast<int>(cand) + 63) / 64 * 64));
         if (const char* e = std::getenv("ESP_PAIR_LCAP")) l = std::max(128, std::min(2048, std::atoi(e) / 32 * 32));
-        a.lcap = std::min(l, a.cap) + 32;
+        a.lcap = std::min(l, a.cap) + 128;  // two-phase targets: carry zone (32) + padding rounds (96)
     }
     a.nent_max = (a.bx + M) * (a.bx + 2 * M) * (a.bz + 2 * Mz);
     const long nblocks_all = static_cast<long>((F_[0] + a.bx - 1) / a.bx) *
@@ -3970,15 +4016,21 @@ bool Engine::run_pair_half(long N, cudaStream_t s, int rank, int nranks, bool ow
     if (nblocks_all + 1 > ovf_cap_) return false;  // sized in alloc_cells (no allocation under capture)
     a.ovf = d_ovf_;
     CK(cudaMemsetAsync(d_ovf_, 0, sizeof(int), s));
-    size_t sm = (a.cap + 1) * sizeof(float4) + kHalfWarps * 64 * sizeof(int) +
+    const bool tile = tile_mode_ == 1 || (tile_mode_ < 0 && col_div_ == 2);
+    const bool phased = phased_mode_ != 0;
+    // (the two-phase k_pair_half has no per-warp queue.  Shared memory per CTA
+    // matters beyond occupancy: at cfg5 three CTAs of ~65 KB sit just below the
+    // 196 KB carve-out; 1.5 KB more per CTA selects the next one and leaves
+    // 28 instead of 60 KB of L1 for the partner loads -- measured 19.18 vs
+    // 19.53 ms for the same kernel)
+    const bool has_queue = tile || !phased;
+    size_t sm = (a.cap + 1) * sizeof(float4) + (has_queue ? kHalfWarps * 64 * sizeof(int) : 0) +
                 kHalfWarps * a.lcap * sizeof(unsigned short);
     sm = (sm + 3) / 4 * 4 + (2 * a.nent_max + 1) * sizeof(int) + a.nent_max;
     const int ovf_grid = 2 * sms;
     // cluster-pair kernel: measured faster at ~200 in-range pairs per atom
     // (cfg4: 1.69 vs 1.76 ms), slower at ~400 (cfg5: 20.5 vs 20.1 ms), where
     // the per-target search work it amortises is a smaller share
-    const bool tile = tile_mode_ == 1 || (tile_mode_ < 0 && col_div_ == 2);
-    const bool phased = phased_mode_ != 0;
     pair_kernel_ = (!own_bins && tile) ? 2 : 1;
     auto go = [&](auto kern, auto ovfk) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
