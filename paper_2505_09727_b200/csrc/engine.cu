@@ -480,6 +480,17 @@ __device__ __forceinline__ void fill_range(unsigned short* lw, int lb, int p0, i
     for (; p < p1; ++p) lw[p - lb] = static_cast<unsigned short>(off + p);
 }
 
+// 1 / sqrt(x) for a positive normal x: the MUFU seed (rsqrt.approx.f64,
+// relative error e0 ~ 2^-22) and ONE third-order step
+//   y = y0 (1 + e/2 + 3 e^2 / 8),  e = 1 - x y0^2   (error ~ 5/16 e0^3 < 2^-64)
+// -- five fp64 operations instead of the seven of two Newton steps.
+__device__ __forceinline__ double rsqrt_pos(double x) {
+    double y0;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(x));
+    const double e = fma(-(x * y0), y0, 1.0);
+    return fma(y0 * e, fma(0.375, e, 0.5), y0);
+}
+
 // d = (r_j - r_i) + image shift, in that order: the reference's min-image
 // displacement (ewald.hpp:436-443) bit for bit, hence F_ij = -F_ji exactly.
 template <int ND>
@@ -490,16 +501,7 @@ __device__ __forceinline__ void pair_eval(const PairConsts& k, double4 pj, doubl
     const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
     if (r2 < k.rc2 && r2 > 0.0) {
         ++npair;
-        // 1/sqrt(r2): MUFU seed + two Newton steps (r2 is a positive normal here)
-        double rinv;
-        asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rinv) : "d"(r2));
-        {
-            const double hr = 0.5 * r2;
-            double e = fma(-hr * rinv, rinv, 0.5);
-            rinv = fma(rinv, e, rinv);
-            e = fma(-hr * rinv, rinv, 0.5);
-            rinv = fma(rinv, e, rinv);
-        }
+        const double rinv = rsqrt_pos(r2);  // r2 is a positive normal here
         const double z = fma(r2, k.two_irc2, -1.0);
         // Psi(y) = y H(z); chi(y) = H + 2 (z+1) dH/dz, from one Horner pass
         double H = k.H[ND - 1], dH = 0.0;
@@ -969,15 +971,7 @@ __device__ __forceinline__ bool pair_eval2(const PairConsts& k, double4 pj, doub
     const double dx = (pj.x - xi) + sx, dy = (pj.y - yi) + sy, dz = (pj.z - zi) + sz;
     const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
     if (!(r2 < k.rc2 && r2 > 0.0)) return false;
-    double rinv;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rinv) : "d"(r2));
-    {
-        const double hr = 0.5 * r2;
-        double e = fma(-hr * rinv, rinv, 0.5);
-        rinv = fma(rinv, e, rinv);
-        e = fma(-hr * rinv, rinv, 0.5);
-        rinv = fma(rinv, e, rinv);
-    }
+    const double rinv = rsqrt_pos(r2);
     const double z = fma(r2, k.two_irc2, -1.0);
     double H, dH;
     if (kPairSplit) {
@@ -1041,15 +1035,7 @@ __device__ __forceinline__ bool pair_eval3(const PairConsts& k, double4 pj, doub
     }
     const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
     if (!(r2 < k.rc2 && r2 > 0.0)) return false;
-    double rinv;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rinv) : "d"(r2));
-    {
-        const double hr = 0.5 * r2;
-        double e = fma(-hr * rinv, rinv, 0.5);
-        rinv = fma(rinv, e, rinv);
-        e = fma(-hr * rinv, rinv, 0.5);
-        rinv = fma(rinv, e, rinv);
-    }
+    const double rinv = rsqrt_pos(r2);
     const double z = fma(r2, k.two_irc2, -1.0);
     constexpr int NE = (ND + 1) / 2, NO = ND / 2, NDE = ND / 2, NDO = (ND + 1) / 2 - 1;
     const double w = z * z;
@@ -1605,15 +1591,7 @@ __device__ __forceinline__ bool pair_tile(const PairConsts& k, const double4& pj
     const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
     const bool in = ok && r2 < k.rc2 && r2 > 0.0;
     const double r2s = in ? r2 : k.rc2;
-    double rinv;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rinv) : "d"(r2s));
-    {
-        const double hr = 0.5 * r2s;
-        double e = fma(-hr * rinv, rinv, 0.5);
-        rinv = fma(rinv, e, rinv);
-        e = fma(-hr * rinv, rinv, 0.5);
-        rinv = fma(rinv, e, rinv);
-    }
+    const double rinv = rsqrt_pos(r2s);
     const double z = fma(r2s, k.two_irc2, -1.0);
     constexpr int NE = (ND + 1) / 2, NO = ND / 2, NDE = ND / 2, NDO = (ND + 1) / 2 - 1;
     const double w = z * z;
@@ -2224,6 +2202,220 @@ __global__ void __launch_bounds__(512) k_spread(GridArgs g, const double4* __res
                 *dst += val;  // this colour's tiles are disjoint
             else
                 atomicAdd(dst, val);
+        }
+    }
+}
+
+// ----------------------------------------------------------------------------
+// K1, warp-per-bin form (single GPU, N large): no barriers
+// ----------------------------------------------------------------------------
+//
+// k_spread gives every footprint node a thread and separates consecutive
+// atoms by a CTA barrier: one tile read-modify-write per thread per barrier,
+// three weight loads per node.  Here ONE WARP owns a bin and its tile, so
+// atoms follow each other in program order and nothing has to synchronise
+// across warps; the SM holds as many independent bins as tiles fit.
+//   * lane l holds the footprint pair (jx, jz) = (l / P, l % P) and walks the
+//     P rows jy of its pair: its factor c = q w_x[jx] w_z[jz] is formed once
+//     per atom, each node is one fma(w_y[jy], c, tile) -- a broadcast weight
+//     and 16 bytes of tile traffic per node instead of 40.  Pairs beyond 32
+//     (P = 6: 4 pairs x 6 rows) are packed into extra steps.
+//   * tile layout [x][y][z], dense rows (RS = W), plane stride PS = P (mod 16)
+//     doubles: consecutive pairs (jx P + jz) of a half-warp then fall on 16
+//     distinct 8-byte bank pairs.
+//   * window weights for 32 atoms at a time, lane = atom, from a
+//     shared-memory copy of the window tables (lanes differ only in the piece
+//     index s: 4 distinct rows per load).
+// W = S + P + 1 nodes per side (offsets 0..S+1 by construction, as k_spread).
+constexpr int kSwChunk = 32;
+#ifndef ESP_K1_TABG
+#define ESP_K1_TABG 0  // 1: window tables read from global memory (L1) instead of a per-CTA shared copy
+#endif
+#ifndef ESP_K1_ABLATE
+#define ESP_K1_ABLATE 0  // timing builds (wrong results): 1 no atom loop, 2 no flush, 3 no window weights
+#endif
+
+struct SpreadWarpGeom {
+    int W, RS, PS;      // tile extent, row / plane stride (doubles)
+    size_t smem;        // bytes per warp-CTA
+};
+
+inline SpreadWarpGeom spread_warp_geom(int S, int P) {
+    SpreadWarpGeom w;
+    w.W = S + P + 1;
+    w.RS = w.W;
+    w.PS = w.RS * w.W;
+    while (w.PS % 16 != P % 16) ++w.PS;
+    // tile | weights [32][3][P] | window tables 3 x 4P x 13 | tile offsets [32]
+    w.smem = sizeof(double) * (static_cast<size_t>(w.PS) * w.W + kSwChunk * 3 * P +
+                               (ESP_K1_TABG ? 0 : 3 * 4 * P * kNc)) +
+             sizeof(int) * kSwChunk;
+    return w;
+}
+
+template <int P>
+__global__ void __launch_bounds__(32) k_spread_warp(GridArgs g, int W, int RS, int PS,
+                                                    const double4* __restrict__ xyzq,
+                                                    const int* __restrict__ start,
+                                                    double* __restrict__ grid) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* tile = reinterpret_cast<double*>(smem);           // PS * W
+    double* wch = tile + static_cast<size_t>(PS) * W;         // [32][3][P]
+    double* tab = wch + kSwChunk * 3 * P;                     // [3][4P][13]
+    int* fbase = reinterpret_cast<int*>(tab + (ESP_K1_TABG ? 0 : 3 * 4 * P * kNc));
+    const int lane = threadIdx.x;
+    const int bin = blockIdx.x + g.bin0;
+    const int bz = bin % g.nb[2];
+    const int by = (bin / g.nb[2]) % g.nb[1];
+    const int bx = bin / (g.nb[1] * g.nb[2]);
+    const int ib = start[bin * g.kpb], ie = start[(bin + 1) * g.kpb];
+    if (ib == ie) return;
+    const int lo[3] = {bx * g.S - P / 2, by * g.S - P / 2, bz * g.S - P / 2};
+    const int tsize = PS * W;  // even: PS = P (mod 16) and W = S + P + 1 with S even
+    {
+        double2* t2 = reinterpret_cast<double2*>(tile);
+        for (int t = lane; t < tsize / 2; t += 32) t2[t] = make_double2(0.0, 0.0);
+        if (!ESP_K1_TABG)
+            for (int t = lane; t < 3 * 4 * P * kNc; t += 32) tab[t] = g.win[t];
+    }
+    // footprint nodes of this lane: pair (jx, jz) for the P row steps, and the
+    // packed leftovers (pairs >= 32)
+    constexpr int NP = P * P;
+    constexpr int NFULL = NP < 32 ? NP : 32;      // pairs of the row steps
+    constexpr int NLEFT = NP > 32 ? NP - 32 : 0;  // (P <= 8: at most one more pass)
+    static_assert(NP <= 64, "window order above 8: two leftover passes not implemented");
+    constexpr int NXS = (NLEFT * P + 31) / 32;    // extra steps
+    const bool act = lane < NFULL;
+    const int jx = act ? lane / P : 0, jz = act ? lane % P : 0;
+    const int off0 = jx * PS + jz;
+    int xjx[NXS > 0 ? NXS : 1], xjy[NXS > 0 ? NXS : 1], xjz[NXS > 0 ? NXS : 1], xoff[NXS > 0 ? NXS : 1];
+    bool xact[NXS > 0 ? NXS : 1];
+#pragma unroll
+    for (int e = 0; e < NXS; ++e) {
+        const int item = e * 32 + lane;               // (row, leftover pair)
+        xact[e] = item < NLEFT * P;
+        const int pr = 32 + (xact[e] ? item % NLEFT : 0), row = xact[e] ? item / NLEFT : 0;
+        xjx[e] = pr / P;
+        xjz[e] = pr % P;
+        xjy[e] = row;
+        xoff[e] = xjx[e] * PS + row * RS + xjz[e];
+    }
+    __syncwarp();
+    double4 nxt = make_double4(0.0, 0.0, 0.0, 0.0);
+    if (ib + lane < ie) nxt = xyzq[ib + lane];
+    for (int c0 = ib; c0 < ie; c0 += kSwChunk) {
+        const int nc = min(kSwChunk, ie - c0);
+        const double4 me = nxt;
+        if (c0 + kSwChunk + lane < ie) nxt = xyzq[c0 + kSwChunk + lane];
+        __syncwarp();  // the previous chunk's atoms are done with wch / fbase
+        if (lane < nc && !(ESP_K1_ABLATE == 3 && c0 > ib)) {
+            int fb = 0;
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                const double x = d == 0 ? me.x : (d == 1 ? me.y : me.z);
+                const Foot f = footprint(P, x, g.h[d], g.half[d]);
+                const double* td = (ESP_K1_TABG ? g.win : tab) + d * 4 * P * kNc;
+                double* w = wch + (lane * 3 + d) * P;
+                const double scale = d == 0 ? me.w : 1.0;
+#pragma unroll
+                for (int j = 0; j < P; ++j) {
+                    double wj = horner13(td + (4 * (P - 1 - j) + f.s) * kNc, f.t);
+                    if ((j == 0 && f.zero_lo) || (j == P - 1 && f.zero_hi)) wj = 0.0;
+                    w[j] = wj * scale;
+                }
+                ESP_DCHECK(!isfinite(x) || (f.first - lo[d] >= 0 && f.first - lo[d] <= W - P));
+                const int o = clampi(f.first - lo[d], 0, W - P);
+                fb += o * (d == 0 ? PS : (d == 1 ? RS : 1));
+            }
+            fbase[lane] = fb;
+        }
+        __syncwarp();
+        // per atom: all tile loads first (a store to one row could alias the
+        // next row's load, so the compiler would chain them), the next atom's
+        // factors fetched meanwhile, then the fmas and the stores
+        double c = 0.0, wy[P], cx[NXS > 0 ? NXS : 1], wx_[NXS > 0 ? NXS : 1];
+        int fb;
+        auto factors = [&](int ai, double& c_, double (&wy_)[P], double (&cx_)[NXS > 0 ? NXS : 1],
+                           double (&wyx_)[NXS > 0 ? NXS : 1], int& fb_) {
+            const double* w = wch + ai * 3 * P;
+            fb_ = fbase[ai];
+            c_ = w[jx] * w[2 * P + jz];
+            if constexpr (P % 2 == 0) {  // rows of 3P doubles, w_y at P doubles: 16-byte aligned
+                const double2* w2 = reinterpret_cast<const double2*>(w + P);
+#pragma unroll
+                for (int jy = 0; jy < P / 2; ++jy) {
+                    const double2 t2 = w2[jy];
+                    wy_[2 * jy] = t2.x;
+                    wy_[2 * jy + 1] = t2.y;
+                }
+            } else {
+#pragma unroll
+                for (int jy = 0; jy < P; ++jy) wy_[jy] = w[P + jy];
+            }
+#pragma unroll
+            for (int e = 0; e < NXS; ++e) {
+                cx_[e] = w[xjx[e]] * w[2 * P + xjz[e]];
+                wyx_[e] = w[P + xjy[e]];
+            }
+        };
+        factors(0, c, wy, cx, wx_, fb);
+        for (int ai = 0; ai < (ESP_K1_ABLATE == 1 ? 0 : nc); ++ai) {
+            double* t0 = tile + fb + off0;
+            double* tl = tile + fb;
+            double v[P], vx[NXS > 0 ? NXS : 1];
+#pragma unroll
+            for (int jy = 0; jy < P; ++jy) v[jy] = act ? t0[jy * RS] : 0.0;
+#pragma unroll
+            for (int e = 0; e < NXS; ++e) vx[e] = xact[e] ? tl[xoff[e]] : 0.0;
+            double cn = 0.0, wyn[P], cxn[NXS > 0 ? NXS : 1], wxn[NXS > 0 ? NXS : 1];
+            int fbn = 0;
+            factors(ai + 1 < nc ? ai + 1 : ai, cn, wyn, cxn, wxn, fbn);
+#pragma unroll
+            for (int jy = 0; jy < P; ++jy) v[jy] = fma(wy[jy], c, v[jy]);
+#pragma unroll
+            for (int e = 0; e < NXS; ++e) vx[e] = fma(wx_[e], cx[e], vx[e]);
+            if (act) {
+#pragma unroll
+                for (int jy = 0; jy < P; ++jy) t0[jy * RS] = v[jy];
+            }
+#pragma unroll
+            for (int e = 0; e < NXS; ++e)
+                if (xact[e]) tl[xoff[e]] = vx[e];
+            c = cn;
+            fb = fbn;
+#pragma unroll
+            for (int jy = 0; jy < P; ++jy) wy[jy] = wyn[jy];
+#pragma unroll
+            for (int e = 0; e < NXS; ++e) {
+                cx[e] = cxn[e];
+                wx_[e] = wxn[e];
+            }
+            // (register sums over runs of same-cell atoms, one tile
+            // read-modify-write per run, measured slower: cfg5 2.64 vs 2.50 ms)
+            __syncwarp();  // the next atom's nodes may be other lanes' nodes of this one
+        }
+    }
+    // flush: plane by plane, (iy, iz) advanced incrementally (no divisions)
+    const int q32 = 32 / RS, r32 = 32 - q32 * RS;
+    for (int ix = 0; ix < (ESP_K1_ABLATE == 2 ? 0 : W); ++ix) {
+        const int gx = wrap_once(lo[0] + ix, g.nf[0]);
+        const double* tp = tile + ix * PS;
+        double* gp = grid + static_cast<long>(gx) * g.nf[1] * g.nf[2];
+        int iy = lane / RS, iz = lane - iy * RS;
+        for (int r = lane; r < RS * W; r += 32) {
+            const double val = tp[r];
+            if (val != 0.0) {
+                const int gy = wrap_once(lo[1] + iy, g.nf[1]);
+                const int gz = wrap_once(lo[2] + iz, g.nf[2]);
+                ESP_DCHECK(gx >= 0 && gx < g.nf[0] && gy >= 0 && gy < g.nf[1] && gz >= 0 && gz < g.nf[2]);
+                atomicAdd(gp + static_cast<long>(gy) * g.nf[2] + gz, val);
+            }
+            iz += r32;
+            iy += q32;
+            if (iz >= RS) {
+                iz -= RS;
+                ++iy;
+            }
         }
     }
 }
@@ -3036,6 +3228,31 @@ struct SpreadLaunch {
     }
 };
 
+template <int P>
+struct SpreadWarpLaunch {
+    static void run(const GridArgs& g, int nbin, const double4* xyzq, const int* start,
+                    double* grid, cudaStream_t s) {
+        if constexpr (P >= 5 && P <= 8) {
+            const SpreadWarpGeom w = spread_warp_geom(g.S, P);
+            CK(cudaFuncSetAttribute(k_spread_warp<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(w.smem)));
+            // one-warp CTAs: ask for the largest shared-memory carve-out, the
+            // resident bins per SM are what hides the per-atom latency
+            CK(cudaFuncSetAttribute(k_spread_warp<P>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    cudaSharedmemCarveoutMaxShared));
+            if (std::getenv("ESP_DEBUG_OCC")) {
+                int nb = 0;
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_spread_warp<P>, 32, w.smem));
+                std::fprintf(stderr, "k_spread_warp<%d>: smem %zu B, %d CTAs/SM\n", P, w.smem, nb);
+            }
+            k_spread_warp<P><<<nbin, 32, w.smem, s>>>(g, w.W, w.RS, w.PS, xyzq, start, grid);
+            CK(cudaGetLastError());
+        } else {
+            SpreadLaunch<P>::run(g, nbin, xyzq, start, grid, s);
+        }
+    }
+};
+
 // atoms from which K3 stages each bin's field tile in shared memory
 // (ESP_INTERP_TILE_MIN_N overrides; 0 disables)
 inline long interp_tile_min_n() {
@@ -3448,6 +3665,7 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), device_(device) {
     if (const char* e = std::getenv("ESP_PAIR_HALF")) half_mode_ = std::atoi(e);
     if (const char* e = std::getenv("ESP_PAIR_TILE")) tile_mode_ = std::atoi(e);
     if (const char* e = std::getenv("ESP_PAIR_PHASED")) phased_mode_ = std::atoi(e);
+    if (const char* e = std::getenv("ESP_SPREAD_WARP")) spread_warp_mode_ = std::atoi(e);
     pencil_half_ = pencil_half_env() != 0;
 }
 
@@ -4107,7 +4325,15 @@ void Engine::run_spread(long N, cudaStream_t s, int rank, int nranks, double* gr
     if (b0 < 0) slab_bins(rank, nranks, &b0, &b1);
     if (b1 <= b0) return;
     g.bin0 = b0;
-    dispatch_P<SpreadLaunch>(p.P, g, b1 - b0, d_xyzqB_, d_startB_, grid, s);
+    // warp-per-bin kernel: single-GPU evaluations with cell-sorted bins
+    // (ESP_SPREAD_WARP=0 never, 1 whenever P is in [5, 8])
+    const bool warp_kernel = !gslab && p.P >= 5 && p.P <= 8 &&
+                             (spread_warp_mode_ == 1 ||
+                              (spread_warp_mode_ < 0 && N >= (1L << 14)));
+    if (warp_kernel)
+        dispatch_P<SpreadWarpLaunch>(p.P, g, b1 - b0, d_xyzqB_, d_startB_, grid, s);
+    else
+        dispatch_P<SpreadLaunch>(p.P, g, b1 - b0, d_xyzqB_, d_startB_, grid, s);
     ++launches_;
 }
 

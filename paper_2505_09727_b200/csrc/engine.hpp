@@ -284,6 +284,7 @@ private:
     int tile_mode_ = -1;                // cluster-pair K4 (k_pair_tile) on one GPU: -1 auto (col_div 2), 0 never, 1 always (ESP_PAIR_TILE)
     bool tmp_written_ = true;           // prepare() wrote the folded original-order copy d_tmp_
     const double* prep_q_ = nullptr;    // charges of the last prepare() (combine reads them when !tmp_written_)
+    int spread_warp_mode_ = -1;         // warp-per-bin K1 (k_spread_warp): -1 auto (N >= 2^14), 0 never, 1 always (ESP_SPREAD_WARP)
     int phased_mode_ = 1;               // two-phase targets in k_pair_half (ESP_PAIR_PHASED=0: queue flushes inside the screening loop)
     int pair_kernel_ = -1;              // K4 kernel of the last launch (esp_plan_info.pair_kernel)
     int half_mode_ = 1;                 // half-shell K4: 0 never, 1 from kHalfMinN atoms, 2 always (ESP_PAIR_HALF)
