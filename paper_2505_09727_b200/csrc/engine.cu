@@ -2229,7 +2229,7 @@ __global__ void __launch_bounds__(512) k_spread(GridArgs g, const double4* __res
 // W = S + P + 1 nodes per side (offsets 0..S+1 by construction, as k_spread).
 constexpr int kSwChunk = 32;
 #ifndef ESP_K1_TABG
-#define ESP_K1_TABG 0  // 1: window tables read from global memory (L1) instead of a per-CTA shared copy
+#define ESP_K1_TABG 1  // 1: window tables read from global memory (L1), 0: from a per-CTA shared copy
 #endif
 #ifndef ESP_K1_ABLATE
 #define ESP_K1_ABLATE 0  // timing builds (wrong results): 1 no atom loop, 2 no flush, 3 no window weights
@@ -2246,24 +2246,24 @@ inline SpreadWarpGeom spread_warp_geom(int S, int P) {
     w.RS = w.W;
     w.PS = w.RS * w.W;
     while (w.PS % 16 != P % 16) ++w.PS;
-    // tile | weights [32][3][P] | window tables 3 x 4P x 13 | tile offsets [32]
-    w.smem = sizeof(double) * (static_cast<size_t>(w.PS) * w.W + kSwChunk * 3 * P +
+    // tile | weights [2][32][3][P] | window tables 3 x 4P x 13 | tile offsets [2][32]
+    w.smem = sizeof(double) * (static_cast<size_t>(w.PS) * w.W + 2 * kSwChunk * 3 * P +
                                (ESP_K1_TABG ? 0 : 3 * 4 * P * kNc)) +
-             sizeof(int) * kSwChunk;
+             sizeof(int) * 2 * kSwChunk;
     return w;
 }
 
 template <int P>
-__global__ void __launch_bounds__(32) k_spread_warp(GridArgs g, int W, int RS, int PS,
+__global__ void __launch_bounds__(64) k_spread_warp(GridArgs g, int W, int RS, int PS,
                                                     const double4* __restrict__ xyzq,
                                                     const int* __restrict__ start,
                                                     double* __restrict__ grid) {
     extern __shared__ __align__(16) unsigned char smem[];
     double* tile = reinterpret_cast<double*>(smem);           // PS * W
-    double* wch = tile + static_cast<size_t>(PS) * W;         // [32][3][P]
-    double* tab = wch + kSwChunk * 3 * P;                     // [3][4P][13]
-    int* fbase = reinterpret_cast<int*>(tab + (ESP_K1_TABG ? 0 : 3 * 4 * P * kNc));
-    const int lane = threadIdx.x;
+    double* wch0 = tile + static_cast<size_t>(PS) * W;        // [2][32][3][P]
+    double* tab = wch0 + 2 * kSwChunk * 3 * P;                // [3][4P][13]
+    int* fbase0 = reinterpret_cast<int*>(tab + (ESP_K1_TABG ? 0 : 3 * 4 * P * kNc));  // [2][32]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int bin = blockIdx.x + g.bin0;
     const int bz = bin % g.nb[2];
     const int by = (bin / g.nb[2]) % g.nb[1];
@@ -2274,12 +2274,12 @@ __global__ void __launch_bounds__(32) k_spread_warp(GridArgs g, int W, int RS, i
     const int tsize = PS * W;  // even: PS = P (mod 16) and W = S + P + 1 with S even
     {
         double2* t2 = reinterpret_cast<double2*>(tile);
-        for (int t = lane; t < tsize / 2; t += 32) t2[t] = make_double2(0.0, 0.0);
+        for (int t = threadIdx.x; t < tsize / 2; t += 64) t2[t] = make_double2(0.0, 0.0);
         if (!ESP_K1_TABG)
-            for (int t = lane; t < 3 * 4 * P * kNc; t += 32) tab[t] = g.win[t];
+            for (int t = threadIdx.x; t < 3 * 4 * P * kNc; t += 64) tab[t] = g.win[t];
     }
-    // footprint nodes of this lane: pair (jx, jz) for the P row steps, and the
-    // packed leftovers (pairs >= 32)
+    // footprint nodes of a lane of the spreading warp: pair (jx, jz) for the
+    // P row steps, and the packed leftovers (pairs >= 32)
     constexpr int NP = P * P;
     constexpr int NFULL = NP < 32 ? NP : 32;      // pairs of the row steps
     constexpr int NLEFT = NP > 32 ? NP - 32 : 0;  // (P <= 8: at most one more pass)
@@ -2300,22 +2300,20 @@ __global__ void __launch_bounds__(32) k_spread_warp(GridArgs g, int W, int RS, i
         xjy[e] = row;
         xoff[e] = xjx[e] * PS + row * RS + xjz[e];
     }
-    __syncwarp();
-    double4 nxt = make_double4(0.0, 0.0, 0.0, 0.0);
-    if (ib + lane < ie) nxt = xyzq[ib + lane];
-    for (int c0 = ib; c0 < ie; c0 += kSwChunk) {
+    // warp 1 prepares chunk k + 1 (window weights and tile offsets of 32
+    // atoms, lane = atom) while warp 0 spreads chunk k: double-buffered,
+    // one CTA barrier per chunk
+    auto prepare = [&](int c0, int buf) {
         const int nc = min(kSwChunk, ie - c0);
-        const double4 me = nxt;
-        if (c0 + kSwChunk + lane < ie) nxt = xyzq[c0 + kSwChunk + lane];
-        __syncwarp();  // the previous chunk's atoms are done with wch / fbase
         if (lane < nc && !(ESP_K1_ABLATE == 3 && c0 > ib)) {
+            const double4 me = xyzq[c0 + lane];
             int fb = 0;
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
                 const double x = d == 0 ? me.x : (d == 1 ? me.y : me.z);
                 const Foot f = footprint(P, x, g.h[d], g.half[d]);
                 const double* td = (ESP_K1_TABG ? g.win : tab) + d * 4 * P * kNc;
-                double* w = wch + (lane * 3 + d) * P;
+                double* w = wch0 + ((buf * kSwChunk + lane) * 3 + d) * P;
                 const double scale = d == 0 ? me.w : 1.0;
 #pragma unroll
                 for (int j = 0; j < P; ++j) {
@@ -2327,10 +2325,23 @@ __global__ void __launch_bounds__(32) k_spread_warp(GridArgs g, int W, int RS, i
                 const int o = clampi(f.first - lo[d], 0, W - P);
                 fb += o * (d == 0 ? PS : (d == 1 ? RS : 1));
             }
-            fbase[lane] = fb;
+            fbase0[buf * kSwChunk + lane] = fb;
         }
-        __syncwarp();
-        // per atom: all tile loads first (a store to one row could alias the
+    };
+    __syncthreads();  // tile zeroed, tables copied
+    if (warp == 1) prepare(ib, 0);
+    __syncthreads();
+    int buf = 0;
+    for (int c0 = ib; c0 < ie; c0 += kSwChunk, buf ^= 1) {
+        const int nc = min(kSwChunk, ie - c0);
+        if (warp == 1) {
+            if (c0 + kSwChunk < ie) prepare(c0 + kSwChunk, buf ^ 1);
+            __syncthreads();
+            continue;
+        }
+        const double* wch = wch0 + buf * kSwChunk * 3 * P;
+        const int* fbase = fbase0 + buf * kSwChunk;
+    // per atom: all tile loads first (a store to one row could alias the
         // next row's load, so the compiler would chain them), the next atom's
         // factors fetched meanwhile, then the fmas and the stores
         double c = 0.0, wy[P], cx[NXS > 0 ? NXS : 1], wx_[NXS > 0 ? NXS : 1];
@@ -2394,10 +2405,12 @@ __global__ void __launch_bounds__(32) k_spread_warp(GridArgs g, int W, int RS, i
             // read-modify-write per run, measured slower: cfg5 2.64 vs 2.50 ms)
             __syncwarp();  // the next atom's nodes may be other lanes' nodes of this one
         }
+        __syncthreads();
     }
-    // flush: plane by plane, (iy, iz) advanced incrementally (no divisions)
+    // flush: plane by plane (the two warps take alternate planes), (iy, iz)
+    // advanced incrementally (no divisions)
     const int q32 = 32 / RS, r32 = 32 - q32 * RS;
-    for (int ix = 0; ix < (ESP_K1_ABLATE == 2 ? 0 : W); ++ix) {
+    for (int ix = warp; ix < (ESP_K1_ABLATE == 2 ? 0 : W); ix += 2) {
         const int gx = wrap_once(lo[0] + ix, g.nf[0]);
         const double* tp = tile + ix * PS;
         double* gp = grid + static_cast<long>(gx) * g.nf[1] * g.nf[2];
@@ -3242,10 +3255,10 @@ struct SpreadWarpLaunch {
                                     cudaSharedmemCarveoutMaxShared));
             if (std::getenv("ESP_DEBUG_OCC")) {
                 int nb = 0;
-                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_spread_warp<P>, 32, w.smem));
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_spread_warp<P>, 64, w.smem));
                 std::fprintf(stderr, "k_spread_warp<%d>: smem %zu B, %d CTAs/SM\n", P, w.smem, nb);
             }
-            k_spread_warp<P><<<nbin, 32, w.smem, s>>>(g, w.W, w.RS, w.PS, xyzq, start, grid);
+            k_spread_warp<P><<<nbin, 64, w.smem, s>>>(g, w.W, w.RS, w.PS, xyzq, start, grid);
             CK(cudaGetLastError());
         } else {
             SpreadLaunch<P>::run(g, nbin, xyzq, start, grid, s);
