@@ -444,12 +444,14 @@ def run_ours(args):
                 "work": f"{FLOPS_PER_UNORDERED_PAIR} flops x {ordered_pairs // 2} unordered "
                         "in-range pairs (counted on device)",
                 "kernel_ms": stages_ms["local"],
-                "limiter": "instruction issue (profiles/r02_k4_lines_cfg5.md, cfg5: 68 % issue "
-                           "active, fp64 pipe 33 %): ~290 warp instructions per 32 pairs, of "
-                           "which the fp64 pair terms of both sides are ~32 % and the "
-                           "neighbour search the rest -- fp32 screen + ballot compaction 16 %, "
-                           "queue flushes 10 %, candidate-list fill 10 %, staging and "
-                           "per-target setup 12 %, partial rounds 5 %, partner REDs 7 %"}
+                "limiter": "instruction issue and the fp64 pipe (profiles/r02_k4_lines_cfg5.md, "
+                           "cfg5: 73 % issue active, fp64 pipe 34 %): ~300 warp instructions per "
+                           "32 pairs, of which the fp64 pair terms of both sides are ~31 % (62 "
+                           "fp64 operations per pair, ~70 % of the fp64 pipe while they run) and "
+                           "the neighbour search the rest.  Ablation builds (DESIGN.md 4): pair "
+                           "terms + operand fetch 8.8 of 19.2 ms, per-target setup + list fill "
+                           "3.8, fp32 screen + in-place compaction 2.6, partner REDs 2.1, "
+                           "staging 1.5"}
 
     # ---- every grid-pipeline kernel against the HBM roofline (SURVEY 8(d)
     # algorithmic bytes; serialised stage times).  The grids fit in L2 (cfg5:
@@ -465,11 +467,12 @@ def run_ours(args):
     M = int(np.prod(plan.nf))
     Mh = int(plan.nf[0] * plan.nf[1] * (plan.nf[2] // 2 + 1))
     nfld = 4 if args.force_method == "ik" else 1
+    k1name = "K1 k_spread_warp" if plan.spread_kernel == "warp" else "K1 k_spread"
     if plan.fused_xpass:
         # 2-D cuFFT planes + K2 fused into the x pass (read b and p, write the
         # nfld half-transformed fields); the inverse planes write planar fields
         kbytes = {
-            "K1 k_spread": (32 * N + 8 * M, "spread"),
+            k1name: (32 * N + 8 * M, "spread"),
             "K2+x-DFTs k_xpass (fused)": ((24 + 16 * nfld) * Mh, "scale"),
             "K3 k_interp": (8 * nfld * M + 64 * N, "interpolate"),
             "cuFFT D2Z 2-D planes": (8 * M + 16 * Mh, "fft"),
@@ -481,7 +484,7 @@ def run_ours(args):
         }
     else:
         kbytes = {
-            "K1 k_spread": (32 * N + 8 * M, "spread"),
+            k1name: (32 * N + 8 * M, "spread"),
             "K2 k_scale": ((24 + 16 * nfld) * Mh, "scale"),
             "K3 k_interp": (8 * nfld * M + 64 * N, "interpolate"),
             "cuFFT D2Z": (8 * M + 16 * Mh, "fft"),
@@ -510,7 +513,7 @@ def run_ours(args):
     sm_mhz = (clk or {}).get("sm_mhz") or 1965.0
     smem_peak = n_sm * 128.0 * sm_mhz * 1e6 / 1e9  # GB/s
     P3 = int(plan.P) ** 3
-    for name, (nbytes, stage) in {"K1 k_spread (shared-memory tile RMW)": (16 * P3 * N, "spread"),
+    for name, (nbytes, stage) in {k1name + " (shared-memory tile RMW)": (16 * P3 * N, "spread"),
                                   "K3 (footprint node reads)": (32 * P3 * N, "interpolate")}.items():
         kms = stages_ms.get(stage)
         if kms:

@@ -88,6 +88,11 @@ typedef struct {
                              * -1 none yet, 0 full lists (k_pair), 1 half-shell
                              * (k_pair_half), 2 cluster pairs (k_pair_tile),
                              * 3 all pairs (box too small for the cell list) */
+    int spread_kernel;      /* spreading kernel of the plan's last evaluation:
+                             * -1 none yet, 0 k_spread (CTA per bin, thread per
+                             * footprint node), 1 k_spread_warp (a warp per bin;
+                             * single-GPU path, N >= 2^14, P in [5, 8];
+                             * ESP_SPREAD_WARP=0/1 forces) */
 } esp_plan_info;
 
 /* Per-stage wall time in seconds (EnergyForces::timings keys,

@@ -80,7 +80,7 @@ class _Info(C.Structure):
         ("n_split_coef", C.c_int), ("n_window_coef", C.c_int), ("pair_poly_degree", C.c_int),
         ("pair_fit_err", C.c_double), ("device", C.c_int), ("pair_cells", C.c_int * 3),
         ("pencil_half", C.c_int), ("fused_xpass", C.c_int), ("deterministic", C.c_int),
-        ("pair_kernel", C.c_int),
+        ("pair_kernel", C.c_int), ("spread_kernel", C.c_int),
     ]
 
 
@@ -256,6 +256,14 @@ class EwaldPlan:
         info = _Info()
         _check(_lib.esp_plan_get_info(self._h, C.byref(info)))
         return {-1: "none", 0: "full", 1: "half", 2: "tile", 3: "allpairs"}[info.pair_kernel]
+
+    @property
+    def spread_kernel(self) -> str:
+        """Spreading kernel of the plan's last evaluation (esp_plan_info.spread_kernel):
+        "none", "cta" (k_spread) or "warp" (k_spread_warp)."""
+        info = _Info()
+        _check(_lib.esp_plan_get_info(self._h, C.byref(info)))
+        return {-1: "none", 0: "cta", 1: "warp"}[info.spread_kernel]
 
     def __del__(self):
         h = getattr(self, "_h", None)

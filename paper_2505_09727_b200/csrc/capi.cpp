@@ -188,6 +188,7 @@ int esp_plan_get_info(const esp_plan* p, esp_plan_info* o) {
         o->fused_xpass = p->eng && p->eng->fused_xpass() ? 1 : 0;
         o->deterministic = p->eng && p->eng->deterministic() ? 1 : 0;
         o->pair_kernel = p->eng ? p->eng->pair_kernel() : -1;
+        o->spread_kernel = p->eng ? p->eng->spread_kernel() : -1;
         o->pair_fit_err = P.pair_fit_err;
         o->device = p->device;
     });

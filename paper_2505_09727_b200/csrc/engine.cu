@@ -2226,7 +2226,7 @@ __global__ void __launch_bounds__(512) k_spread(GridArgs g, const double4* __res
 //   * window weights for 32 atoms at a time, lane = atom, from a
 //     shared-memory copy of the window tables (lanes differ only in the piece
 //     index s: 4 distinct rows per load).
-// W = S + P + 1 nodes per side (offsets 0..S+1 by construction, as k_spread).
+// W = S + P (+ 1 for odd P) nodes per side, see spread_warp_geom.
 constexpr int kSwChunk = 32;
 #ifndef ESP_K1_TABG
 #define ESP_K1_TABG 1  // 1: window tables read from global memory (L1), 0: from a per-CTA shared copy
@@ -2242,7 +2242,11 @@ struct SpreadWarpGeom {
 
 inline SpreadWarpGeom spread_warp_geom(int S, int P) {
     SpreadWarpGeom w;
-    w.W = S + P + 1;
+    // tile offsets f.first - lo: atoms are binned by floor(x / h) with the last
+    // bin clamped, so with lo = b S - P/2 they lie in [1, S + 1] for even P and
+    // in [0, S + 1] for odd P (first = floor(x / h + 1/2) - (P - 1)/2); even
+    // windows shift lo by one
+    w.W = S + P + (P % 2);
     w.RS = w.W;
     w.PS = w.RS * w.W;
     while (w.PS % 16 != P % 16) ++w.PS;
@@ -2270,8 +2274,9 @@ __global__ void __launch_bounds__(64) k_spread_warp(GridArgs g, int W, int RS, i
     const int bx = bin / (g.nb[1] * g.nb[2]);
     const int ib = start[bin * g.kpb], ie = start[(bin + 1) * g.kpb];
     if (ib == ie) return;
-    const int lo[3] = {bx * g.S - P / 2, by * g.S - P / 2, bz * g.S - P / 2};
-    const int tsize = PS * W;  // even: PS = P (mod 16) and W = S + P + 1 with S even
+    constexpr int LS = P / 2 - (P % 2 == 0 ? 1 : 0);  // see spread_warp_geom
+    const int lo[3] = {bx * g.S - LS, by * g.S - LS, bz * g.S - LS};
+    const int tsize = PS * W;  // even: PS = P (mod 16), W = S + P + (P odd) with S even
     {
         double2* t2 = reinterpret_cast<double2*>(tile);
         for (int t = threadIdx.x; t < tsize / 2; t += 64) t2[t] = make_double2(0.0, 0.0);
@@ -4343,6 +4348,7 @@ void Engine::run_spread(long N, cudaStream_t s, int rank, int nranks, double* gr
     const bool warp_kernel = !gslab && p.P >= 5 && p.P <= 8 &&
                              (spread_warp_mode_ == 1 ||
                               (spread_warp_mode_ < 0 && N >= (1L << 14)));
+    spread_kernel_ = warp_kernel ? 1 : 0;
     if (warp_kernel)
         dispatch_P<SpreadWarpLaunch>(p.P, g, b1 - b0, d_xyzqB_, d_startB_, grid, s);
     else

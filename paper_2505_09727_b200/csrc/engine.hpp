@@ -167,6 +167,7 @@ public:
     bool pencil_half() const { return pencil_half_; }
     bool fused_xpass() const { return xpass_; }
     int pair_kernel() const { return pair_kernel_; }
+    int spread_kernel() const { return spread_kernel_; }
     // Deterministic mode: bitwise-identical results run to run for the same
     // inputs (stable sorts instead of atomic ranks, full-list K4 without
     // partner REDs, K1 tiles flushed by bin colours with plain adds); the
@@ -286,6 +287,7 @@ private:
     const double* prep_q_ = nullptr;    // charges of the last prepare() (combine reads them when !tmp_written_)
     int spread_warp_mode_ = -1;         // warp-per-bin K1 (k_spread_warp): -1 auto (N >= 2^14), 0 never, 1 always (ESP_SPREAD_WARP)
     int phased_mode_ = 1;               // two-phase targets in k_pair_half (ESP_PAIR_PHASED=0: queue flushes inside the screening loop)
+    int spread_kernel_ = -1;            // K1 kernel of the last launch (esp_plan_info.spread_kernel)
     int pair_kernel_ = -1;              // K4 kernel of the last launch (esp_plan_info.pair_kernel)
     int half_mode_ = 1;                 // half-shell K4: 0 never, 1 from kHalfMinN atoms, 2 always (ESP_PAIR_HALF)
 
