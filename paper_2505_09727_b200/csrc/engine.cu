@@ -480,6 +480,25 @@ __device__ __forceinline__ void fill_range(unsigned short* lw, int lb, int p0, i
     for (; p < p1; ++p) lw[p - lb] = static_cast<unsigned short>(off + p);
 }
 
+// The same for ranges padded to whole groups of four: p0, p1 and lb are
+// multiples of 4, entries at list positions >= pv (the range's padding, at
+// most 3, all in its last group) get the sentinel index `sent`.  64-bit
+// stores only: no scalar head and tail loops.
+__device__ __forceinline__ void fill_range4(unsigned short* lw, int lb, int p0, int p1, int off,
+                                            int pv, unsigned sent) {
+    ESP_DCHECK(((p0 | p1 | lb) & 3) == 0 && (p1 <= p0 || (p0 >= lb && off + pv - 1 < 65536)));
+    for (int p = p0; p < p1; p += 4) {
+        unsigned long long v = static_cast<unsigned long long>(off + p) * 0x0001000100010001ull +
+                               0x0003000200010000ull;
+        const int nv = pv - p;  // valid entries of this group (>= 1)
+        if (nv < 4) {
+            const unsigned long long m = ~0ull >> (64 - 16 * nv);
+            v = (v & m) | (static_cast<unsigned long long>(sent) * 0x0001000100010001ull & ~m);
+        }
+        *reinterpret_cast<unsigned long long*>(lw + (p - lb)) = v;
+    }
+}
+
 // 1 / sqrt(x) for a positive normal x: the MUFU seed (rsqrt.approx.f64,
 // relative error e0 ~ 2^-22) and ONE third-order step
 //   y = y0 (1 + e/2 + 3 e^2 / 8),  e = 1 - x y0^2   (error ~ 5/16 e0^3 < 2^-64)
@@ -923,6 +942,9 @@ struct HalfArgs {
     const int* orig;
     const int* start;     // ncell + 1
     double* acc;          // pair-sorted order, planar: u | Fx | Fy | Fz (stride nacc), zero at rest
+    double* acc1;         // acc + nacc, acc + 2 nacc, acc + 3 nacc: the component planes as
+    double* acc2;         // kernel parameters (one IMAD.WIDE per RED address instead of
+    double* acc3;         // 64-bit stride arithmetic in every round)
     long nacc;
     unsigned long long* npairs;  // ordered in-range pairs (2 per evaluated unordered pair)
     int* ovf;                    // [0] overflowed blocks, [1..] their ids
@@ -946,6 +968,12 @@ struct HalfArgs {
 
 #ifndef ESP_K4_P2
 #define ESP_K4_P2 1  // rounds loop of the two-phase targets: 0 no prefetch, 1 one round ahead, 2 ping-pong x2
+#endif
+#ifndef ESP_K4_RED4
+#define ESP_K4_RED4 1  // partner REDs: component plane pointers from the kernel parameters
+#endif
+#ifndef ESP_K4_FILL4
+#define ESP_K4_FILL4 1  // two-phase targets: every column's list range padded to a multiple of 4 entries (64-bit stores only)
 #endif
 #ifndef ESP_K4_ABLATE
 #define ESP_K4_ABLATE 0  // timing builds (wrong results): 1 staging only, 2 + target setup and list fill, 3 + screening, 4 all but the partner REDs
@@ -1065,12 +1093,22 @@ __device__ __forceinline__ bool pair_eval3(const PairConsts& k, double4 pj, doub
 // (u, F) terms of sorted atom j into the planar accumulators (global REDs;
 // the 32 lanes of a round mostly hold consecutive sorted atoms, so one RED
 // instruction touches a few 32-byte sectors per component)
-__device__ __forceinline__ void red_acc(double* acc, long n, int j, double a, double b, double c,
+__device__ __forceinline__ void red_acc(const HalfArgs& h, int j, double a, double b, double c,
                                         double d) {
+#if ESP_K4_RED4
+    const unsigned uj = static_cast<unsigned>(j);
+    atomicAdd(h.acc + uj, a);
+    atomicAdd(h.acc1 + uj, b);
+    atomicAdd(h.acc2 + uj, c);
+    atomicAdd(h.acc3 + uj, d);
+#else
+    double* acc = h.acc;
+    const long n = h.nacc;
     atomicAdd(acc + j, a);
     atomicAdd(acc + n + j, b);
     atomicAdd(acc + 2 * n + j, c);
     atomicAdd(acc + 3 * n + j, d);
+#endif
 }
 
 // forward column l of a target (lane l < M(2M+1) + M + 1): offsets (dx, dy)
@@ -1320,7 +1358,9 @@ __global__ void __launch_bounds__(kHalfThreads, ESP_K4_MINB) k_pair_half(HalfArg
                 }
             }
         }
-        int inc = cnt;
+        // list positions per column (ESP_K4_FILL4: padded to groups of four)
+        const int cntl = (TWO && ESP_K4_FILL4) ? (cnt + 3) & ~3 : cnt;
+        int inc = cntl;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int v = __shfl_up_sync(0xffffffffu, inc, o);
@@ -1337,7 +1377,11 @@ __global__ void __launch_bounds__(kHalfThreads, ESP_K4_MINB) k_pair_half(HalfArg
             unsigned short* lin = lw + 32;
             for (int lb = 0; lb < T; lb += piece) {
                 const int le = min(T, lb + piece);
-                fill_range(lin, lb, max(inc - cnt, lb), min(inc, le), beg - (inc - cnt));
+                if (ESP_K4_FILL4)
+                    fill_range4(lin, lb, max(inc - cntl, lb), min(inc, le), beg - (inc - cntl),
+                                inc - cntl + cnt, static_cast<unsigned>(a.cap));
+                else
+                    fill_range(lin, lb, max(inc - cnt, lb), min(inc, le), beg - (inc - cnt));
                 const int n = le - lb;
                 const int n64 = (n + 63) & ~63;
                 ESP_DCHECK(32 + n64 + 96 <= a.lcap);
@@ -1402,7 +1446,7 @@ __global__ void __launch_bounds__(kHalfThreads, ESP_K4_MINB) k_pair_half(HalfArg
                                                           pi.w, u, fx, fy, fz, g))) {
                             ++npair;
                             if (ESP_K4_ABLATE == 4) { u += g.x + g.y + g.z + g.w; } else
-                            red_acc(a.acc, a.nacc, sj, g.x, g.y, g.z, g.w);
+                            red_acc(a, sj, g.x, g.y, g.z, g.w);
                         }
                     };
                     const unsigned short* lp = lw + lane;
@@ -1483,7 +1527,7 @@ __global__ void __launch_bounds__(kHalfThreads, ESP_K4_MINB) k_pair_half(HalfArg
                                   : pair_eval3<ND, false>(k, pf, 0.0, 0.0, 0.0, pi.x, pi.y, pi.z,
                                                           pi.w, u, fx, fy, fz, g))) {
                             ++npair;
-                            red_acc(a.acc, a.nacc, sf, g.x, g.y, g.z, g.w);
+                            red_acc(a, sf, g.x, g.y, g.z, g.w);
                         }
                     }
                     const int cd = __float_as_int(cand[sq].w);
@@ -1505,7 +1549,7 @@ __global__ void __launch_bounds__(kHalfThreads, ESP_K4_MINB) k_pair_half(HalfArg
                       : pair_eval3<ND, false>(k, pf, 0.0, 0.0, 0.0, pi.x, pi.y, pi.z, pi.w, u,
                                               fx, fy, fz, g))) {
                 ++npair;
-                red_acc(a.acc, a.nacc, sf, g.x, g.y, g.z, g.w);
+                red_acc(a, sf, g.x, g.y, g.z, g.w);
             }
         }
         if (lane < qn) {
@@ -1522,7 +1566,7 @@ __global__ void __launch_bounds__(kHalfThreads, ESP_K4_MINB) k_pair_half(HalfArg
                       : pair_eval3<ND, false>(k, pj, 0.0, 0.0, 0.0, pi.x, pi.y, pi.z, pi.w, u,
                                               fx, fy, fz, g))) {
                 ++npair;
-                red_acc(a.acc, a.nacc, cd & 0x7ffffff, g.x, g.y, g.z, g.w);
+                red_acc(a, cd & 0x7ffffff, g.x, g.y, g.z, g.w);
             }
         }
         }  // !TWO
@@ -1856,7 +1900,7 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_tile(HalfArgs a, const
             g.y += __shfl_xor_sync(0xffffffffu, g.y, 16);
             g.z += __shfl_xor_sync(0xffffffffu, g.z, 16);
             g.w += __shfl_xor_sync(0xffffffffu, g.w, 16);
-            if (isub == 0 && jv) red_acc(a.acc, a.nacc, sf, g.x, g.y, g.z, g.w);
+            if (isub == 0 && jv) red_acc(a, sf, g.x, g.y, g.z, g.w);
         };
         auto fetch = [&](int sq, double4& pf, int& tf, int& sf) {
             const int cd = __float_as_int(cand[sq].w);
@@ -2004,7 +2048,7 @@ __global__ void __launch_bounds__(256) k_pair_half_ovf(HalfArgs a, const __grid_
                                                shiftv[t][2], pi.x, pi.y, pi.z, pi.w, u, fx, fy,
                                                fz, g)) {
                                 ++npair;
-                                red_acc(a.acc, a.nacc, j, g.x, g.y, g.z, g.w);
+                                red_acc(a, j, g.x, g.y, g.z, g.w);
                             }
                         }
                     }
@@ -2016,7 +2060,7 @@ __global__ void __launch_bounds__(256) k_pair_half_ovf(HalfArgs a, const __grid_
                     fy += __shfl_xor_sync(0xffffffffu, fy, o);
                     fz += __shfl_xor_sync(0xffffffffu, fz, o);
                 }
-                if (lane == 0) red_acc(a.acc, a.nacc, i, u, -pi.w * fx, -pi.w * fy, -pi.w * fz);
+                if (lane == 0) red_acc(a, i, u, -pi.w * fx, -pi.w * fy, -pi.w * fz);
             }
         }
     }
@@ -4200,6 +4244,9 @@ bool Engine::run_pair_half(long N, cudaStream_t s, int rank, int nranks, bool ow
     a.orig = d_origA_;
     a.start = d_startA_;
     a.acc = d_acc_;
+    a.acc1 = d_acc_ + N;
+    a.acc2 = d_acc_ + 2 * N;
+    a.acc3 = d_acc_ + 3 * N;
     a.nacc = N;
     a.npairs = d_npairs_;
     for (int d = 0; d < 3; ++d) {
