@@ -982,7 +982,10 @@ struct HalfArgs {
 #define ESP_K4_MINB 3  // resident CTAs per SM k_pair_half is compiled for (80 registers)
 #endif
 constexpr int kHalfMaxBX = 4;
-constexpr int kHalfWarps = 8;
+#ifndef ESP_K4_WARPS
+#define ESP_K4_WARPS 8  // warps per CTA of the half-shell kernels (9: 72 registers, 27 warps per SM)
+#endif
+constexpr int kHalfWarps = ESP_K4_WARPS;
 constexpr int kHalfThreads = 32 * kHalfWarps;
 
 // (u, F) terms of one pair from both sides, scaled by 4 pi (the caller applies
