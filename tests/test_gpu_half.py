@@ -75,6 +75,19 @@ def test_half_overflow_path(esp, gpu, monkeypatch):
     _compare_to_full(esp, monkeypatch, gpu, esp.ParticleSystem(box, q, pos), c.eps, c.r_c)
 
 
+@pytest.mark.parametrize("lcap", ["128", "256"])
+def test_half_short_list_pieces(esp, gpu, monkeypatch, lcap):
+    """Per-warp list capacity far below a target's candidate count (cfg2:
+    ~400 candidates, pieces of 128 / 256 entries): every target takes several
+    list pieces, padded column ranges are clipped at piece boundaries and
+    survivors that do not fill a round are carried into the next piece."""
+    from paper_2505_09727_b200 import systems as S
+    c = S.config("cfg2")
+    pos, q, box = c.system()
+    monkeypatch.setenv("ESP_PAIR_LCAP", lcap)
+    _compare_to_full(esp, monkeypatch, gpu, esp.ParticleSystem(box, q, pos), c.eps, c.r_c)
+
+
 def test_half_clustered_system(esp, gpu, monkeypatch):
     """Strongly non-uniform density: the dense region's blocks overflow the
     capacity sized for the mean density, the rest take the staged path."""
