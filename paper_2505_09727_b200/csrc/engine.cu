@@ -969,6 +969,12 @@ struct HalfArgs {
 #ifndef ESP_K4_P2
 #define ESP_K4_P2 1  // rounds loop of the two-phase targets: 0 no prefetch, 1 one round ahead, 2 ping-pong x2
 #endif
+#ifndef ESP_K4_DHORNER
+#define ESP_K4_DHORNER 1  // pair terms: H and dH/dz from one set of coefficients (Horner with derivative)
+#endif
+#ifndef ESP_K4_SCR128
+#define ESP_K4_SCR128 1  // two-phase targets: screen 128 candidates per iteration while 128 remain
+#endif
 #ifndef ESP_K4_RED4
 #define ESP_K4_RED4 1  // partner REDs: component plane pointers from the kernel parameters
 #endif
@@ -994,6 +1000,51 @@ constexpr int kHalfThreads = 32 * kHalfWarps;
 //   4 pi S(r)      = (1 - y H) / r       = 1/r - Hs
 //   4 pi (-dS/dr)  = chi/(r_c r) + 4 pi S / r = (Gs + 4 pi S) / r
 // which drops y = r / r_c, w = 1/(4 pi r) and two products from every pair.
+// Hs(z) = He(w) + z Ho(w), w = z^2, and dHs/dz.  ESP_K4_DHORNER: the
+// derivative comes out of the same Horner recurrences (dp <- dp w + p;
+// p <- p w + c), dHs/dz = Ho + 2 (z He'(w) + w Ho'(w)): half the coefficient
+// operands of separate derivative polynomials (De, Do) for one more fp64
+// operation.  On sm_100a every coefficient is a constant-bank load (LDCU /
+// LDC) per evaluation and the rounds loop is issue-bound (a DFMA holds the
+// issue port ~1.4 cycles, any other instruction ~1.2:
+// tools/micro/fp64_issue.cu): cfg5 K4 19.08 -> 18.83 ms.
+template <int ND>
+__device__ __forceinline__ void poly_H_dH(const PairConsts& k, double z, double& H, double& dH) {
+    static_assert(ND >= 6, "even/odd split needs at least three terms per part");
+    constexpr int NE = (ND + 1) / 2, NO = ND / 2;
+    const double w = z * z;
+#if ESP_K4_DHORNER
+    double he = k.He[NE - 1], ho = k.Ho[NO - 1];
+    double dhe = he, dho = ho;
+    he = fma(he, w, k.He[NE - 2]);
+    ho = fma(ho, w, k.Ho[NO - 2]);
+#pragma unroll
+    for (int m = NE - 3; m >= 0; --m) {
+        dhe = fma(dhe, w, he);
+        he = fma(he, w, k.He[m]);
+        if (m <= NO - 3) {
+            dho = fma(dho, w, ho);
+            ho = fma(ho, w, k.Ho[m]);
+        }
+    }
+    H = fma(z, ho, he);
+    dH = fma(2.0, fma(w, dho, z * dhe), ho);
+#else
+    // De floor(ND/2) coefficients (odd k >= 1), Do ceil(ND/2)-1 (even k >= 2)
+    constexpr int NDE = ND / 2, NDO = (ND + 1) / 2 - 1;
+    double he = k.He[NE - 1], ho = k.Ho[NO - 1], de = k.De[NDE - 1], dO = k.Do[NDO - 1];
+#pragma unroll
+    for (int m = NE - 2; m >= 0; --m) {
+        he = fma(he, w, k.He[m]);
+        if (m < NO - 1) ho = fma(ho, w, k.Ho[m]);
+        if (m < NDE - 1) de = fma(de, w, k.De[m]);
+        if (m < NDO - 1) dO = fma(dO, w, k.Do[m]);
+    }
+    H = fma(z, ho, he);
+    dH = fma(z, dO, de);
+#endif
+}
+
 template <int ND>
 __device__ __forceinline__ bool pair_eval2(const PairConsts& k, double4 pj, double sx, double sy,
                                            double sz, double xi, double yi, double zi, double qi,
@@ -1006,20 +1057,7 @@ __device__ __forceinline__ bool pair_eval2(const PairConsts& k, double4 pj, doub
     const double z = fma(r2, k.two_irc2, -1.0);
     double H, dH;
     if (kPairSplit) {
-        // Hs has ND coefficients (degree ND-1): He ceil(ND/2), Ho floor(ND/2),
-        // De floor(ND/2) (odd k >= 1), Do ceil(ND/2)-1 (even k >= 2)
-        constexpr int NE = (ND + 1) / 2, NO = ND / 2, NDE = ND / 2, NDO = (ND + 1) / 2 - 1;
-        const double w = z * z;
-        double he = k.He[NE - 1], ho = k.Ho[NO - 1], de = k.De[NDE - 1], dO = k.Do[NDO - 1];
-#pragma unroll
-        for (int m = NE - 2; m >= 0; --m) {
-            he = fma(he, w, k.He[m]);
-            if (m < NO - 1) ho = fma(ho, w, k.Ho[m]);
-            if (m < NDE - 1) de = fma(de, w, k.De[m]);
-            if (m < NDO - 1) dO = fma(dO, w, k.Do[m]);
-        }
-        H = fma(z, ho, he);
-        dH = fma(z, dO, de);
+        poly_H_dH<ND>(k, z, H, dH);
     } else {
         H = k.Hs[ND - 1];
         dH = 0.0;
@@ -1068,18 +1106,8 @@ __device__ __forceinline__ bool pair_eval3(const PairConsts& k, double4 pj, doub
     if (!(r2 < k.rc2 && r2 > 0.0)) return false;
     const double rinv = rsqrt_pos(r2);
     const double z = fma(r2, k.two_irc2, -1.0);
-    constexpr int NE = (ND + 1) / 2, NO = ND / 2, NDE = ND / 2, NDO = (ND + 1) / 2 - 1;
-    const double w = z * z;
-    double he = k.He[NE - 1], ho = k.Ho[NO - 1], de = k.De[NDE - 1], dO = k.Do[NDO - 1];
-#pragma unroll
-    for (int m = NE - 2; m >= 0; --m) {
-        he = fma(he, w, k.He[m]);
-        if (m < NO - 1) ho = fma(ho, w, k.Ho[m]);
-        if (m < NDE - 1) de = fma(de, w, k.De[m]);
-        if (m < NDO - 1) dO = fma(dO, w, k.Do[m]);
-    }
-    const double H = fma(z, ho, he);
-    const double dH = fma(z, dO, de);
+    double H, dH;
+    poly_H_dH<ND>(k, z, H, dH);
     const double G = fma(fma(2.0, z, 2.0), dH, H);  // chi / r_c
     const double pot = rinv - H;                     // 4 pi S
     const double c0 = (G + pot) * (rinv * rinv);     // 4 pi (-dS/dr) / r
@@ -1393,7 +1421,34 @@ __global__ void __launch_bounds__(kHalfThreads, ESP_K4_MINB) k_pair_half(HalfArg
                 __syncwarp();
                 if (ESP_K4_ABLATE == 2) continue;
                 // phase 1: screen 64 candidates per iteration, compact in place
-                for (const unsigned short* lp = lin + lane; lp < lin + n64; lp += 64) {
+                const unsigned short* lp = lin + lane;
+#if ESP_K4_SCR128
+                // 128 candidates per iteration while at least 128 remain (four
+                // independent load chains in flight), then one 64-wide step
+                for (; lp + 64 < lin + n64; lp += 128) {
+                    const int s0 = lp[0], s1 = lp[32], s2 = lp[64], s3 = lp[96];
+                    const float4 a0 = cand[s0], a1 = cand[s1], a2 = cand[s2], a3 = cand[s3];
+                    const float dx0 = a0.x - xf, dy0 = a0.y - yf, dz0 = a0.z - zf;
+                    const float dx1 = a1.x - xf, dy1 = a1.y - yf, dz1 = a1.z - zf;
+                    const float dx2 = a2.x - xf, dy2 = a2.y - yf, dz2 = a2.z - zf;
+                    const float dx3 = a3.x - xf, dy3 = a3.y - yf, dz3 = a3.z - zf;
+                    const bool in0 = fmaf(dz0, dz0, fmaf(dy0, dy0, dx0 * dx0)) < R2;
+                    const bool in1 = fmaf(dz1, dz1, fmaf(dy1, dy1, dx1 * dx1)) < R2;
+                    const bool in2 = fmaf(dz2, dz2, fmaf(dy2, dy2, dx2 * dx2)) < R2;
+                    const bool in3 = fmaf(dz3, dz3, fmaf(dy3, dy3, dx3 * dx3)) < R2;
+                    const unsigned m0 = __ballot_sync(0xffffffffu, in0);
+                    const unsigned m1 = __ballot_sync(0xffffffffu, in1);
+                    const unsigned m2 = __ballot_sync(0xffffffffu, in2);
+                    const unsigned m3 = __ballot_sync(0xffffffffu, in3);
+                    const int q1 = qn + __popc(m0), q2 = q1 + __popc(m1), q3 = q2 + __popc(m2);
+                    if (in0) lw[qn + __popc(m0 & lt_mask)] = static_cast<unsigned short>(s0);
+                    if (in1) lw[q1 + __popc(m1 & lt_mask)] = static_cast<unsigned short>(s1);
+                    if (in2) lw[q2 + __popc(m2 & lt_mask)] = static_cast<unsigned short>(s2);
+                    if (in3) lw[q3 + __popc(m3 & lt_mask)] = static_cast<unsigned short>(s3);
+                    qn = q3 + __popc(m3);
+                }
+#endif
+                for (; lp < lin + n64; lp += 64) {
                     const int s0 = lp[0], s1 = lp[32];
                     ESP_DCHECK(s0 <= a.cap && s1 <= a.cap);
                     const float4 a0 = cand[s0], a1 = cand[s1];
@@ -1640,18 +1695,8 @@ __device__ __forceinline__ bool pair_tile(const PairConsts& k, const double4& pj
     const double r2s = in ? r2 : k.rc2;
     const double rinv = rsqrt_pos(r2s);
     const double z = fma(r2s, k.two_irc2, -1.0);
-    constexpr int NE = (ND + 1) / 2, NO = ND / 2, NDE = ND / 2, NDO = (ND + 1) / 2 - 1;
-    const double w = z * z;
-    double he = k.He[NE - 1], ho = k.Ho[NO - 1], de = k.De[NDE - 1], dO = k.Do[NDO - 1];
-#pragma unroll
-    for (int m = NE - 2; m >= 0; --m) {
-        he = fma(he, w, k.He[m]);
-        if (m < NO - 1) ho = fma(ho, w, k.Ho[m]);
-        if (m < NDE - 1) de = fma(de, w, k.De[m]);
-        if (m < NDO - 1) dO = fma(dO, w, k.Do[m]);
-    }
-    const double H = fma(z, ho, he);
-    const double dH = fma(z, dO, de);
+    double H, dH;
+    poly_H_dH<ND>(k, z, H, dH);
     const double G = fma(fma(2.0, z, 2.0), dH, H);  // chi / r_c
     double pot = rinv - H;                           // 4 pi S
     double c0 = (G + pot) * (rinv * rinv);           // 4 pi (-dS/dr) / r
