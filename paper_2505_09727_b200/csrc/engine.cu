@@ -14,6 +14,7 @@
 // stream; K3 joins them.  All arithmetic is fp64; no tensor cores (nothing on
 // the path is a dense contraction).
 
+#include <type_traits>
 #include "engine.hpp"
 
 #include <cub/device/device_radix_sort.cuh>
@@ -967,7 +968,13 @@ struct HalfArgs {
 };
 
 #ifndef ESP_K4_P2
-#define ESP_K4_P2 1  // rounds loop of the two-phase targets: 0 no prefetch, 1 one round ahead, 2 ping-pong x2
+#define ESP_K4_P2 4  // rounds loop of the two-phase targets: 0 no prefetch, 1 one round ahead (operand copies), 2 ping-pong x2, 4 one round ahead into the same registers (displacement first)
+#endif
+#ifndef ESP_K4_FENCE
+#define ESP_K4_FENCE 0  // P2 = 4: compiler fence between the displacement and the refetch
+#endif
+#ifndef ESP_K4_PTRREG
+#define ESP_K4_PTRREG 0  // P2 = 4: accumulator plane pointers pinned in registers across the rounds of a piece
 #endif
 #ifndef ESP_K4_DHORNER
 #define ESP_K4_DHORNER 1  // pair terms: H and dH/dz from one set of coefficients (Horner with derivative)
@@ -1113,6 +1120,32 @@ __device__ __forceinline__ bool pair_eval3(const PairConsts& k, double4 pj, doub
     const double c0 = (G + pot) * (rinv * rinv);     // 4 pi (-dS/dr) / r
     u = fma(pj.w, pot, u);
     const double c = pj.w * c0;
+    fx = fma(c, dx, fx);
+    fy = fma(c, dy, fy);
+    fz = fma(c, dz, fz);
+    const double b = qi * c;
+    gj = make_double4(qi * pot, b * dx, b * dy, b * dz);
+    return true;
+}
+
+// The same from the displacement d = (r_j - r_i) [+ s] and q_j (the rounds
+// loop computes d first and then reuses r_j's registers for the next round's
+// operands)
+template <int ND>
+__device__ __forceinline__ bool pair_eval_d(const PairConsts& k, double dx, double dy, double dz,
+                                            double qj, double qi, double& u, double& fx,
+                                            double& fy, double& fz, double4& gj) {
+    const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+    if (!(r2 < k.rc2 && r2 > 0.0)) return false;
+    const double rinv = rsqrt_pos(r2);
+    const double z = fma(r2, k.two_irc2, -1.0);
+    double H, dH;
+    poly_H_dH<ND>(k, z, H, dH);
+    const double G = fma(fma(2.0, z, 2.0), dH, H);  // chi / r_c
+    const double pot = rinv - H;                     // 4 pi S
+    const double c0 = (G + pot) * (rinv * rinv);     // 4 pi (-dS/dr) / r
+    u = fma(qj, pot, u);
+    const double c = qj * c0;
     fx = fma(c, dx, fx);
     fy = fma(c, dy, fy);
     fz = fma(c, dz, fz);
@@ -1519,6 +1552,55 @@ __global__ void __launch_bounds__(kHalfThreads, ESP_K4_MINB) k_pair_half(HalfArg
                         fetch(lp + 64, pa, ta, sa);
                         evalr(pb, tb, sb);
                     }
+#elif ESP_K4_P2 == 4
+                    // one round ahead WITHOUT register copies: the displacement
+                    // (all that depends on r_j) is taken first, then the next
+                    // round's operands are fetched into the same registers.
+                    // One loop per image mode (a predicated shift would still
+                    // issue its nine instructions in interior blocks).
+#if ESP_K4_PTRREG
+                    // plane pointers pinned in registers across the rounds
+                    double *acc0 = a.acc, *acc1 = a.acc1, *acc2 = a.acc2, *acc3 = a.acc3;
+                    asm volatile("" : "+l"(acc0), "+l"(acc1), "+l"(acc2), "+l"(acc3));
+#endif
+                    auto rounds = [&](auto wr) {
+                        constexpr bool WR = decltype(wr)::value;
+                        double4 pn;
+                        int tn, sn;
+                        fetch(lp, pn, tn, sn);
+                        for (; lp < lend; lp += 32) {
+                            double dx = pn.x - pi.x, dy = pn.y - pi.y, dz = pn.z - pi.z;
+                            if (WR) {
+                                dx += shiftv[tn][0];
+                                dy += shiftv[tn][1];
+                                dz += shiftv[tn][2];
+                            }
+                            const double qj = pn.w;
+                            const int sj = sn;
+                            const bool take = !(OWN && sj >= cs && sj < ce) || pos_after(pn, pi);
+#if ESP_K4_FENCE
+                            // the displacement is complete before the refetch is
+                            // issued (otherwise the loads land in other registers
+                            // and are copied at the loop end)
+                            asm volatile("" : "+d"(dx), "+d"(dy), "+d"(dz) : : "memory");
+#endif
+                            fetch(lp + 32, pn, tn, sn);
+                            double4 g;
+                            if (take && pair_eval_d<ND>(k, dx, dy, dz, qj, pi.w, u, fx, fy, fz, g)) {
+                                ++npair;
+#if ESP_K4_PTRREG
+                                const unsigned uj = static_cast<unsigned>(sj);
+                                atomicAdd(acc0 + uj, g.x);
+                                atomicAdd(acc1 + uj, g.y);
+                                atomicAdd(acc2 + uj, g.z);
+                                atomicAdd(acc3 + uj, g.w);
+#else
+                                red_acc(a, sj, g.x, g.y, g.z, g.w);
+#endif
+                            }
+                        }
+                    };
+                    if (wrap) rounds(std::true_type{}); else rounds(std::false_type{});
 #elif ESP_K4_P2 == 1
                     double4 pn;
                     int tn, sn;
