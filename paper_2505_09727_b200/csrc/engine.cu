@@ -970,12 +970,6 @@ struct HalfArgs {
 #ifndef ESP_K4_P2
 #define ESP_K4_P2 4  // rounds loop of the two-phase targets: 0 no prefetch, 1 one round ahead (operand copies), 2 ping-pong x2, 4 one round ahead into the same registers (displacement first)
 #endif
-#ifndef ESP_K4_FENCE
-#define ESP_K4_FENCE 0  // P2 = 4: compiler fence between the displacement and the refetch
-#endif
-#ifndef ESP_K4_PTRREG
-#define ESP_K4_PTRREG 0  // P2 = 4: accumulator plane pointers pinned in registers across the rounds of a piece
-#endif
 #ifndef ESP_K4_DHORNER
 #define ESP_K4_DHORNER 1  // pair terms: H and dH/dz from one set of coefficients (Horner with derivative)
 #endif
@@ -1558,11 +1552,6 @@ __global__ void __launch_bounds__(kHalfThreads, ESP_K4_MINB) k_pair_half(HalfArg
                     // round's operands are fetched into the same registers.
                     // One loop per image mode (a predicated shift would still
                     // issue its nine instructions in interior blocks).
-#if ESP_K4_PTRREG
-                    // plane pointers pinned in registers across the rounds
-                    double *acc0 = a.acc, *acc1 = a.acc1, *acc2 = a.acc2, *acc3 = a.acc3;
-                    asm volatile("" : "+l"(acc0), "+l"(acc1), "+l"(acc2), "+l"(acc3));
-#endif
                     auto rounds = [&](auto wr) {
                         constexpr bool WR = decltype(wr)::value;
                         double4 pn;
@@ -1578,25 +1567,11 @@ __global__ void __launch_bounds__(kHalfThreads, ESP_K4_MINB) k_pair_half(HalfArg
                             const double qj = pn.w;
                             const int sj = sn;
                             const bool take = !(OWN && sj >= cs && sj < ce) || pos_after(pn, pi);
-#if ESP_K4_FENCE
-                            // the displacement is complete before the refetch is
-                            // issued (otherwise the loads land in other registers
-                            // and are copied at the loop end)
-                            asm volatile("" : "+d"(dx), "+d"(dy), "+d"(dz) : : "memory");
-#endif
                             fetch(lp + 32, pn, tn, sn);
                             double4 g;
                             if (take && pair_eval_d<ND>(k, dx, dy, dz, qj, pi.w, u, fx, fy, fz, g)) {
                                 ++npair;
-#if ESP_K4_PTRREG
-                                const unsigned uj = static_cast<unsigned>(sj);
-                                atomicAdd(acc0 + uj, g.x);
-                                atomicAdd(acc1 + uj, g.y);
-                                atomicAdd(acc2 + uj, g.z);
-                                atomicAdd(acc3 + uj, g.w);
-#else
                                 red_acc(a, sj, g.x, g.y, g.z, g.w);
-#endif
                             }
                         }
                     };
