@@ -488,15 +488,21 @@ __device__ __forceinline__ void fill_range(unsigned short* lw, int lb, int p0, i
 __device__ __forceinline__ void fill_range4(unsigned short* lw, int lb, int p0, int p1, int off,
                                             int pv, unsigned sent) {
     ESP_DCHECK(((p0 | p1 | lb) & 3) == 0 && (p1 <= p0 || (p0 >= lb && off + pv - 1 < 65536)));
-    for (int p = p0; p < p1; p += 4) {
-        unsigned long long v = static_cast<unsigned long long>(off + p) * 0x0001000100010001ull +
-                               0x0003000200010000ull;
-        const int nv = pv - p;  // valid entries of this group (>= 1)
-        if (nv < 4) {
-            const unsigned long long m = ~0ull >> (64 - 16 * nv);
-            v = (v & m) | (static_cast<unsigned long long>(sent) * 0x0001000100010001ull & ~m);
-        }
-        *reinterpret_cast<unsigned long long*>(lw + (p - lb)) = v;
+    // two 32-bit halves per group (b | b+1 << 16, b+2 | b+3 << 16) from one
+    // 32-bit multiply-add: the 64-bit multiply and the per-group padding test
+    // were half of this loop's instructions
+    const int pf = min(p1, pv & ~3);  // end of the full groups
+    int p = p0;
+    for (; p < pf; p += 4) {
+        const unsigned lo = static_cast<unsigned>(off + p) * 0x00010001u + 0x00010000u;
+        *reinterpret_cast<uint2*>(lw + (p - lb)) = make_uint2(lo, lo + 0x00020002u);
+    }
+    if (p < p1) {
+        // the range's last group: nv = pv - p in 1..3 valid entries, then sentinels
+        const int nv = pv - p;
+        const unsigned b = static_cast<unsigned>(off + p);
+        const unsigned e1 = nv > 1 ? b + 1 : sent, e2 = nv > 2 ? b + 2 : sent;
+        *reinterpret_cast<uint2*>(lw + (p - lb)) = make_uint2(b | (e1 << 16), e2 | (sent << 16));
     }
 }
 
