@@ -944,14 +944,41 @@ __global__ void __launch_bounds__(128) k_pair_allpairs(long N, long i0, long i1,
 // and re-zeroes the accumulators.  A block whose neighbourhood exceeds the
 // staging capacity is queued for k_pair_half_ovf.
 
+// Accumulator layout.  ESP_K4_ACCCHUNK: the four components are interleaved in
+// chunks of kAccChunk atoms -- u | Fx | Fy | Fz of atoms [0, 65536), then of
+// the next 65536, ... -- so that one address reaches all four with immediate
+// offsets (0, 512 KB, 1 MB, 1.5 MB): 4 instead of 8 address instructions per
+// round of partner REDs, the same sectors per RED as the planar layout.
+#ifndef ESP_K4_ACCCHUNK
+#define ESP_K4_ACCCHUNK 1
+#endif
+constexpr unsigned kAccChunk = 65536;
+__host__ __device__ __forceinline__ long acc_capacity(long n) {
+#if ESP_K4_ACCCHUNK
+    return 4 * ((n + kAccChunk - 1) / kAccChunk) * static_cast<long>(kAccChunk);
+#else
+    return 4 * n;
+#endif
+}
+// element index of component 0 of sorted atom j (N < 2^27: fits 32 bits);
+// component c is acc_stride(n) elements further
+__device__ __forceinline__ unsigned acc_index(unsigned j) {
+#if ESP_K4_ACCCHUNK
+    return j + 3u * kAccChunk * (j >> 16);
+#else
+    return j;
+#endif
+}
+static_assert(kAccChunk == 1u << 16, "acc_index shifts by 16");
+
 struct HalfArgs {
     const double4* xyzq;  // sorted by pair cell
     const int* orig;
     const int* start;     // ncell + 1
-    double* acc;          // pair-sorted order, planar: u | Fx | Fy | Fz (stride nacc), zero at rest
-    double* acc1;         // acc + nacc, acc + 2 nacc, acc + 3 nacc: the component planes as
-    double* acc2;         // kernel parameters (one IMAD.WIDE per RED address instead of
-    double* acc3;         // 64-bit stride arithmetic in every round)
+    double* acc;          // pair-sorted order, u | Fx | Fy | Fz chunk-interleaved (acc_index), zero at rest
+    double* acc1;         // planar layout (ESP_K4_ACCCHUNK=0 builds): acc + nacc, acc + 2 nacc,
+    double* acc2;         // acc + 3 nacc as kernel parameters
+    double* acc3;
     long nacc;
     unsigned long long* npairs;  // ordered in-range pairs (2 per evaluated unordered pair)
     int* ovf;                    // [0] overflowed blocks, [1..] their ids
@@ -1159,7 +1186,13 @@ __device__ __forceinline__ bool pair_eval_d(const PairConsts& k, double dx, doub
 // instruction touches a few 32-byte sectors per component)
 __device__ __forceinline__ void red_acc(const HalfArgs& h, int j, double a, double b, double c,
                                         double d) {
-#if ESP_K4_RED4
+#if ESP_K4_ACCCHUNK
+    double* p = h.acc + acc_index(static_cast<unsigned>(j));
+    atomicAdd(p, a);
+    atomicAdd(p + kAccChunk, b);
+    atomicAdd(p + 2 * kAccChunk, c);
+    atomicAdd(p + 3 * kAccChunk, d);
+#elif ESP_K4_RED4
     const unsigned uj = static_cast<unsigned>(j);
     atomicAdd(h.acc + uj, a);
     atomicAdd(h.acc1 + uj, b);
@@ -1704,7 +1737,8 @@ __global__ void __launch_bounds__(kHalfThreads, ESP_K4_MINB) k_pair_half(HalfArg
             w += __shfl_xor_sync(0xffffffffu, w, 1);
             if ((lane & 7) == 0) {
                 const int comp = lane >> 3;  // 0 u, 1 Fx, 2 Fy, 3 Fz (4 pi-scaled, as acc)
-                atomicAdd(a.acc + comp * a.nacc + gi, comp == 0 ? w : -pi.w * w);
+                atomicAdd(a.acc + acc_index(gi) + comp * (ESP_K4_ACCCHUNK ? long(kAccChunk) : a.nacc),
+                          comp == 0 ? w : -pi.w * w);
             }
         }
         // next target: dynamic assignment balances the warps of the CTA
@@ -2080,7 +2114,8 @@ __global__ void __launch_bounds__(kHalfThreads, 3) k_pair_tile(HalfArgs a, const
             w += __shfl_xor_sync(0xffffffffu, w, 1);
             if ((lane & 3) == 0 && vi) {
                 const int comp = (lane >> 2) & 3;  // 0 u, 1 Fx, 2 Fy, 3 Fz
-                atomicAdd(a.acc + comp * a.nacc + gi, comp == 0 ? w : -pi.w * w);
+                atomicAdd(a.acc + acc_index(gi) + comp * (ESP_K4_ACCCHUNK ? long(kAccChunk) : a.nacc),
+                          comp == 0 ? w : -pi.w * w);
             }
         }
         int nx = 0;
@@ -2188,11 +2223,13 @@ __global__ void __launch_bounds__(256) k_acc_to_loc(long N, double* __restrict__
     const long j = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
     if (j >= N) return;
     constexpr double s = 1.0 / (4.0 * kPi);
-    const double4 v = make_double4(s * acc[j], s * acc[N + j], s * acc[2 * N + j], s * acc[3 * N + j]);
-    acc[j] = 0.0;
-    acc[N + j] = 0.0;
-    acc[2 * N + j] = 0.0;
-    acc[3 * N + j] = 0.0;
+    double* p = acc + acc_index(static_cast<unsigned>(j));
+    const long cs = ESP_K4_ACCCHUNK ? static_cast<long>(kAccChunk) : N;
+    const double4 v = make_double4(s * p[0], s * p[cs], s * p[2 * cs], s * p[3 * cs]);
+    p[0] = 0.0;
+    p[cs] = 0.0;
+    p[2 * cs] = 0.0;
+    p[3 * cs] = 0.0;
     loc[orig[j]] = v;
 }
 
@@ -3995,8 +4032,8 @@ void Engine::ensure_capacity(long N) {
     dalloc(d_origB_, c);
     dalloc(d_loc_, c);
     dalloc(d_specres_, c);
-    dalloc(d_acc_, 4 * c);  // half-shell K4 accumulators: zero at rest
-    CK(cudaMemset(d_acc_, 0, sizeof(double) * 4 * c));
+    dalloc(d_acc_, acc_capacity(c));  // half-shell K4 accumulators: zero at rest
+    CK(cudaMemset(d_acc_, 0, sizeof(double) * acc_capacity(c)));
     dalloc(d_epart_, grid1(c, 128) + 1);
     cap_ = c;
     if (deterministic_) alloc_det(c);
