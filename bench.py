@@ -444,14 +444,14 @@ def run_ours(args):
                 "work": f"{FLOPS_PER_UNORDERED_PAIR} flops x {ordered_pairs // 2} unordered "
                         "in-range pairs (counted on device)",
                 "kernel_ms": stages_ms["local"],
-                "limiter": "instruction issue and the fp64 pipe (profiles/r02_k4_lines_cfg5.md, "
-                           "cfg5: 73 % issue active, fp64 pipe 34 %): ~300 warp instructions per "
-                           "32 pairs, of which the fp64 pair terms of both sides are ~31 % (62 "
-                           "fp64 operations per pair, ~70 % of the fp64 pipe while they run) and "
-                           "the neighbour search the rest.  Ablation builds (DESIGN.md 4): pair "
-                           "terms + operand fetch 8.8 of 19.2 ms, per-target setup + list fill "
-                           "3.8, fp32 screen + in-place compaction 2.6, partner REDs 2.1, "
-                           "staging 1.5"}
+                "limiter": "instruction issue (profiles/r02j_full_cfg5.md, r02i_k4_lines_cfg5.md; "
+                           "cfg5: issue 65-70 % active, fp64 pipe 35 %): ~250 warp instructions per "
+                           "32 pairs, 63 of them fp64 pair terms.  On the B200 a warp DFMA holds "
+                           "the issue port ~1.4 cycles and any other instruction ~1.2 "
+                           "(tools/micro/fp64_issue.cu), so the rounds loop (63 fp64 + ~50 other "
+                           "instructions per round) and the neighbour search (~130 per 32 pairs) "
+                           "are both issue-bound; DESIGN.md 4 lists what was removed and what is "
+                           "left"}
 
     # ---- every grid-pipeline kernel against the HBM roofline (SURVEY 8(d)
     # algorithmic bytes; serialised stage times).  The grids fit in L2 (cfg5:
