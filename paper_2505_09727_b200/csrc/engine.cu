@@ -1181,7 +1181,7 @@ __device__ __forceinline__ bool pair_eval_d(const PairConsts& k, double dx, doub
     return true;
 }
 
-// (u, F) terms of sorted atom j into the planar accumulators (global REDs;
+// (u, F) terms of sorted atom j into the component-wise accumulators (global REDs;
 // the 32 lanes of a round mostly hold consecutive sorted atoms, so one RED
 // instruction touches a few 32-byte sectors per component)
 __device__ __forceinline__ void red_acc(const HalfArgs& h, int j, double a, double b, double c,
