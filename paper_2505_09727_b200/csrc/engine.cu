@@ -4447,7 +4447,10 @@ bool Engine::run_pair_half(long N, cudaStream_t s, int rank, int nranks, bool ow
     if (nblocks_all + 1 > ovf_cap_) return false;  // sized in alloc_cells (no allocation under capture)
     a.ovf = d_ovf_;
     CK(cudaMemsetAsync(d_ovf_, 0, sizeof(int), s));
-    const bool tile = tile_mode_ == 1 || (tile_mode_ < 0 && col_div_ == 2);
+    // cluster-pair kernel only on request: with the rounds-loop work of the
+    // last session of round 2 the warp-per-target kernel is faster at cfg4
+    // too (1.52 vs 1.65 ms)
+    const bool tile = tile_mode_ == 1;
     const bool phased = phased_mode_ != 0;
     // (the two-phase k_pair_half has no per-warp queue.  Shared memory per CTA
     // matters beyond occupancy: at cfg5 three CTAs of ~65 KB sit just below the

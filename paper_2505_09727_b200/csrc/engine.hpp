@@ -282,7 +282,7 @@ private:
     double density_hint_ = 0.0;        // set_density_hint
     bool pencil_half_ = true;           // distributed FFT with half-shell K4 (ESP_PENCIL_HALF=0: full
                                         // lists); local inputs return the ghost partner terms (dist.py)
-    int tile_mode_ = -1;                // cluster-pair K4 (k_pair_tile) on one GPU: -1 auto (col_div 2), 0 never, 1 always (ESP_PAIR_TILE)
+    int tile_mode_ = -1;                // cluster-pair K4 (k_pair_tile) on one GPU: 1 always, otherwise never (ESP_PAIR_TILE)
     bool tmp_written_ = true;           // prepare() wrote the folded original-order copy d_tmp_
     const double* prep_q_ = nullptr;    // charges of the last prepare() (combine reads them when !tmp_written_)
     int spread_warp_mode_ = -1;         // warp-per-bin K1 (k_spread_warp): -1 auto (N >= 2^14), 0 never, 1 always (ESP_SPREAD_WARP)

@@ -79,12 +79,13 @@ def test_tile_evaluate_matches_reference(esp, gpu, monkeypatch, name):
 
 
 def test_tile_auto_selection(esp, gpu, monkeypatch):
-    """Default (-1): cluster pairs for cfg4 (r_c/2 columns), the half-shell
-    warp-per-target kernel for cfg2 (r_c/3 columns), full lists below 4096."""
+    """Default: the half-shell warp-per-target kernel from 4096 atoms (cfg4 with
+    r_c/2 columns included: since the end of round 2 it is faster there than
+    the cluster pairs, which run only with ESP_PAIR_TILE=1), full lists below."""
     from paper_2505_09727_b200 import systems as S
     monkeypatch.delenv("ESP_PAIR_TILE", raising=False)
     monkeypatch.delenv("ESP_PAIR_HALF", raising=False)
-    for name, want in (("cfg4", "tile"), ("cfg2", "half"), ("cfg1", "full")):
+    for name, want in (("cfg4", "half"), ("cfg2", "half"), ("cfg1", "full")):
         c = S.config(name)
         pos, q, box = c.system()
         plan = esp.build_plan(box, "pswf", c.eps, c.r_c, device=gpu)
