@@ -4356,10 +4356,13 @@ bool Engine::run_pair_half(long N, cudaStream_t s, int rank, int nranks, bool ow
                                  ((F_[2] + bz - 1) / bz);
             const double tgt = per_cell * bx * bx * bz;
             // prefer enough blocks to fill the GPU (>= 2 waves of 3 CTAs per
-            // SM), then ~140 targets per block (measured optimum across cfg2-5:
-            // staging amortised, dynamic target assignment still balanced)
+            // SM), then ~150 targets per block (measured optimum across cfg2-5:
+            // staging amortised, dynamic target assignment still balanced; 150
+            // rather than 140 since the end of round 2: it picks 3 x 3 x 6
+            // blocks instead of 4 x 4 x 3 at cfg5 -- 14 instead of 16 staged
+            // atoms per target -- 18.31 -> 18.12 ms)
             const double score = (nblocks >= want_blocks ? 1e9 : 0.0) +
-                                 (nblocks >= want_blocks ? -std::fabs(std::log(tgt / 140.0)) : tgt);
+                                 (nblocks >= want_blocks ? -std::fabs(std::log(tgt / 150.0)) : tgt);
             if (score > best_t) {
                 best_t = score;
                 best_bx = bx;
